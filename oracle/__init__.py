@@ -1,0 +1,357 @@
+"""ORACLE — test infrastructure only.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference
+legs may import this package.  The product path (paper_2101_08143_b200) never
+imports it, and this package never imports the product path: they share no code,
+headers, tables or constants.  Only the seeded input generators (synth/) serve both.
+
+A plain, slow, obviously-correct CPU fp64 implementation of what the hot path
+computes, written from PAPER.md (/root/reference/PAPER.md, cited as P:L<n>) and
+SURVEY.md §8(c).  Every function cites the passage it follows.  Pins (tests/
+test_oracle_pins.py) tie each function to something other than itself: the
+paper's P5 forest matrix, closed forms (K_n, star, path via Fibonacci, 2-node
+path), brute-force forest enumeration and the FJ iteration (Eq. 1), and exact
+identities.  No function here is "parity unpinned".
+
+Functions
+---------
+canonical_csr     O-1: simple undirected graph from raw edges -> CSR ("simple graph",
+                  P:L88 adjacency A=(w_ij) symmetric; SURVEY §8(c) O-1 readings for self-loops
+                  and duplicates).
+degrees           O-2: d_i = sum_j w_ij.
+ipl_apply         (I + L) x with L = D - A.
+incidence_apply   W^{1/2} B x, one entry per edge, head = lower id.
+dense_ipl         dense I + L (P:L103 forest matrix Omega = (I+L)^{-1}).
+solve_dense       z = (I+L)^{-1} s by dense Cholesky (Eq. (2); "Exact" P:L631).
+solve_pcg         z by plain fp64 Jacobi-PCG in C, for n too large for dense.
+quantities        C_I, D, P, C, I_dc by Definitions 3.1-3.5,
+                  PDI = P + D (BASELINE.json north_star), cross-checks s^T z.
+fj_iterate        synchronous iteration of the FJ update rule, Eq. (1).
+forest_census     spanning rooted forest weights eps(Gamma), eps(Gamma_ij).
+"""
+from __future__ import annotations
+
+import ctypes
+import itertools
+import math
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+WT_UNIT, WT_U8, WT_F64 = 0, 1, 3
+
+
+def build(force: bool = False) -> str:
+    src = os.path.join(_HERE, "oracle_cg.c")
+    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(src):
+        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-o", _SO, src, "-lm"])
+    return _SO
+
+
+def _L():
+    global _lib
+    if _lib is None:
+        build()
+        lib = ctypes.CDLL(_SO)
+        i64, ptr, dbl, cint = ctypes.c_int64, ctypes.c_void_p, ctypes.c_double, ctypes.c_int
+        lib.oracle_degrees.argtypes = [i64, ptr, cint, ptr, ptr]
+        lib.oracle_ipl_apply.argtypes = [i64, ptr, ptr, cint, ptr, ptr, ptr, ptr]
+        lib.oracle_pcg.argtypes = [i64, ptr, ptr, cint, ptr, ptr, dbl, i64, cint, ptr, ptr]
+        lib.oracle_pcg.restype = cint
+        lib.oracle_pcg_fixed_iters.argtypes = [i64, ptr, ptr, cint, ptr, ptr, i64, ptr]
+        lib.oracle_pcg_fixed_iters.restype = cint
+        lib.oracle_num_threads.restype = cint
+        _lib = lib
+    return _lib
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+def num_threads() -> int:
+    return int(_L().oracle_num_threads())
+
+
+# --------------------------------------------------------------------------- graph
+class CSR:
+    """Canonical CSR of a simple undirected graph: int64 row_ptr, int32 col, weights or None."""
+
+    def __init__(self, n, row_ptr, col, w, selfloops=0, duplicates=0):
+        self.n, self.row_ptr, self.col, self.w = int(n), row_ptr, col, w
+        self.selfloops, self.duplicates = int(selfloops), int(duplicates)
+
+    @property
+    def nnz(self) -> int:
+        return int(self.row_ptr[-1])
+
+    @property
+    def wtype(self) -> int:
+        if self.w is None:
+            return WT_UNIT
+        return WT_U8 if self.w.dtype == np.uint8 else WT_F64
+
+    def rows(self) -> np.ndarray:
+        return np.repeat(np.arange(self.n, dtype=np.int64), np.diff(self.row_ptr))
+
+    def wf(self) -> np.ndarray:
+        return np.ones(self.nnz) if self.w is None else self.w.astype(np.float64)
+
+
+def canonical_csr(n: int, u, v, w=None) -> CSR:
+    """SURVEY §8(c) O-1, from the simple-graph assumption of P:L86 and the symmetric
+    adjacency of P:L88 ("w_ij = w_ji = w_e"):
+      1. drop self-loops (u == v);
+      2. canonical key (min(u,v), max(u,v));
+      3. duplicates: keep the FIRST occurrence in input order (stable sort);
+      4. mirror each kept edge (lo,hi,w), (hi,lo,w);
+      5. row i holds its neighbours in ascending column order; row_ptr int64."""
+    u = np.asarray(u, dtype=np.int64)
+    v = np.asarray(v, dtype=np.int64)
+    if len(u) and (u.min() < 0 or v.min() < 0 or u.max() >= n or v.max() >= n):
+        raise ValueError("vertex id out of range")
+    keep = u != v
+    selfloops = int(len(u) - keep.sum())
+    idx = np.nonzero(keep)[0]
+    lo = np.minimum(u[idx], v[idx])
+    hi = np.maximum(u[idx], v[idx])
+    key = lo * np.int64(n) + hi
+    order = np.argsort(key, kind="stable")
+    ks = key[order]
+    first = np.ones(len(ks), dtype=bool)
+    first[1:] = ks[1:] != ks[:-1]
+    kept = idx[order[first]]                 # original edge indices, first occurrence per key
+    duplicates = int(len(idx) - len(kept))
+    lo = np.minimum(u[kept], v[kept])
+    hi = np.maximum(u[kept], v[kept])
+    rows = np.concatenate([lo, hi])
+    cols = np.concatenate([hi, lo])
+    o = np.lexsort((cols, rows))
+    rows, cols = rows[o], cols[o]
+    row_ptr = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(np.bincount(rows, minlength=n), out=row_ptr[1:])
+    wo = None
+    if w is not None:
+        w = np.asarray(w)
+        wk = w[kept]
+        wo = np.concatenate([wk, wk])[o]
+        if np.any(~np.isfinite(wo.astype(np.float64))) or np.any(wo.astype(np.float64) <= 0):
+            raise ValueError("weights must be finite and > 0 (P:L86, w: E -> R_+)")
+    return CSR(n, row_ptr, cols.astype(np.int32), wo, selfloops, duplicates)
+
+
+def degrees(g: CSR) -> np.ndarray:
+    """O-2: d_i = sum_{j in Theta_i} w_ij, summed in ascending column order (C loop)."""
+    d = np.empty(g.n, dtype=np.float64)
+    _L().oracle_degrees(g.n, _p(g.row_ptr), g.wtype, _p(g.w), _p(d))
+    return d
+
+
+def ipl_apply(g: CSR, x: np.ndarray) -> np.ndarray:
+    """y = (I + L) x, L = D - A."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    d = degrees(g)
+    y = np.empty(g.n, dtype=np.float64)
+    _L().oracle_ipl_apply(g.n, _p(g.row_ptr), _p(g.col), g.wtype, _p(g.w), _p(d), _p(x), _p(y))
+    return y
+
+
+def laplacian_apply(g: CSR, x: np.ndarray) -> np.ndarray:
+    """(Lx)_i = d_i x_i - sum_j w_ij x_j, plain numpy."""
+    rows = g.rows()
+    ax = np.bincount(rows, weights=g.wf() * x[g.col], minlength=g.n)
+    return np.bincount(rows, weights=g.wf(), minlength=g.n) * x - ax
+
+
+def incidence_apply(g: CSR, x: np.ndarray) -> np.ndarray:
+    """W^{1/2} B x: one entry per undirected edge e = (i, j), i < j (head = lower id),
+    value sqrt(w_e) (x_i - x_j)  (b_e = e_i - e_j, W = diag(w_e))."""
+    rows = g.rows()
+    up = g.col > rows
+    return np.sqrt(g.wf()[up]) * (x[rows[up]] - x[g.col[up]])
+
+
+def dense_ipl(g: CSR) -> np.ndarray:
+    """Dense I + L = I + D - A."""
+    M = np.zeros((g.n, g.n))
+    rows = g.rows()
+    np.add.at(M, (rows, g.col), -g.wf())
+    M[np.arange(g.n), np.arange(g.n)] += 1.0 + degrees(g)
+    return M
+
+
+# --------------------------------------------------------------------------- solves
+def solve_dense(g: CSR, s: np.ndarray) -> np.ndarray:
+    """z = (I + L)^{-1} s (Eq. (2)) via LAPACK Cholesky of the SPD matrix I + L
+    (the paper's Exact).  s may be [n] or [n][k]."""
+    import scipy.linalg as sla
+    c = sla.cho_factor(dense_ipl(g), lower=False)
+    return sla.cho_solve(c, s)
+
+
+def solve_pcg(g: CSR, s: np.ndarray, tol: float = 1e-13, max_iter: int = 100000,
+              precond: bool = True):
+    """z = (I + L)^{-1} s by plain fp64 Jacobi-PCG (C). Returns (z, info)."""
+    s2 = np.asarray(s, dtype=np.float64)
+    cols = s2.reshape(g.n, -1)
+    Z = np.empty_like(cols)
+    infos = []
+    for j in range(cols.shape[1]):
+        sj = np.ascontiguousarray(cols[:, j])
+        x = np.empty(g.n)
+        out = np.zeros(3)
+        st = _L().oracle_pcg(g.n, _p(g.row_ptr), _p(g.col), g.wtype, _p(g.w), _p(sj), tol,
+                             max_iter, 1 if precond else 0, _p(x), _p(out))
+        if st < 0:
+            raise MemoryError("oracle_pcg allocation failed")
+        Z[:, j] = x
+        infos.append({"converged": st == 0, "iterations": int(out[0]), "rel_res": float(out[1]),
+                      "restarts": int(out[2])})
+    return Z.reshape(s2.shape), (infos[0] if s2.ndim == 1 else infos)
+
+
+def pcg_fixed_iters(g: CSR, s: np.ndarray, iters: int) -> np.ndarray:
+    x = np.empty(g.n)
+    s = np.ascontiguousarray(s, dtype=np.float64)
+    _L().oracle_pcg_fixed_iters(g.n, _p(g.row_ptr), _p(g.col), g.wtype, _p(g.w), _p(s), iters, _p(x))
+    return x
+
+
+def solve(g: CSR, s: np.ndarray, dense_max: int = 4096, tol: float = 1e-13):
+    """Dense Cholesky for n <= 4096 (BASELINE.json north_star), PCG at rtol 1e-13 above."""
+    if g.n <= dense_max:
+        return solve_dense(g, s)
+    return solve_pcg(g, s, tol=tol)[0]
+
+
+# --------------------------------------------------------------------------- quantities
+def _fsum(a: np.ndarray) -> float:
+    return math.fsum(np.asarray(a, dtype=np.float64).ravel().tolist())
+
+
+def quantities(g: CSR, s: np.ndarray, z: np.ndarray) -> dict:
+    """The five quantities by their definitions, on a given z, summed with math.fsum
+    (correctly-rounded summation):
+      C_I  = sum_i (z_i - s_i)^2                          Def. 3.1
+      D    = sum_{(i,j) in E} w_ij (z_i - z_j)^2          Def. 3.2, P:L183 (each edge once)
+      P    = sum_i (z_i - mean(z))^2                       Def. 3.3
+      C    = sum_i z_i^2                                   Def. 3.4
+      I_dc = D + C                                         Def. 3.5
+      PDI  = P + D                                         BASELINE.json north_star (DESIGN reading R1)
+    cross-checks: sz = s^T z (= I_dc), sbzb = s_bar^T z_bar (= PDI), ss = s^T s
+    (= C_I + 2D + C, DESIGN reading R2), Lz2 = ||L z||^2 (Alg. 1 line 5 form of C_I)."""
+    s = np.asarray(s, dtype=np.float64)
+    z = np.asarray(z, dtype=np.float64)
+    n = g.n
+    rows = g.rows()
+    up = g.col > rows
+    wu = g.wf()[up]
+    CI = _fsum((z - s) ** 2)
+    D = _fsum(wu * (z[rows[up]] - z[g.col[up]]) ** 2)
+    mz = _fsum(z) / n
+    P = _fsum((z - mz) ** 2)
+    C = _fsum(z * z)
+    ms = _fsum(s) / n
+    return {
+        "CI": CI, "D": D, "P": P, "C": C, "Idc": D + C, "PDI": P + D,
+        "sz": _fsum(s * z), "sbzb": _fsum((s - ms) * (z - mz)), "ss": _fsum(s * s),
+        "mean_s": ms, "mean_z": mz, "Lz2": _fsum(laplacian_apply(g, z) ** 2),
+    }
+
+
+# --------------------------------------------------------------------------- tiny-graph pins
+def fj_iterate(g: CSR, s: np.ndarray, tol: float = 1e-14, max_steps: int = 10_000_000):
+    """Synchronous iteration of the FJ update rule, Eq. (1):
+        z_i <- (s_i + sum_{j in Theta_i} w_ij z_j) / (1 + sum_{j in Theta_i} w_ij),
+    from z^0 = s, until max_i |z^{t+1}_i - z^t_i| < tol (S:L263-279 reading).  Converges since
+    the iteration matrix (I+D)^{-1}A has spectral radius <= max d_i/(1+d_i) < 1."""
+    s = np.asarray(s, dtype=np.float64)
+    rows = g.rows()
+    wf = g.wf()
+    d = np.bincount(rows, weights=wf, minlength=g.n)
+    z = s.copy()
+    for step in range(max_steps):
+        az = np.bincount(rows, weights=wf * z[g.col], minlength=g.n)
+        zn = (s + az) / (1.0 + d)
+        if np.max(np.abs(zn - z), initial=0.0) < tol:
+            return zn, step + 1
+        z = zn
+    raise RuntimeError("FJ iteration did not converge")
+
+
+def forest_census(n: int, edges, weights=None):
+    """Spanning rooted forests by brute-force enumeration, n <= ~8:
+    a spanning forest F (acyclic edge subset) with trees T_1..T_r yields prod |T| rooted
+    forests (one root per tree), each of weight eps(F) = prod_{e in F} w_e.
+      eps(Gamma)    = sum_F eps(F) prod_T |T|
+      eps(Gamma_ij) = sum_{F: i,j in same tree} eps(F) prod_{T not containing i} |T|
+                      (the tree holding i and j is rooted at i).
+    Returns (eps_Gamma, E) with E[i][j] = eps(Gamma_ij); Omega = E / eps_Gamma."""
+    edges = [tuple(e) for e in edges]
+    m = len(edges)
+    wts = [1] * m if weights is None else list(weights)
+    total = 0
+    E = [[0] * n for _ in range(n)]
+    for r in range(m + 1):
+        for sub in itertools.combinations(range(m), r):
+            parent = list(range(n))
+
+            def find(a):
+                while parent[a] != a:
+                    parent[a] = parent[parent[a]]
+                    a = parent[a]
+                return a
+            acyclic = True
+            for e in sub:
+                a, b = find(edges[e][0]), find(edges[e][1])
+                if a == b:
+                    acyclic = False
+                    break
+                parent[a] = b
+            if not acyclic:
+                continue
+            wF = 1
+            for e in sub:
+                wF *= wts[e]
+            comp = [find(a) for a in range(n)]
+            size = {}
+            for c in comp:
+                size[c] = size.get(c, 0) + 1
+            prod_all = 1
+            for c in size.values():
+                prod_all *= c
+            total += wF * prod_all
+            for i in range(n):
+                rest = prod_all // size[comp[i]]   # product over trees not containing i
+                for j in range(n):
+                    if comp[j] == comp[i]:
+                        E[i][j] += wF * rest
+    return total, E
+
+
+# --------------------------------------------------------------------------- sampled checks
+def csr_rows_from_edges(n: int, u, v, rows_wanted, w=None):
+    """Rows of the canonical CSR for a SAMPLE of vertices, computed one by one from the raw
+    edge list (same O-1 rules: drop self-loops, keep-first duplicates, ascending columns).
+    For full-size parity where the whole oracle CSR would be too slow.  Returns
+    {i: (cols int32 array, weights or None)}."""
+    u = np.asarray(u, dtype=np.int64)
+    v = np.asarray(v, dtype=np.int64)
+    out = {}
+    want = np.asarray(sorted(set(int(i) for i in rows_wanted)), dtype=np.int64)
+    hit = np.isin(u, want) | np.isin(v, want)
+    eidx = np.nonzero(hit & (u != v))[0]           # input order preserved
+    for i in want:
+        sel = eidx[(u[eidx] == i) | (v[eidx] == i)]
+        nb = np.where(u[sel] == i, v[sel], u[sel])
+        _, first = np.unique(nb, return_index=True)   # first occurrence in input order
+        keep = sel[np.sort(first)]
+        nbk = np.where(u[keep] == i, v[keep], u[keep])
+        o = np.argsort(nbk, kind="stable")
+        out[int(i)] = (nbk[o].astype(np.int32), None if w is None else np.asarray(w)[keep][o])
+    return out
