@@ -1,0 +1,335 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path on B200: one JSON line on rank 0.
+
+A "step" = one pass of the whole hot path over one batch of synthetic input resident in HBM:
+  a1 fj_csr_from_edges (raw edges -> canonical CSR)  a2 fj_graph_create (degrees, schedule)
+  a3-a7 fj_approxim (statistics, Jacobi-PCG solve per opinion column, fused quantities pass,
+  certificate).  Default workload: BASELINE.json configs[2] (C3: BA n=4e6, m=8, three opinion
+  distributions), the config the metric is quoted on at 1/2/4/8 B200.
+
+value = CG-iteration GB/s = canonical bytes per PCG iteration B(k) x PCG iterations
+        / device time of the PCG iterations (CUDA events inside the library, on the caller's stream),
+        summed over the K timed steps (max over ranks for the time).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "CG-iteration GB/s & fraction of HBM roofline; time-to-{P,D,I,C} at 1/2/4/8 B200"
+L2_FLUSH_BYTES = 512 << 20
+
+
+def canonical_bytes(n, nnz, wb, k):
+    """B(k) = (4 + w_b) nnz + 8 (n+1) + 16 n + 88 n k  (one PCG iteration)."""
+    return (4 + wb) * nnz + 8 * (n + 1) + 16 * n + 88 * n * k
+
+
+def spmv_bytes(n, nnz, wb, k):
+    """B_spmv = (4 + w_b) nnz + 8 (n+1) + 16 n k  (one (I+L)p product)."""
+    return (4 + wb) * nnz + 8 * (n + 1) + 16 * n * k
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons DURING the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, index=0):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.p.kill()
+        self.f.flush()
+        rows = []
+        with open(self.f.name) as fh:
+            for line in fh:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 8:
+                    rows.append(parts)
+        os.unlink(self.f.name)
+        if not rows:
+            return None
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = max(float(r[1]) for r in rows if r[1].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(rows)}
+
+
+def dist_init():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_baseline(wl, g, seconds=12.0):
+    """The oracle's Jacobi-PCG (plain C/OpenMP, as it stands) on the full workload graph: a bounded
+    sample of PCG iterations timed on the host cores.  Same unit as the line's metric."""
+    import oracle as O
+    s = np.ascontiguousarray(wl.S[:, 0])
+    t = time.perf_counter()
+    O.pcg_fixed_iters(g, s, 1)                       # 1 iteration (+ setup/residual passes)
+    t1 = time.perf_counter() - t
+    iters = int(max(2, min(200, seconds / max(t1, 1e-3))))
+    t = time.perf_counter()
+    O.pcg_fixed_iters(g, s, iters)
+    dt = time.perf_counter() - t
+    wb = 0 if wl.w is None else wl.w.dtype.itemsize
+    B = canonical_bytes(g.n, g.nnz, wb, 1)
+    return {"value": B * iters / dt / 1e9, "unit": "GB/s", "cores": O.num_threads(), "kind": "oracle",
+            "sample": f"{iters} oracle Jacobi-PCG iterations (column 0, {wl.kinds[0]}) on the full {wl.name} graph "
+                      f"(n={g.n}, nnz={g.nnz}); includes the oracle's per-call setup and true-residual pass; "
+                      f"{dt:.1f} s"}
+
+
+def run_reference(args, ws, rank):
+    """--impl reference: the CPU oracle as it stands, on this arm's config / metric / unit."""
+    if rank != 0:
+        return 0
+    import oracle as O
+    import synth
+    wl = synth.make_config(args.config)
+    g = O.canonical_csr(wl.n, wl.u, wl.v, wl.w)      # setup, untimed
+    wb = 0 if wl.w is None else wl.w.dtype.itemsize
+    B = canonical_bytes(g.n, g.nnz, wb, 1)
+    s = np.ascontiguousarray(wl.S[:, 0])
+    t = time.perf_counter()
+    O.pcg_fixed_iters(g, s, 1)
+    t1 = time.perf_counter() - t
+    iters = int(max(1, min(50, args.ref_seconds / max(t1, 1e-3))))
+    for _ in range(args.warmup):
+        O.pcg_fixed_iters(g, s, iters)
+    times = []
+    for _ in range(args.steps):
+        t = time.perf_counter()
+        O.pcg_fixed_iters(g, s, iters)
+        times.append(time.perf_counter() - t)
+    tot = sum(times)
+    value = B * iters * args.steps / tot / 1e9
+    sample = (f"each step: {iters} oracle Jacobi-PCG iterations (column 0) on the full {wl.name} graph "
+              f"(n={g.n}, nnz={g.nnz}), CSR built once untimed")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{wl.name}: {wl.desc}", "n": g.n, "nnz": g.nnz},
+            "cpu_baseline": {"value": value, "unit": "GB/s", "cores": O.num_threads(), "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="fj", choices=["fj", "reference"])
+    ap.add_argument("--config", default="c3")
+    ap.add_argument("--rtol", type=float, default=1e-10)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--spmv-reps", type=int, default=20)
+    ap.add_argument("--ref-seconds", type=float, default=10.0)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    args = ap.parse_args()
+    ws, rank, local = dist_init()
+    if args.impl == "reference":
+        return run_reference(args, ws, rank)
+
+    import torch
+    import torch.distributed as dist
+    import paper_2101_08143_b200 as fj
+    import synth
+    from paper_2101_08143_b200 import binding
+
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    fj.load_library()
+    wl = synth.make_config(args.config)
+    n, k = wl.n, wl.k
+    wb = 0 if wl.w is None else wl.w.dtype.itemsize
+    u = torch.from_numpy(wl.u).cuda()
+    v = torch.from_numpy(wl.v).cuda()
+    w = None if wl.w is None else torch.from_numpy(wl.w).cuda()
+    S = torch.from_numpy(wl.S).cuda()
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device="cuda")
+    opts = fj.SolveOpts.make(rtol=args.rtol)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        rp, col, wo, st = fj.csr_from_edges(n, u, v, w)
+        G = fj.Graph(n, rp, col, wo, validate=False)
+        z, q, rep = G.approxim(S, opts=opts)
+        info = G.info()
+        G.close()
+        return q, rep, info, st
+
+    for _ in range(args.warmup):
+        q, rep, info, bst = step()
+    torch.cuda.synchronize()
+    nnz = info["nnz"]
+    B = canonical_bytes(n, nnz, wb, 1)
+
+    sampler = ClockSampler(local)
+    launches0, cub0 = binding.kernel_launches()
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_wall = time.perf_counter()
+    step_ms, loop_ms, iters, ttq_ms, results = [], 0.0, 0, [], []
+    for _ in range(args.steps):
+        flush.fill_(1)                                   # L2 flush (512 MiB write), outside the events
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        q, rep, info, bst = step()
+        e1.record(stream)
+        e1.synchronize()
+        step_ms.append(e0.elapsed_time(e1))
+        loop_ms += rep["ms_loop"]
+        iters += rep["iterations_total"]
+        ttq_ms.append(rep["ms"])
+        results.append((q, rep))
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    wall = time.perf_counter() - t_wall
+    launches1, cub1 = binding.kernel_launches()
+    clocks = sampler.stop()
+
+    # dominant kernel: the (I+L)p tile SpMV, timed live with CUDA events on the launching stream
+    rp, col, wo, _ = fj.csr_from_edges(n, u, v, w)
+    G = fj.Graph(n, rp, col, wo, validate=False)
+    x = S[:, 0].contiguous()
+    for _ in range(3):
+        G.apply(x)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    flush.fill_(1)
+    e0.record(stream)
+    for _ in range(args.spmv_reps):
+        y = G.apply(x)
+    e1.record(stream)
+    e1.synchronize()
+    spmv_ms = e0.elapsed_time(e1) / args.spmv_reps
+    G.close()
+
+    # aggregate over ranks: time = max over ranks, bytes = sum over ranks
+    tot_loop_ms = loop_ms
+    tot_bytes = B * iters
+    max_step_ms = sum(step_ms)
+    if ws > 1:
+        t = torch.tensor([loop_ms, sum(step_ms)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tb = torch.tensor([float(tot_bytes)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tb, op=dist.ReduceOp.SUM)
+        tot_loop_ms, max_step_ms, tot_bytes = float(t[0]), float(t[1]), float(tb[0])
+    value = tot_bytes / (tot_loop_ms / 1e3) / 1e9
+
+    peak, peak_src = load_peaks()
+    Bs = spmv_bytes(n, nnz, wb, 1)
+    achieved = Bs / (spmv_ms / 1e3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get(args.config, {}).get("spmv_dram_bytes_per_launch")
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": max_step_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{wl.name}: {wl.desc}", "n": n, "nnz": nnz, "k": k, "rtol": args.rtol,
+                   "opinions": wl.kinds, "parallelism": f"replicas{ws}" if ws > 1 else "1 GPU",
+                   "l2": "flushed between steps (512 MiB write, outside the timed events)",
+                   "pcg_iterations_per_step": iters / args.steps,
+                   "bytes_per_iteration": B, "fraction_of_measured_hbm": value / peak},
+        "time_to_quantities_ms": statistics.median(ttq_ms),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "kernel": "tile_kernel<ApplyOp> ((I+L)p SpMV)",
+                     "algorithmic_bytes_per_launch": Bs, "launch_ms": spmv_ms, "peak_source": peak_src},
+        "clocks": clocks, "gpu_launches": launches1 - launches0,
+        "cub_calls": cub1 - cub0, "wall_s_timed_region": wall,
+        "quantities_step0": {kk: results[0][0][0][kk] for kk in ["CI", "D", "P", "C", "Idc", "PDI"]},
+        "max_rel_res_true": max(r[1]["rel_res_true"] for r in results),
+    }
+
+    # e2e: the public host-buffer call; H2D of the inputs and D2H of z + quantities inside the timing
+    if not args.no_e2e:
+        uh = torch.from_numpy(wl.u).pin_memory().numpy()
+        vh = torch.from_numpy(wl.v).pin_memory().numpy()
+        wh = None if wl.w is None else torch.from_numpy(wl.w).pin_memory().numpy()
+        Sh = torch.from_numpy(wl.S).pin_memory().numpy()
+        h2d = uh.nbytes + vh.nbytes + (0 if wh is None else wh.nbytes) + Sh.nbytes
+        d2h = Sh.nbytes + k * 200
+        fj.approxim_host(n, uh, vh, wh, Sh, opts=opts, want_z=True)    # warm
+        e_loop, e_iters, e_ms = 0.0, 0, 0.0
+        reps = max(1, min(args.steps, 3))
+        for _ in range(reps):
+            flush.fill_(1)
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            zh, qh, reph = fj.approxim_host(n, uh, vh, wh, Sh, opts=opts, want_z=True)
+            e_ms += (time.perf_counter() - t) * 1e3
+            e_iters += reph["iterations_total"]
+        e_bytes = B * e_iters
+        if ws > 1:
+            t = torch.tensor([e_ms], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            tb = torch.tensor([float(e_bytes)], dtype=torch.float64, device="cuda")
+            dist.all_reduce(tb, op=dist.ReduceOp.SUM)
+            e_ms, e_bytes = float(t[0]), float(tb[0])
+        line["e2e"] = {"value": e_bytes / (e_ms / 1e3) / 1e9, "unit": "GB/s", "h2d_bytes_per_step": h2d,
+                       "d2h_bytes_per_step": d2h, "ms_per_step": e_ms / reps,
+                       "note": "fj_approxim_host from pinned host buffers: H2D edges+opinions, CSR build, "
+                               "graph, Algorithm 1, D2H z; host wall clock"}
+
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        import oracle as O
+        g = O.canonical_csr(wl.n, wl.u, wl.v, wl.w)
+        line["cpu_baseline"] = cpu_baseline(wl, g, args.cpu_seconds)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

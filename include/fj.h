@@ -1,0 +1,202 @@
+/*
+ * fj.h — C ABI of the B200 library for Friedkin–Johnsen opinion quantities
+ * (arXiv 2101.08143, "Fast Evaluation for Relevant Quantities of Opinion Dynamics").
+ * Citations "P:L<n>" are lines of the paper's text; §8(b) of SURVEY.md is the
+ * contract this header implements.
+ *
+ * Conventions (apply to every entry point unless stated otherwise)
+ *  - Every call returns fj_status; FJ_OK == 0.  No C++ exception crosses the ABI.  On failure
+ *    fj_last_error() returns a thread-local, human-readable message (valid until the next call
+ *    on the same thread).
+ *  - Pointers named *_dev are DEVICE pointers (cudaMalloc / torch CUDA tensors) on the current
+ *    CUDA device; pointers named *_host are host pointers.  Inputs are BORROWED: the library
+ *    never frees them, and a graph handle borrows its CSR arrays until fj_graph_destroy.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).  All device
+ *    work is stream-ordered on it.  Calls that fill a HOST struct synchronise that stream.
+ *  - Layouts: CSR row_ptr int64 [n+1] (row_ptr[0] = 0), col int32 [nnz], weights [nnz] in the
+ *    type given by fj_wtype (FJ_W_UNIT: no array, every w_ij = 1).  Opinion / solution matrices
+ *    with k columns are ROW-MAJOR fp64 [n][k] (k = 1: a plain vector).
+ *  - Internal workspace is allocated with cudaMallocAsync on `stream` and owned by the handle.
+ *  - There is NO CPU fallback: without a CUDA device every compute call returns FJ_E_CUDA.
+ */
+#ifndef FJ_H
+#define FJ_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FJ_ABI_VERSION 1
+
+typedef enum {
+  FJ_OK = 0,
+  FJ_E_INVALID_ARG = 1,      /* null pointer, negative size, k out of range, bad enum        */
+  FJ_E_NOT_SIMPLE = 2,       /* self-loop, duplicate / unsorted column, column out of range  */
+  FJ_E_ASYMMETRIC = 3,       /* (i,j,w) present without (j,i,w)  (P:L88 w_ij = w_ji)         */
+  FJ_E_BAD_WEIGHT = 4,       /* weight <= 0 or non-finite  (P:L86 w: E -> R_+)               */
+  FJ_E_NONFINITE_INPUT = 5,  /* NaN/Inf in an opinion vector                                 */
+  FJ_E_NO_CONVERGENCE = 6,   /* iteration cap hit; best iterate left in z, report filled     */
+  FJ_E_CUDA = 7,             /* CUDA runtime error (message in fj_last_error)               */
+  FJ_E_NCCL = 8,
+  FJ_E_OOM = 9,
+  FJ_E_INTERNAL = 10,
+  FJ_E_UNSUPPORTED = 11
+} fj_status;
+
+typedef enum { FJ_W_UNIT = 0, FJ_W_U8 = 1, FJ_W_F32 = 2, FJ_W_F64 = 3 } fj_wtype;
+typedef enum { FJ_OP_L = 0, FJ_OP_IPL = 1 } fj_op;
+
+typedef struct fj_graph fj_graph;
+
+typedef struct {
+  int64_t n, nnz;           /* nodes, stored CSR entries (= 2 m)                              */
+  int64_t m;                /* undirected edges                                              */
+  int64_t n_isolated;       /* rows with no neighbour (z_i = s_i)                            */
+  int64_t deg_max;          /* largest row length                                            */
+  double w_min, w_max;      /* extremal edge weights; 0 if nnz == 0                  */
+  double d_max;             /* largest weighted degree                                       */
+  int64_t n_tiles, n_long_rows, n_long_chunks;  /* SpMV schedule       */
+  int32_t wtype, reserved;
+} fj_graph_info_t;
+
+typedef struct {
+  double rtol;              /* stop when ||s - (I+L)z||_2 <= rtol ||s||_2 (default 1e-10)    */
+  double eps_target;        /* fj_approxim only: tighten rtol until every certified relative
+                               bound <= eps_target (0 = off).                                */
+  int32_t max_iter;         /* total PCG iterations over all restarts (default 10000)         */
+  int32_t max_restarts;     /* true-residual restarts (default 3)                             */
+  int32_t use_cuda_graph;   /* 1 (default): device-driven conditional-while CUDA graph loop  */
+  int32_t reserved;
+} fj_solve_opts;
+
+typedef struct {
+  int32_t iterations;       /* PCG iterations (max over the k columns)                       */
+  int32_t converged;        /* 1 when every column met rtol on its TRUE residual             */
+  int32_t restarts;
+  int32_t reserved;
+  double rel_res_recursive; /* max_j ||r_j|| / ||s_j|| of the recursion at exit               */
+  double rel_res_true;      /* max_j ||s_j - (I+L) z_j|| / ||s_j||, recomputed (NaN if not)  */
+  double ms;                /* device time of the whole call (CUDA events on `stream`)       */
+  double ms_loop;           /* device time of the PCG iterations only (init + loop), summed
+                               over columns and restarts (CUDA events on `stream`)           */
+  int64_t iterations_total; /* PCG iterations summed over columns and restarts               */
+} fj_solve_report;
+
+/* Quantities for ONE opinion column (fj_quantities / fj_approxim fill k of them).
+ * Definitions (on the returned z):                                      [P:L<n>]
+ *   CI  = sum_i (z_i - s_i)^2          internal conflict, Def. 3.1       L167
+ *   D   = sum_{(i,j) in E} w_ij (z_i - z_j)^2, each edge once, Def. 3.2  L183
+ *   P   = sum_i (z_i - mean(s))^2      polarization, Def. 3.3            L204-206 (mean(z) = mean(s), L152)
+ *   C   = sum_i z_i^2                  controversy, Def. 3.4             L215
+ *   Idc = D + C                        disagreement-controversy index    L224 (= s^T z, L228)
+ *   PDI = P + D                        polarization-disagreement index (BASELINE north_star)
+ * eps[6] are CERTIFIED relative error bounds |Q - Q_exact| / Q_exact <= eps for
+ * (CI, D, P, C, Idc, PDI), derived a posteriori from the true residual (
+ * proof pattern of Lemma 4.3, with lambda_min(I+L) = 1).
+ * +Inf means "not certified" (e.g. near-consensus input). */
+typedef struct {
+  double CI, D, P, C, Idc, PDI;
+  double mean_s;            /* 1^T s / n                                                     */
+  double ss;                /* s^T s   (cross-check: CI + 2D + C = s^T s)                    */
+  double sz;                /* s^T z   (cross-check: = Idc)                          */
+  double sbzb;              /* (s - mean s)^T (z - mean s)  (cross-check: = PDI)             */
+  double Lz2;               /* ||L z||^2 (Algorithm 1 line 5 form of CI; diagnostic) */
+  double res_norm;          /* ||s - (I+L) z||_2                                             */
+  double s_norm;            /* ||s||_2                                                       */
+  double fp_bound;          /* rounding allowance added to res_norm in the certificate       */
+  double eps[6];
+  int32_t consensus;        /* 1 if s is constant: z = s exactly, P = D = CI = 0             */
+  int32_t certified;        /* 1 if all six eps are finite                                   */
+} fj_quantities_t;
+
+/* ---------------------------------------------------------------- misc */
+int fj_abi_version(void);
+/* Number of CUDA kernels this library has launched in this process (host-side counter; kernels
+ * executed by a device-driven graph loop are counted from the iteration counts).  Library
+ * kernels (CUB radix sort / scan / select) are counted separately in *cub_launches if non-NULL. */
+int64_t fj_kernel_launches(int64_t* cub_launches);
+const char* fj_status_str(int status);
+const char* fj_last_error(void);
+void fj_default_solve_opts(fj_solve_opts* opts);
+
+/* ---------------------------------------------------------------- a1: canonical CSR
+ * Build the CSR of the simple undirected graph given by m_in raw edges (u_dev[e], v_dev[e]),
+ * e = 0..m_in-1, with 0 <= u,v < n:
+ *   self-loops dropped; (u,v) canonicalised to (min,max); duplicate pairs keep the FIRST
+ *   occurrence in input order (its weight); every kept edge is mirrored; columns ascend in
+ *   each row.  w_dev may be NULL iff wtype == FJ_W_UNIT.
+ * Outputs (caller-allocated DEVICE buffers): row_ptr_dev int64 [n+1]; col_dev int32 with
+ * capacity 2*m_in; w_out_dev (same type as input, capacity 2*m_in; ignored for FJ_W_UNIT).
+ * Host outputs: *nnz_out = 2 * kept edges; *selfloops_out, *dups_out may be NULL.
+ * Errors: FJ_E_INVALID_ARG (n < 1, n > 2^31-1, m_in < 0, vertex id out of range),
+ * FJ_E_OOM, FJ_E_CUDA.  Synchronises `stream`. */
+fj_status fj_csr_from_edges(int64_t n, int64_t m_in, const int32_t* u_dev, const int32_t* v_dev,
+                            const void* w_dev, int wtype, int64_t* row_ptr_dev, int32_t* col_dev,
+                            void* w_out_dev, int64_t* nnz_out, int64_t* selfloops_out,
+                            int64_t* dups_out, void* stream);
+
+/* ---------------------------------------------------------------- a2: graph handle, degrees
+ * Borrow a caller-owned device CSR (it must outlive the handle), optionally validate it
+ * (validate != 0: sorted/in-range/no self-loop columns, symmetric weights, w > 0 finite;
+ * FJ_E_NOT_SIMPLE / FJ_E_ASYMMETRIC / FJ_E_BAD_WEIGHT on failure), compute the weighted degrees
+ * d_i = sum_j w_ij (in ascending column order), the Jacobi diagonal 1/(1 + d_i), the graph
+ * statistics and the SpMV schedule.  Synchronises `stream`.  *out receives the handle. */
+fj_status fj_graph_create(int64_t n, int64_t nnz, const int64_t* row_ptr_dev, const int32_t* col_dev,
+                          const void* w_dev, int wtype, int validate, void* stream, fj_graph** out);
+fj_status fj_graph_info(const fj_graph* g, fj_graph_info_t* out);
+/* d_dev: fp64 [n] device output, d_i = sum_j w_ij (bit-exact: ascending column order). */
+fj_status fj_graph_degrees(const fj_graph* g, double* d_dev, void* stream);
+fj_status fj_graph_destroy(fj_graph* g);
+
+/* ---------------------------------------------------------------- operators
+ * y = L x (op = FJ_OP_L) or y = (I + L) x (op = FJ_OP_IPL) for row-major [n][k] fp64 x, y
+ * (device).  x and y must not alias. */
+fj_status fj_apply(const fj_graph* g, int op, int k, const double* x_dev, double* y_dev, void* stream);
+
+/* ---------------------------------------------------------------- a3: opinion statistics
+ * stats_host[4*j + 0..3] = (sum s_j, sum s_j^2, min s_j, max s_j) for each column j of the
+ * row-major [n][k] s_dev.  FJ_E_NONFINITE_INPUT if any entry is NaN/Inf.  Synchronises. */
+fj_status fj_opinion_stats(const fj_graph* g, int k, const double* s_dev, double* stats_host, void* stream);
+
+/* ---------------------------------------------------------------- a4: SOLVE (Lemma 4.2)
+ * z = (I + L)^{-1} s (Eq. (2)) for every column, by Jacobi-preconditioned CG from
+ * z0 = 0, stopping when ||r|| <= rtol ||s|| (recursive residual), then recomputing the true
+ * residual and restarting from z while it exceeds rtol ||s|| (<= max_restarts).  Since
+ * lambda_min(I+L) = 1, ||z - z*||_{I+L} <= ||r||, which meets the SOLVE contract of Lemma 4.2
+ * with delta = ||r|| / ||z*||_{I+L}.  k in [1, 64]; s_dev, z_dev row-major [n][k] device
+ * (must not alias).  opts may be NULL (defaults).  rep (host, may be NULL) is filled.
+ * FJ_E_NO_CONVERGENCE: cap reached; z holds the last iterate.  Synchronises `stream`. */
+fj_status fj_solve(const fj_graph* g, int k, const double* s_dev, double* z_dev,
+                   const fj_solve_opts* opts, fj_solve_report* rep, void* stream);
+
+/* ---------------------------------------------------------------- a5-a7: quantities + certificate
+ * One fused CSR pass over (s, z) per column computing the sums listed in fj_quantities_t and the
+ * true residual, then the certificate on the host.  out_host: k structs.  Synchronises. */
+fj_status fj_quantities(const fj_graph* g, int k, const double* s_dev, const double* z_dev,
+                        fj_quantities_t* out_host, void* stream);
+
+/* Algorithm 1 in single-solve form (reading R4): statistics, one solve
+ * per column (q = z - mean(s) 1 replaces the second solve exactly since Omega 1 = 1),
+ * fused quantities with certificate; restarts if the certified true residual misses rtol and,
+ * when opts->eps_target > 0, tightens rtol (x0.01, warm start) until every eps <= eps_target.
+ * z_dev may be NULL (internal buffer).  q_host: k structs; rep may be NULL. */
+fj_status fj_approxim(const fj_graph* g, int k, const double* s_dev, double* z_dev,
+                      const fj_solve_opts* opts, fj_quantities_t* q_host, fj_solve_report* rep,
+                      void* stream);
+
+/* End-to-end convenience from HOST buffers: copies the raw edge list (u_host, v_host, w_host)
+ * and s_host [n][k] to the device, builds the CSR (a1), the handle (a2), runs fj_approxim, and
+ * copies z back to z_host (may be NULL) and the quantities to q_host.  Pinned host buffers make
+ * the copies asynchronous.  Device memory is released before return. */
+fj_status fj_approxim_host(int64_t n, int64_t m_in, const int32_t* u_host, const int32_t* v_host,
+                           const void* w_host, int wtype, int k, const double* s_host,
+                           double* z_host, const fj_solve_opts* opts, fj_quantities_t* q_host,
+                           fj_solve_report* rep, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FJ_H */

@@ -1,0 +1,295 @@
+"""ctypes binding of include/fj.h.  Marshalling only (pointers, sizes, streams, result structs)."""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SO = os.path.join(HERE, "libfj.so")
+
+FJ_W_UNIT, FJ_W_U8, FJ_W_F32, FJ_W_F64 = 0, 1, 2, 3
+FJ_OP_L, FJ_OP_IPL = 0, 1
+FJ_E_NO_CONVERGENCE = 6
+
+_i64, _i32, _dbl, _vp = ctypes.c_int64, ctypes.c_int32, ctypes.c_double, ctypes.c_void_p
+
+
+class GraphInfo(ctypes.Structure):
+    _fields_ = [("n", _i64), ("nnz", _i64), ("m", _i64), ("n_isolated", _i64), ("deg_max", _i64),
+                ("w_min", _dbl), ("w_max", _dbl), ("d_max", _dbl), ("n_tiles", _i64),
+                ("n_long_rows", _i64), ("n_long_chunks", _i64), ("wtype", _i32), ("reserved", _i32)]
+
+
+class SolveOpts(ctypes.Structure):
+    _fields_ = [("rtol", _dbl), ("eps_target", _dbl), ("max_iter", _i32), ("max_restarts", _i32),
+                ("use_cuda_graph", _i32), ("reserved", _i32)]
+
+    @classmethod
+    def make(cls, rtol=1e-10, eps_target=0.0, max_iter=10000, max_restarts=3, use_cuda_graph=True):
+        return cls(rtol, eps_target, max_iter, max_restarts, 1 if use_cuda_graph else 0, 0)
+
+
+class SolveReport(ctypes.Structure):
+    _fields_ = [("iterations", _i32), ("converged", _i32), ("restarts", _i32), ("reserved", _i32),
+                ("rel_res_recursive", _dbl), ("rel_res_true", _dbl), ("ms", _dbl), ("ms_loop", _dbl),
+                ("iterations_total", _i64)]
+
+    def to_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_ if f != "reserved"}
+
+
+class Quantities(ctypes.Structure):
+    _fields_ = [("CI", _dbl), ("D", _dbl), ("P", _dbl), ("C", _dbl), ("Idc", _dbl), ("PDI", _dbl),
+                ("mean_s", _dbl), ("ss", _dbl), ("sz", _dbl), ("sbzb", _dbl), ("Lz2", _dbl),
+                ("res_norm", _dbl), ("s_norm", _dbl), ("fp_bound", _dbl), ("eps", _dbl * 6),
+                ("consensus", _i32), ("certified", _i32)]
+
+    def to_dict(self):
+        d = {f: getattr(self, f) for f, _ in self._fields_ if f != "eps"}
+        d["eps"] = dict(zip(["CI", "D", "P", "C", "Idc", "PDI"], list(self.eps)))
+        return d
+
+
+class FJError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{_lib.fj_status_str(status).decode()}: {msg}")
+        self.status = status
+
+
+_lib = None
+
+
+def load_library(path: str = SO):
+    """Load libfj.so.  Raises (never falls back) if the CUDA extension has not been built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} is missing: build it with `python __graft_entry__.py build` "
+                          "(the CUDA extension is required; there is no CPU fallback)")
+    L = ctypes.CDLL(path)
+    P = ctypes.POINTER
+    L.fj_abi_version.restype = ctypes.c_int
+    L.fj_kernel_launches.restype = _i64
+    L.fj_kernel_launches.argtypes = [P(_i64)]
+    L.fj_status_str.restype = ctypes.c_char_p
+    L.fj_status_str.argtypes = [ctypes.c_int]
+    L.fj_last_error.restype = ctypes.c_char_p
+    L.fj_default_solve_opts.argtypes = [P(SolveOpts)]
+    L.fj_default_solve_opts.restype = None
+    L.fj_csr_from_edges.argtypes = [_i64, _i64, _vp, _vp, _vp, ctypes.c_int, _vp, _vp, _vp, P(_i64), P(_i64),
+                                    P(_i64), _vp]
+    L.fj_graph_create.argtypes = [_i64, _i64, _vp, _vp, _vp, ctypes.c_int, ctypes.c_int, _vp, P(_vp)]
+    L.fj_graph_info.argtypes = [_vp, P(GraphInfo)]
+    L.fj_graph_degrees.argtypes = [_vp, _vp, _vp]
+    L.fj_graph_destroy.argtypes = [_vp]
+    L.fj_apply.argtypes = [_vp, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp]
+    L.fj_opinion_stats.argtypes = [_vp, ctypes.c_int, _vp, _vp, _vp]
+    L.fj_solve.argtypes = [_vp, ctypes.c_int, _vp, _vp, P(SolveOpts), P(SolveReport), _vp]
+    L.fj_quantities.argtypes = [_vp, ctypes.c_int, _vp, _vp, P(Quantities), _vp]
+    L.fj_approxim.argtypes = [_vp, ctypes.c_int, _vp, _vp, P(SolveOpts), P(Quantities), P(SolveReport), _vp]
+    L.fj_approxim_host.argtypes = [_i64, _i64, _vp, _vp, _vp, ctypes.c_int, ctypes.c_int, _vp, _vp,
+                                   P(SolveOpts), P(Quantities), P(SolveReport), _vp]
+    for name in ["fj_csr_from_edges", "fj_graph_create", "fj_graph_info", "fj_graph_degrees", "fj_graph_destroy",
+                 "fj_apply", "fj_opinion_stats", "fj_solve", "fj_quantities", "fj_approxim", "fj_approxim_host"]:
+        getattr(L, name).restype = ctypes.c_int
+    _lib = L
+    return L
+
+
+def lib():
+    return load_library()
+
+
+def kernel_launches():
+    """(own kernels launched, CUB library calls) so far in this process."""
+    c = _i64()
+    n = lib().fj_kernel_launches(ctypes.byref(c))
+    return int(n), int(c.value)
+
+
+def _check(st: int, allow=()):
+    if st != 0 and st not in allow:
+        raise FJError(st, _lib.fj_last_error().decode(errors="replace"))
+    return st
+
+
+def _stream(stream=None):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _wtype(w):
+    if w is None:
+        return FJ_W_UNIT
+    import torch
+    return {torch.uint8: FJ_W_U8, torch.float32: FJ_W_F32, torch.float64: FJ_W_F64}[w.dtype]
+
+
+def _need_cuda(*ts):
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise ValueError("device tensors required (torch CUDA tensors)")
+        if t is not None and not t.is_contiguous():
+            raise ValueError("contiguous tensors required")
+
+
+def csr_from_edges(n: int, u, v, w=None, stream=None):
+    """Row a1: canonical CSR (device) from a raw device edge list.  Returns
+    (row_ptr int64 [n+1], col int32 [nnz], w_out or None, stats dict)."""
+    import torch
+    L = lib()
+    _need_cuda(u, v, w)
+    m = int(u.numel())
+    dev = u.device
+    row_ptr = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    col = torch.empty(max(2 * m, 1), dtype=torch.int32, device=dev)
+    w_out = None if w is None else torch.empty(max(2 * m, 1), dtype=w.dtype, device=dev)
+    nnz, loops, dups = _i64(), _i64(), _i64()
+    _check(L.fj_csr_from_edges(n, m, _ptr(u), _ptr(v), _ptr(w), _wtype(w), _ptr(row_ptr), _ptr(col), _ptr(w_out),
+                               ctypes.byref(nnz), ctypes.byref(loops), ctypes.byref(dups), _stream(stream)))
+    k = nnz.value
+    col = col[:k]
+    if w_out is not None:
+        w_out = w_out[:k]
+    return row_ptr, col, w_out, {"nnz": k, "selfloops": loops.value, "duplicates": dups.value}
+
+
+def _cols(t, n):
+    if t.dim() == 1:
+        if t.numel() != n:
+            raise ValueError("length mismatch")
+        return 1
+    if t.dim() != 2 or t.shape[0] != n:
+        raise ValueError("expected [n] or [n][k]")
+    return int(t.shape[1])
+
+
+class Graph:
+    """Handle over a borrowed device CSR (rows a2..a7).  Keeps references to the CSR tensors."""
+
+    def __init__(self, n: int, row_ptr, col, w=None, validate: bool = True, stream=None):
+        L = lib()
+        _need_cuda(row_ptr, col, w)
+        self.n = int(n)
+        self._keep = (row_ptr, col, w)
+        h = _vp()
+        _check(L.fj_graph_create(self.n, int(col.numel()), _ptr(row_ptr), _ptr(col), _ptr(w), _wtype(w),
+                                 1 if validate else 0, _stream(stream), ctypes.byref(h)))
+        self._h = h
+
+    @classmethod
+    def from_edges(cls, n, u, v, w=None, validate=False, stream=None):
+        rp, col, wo, stats = csr_from_edges(n, u, v, w, stream)
+        g = cls(n, rp, col, wo, validate=validate, stream=stream)
+        g.build_stats = stats
+        return g
+
+    @property
+    def handle(self):
+        if self._h is None:
+            raise RuntimeError("graph destroyed")
+        return self._h
+
+    def info(self) -> dict:
+        gi = GraphInfo()
+        _check(lib().fj_graph_info(self.handle, ctypes.byref(gi)))
+        return {f: getattr(gi, f) for f, _ in gi._fields_ if f != "reserved"}
+
+    def degrees(self, stream=None):
+        import torch
+        d = torch.empty(self.n, dtype=torch.float64, device=self._keep[0].device)
+        _check(lib().fj_graph_degrees(self.handle, _ptr(d), _stream(stream)))
+        return d
+
+    def apply(self, x, op: int = FJ_OP_IPL, stream=None):
+        import torch
+        _need_cuda(x)
+        k = _cols(x, self.n)
+        y = torch.empty_like(x)
+        _check(lib().fj_apply(self.handle, op, k, _ptr(x), _ptr(y), _stream(stream)))
+        return y
+
+    def opinion_stats(self, s, stream=None):
+        import numpy as np
+        _need_cuda(s)
+        k = _cols(s, self.n)
+        out = np.zeros(4 * k)
+        _check(lib().fj_opinion_stats(self.handle, k, _ptr(s), ctypes.c_void_p(out.ctypes.data), _stream(stream)))
+        return out.reshape(k, 4)
+
+    def solve(self, s, opts: SolveOpts | None = None, z=None, stream=None, allow_no_convergence=False):
+        import torch
+        _need_cuda(s)
+        k = _cols(s, self.n)
+        z = torch.empty_like(s) if z is None else z
+        rep = SolveReport()
+        o = opts or SolveOpts.make()
+        _check(lib().fj_solve(self.handle, k, _ptr(s), _ptr(z), ctypes.byref(o), ctypes.byref(rep), _stream(stream)),
+               allow=(FJ_E_NO_CONVERGENCE,) if allow_no_convergence else ())
+        return z, rep.to_dict()
+
+    def quantities(self, s, z, stream=None):
+        _need_cuda(s, z)
+        k = _cols(s, self.n)
+        q = (Quantities * k)()
+        _check(lib().fj_quantities(self.handle, k, _ptr(s), _ptr(z), q, _stream(stream)))
+        return [x.to_dict() for x in q]
+
+    def approxim(self, s, opts: SolveOpts | None = None, z=None, stream=None):
+        """Algorithm 1 (single-solve form): returns (z, [quantities per column], report)."""
+        import torch
+        _need_cuda(s)
+        k = _cols(s, self.n)
+        z = torch.empty_like(s) if z is None else z
+        q = (Quantities * k)()
+        rep = SolveReport()
+        o = opts or SolveOpts.make()
+        _check(lib().fj_approxim(self.handle, k, _ptr(s), _ptr(z), ctypes.byref(o), q, ctypes.byref(rep),
+                                 _stream(stream)))
+        return z, [x.to_dict() for x in q], rep.to_dict()
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and _lib is not None:
+            _lib.fj_graph_destroy(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def approxim_host(n, u, v, w, S, opts: SolveOpts | None = None, want_z=False, stream=None):
+    """End-to-end from HOST numpy buffers (pinned memory recommended): H2D copies, CSR build, handle,
+    Algorithm 1, D2H.  Returns (z or None, [quantities], report)."""
+    import numpy as np
+    L = lib()
+    S = np.ascontiguousarray(S, dtype=np.float64)
+    k = 1 if S.ndim == 1 else S.shape[1]
+    u = np.ascontiguousarray(u, dtype=np.int32)
+    v = np.ascontiguousarray(v, dtype=np.int32)
+    wt = FJ_W_UNIT if w is None else {np.dtype(np.uint8): FJ_W_U8, np.dtype(np.float32): FJ_W_F32,
+                                      np.dtype(np.float64): FJ_W_F64}[np.asarray(w).dtype]
+    z = np.empty_like(S) if want_z else None
+    q = (Quantities * k)()
+    rep = SolveReport()
+    o = opts or SolveOpts.make()
+    wc = None if w is None else np.ascontiguousarray(w)   # keep alive across the call
+
+    def ptr(a):
+        return None if a is None else ctypes.c_void_p(a.ctypes.data)
+    _check(L.fj_approxim_host(n, len(u), ptr(u), ptr(v), ptr(wc), wt, k, ptr(S), ptr(z), ctypes.byref(o), q,
+                              ctypes.byref(rep), _stream(stream)))
+    return z, [x.to_dict() for x in q], rep.to_dict()
+
+
+def _isnan(x):
+    return isinstance(x, float) and math.isnan(x)

@@ -1,0 +1,154 @@
+// common.cuh — internal helpers of libfj (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+#include <cstdio>
+#include <cmath>
+
+#include "../../include/fj.h"
+
+namespace fj {
+
+// ---------------------------------------------------------------- errors
+void set_error(const std::string& msg);
+fj_status fail(fj_status st, const std::string& msg);
+fj_status cuda_fail(cudaError_t e, const char* what, const char* file, int line);
+
+#define FJ_CK(call)                                                            \
+  do {                                                                         \
+    cudaError_t _e = (call);                                                   \
+    if (_e != cudaSuccess) return ::fj::cuda_fail(_e, #call, __FILE__, __LINE__); \
+  } while (0)
+
+#define FJ_TRY(call)                                                           \
+  do {                                                                         \
+    fj_status _s = (call);                                                     \
+    if (_s != FJ_OK) return _s;                                                \
+  } while (0)
+
+// kernel launch accounting (fj_kernel_launches)
+void count_launch(int64_t n = 1);
+void count_cub(int64_t n = 1);
+extern thread_local bool g_capturing;
+
+#define FJ_CK_LAUNCH()                                 \
+  do {                                                 \
+    FJ_CK(cudaGetLastError());                         \
+    if (!::fj::g_capturing) ::fj::count_launch();      \
+  } while (0)
+
+// ---------------------------------------------------------------- constants
+constexpr int TPB = 256;            // threads per block for the tile kernels
+constexpr int TILE_UNITS = 1024;    // merge-path units per tile: 4 per row + 1 per nonzero
+constexpr int ROW_COST = 4;         // -> at most 256 rows per tile (one thread per row)
+constexpr int LONG_ROW = 1024;      // rows with more nonzeros are processed in chunks
+constexpr int LONG_CHUNK = 4096;    // nonzeros per long-row chunk (16 per thread)
+constexpr int TILE_MAX_NNZ = TILE_UNITS + LONG_ROW;   // 2048
+constexpr int TILE_MAX_ROWS = TILE_UNITS / ROW_COST;  // 256
+constexpr int MAXK = 64;
+
+// ---------------------------------------------------------------- device workspace per solve
+struct SolveWs;   // pcg.cu
+struct QuantWs;   // quantities.cu
+
+}  // namespace fj
+
+// The graph handle (borrowed CSR + derived arrays + schedule).
+struct fj_graph {
+  int device = 0;
+  int64_t n = 0, nnz = 0;
+  int wtype = FJ_W_UNIT;
+  const int64_t* row_ptr = nullptr;
+  const int32_t* col = nullptr;
+  const void* w = nullptr;
+  // derived (owned)
+  double* deg = nullptr;        // weighted degree d_i            [n]
+  double* dinv = nullptr;       // 1 / (1 + d_i)                  [n]
+  // schedule (owned): items [0, n_long_chunks) are long-row chunks, then n_tiles tiles
+  int64_t n_tiles = 0, n_long = 0, n_long_chunks = 0;
+  int32_t* tile_begin = nullptr;  // [n_tiles]
+  int32_t* tile_end = nullptr;    // [n_tiles]
+  int32_t* long_row = nullptr;    // [n_long]
+  int32_t* chunk_row = nullptr;   // [n_long_chunks] index into long_row
+  int32_t* chunk_idx = nullptr;   // [n_long_chunks] chunk index within its row
+  int32_t* long_nchunks = nullptr;// [n_long]
+  fj_graph_info_t info{};
+  int num_sms = 148;
+  // caches
+  fj::SolveWs* solve_ws = nullptr;
+  fj::QuantWs* quant_ws = nullptr;
+};
+
+namespace fj {
+
+inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ---------------------------------------------------------------- weights
+template <int WT> struct WeightT;
+template <> struct WeightT<FJ_W_UNIT> {
+  __device__ static __forceinline__ double get(const void*, int64_t) { return 1.0; }
+};
+template <> struct WeightT<FJ_W_U8> {
+  __device__ static __forceinline__ double get(const void* w, int64_t p) {
+    return (double)__ldg(reinterpret_cast<const uint8_t*>(w) + p);
+  }
+};
+template <> struct WeightT<FJ_W_F32> {
+  __device__ static __forceinline__ double get(const void* w, int64_t p) {
+    return (double)__ldg(reinterpret_cast<const float*>(w) + p);
+  }
+};
+template <> struct WeightT<FJ_W_F64> {
+  __device__ static __forceinline__ double get(const void* w, int64_t p) {
+    return __ldg(reinterpret_cast<const double*>(w) + p);
+  }
+};
+
+// ---------------------------------------------------------------- deterministic reductions
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block-wide sum of NP values per thread; result valid in thread 0.  Fixed tree -> deterministic.
+template <int NP, int BLOCK>
+__device__ __forceinline__ void block_sum(double (&v)[NP], double* smem /* >= NP*BLOCK/32 */) {
+  constexpr int NW = BLOCK / 32;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int j = 0; j < NP; ++j) v[j] = warp_sum(v[j]);
+  __syncthreads();
+  if (lane == 0) {
+#pragma unroll
+    for (int j = 0; j < NP; ++j) smem[j * NW + wid] = v[j];
+  }
+  __syncthreads();
+  if (wid == 0) {
+#pragma unroll
+    for (int j = 0; j < NP; ++j) {
+      double x = lane < NW ? smem[j * NW + lane] : 0.0;
+      v[j] = warp_sum(x);
+    }
+  }
+  __syncthreads();
+}
+
+// "Last block" ticket: returns true in ALL threads of the block that arrives last.
+__device__ __forceinline__ bool last_block_ticket(unsigned int* counter, unsigned int total) {
+  __shared__ bool am_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned int t = atomicAdd(counter, 1u);
+    am_last = (t == total - 1);
+  }
+  __syncthreads();
+  if (am_last) __threadfence();
+  return am_last;
+}
+
+__device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
+
+}  // namespace fj

@@ -1,0 +1,414 @@
+// graph.cu — graph handle (row a2): validation, weighted degrees d_i = sum_j w_ij,
+// Jacobi diagonal 1/(1+d_i), statistics (P:L86 w_min/w_max) and the tile-engine schedule.
+#include <cub/cub.cuh>
+#include <atomic>
+#include <cstring>
+#include <vector>
+
+#include "common.cuh"
+#include "workspace.cuh"
+
+namespace fj {
+
+thread_local std::string g_last_error;
+thread_local bool g_capturing = false;
+static std::atomic<int64_t> g_launches{0}, g_cub{0};
+void count_launch(int64_t n) { g_launches += n; }
+void count_cub(int64_t n) { g_cub += n; }
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+fj_status fail(fj_status st, const std::string& msg) {
+  g_last_error = msg;
+  return st;
+}
+
+fj_status cuda_fail(cudaError_t e, const char* what, const char* file, int line) {
+  char buf[512];
+  snprintf(buf, sizeof buf, "CUDA error %d (%s) in %s at %s:%d", (int)e, cudaGetErrorString(e), what,
+           file, line);
+  g_last_error = buf;
+  if (e == cudaErrorMemoryAllocation) return FJ_E_OOM;
+  return FJ_E_CUDA;
+}
+
+// ---------------------------------------------------------------- stats / degree kernel
+struct GStats {
+  unsigned long long deg_max;
+  unsigned long long dmax_bits;   // positive doubles order like their bit patterns
+  unsigned long long wmin_bits;
+  unsigned long long wmax_bits;
+  unsigned long long n_isolated;
+  unsigned int bad_flags;         // validation: 1 not-simple, 2 asymmetric, 4 bad weight
+};
+
+__device__ __forceinline__ unsigned long long dbits(double x) {
+  return (unsigned long long)__double_as_longlong(x);
+}
+
+template <int WT>
+__global__ void k_degree(int64_t n, const int64_t* __restrict__ rp, const void* __restrict__ w,
+                         double* __restrict__ deg, double* __restrict__ dinv, GStats* st) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t len = 0;
+  double d = 0.0, wmn = INFINITY, wmx = 0.0;
+  if (i < n) {
+    const int64_t b = rp[i], e = rp[i + 1];
+    len = e - b;
+    if (WT == FJ_W_UNIT) {
+      d = (double)len;
+      if (len) { wmn = 1.0; wmx = 1.0; }
+    } else {
+      for (int64_t p = b; p < e; ++p) {   // ascending column order: bit-exact with the oracle
+        const double x = WeightT<WT>::get(w, p);
+        d += x;
+        wmn = fmin(wmn, x);
+        wmx = fmax(wmx, x);
+      }
+    }
+    deg[i] = d;
+    dinv[i] = 1.0 / (1.0 + d);   // IEEE division (no fast-math)
+  }
+  // warp-aggregated statistics
+  const unsigned iso = __ballot_sync(0xffffffffu, i < n && len == 0);
+  unsigned long long lm = (unsigned long long)len;
+  unsigned long long dm = dbits(d);
+  unsigned long long mn = dbits(wmn > 0 && wmn < INFINITY ? wmn : INFINITY);
+  unsigned long long mx = dbits(wmx);
+  for (int o = 16; o > 0; o >>= 1) {
+    lm = max(lm, __shfl_xor_sync(0xffffffffu, lm, o));
+    dm = max(dm, __shfl_xor_sync(0xffffffffu, dm, o));
+    mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(&st->deg_max, lm);
+    atomicMax(&st->dmax_bits, dm);
+    atomicMin(&st->wmin_bits, mn);
+    atomicMax(&st->wmax_bits, mx);
+    if (iso) atomicAdd(&st->n_isolated, (unsigned long long)__popc(iso));
+  }
+}
+
+// Validation (P:L86 simple graph, w > 0; P:L88 symmetric adjacency): one thread per row.
+template <int WT>
+__global__ void k_validate(int64_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                           const void* __restrict__ w, GStats* st) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  unsigned flags = 0;
+  const int64_t b = rp[i], e = rp[i + 1];
+  if (e < b) flags |= 1;
+  int64_t prev = -1;
+  for (int64_t p = b; p < e && !(flags & 1); ++p) {
+    const int64_t j = col[p];
+    if (j < 0 || j >= n || j == i || j <= prev) { flags |= 1; break; }
+    prev = j;
+    const double x = WeightT<WT>::get(w, p);
+    if (!(x > 0.0) || !isfinite(x)) flags |= 4;
+    // mirror entry (j, i) with the same weight: binary search in row j
+    int64_t lo = rp[j], hi = rp[j + 1];
+    bool found = false;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      const int32_t c = col[mid];
+      if (c == i) { found = (WeightT<WT>::get(w, mid) == x); break; }
+      if (c < i) lo = mid + 1; else hi = mid;
+    }
+    if (!found) flags |= 2;
+  }
+  if (flags) atomicOr(&st->bad_flags, flags);
+}
+
+__global__ void k_check_rowptr(int64_t n, int64_t nnz, const int64_t* rp, GStats* st) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i > n) return;
+  const int64_t v = rp[i];
+  bool bad = (v < 0 || v > nnz) || (i == 0 && v != 0) || (i == n && v != nnz) ||
+             (i > 0 && rp[i - 1] > v);
+  if (bad) atomicOr(&st->bad_flags, 1u);
+}
+
+// ---------------------------------------------------------------- schedule kernels
+__global__ void k_units(int64_t n, const int64_t* __restrict__ rp, int64_t* __restrict__ c) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i > n) return;
+  if (i == n) { c[i] = 0; return; }
+  const int64_t len = rp[i + 1] - rp[i];
+  c[i] = len > LONG_ROW ? 0 : ROW_COST + len;
+}
+
+__device__ __forceinline__ bool is_long(const int64_t* rp, int64_t i) { return rp[i + 1] - rp[i] > LONG_ROW; }
+
+// boundary flags over i in [0, n]
+__global__ void k_bflags(int64_t n, const int64_t* __restrict__ rp, const int64_t* __restrict__ e,
+                         uint8_t* __restrict__ f) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i > n) return;
+  bool b = (i == 0) || (i == n);
+  if (!b) {
+    b = is_long(rp, i) || is_long(rp, i - 1) || (e[i] / TILE_UNITS != e[i - 1] / TILE_UNITS);
+  }
+  f[i] = b ? 1 : 0;
+}
+
+// per segment j (begin B[j], end B[j+1]): flag tile vs long
+__global__ void k_segflags(int64_t nseg, const int32_t* __restrict__ B, const int64_t* __restrict__ rp,
+                           uint8_t* __restrict__ ft, uint8_t* __restrict__ fl) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= nseg) return;
+  const bool l = is_long(rp, B[j]);
+  ft[j] = l ? 0 : 1;
+  fl[j] = l ? 1 : 0;
+}
+
+__global__ void k_tiles_from_segs(int64_t nt, const int32_t* __restrict__ segs, const int32_t* __restrict__ B,
+                                  int32_t* __restrict__ tb, int32_t* __restrict__ te) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= nt) return;
+  const int32_t j = segs[t];
+  tb[t] = B[j];
+  te[t] = B[j + 1];
+}
+
+__global__ void k_long_from_segs(int64_t nl, const int32_t* __restrict__ segs, const int32_t* __restrict__ B,
+                                 const int64_t* __restrict__ rp, int32_t* __restrict__ lrow,
+                                 int32_t* __restrict__ lnch) {
+  const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (l >= nl) return;
+  const int32_t i = B[segs[l]];
+  lrow[l] = i;
+  const int64_t len = rp[i + 1] - rp[i];
+  lnch[l] = (int32_t)((len + LONG_CHUNK - 1) / LONG_CHUNK);
+}
+
+__global__ void k_chunks(int64_t nl, const int32_t* __restrict__ lnch, const int32_t* __restrict__ cstart,
+                         int32_t* __restrict__ crow, int32_t* __restrict__ cidx) {
+  const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (l >= nl) return;
+  const int32_t s = cstart[l];
+  for (int32_t c = 0; c < lnch[l]; ++c) { crow[s + c] = (int32_t)l; cidx[s + c] = c; }
+}
+
+static inline double bits2d(unsigned long long b) { double d; memcpy(&d, &b, sizeof d); return d; }
+
+static inline unsigned nblk(int64_t n, int t = 256) { return (unsigned)((n + t - 1) / t); }
+
+static fj_status build_schedule(fj_graph* g, cudaStream_t st) {
+  const int64_t n = g->n;
+  DevBuf<int64_t> c, e;
+  DevBuf<uint8_t> f;
+  DevBuf<int32_t> B, nsel;
+  FJ_TRY(c.alloc(n + 1, st));
+  FJ_TRY(e.alloc(n + 1, st));
+  FJ_TRY(f.alloc(n + 1, st));
+  FJ_TRY(B.alloc(n + 1, st));
+  FJ_TRY(nsel.alloc(1, st));
+  k_units<<<nblk(n + 1), 256, 0, st>>>(n, g->row_ptr, c.p);
+  FJ_CK_LAUNCH();
+  FJ_TRY(cub_exclusive_sum(c.p, e.p, n + 1, st));
+  k_bflags<<<nblk(n + 1), 256, 0, st>>>(n, g->row_ptr, e.p, f.p);
+  FJ_CK_LAUNCH();
+  FJ_TRY(cub_select_index(f.p, B.p, nsel.p, n + 1, st));
+  int32_t nb = 0;
+  FJ_CK(cudaMemcpyAsync(&nb, nsel.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  FJ_CK(cudaStreamSynchronize(st));
+  const int64_t nseg = nb - 1;
+  int32_t nt = 0, nl = 0;
+  if (nseg > 0) {
+    DevBuf<uint8_t> ft, fl;
+    DevBuf<int32_t> segt, segl, ns2;
+    FJ_TRY(ft.alloc(nseg, st));
+    FJ_TRY(fl.alloc(nseg, st));
+    FJ_TRY(segt.alloc(nseg, st));
+    FJ_TRY(segl.alloc(nseg, st));
+    FJ_TRY(ns2.alloc(2, st));
+    k_segflags<<<nblk(nseg), 256, 0, st>>>(nseg, B.p, g->row_ptr, ft.p, fl.p);
+    FJ_CK_LAUNCH();
+    FJ_TRY(cub_select_index(ft.p, segt.p, ns2.p, nseg, st));
+    FJ_TRY(cub_select_index(fl.p, segl.p, ns2.p + 1, nseg, st));
+    int32_t cnt[2];
+    FJ_CK(cudaMemcpyAsync(cnt, ns2.p, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    FJ_CK(cudaStreamSynchronize(st));
+    nt = cnt[0];
+    nl = cnt[1];
+    if (nt > 0) {
+      FJ_CK(cudaMallocAsync(&g->tile_begin, sizeof(int32_t) * nt, st));
+      FJ_CK(cudaMallocAsync(&g->tile_end, sizeof(int32_t) * nt, st));
+      k_tiles_from_segs<<<nblk(nt), 256, 0, st>>>(nt, segt.p, B.p, g->tile_begin, g->tile_end);
+      FJ_CK_LAUNCH();
+    }
+    if (nl > 0) {
+      FJ_CK(cudaMallocAsync(&g->long_row, sizeof(int32_t) * nl, st));
+      FJ_CK(cudaMallocAsync(&g->long_nchunks, sizeof(int32_t) * nl, st));
+      k_long_from_segs<<<nblk(nl), 256, 0, st>>>(nl, segl.p, B.p, g->row_ptr, g->long_row, g->long_nchunks);
+      FJ_CK_LAUNCH();
+      DevBuf<int32_t> cs;
+      FJ_TRY(cs.alloc(nl + 1, st));
+      FJ_TRY(cub_exclusive_sum_i32(g->long_nchunks, cs.p, nl, st));
+      int32_t last_start = 0, last_n = 0;
+      FJ_CK(cudaMemcpyAsync(&last_start, cs.p + nl - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+      FJ_CK(cudaMemcpyAsync(&last_n, g->long_nchunks + nl - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+      FJ_CK(cudaStreamSynchronize(st));
+      const int64_t nch = (int64_t)last_start + last_n;
+      FJ_CK(cudaMallocAsync(&g->chunk_row, sizeof(int32_t) * nch, st));
+      FJ_CK(cudaMallocAsync(&g->chunk_idx, sizeof(int32_t) * nch, st));
+      k_chunks<<<nblk(nl), 256, 0, st>>>(nl, g->long_nchunks, cs.p, g->chunk_row, g->chunk_idx);
+      FJ_CK_LAUNCH();
+      g->n_long_chunks = nch;
+    }
+  }
+  g->n_tiles = nt;
+  g->n_long = nl;
+  return FJ_OK;
+}
+
+template <int WT>
+static fj_status launch_degree(fj_graph* g, GStats* st_d, int validate, cudaStream_t st) {
+  if (validate) {
+    k_check_rowptr<<<nblk(g->n + 1), 256, 0, st>>>(g->n, g->nnz, g->row_ptr, st_d);
+    FJ_CK_LAUNCH();
+    GStats h;
+    FJ_CK(cudaMemcpyAsync(&h, st_d, sizeof h, cudaMemcpyDeviceToHost, st));
+    FJ_CK(cudaStreamSynchronize(st));
+    if (h.bad_flags) return fail(FJ_E_NOT_SIMPLE, "row_ptr is not a valid CSR row pointer");
+    k_validate<WT><<<nblk(g->n), 256, 0, st>>>(g->n, g->row_ptr, g->col, g->w, st_d);
+    FJ_CK_LAUNCH();
+  }
+  k_degree<WT><<<nblk(g->n), 256, 0, st>>>(g->n, g->row_ptr, g->w, g->deg, g->dinv, st_d);
+  FJ_CK_LAUNCH();
+  return FJ_OK;
+}
+
+}  // namespace fj
+
+using namespace fj;
+
+extern "C" {
+
+int fj_abi_version(void) { return FJ_ABI_VERSION; }
+
+int64_t fj_kernel_launches(int64_t* cub_launches) {
+  if (cub_launches) *cub_launches = g_cub.load();
+  return g_launches.load();
+}
+
+const char* fj_last_error(void) { return g_last_error.c_str(); }
+
+const char* fj_status_str(int s) {
+  switch (s) {
+    case FJ_OK: return "FJ_OK";
+    case FJ_E_INVALID_ARG: return "FJ_E_INVALID_ARG";
+    case FJ_E_NOT_SIMPLE: return "FJ_E_NOT_SIMPLE";
+    case FJ_E_ASYMMETRIC: return "FJ_E_ASYMMETRIC";
+    case FJ_E_BAD_WEIGHT: return "FJ_E_BAD_WEIGHT";
+    case FJ_E_NONFINITE_INPUT: return "FJ_E_NONFINITE_INPUT";
+    case FJ_E_NO_CONVERGENCE: return "FJ_E_NO_CONVERGENCE";
+    case FJ_E_CUDA: return "FJ_E_CUDA";
+    case FJ_E_NCCL: return "FJ_E_NCCL";
+    case FJ_E_OOM: return "FJ_E_OOM";
+    case FJ_E_INTERNAL: return "FJ_E_INTERNAL";
+    case FJ_E_UNSUPPORTED: return "FJ_E_UNSUPPORTED";
+    default: return "FJ_E_UNKNOWN";
+  }
+}
+
+void fj_default_solve_opts(fj_solve_opts* o) {
+  if (!o) return;
+  o->rtol = 1e-10;
+  o->eps_target = 0.0;
+  o->max_iter = 10000;
+  o->max_restarts = 3;
+  o->use_cuda_graph = 1;
+  o->reserved = 0;
+}
+
+fj_status fj_graph_create(int64_t n, int64_t nnz, const int64_t* row_ptr, const int32_t* col, const void* w,
+                          int wtype, int validate, void* stream, fj_graph** out) {
+  if (!out) return fail(FJ_E_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  if (n < 1 || n >= INT32_MAX) return fail(FJ_E_INVALID_ARG, "n must be in [1, 2^31-2]");
+  if (nnz < 0 || !row_ptr || (nnz > 0 && !col)) return fail(FJ_E_INVALID_ARG, "bad CSR arrays");
+  if (wtype < FJ_W_UNIT || wtype > FJ_W_F64) return fail(FJ_E_INVALID_ARG, "bad wtype");
+  if (wtype != FJ_W_UNIT && nnz > 0 && !w) return fail(FJ_E_INVALID_ARG, "weights are NULL");
+  cudaStream_t st = S(stream);
+  fj_graph* g = new fj_graph();
+  g->n = n; g->nnz = nnz; g->wtype = wtype; g->row_ptr = row_ptr; g->col = col;
+  g->w = (wtype == FJ_W_UNIT) ? nullptr : w;
+  auto cleanup = [&](fj_status s) { fj_graph_destroy(g); return s; };
+  cudaError_t ce = cudaGetDevice(&g->device);
+  if (ce != cudaSuccess) return cleanup(cuda_fail(ce, "cudaGetDevice", __FILE__, __LINE__));
+  cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, g->device);
+  ce = cudaMallocAsync(&g->deg, sizeof(double) * n, st);
+  if (ce == cudaSuccess) ce = cudaMallocAsync(&g->dinv, sizeof(double) * n, st);
+  if (ce != cudaSuccess) return cleanup(cuda_fail(ce, "cudaMallocAsync", __FILE__, __LINE__));
+  GStats* st_d = nullptr;
+  ce = cudaMallocAsync(&st_d, sizeof(GStats), st);
+  if (ce != cudaSuccess) return cleanup(cuda_fail(ce, "cudaMallocAsync", __FILE__, __LINE__));
+  GStats init{};
+  init.wmin_bits = (unsigned long long)0x7FF0000000000000ULL;  // +inf
+  cudaMemcpyAsync(st_d, &init, sizeof init, cudaMemcpyHostToDevice, st);
+  fj_status s = FJ_OK;
+  switch (wtype) {
+    case FJ_W_UNIT: s = launch_degree<FJ_W_UNIT>(g, st_d, validate, st); break;
+    case FJ_W_U8: s = launch_degree<FJ_W_U8>(g, st_d, validate, st); break;
+    case FJ_W_F32: s = launch_degree<FJ_W_F32>(g, st_d, validate, st); break;
+    default: s = launch_degree<FJ_W_F64>(g, st_d, validate, st); break;
+  }
+  GStats h{};
+  if (s == FJ_OK) {
+    ce = cudaMemcpyAsync(&h, st_d, sizeof h, cudaMemcpyDeviceToHost, st);
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
+    if (ce != cudaSuccess) s = cuda_fail(ce, "stats readback", __FILE__, __LINE__);
+  }
+  cudaFreeAsync(st_d, st);
+  if (s != FJ_OK) return cleanup(s);
+  if (validate && h.bad_flags) {
+    if (h.bad_flags & 1) return cleanup(fail(FJ_E_NOT_SIMPLE, "CSR not simple: column out of range, self-loop, or columns not strictly ascending"));
+    if (h.bad_flags & 4) return cleanup(fail(FJ_E_BAD_WEIGHT, "edge weight <= 0 or non-finite"));
+    return cleanup(fail(FJ_E_ASYMMETRIC, "adjacency not symmetric: (i,j,w) without (j,i,w)"));
+  }
+  if (nnz % 2 != 0 && validate) return cleanup(fail(FJ_E_ASYMMETRIC, "odd nnz"));
+  s = build_schedule(g, st);
+  if (s != FJ_OK) return cleanup(s);
+  fj_graph_info_t& I = g->info;
+  I.n = n; I.nnz = nnz; I.m = nnz / 2;
+  I.n_isolated = (int64_t)h.n_isolated;
+  I.deg_max = (int64_t)h.deg_max;
+  I.d_max = bits2d(h.dmax_bits);
+  I.w_min = nnz ? bits2d(h.wmin_bits) : 0.0;
+  I.w_max = nnz ? bits2d(h.wmax_bits) : 0.0;
+  I.n_tiles = g->n_tiles; I.n_long_rows = g->n_long; I.n_long_chunks = g->n_long_chunks;
+  I.wtype = wtype;
+  ce = cudaStreamSynchronize(st);
+  if (ce != cudaSuccess) return cleanup(cuda_fail(ce, "graph create", __FILE__, __LINE__));
+  *out = g;
+  return FJ_OK;
+}
+
+fj_status fj_graph_info(const fj_graph* g, fj_graph_info_t* out) {
+  if (!g || !out) return fail(FJ_E_INVALID_ARG, "null argument");
+  *out = g->info;
+  return FJ_OK;
+}
+
+fj_status fj_graph_degrees(const fj_graph* g, double* d, void* stream) {
+  if (!g || !d) return fail(FJ_E_INVALID_ARG, "null argument");
+  FJ_CK(cudaMemcpyAsync(d, g->deg, sizeof(double) * g->n, cudaMemcpyDeviceToDevice, S(stream)));
+  return FJ_OK;
+}
+
+fj_status fj_graph_destroy(fj_graph* g) {
+  if (!g) return FJ_OK;
+  cudaDeviceSynchronize();
+  free_solve_ws(g);
+  free_quant_ws(g);
+  cudaFree(g->deg); cudaFree(g->dinv);
+  cudaFree(g->tile_begin); cudaFree(g->tile_end);
+  cudaFree(g->long_row); cudaFree(g->long_nchunks);
+  cudaFree(g->chunk_row); cudaFree(g->chunk_idx);
+  delete g;
+  return FJ_OK;
+}
+
+}  // extern "C"

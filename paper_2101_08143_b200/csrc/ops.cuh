@@ -1,0 +1,160 @@
+// ops.cuh — row operators plugged into the tile engine (tiles.cuh) and the per-solve workspace.
+#pragma once
+#include "tiles.cuh"
+
+namespace fj {
+
+// Device scalars of one PCG solve (one column).  Written only by "last block" finalisers.
+struct PcgScalars {
+  double rho;        // r^T y, y = dinv o r
+  double alpha, beta;
+  double pq;         // p^T (I+L) p
+  double rr;         // ||r||^2 (recursive)
+  double ss;         // ||s||^2
+  double tol2;       // rtol^2 ||s||^2
+  double res2;       // ||s - (I+L) x||^2 (true residual, when computed)
+  int32_t iter, max_iter, done, converged, breakdown, pad;
+};
+
+// y = (I+L) x  (mode IPL) or y = L x (mode L) for column c of row-major [n][ld] arrays.
+// (I+L)x_i = (1 + d_i) x_i - sum_j w_ij x_j   (P:L88 L = D - A).
+// If sc != nullptr this is the PCG search-direction product: skip when the solve is done and
+// finalise alpha = rho / p^T q on device.
+template <int WT>
+struct ApplyOp {
+  static constexpr int NA = 1, NP = 1;
+  static constexpr bool NEEDS_XI = false;
+  const double* __restrict__ x;
+  double* __restrict__ y;
+  const double* __restrict__ deg;   // weighted degree (unused for unit weights)
+  int64_t ld, c;
+  int opL;                          // 1: L x, 0: (I + L) x
+  PcgScalars* sc;                   // PCG mode when non-null
+  double* dot_out;                  // optional: x^T y
+  __device__ __forceinline__ bool skip() const { return sc && *(volatile int32_t*)&sc->done; }
+  __device__ __forceinline__ double gather(int32_t j) const { return __ldg(x + (int64_t)j * ld + c); }
+  __device__ __forceinline__ double row_value(int64_t) const { return 0.0; }
+  __device__ __forceinline__ void add(double (&a)[NA], double w, double xj, double) const {
+    if (WT == FJ_W_UNIT) a[0] += xj; else a[0] = fma(w, xj, a[0]);
+  }
+  __device__ __forceinline__ void finish_row(int64_t i, int64_t len, const double (&a)[NA], double (&part)[NP]) const {
+    const double d = (WT == FJ_W_UNIT) ? (double)len : deg[i];
+    const double xi = x[i * ld + c];
+    const double yi = opL ? fma(d, xi, -a[0]) : fma(1.0 + d, xi, -a[0]);
+    y[i * ld + c] = yi;
+    part[0] = fma(xi, yi, part[0]);
+  }
+  __device__ __forceinline__ void finalize(const double (&tot)[NP]) const {
+    if (dot_out) *dot_out = tot[0];
+    if (sc) {
+      sc->pq = tot[0];
+      if (!(tot[0] > 0.0) || !isfinite(tot[0])) {   // (I+L) is SPD: p^T q > 0 unless p = 0
+        sc->alpha = 0.0;
+        sc->breakdown = 1;
+        sc->done = 1;
+      } else {
+        sc->alpha = sc->rho / tot[0];
+      }
+    }
+  }
+};
+
+// ||s - (I+L) z||^2 for column c (true residual).
+template <int WT>
+struct ResidOp {
+  static constexpr int NA = 1, NP = 1;
+  static constexpr bool NEEDS_XI = false;
+  const double* __restrict__ z;     // contiguous [n]
+  const double* __restrict__ s;     // column c of row-major [n][ld]
+  const double* __restrict__ deg;
+  int64_t ld, c;
+  double* res2_out;
+  __device__ __forceinline__ bool skip() const { return false; }
+  __device__ __forceinline__ double gather(int32_t j) const { return __ldg(z + j); }
+  __device__ __forceinline__ double row_value(int64_t) const { return 0.0; }
+  __device__ __forceinline__ void add(double (&a)[NA], double w, double xj, double) const {
+    if (WT == FJ_W_UNIT) a[0] += xj; else a[0] = fma(w, xj, a[0]);
+  }
+  __device__ __forceinline__ void finish_row(int64_t i, int64_t len, const double (&a)[NA], double (&part)[NP]) const {
+    const double d = (WT == FJ_W_UNIT) ? (double)len : deg[i];
+    const double zi = z[i];
+    const double r = s[i * ld + c] - fma(1.0 + d, zi, -a[0]);
+    part[0] = fma(r, r, part[0]);
+  }
+  __device__ __forceinline__ void finalize(const double (&tot)[NP]) const { *res2_out = tot[0]; }
+};
+
+// Fused quantities pass (rows a5-a7) for column c.  Per row i, with A = sum_j w_ij z_j,
+// Dd = sum_j w_ij (z_i - z_j)^2, Aa = sum_j w_ij |z_j|, t = (I+L)z_i, m = mean(s):
+//  0 (z-s)^2 [CI, Def 3.1]   1 Dd [2D, Def 3.2 counts each edge from both ends]
+//  2 (z-m)^2 [P, Def 3.3]    3 z^2 [C, Def 3.4]   4 s z [= Idc, P:L228]
+//  5 (s-m)(z-m) [= PDI]      6 (s - t)^2 [true residual]   7 (d z - A)^2 [||Lz||^2, Alg.1 l.5]
+//  8 (|s| + (1+d)|z| + Aa)^2 [rounding allowance]          9 s^2
+template <int WT>
+struct QuantOp {
+  static constexpr int NA = 3, NP = 10;
+  static constexpr bool NEEDS_XI = true;
+  const double* __restrict__ z;
+  const double* __restrict__ s;
+  const double* __restrict__ deg;
+  int64_t ld, c;
+  double m;
+  double* out;   // [NP]
+  __device__ __forceinline__ bool skip() const { return false; }
+  __device__ __forceinline__ double gather(int32_t j) const { return __ldg(z + (int64_t)j * ld + c); }
+  __device__ __forceinline__ double row_value(int64_t i) const { return z[i * ld + c]; }
+  __device__ __forceinline__ void add(double (&a)[NA], double w, double zj, double zi) const {
+    const double df = zi - zj;
+    a[0] = fma(w, zj, a[0]);
+    a[1] = fma(w * df, df, a[1]);
+    a[2] = fma(w, fabs(zj), a[2]);
+  }
+  __device__ __forceinline__ void finish_row(int64_t i, int64_t len, const double (&a)[NA], double (&part)[NP]) const {
+    const double d = (WT == FJ_W_UNIT) ? (double)len : deg[i];
+    const double zi = z[i * ld + c], si = s[i * ld + c];
+    const double t = fma(1.0 + d, zi, -a[0]);
+    const double lz = fma(d, zi, -a[0]);
+    const double r = si - t;
+    const double e1 = zi - si, e2 = zi - m, e3 = si - m;
+    const double ab = fabs(si) + fma(1.0 + d, fabs(zi), a[2]);
+    part[0] = fma(e1, e1, part[0]);
+    part[1] += a[1];
+    part[2] = fma(e2, e2, part[2]);
+    part[3] = fma(zi, zi, part[3]);
+    part[4] = fma(si, zi, part[4]);
+    part[5] = fma(e3, e2, part[5]);
+    part[6] = fma(r, r, part[6]);
+    part[7] = fma(lz, lz, part[7]);
+    part[8] = fma(ab, ab, part[8]);
+    part[9] = fma(si, si, part[9]);
+  }
+  __device__ __forceinline__ void finalize(const double (&tot)[NP]) const {
+#pragma unroll
+    for (int j = 0; j < NP; ++j) out[j] = tot[j];
+  }
+};
+
+// Per-graph workspace shared by the solver and the quantities pass (stream-ordered use only).
+struct SolveWs {
+  int64_t n = 0;
+  int grid_tile = 0, grid_elem = 0;
+  double *r = nullptr, *p = nullptr, *q = nullptr, *x = nullptr, *col_s = nullptr;
+  PcgScalars* sc = nullptr;
+  double* elem_part = nullptr;       // [grid_elem][4]
+  unsigned int* elem_ticket = nullptr;
+  TileScratch ts{};
+  double* qout = nullptr;            // [16] quantities totals
+  double* stat = nullptr;            // [4 * MAXK] opinion statistics
+  // captured loop
+  cudaGraphExec_t exec = nullptr;
+  cudaGraph_t graph = nullptr;
+  cudaStream_t cap_stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
+};
+
+fj_status get_ws(fj_graph* g, cudaStream_t st, SolveWs** out);
+
+template <class Op>
+inline fj_status launch_tiles(const fj_graph* g, const SolveWs* ws, const Op& op, cudaStream_t st);
+
+}  // namespace fj

@@ -1,0 +1,328 @@
+// quantities.cu — rows a3 (opinion statistics), a5-a7 (fused quantities pass + certificate) and
+// Algorithm 1 in single-solve form (fj_approxim), plus the host-buffer e2e entry point.
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <vector>
+
+#include "ops.cuh"
+#include "workspace.cuh"
+
+namespace fj {
+
+fj_status solve_col(fj_graph* g, const double* s, double* z, int64_t ld, int64_t c, const fj_solve_opts& o,
+                    int warm, fj_solve_report* rep, cudaStream_t st, int* iters_out);
+
+void free_quant_ws(fj_graph*) {}
+
+// ---------------------------------------------------------------- a3: statistics of column c
+constexpr int STPB = 256;
+__global__ void __launch_bounds__(STPB) k_stats(int64_t n, const double* __restrict__ s, int64_t ld, int64_t c,
+                                                double* part /*[grid][4]*/, unsigned int* ticket, double* out,
+                                                int* nonfinite) {
+  __shared__ double s_red[4 * STPB / 32];
+  __shared__ bool s_last;
+  double sm = 0.0, sq = 0.0, mn = INFINITY, mx = -INFINITY;
+  int bad = 0;
+  for (int64_t i = blockIdx.x * (int64_t)STPB + threadIdx.x; i < n; i += (int64_t)gridDim.x * STPB) {
+    const double x = s[i * ld + c];
+    if (!isfinite(x)) { bad = 1; continue; }
+    sm += x;
+    sq = fma(x, x, sq);
+    mn = fmin(mn, x);
+    mx = fmax(mx, x);
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(nonfinite, 1);
+  double v[2] = {sm, sq};
+  block_sum<2, STPB>(v, s_red);
+  // min / max: warp + smem
+  for (int o = 16; o > 0; o >>= 1) {
+    mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  __shared__ double s_mm[2 * STPB / 32];
+  if ((threadIdx.x & 31) == 0) { s_mm[threadIdx.x >> 5] = mn; s_mm[STPB / 32 + (threadIdx.x >> 5)] = mx; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < STPB / 32; ++w) { mn = fmin(mn, s_mm[w]); mx = fmax(mx, s_mm[STPB / 32 + w]); }
+    part[blockIdx.x * 4 + 0] = v[0];
+    part[blockIdx.x * 4 + 1] = v[1];
+    part[blockIdx.x * 4 + 2] = mn;
+    part[blockIdx.x * 4 + 3] = mx;
+    __threadfence();
+    s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) {
+    __threadfence();
+    double a = 0.0, b = 0.0, lo = INFINITY, hi = -INFINITY;
+    for (unsigned q = 0; q < gridDim.x; ++q) {   // fixed order
+      a += __ldcg(part + q * 4 + 0);
+      b += __ldcg(part + q * 4 + 1);
+      lo = fmin(lo, __ldcg(part + q * 4 + 2));
+      hi = fmax(hi, __ldcg(part + q * 4 + 3));
+    }
+    out[0] = a; out[1] = b; out[2] = lo; out[3] = hi;
+    *ticket = 0u;
+  }
+}
+
+static fj_status stats_cols(fj_graph* g, SolveWs* w, int k, const double* s, std::vector<double>& st4,
+                            cudaStream_t st) {
+  int* d_bad = nullptr;
+  FJ_CK(cudaMallocAsync(&d_bad, sizeof(int), st));
+  FJ_CK(cudaMemsetAsync(d_bad, 0, sizeof(int), st));
+  for (int c = 0; c < k; ++c) {
+    k_stats<<<w->grid_elem, STPB, 0, st>>>(g->n, s, k, c, w->elem_part, w->elem_ticket, w->stat + 4 * c, d_bad);
+    FJ_CK_LAUNCH();
+  }
+  st4.assign(4 * k, 0.0);
+  int bad = 0;
+  FJ_CK(cudaMemcpyAsync(st4.data(), w->stat, sizeof(double) * 4 * k, cudaMemcpyDeviceToHost, st));
+  FJ_CK(cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+  FJ_CK(cudaFreeAsync(d_bad, st));
+  FJ_CK(cudaStreamSynchronize(st));
+  if (bad) return fail(FJ_E_NONFINITE_INPUT, "opinion vector contains NaN or Inf");
+  return FJ_OK;
+}
+
+// ---------------------------------------------------------------- a6: fused pass for column c
+template <int WT>
+static fj_status launch_quant_wt(const fj_graph* g, const SolveWs* w, const double* s, const double* z, int64_t ld,
+                                 int64_t c, double m, cudaStream_t st) {
+  QuantOp<WT> op{z, s, g->deg, ld, c, m, w->qout};
+  tile_kernel<WT, QuantOp<WT>><<<w->grid_tile, TPB, 0, st>>>(make_sched(g), op, w->ts);
+  FJ_CK_LAUNCH();
+  return FJ_OK;
+}
+
+static fj_status quant_pass(const fj_graph* g, const SolveWs* w, const double* s, const double* z, int64_t ld,
+                            int64_t c, double m, double* host10, cudaStream_t st) {
+  fj_status r;
+  switch (g->wtype) {
+    case FJ_W_UNIT: r = launch_quant_wt<FJ_W_UNIT>(g, w, s, z, ld, c, m, st); break;
+    case FJ_W_U8: r = launch_quant_wt<FJ_W_U8>(g, w, s, z, ld, c, m, st); break;
+    case FJ_W_F32: r = launch_quant_wt<FJ_W_F32>(g, w, s, z, ld, c, m, st); break;
+    default: r = launch_quant_wt<FJ_W_F64>(g, w, s, z, ld, c, m, st); break;
+  }
+  FJ_TRY(r);
+  FJ_CK(cudaMemcpyAsync(host10, w->qout, sizeof(double) * 10, cudaMemcpyDeviceToHost, st));
+  FJ_CK(cudaStreamSynchronize(st));
+  return FJ_OK;
+}
+
+// ---------------------------------------------------------------- a7: certificate (host)
+// For Q = ||v||^2 computed as Qt = ||vt||^2 with ||vt - v|| <= R:
+//   Q in [(a - R)^2, (a + R)^2], a = sqrt(Qt)  =>  |Qt - Q| / Q <= (2 a R + R^2) / (a - R)^2.
+// R bounds ||z - z*||: lambda_min(I+L) = 1 gives ||e|| <= ||e||_{I+L} <= ||r|| and
+// ||W^{1/2} B e|| = ||e||_L <= ||e||_{I+L} <= ||r||; this is the proof pattern of Lemma 4.3
+// applied a posteriori.  R = computed ||r|| + rounding allowance gamma ||a||.
+static double cert_eps(double Qt, double R, double rel_sum) {
+  if (Qt <= 0.0) return R == 0.0 ? 0.0 : std::numeric_limits<double>::infinity();
+  const double a = std::sqrt(Qt);
+  if (!(a > R)) return std::numeric_limits<double>::infinity();
+  return (2.0 * a * R + R * R) / ((a - R) * (a - R)) + rel_sum;
+}
+
+static void fill_quantities(const fj_graph* g, const double* t, double mean_s, fj_quantities_t& q) {
+  const double n = (double)g->n;
+  q.CI = t[0];
+  q.D = 0.5 * t[1];   // each undirected edge was visited from both ends
+  q.P = t[2];
+  q.C = t[3];
+  q.Idc = q.D + q.C;
+  q.PDI = q.P + q.D;
+  q.mean_s = mean_s;
+  q.sz = t[4];
+  q.sbzb = t[5];
+  q.Lz2 = t[7];
+  q.ss = t[9];
+  q.res_norm = std::sqrt(t[6]);
+  q.s_norm = std::sqrt(t[9]);
+  const double u = std::ldexp(1.0, -53);
+  const double lg = std::ceil(std::log2(g->info.d_max + 2.0));
+  const double gamma = (32.0 + lg + 4.0) * u;     // row sums: <= 32 sequential + tree levels
+  q.fp_bound = gamma * std::sqrt(t[8]);
+  const double R = q.res_norm * (1.0 + 1e-12) + q.fp_bound;
+  const double rel_sum = (std::ceil(std::log2(n + 1.0)) + 40.0) * u;   // summation of the squares
+  const double eC = cert_eps(q.C, R, rel_sum), eD = cert_eps(q.D, R, rel_sum);
+  const double eP = cert_eps(q.P, R, rel_sum), eI = cert_eps(q.CI, R, rel_sum);
+  q.eps[0] = eI;
+  q.eps[1] = eD;
+  q.eps[2] = eP;
+  q.eps[3] = eC;
+  q.eps[4] = std::max(eD, eC);   // eps-approximation closed under sums
+  q.eps[5] = std::max(eP, eD);
+  q.certified = 1;
+  for (int j = 0; j < 6; ++j)
+    if (!std::isfinite(q.eps[j])) q.certified = 0;
+  q.consensus = 0;
+}
+
+static void consensus_quantities(const fj_graph* g, double c, fj_quantities_t& q) {
+  memset(&q, 0, sizeof q);
+  const double n = (double)g->n;
+  q.C = n * c * c;          // z = s = c 1 exactly (Omega 1 = 1)
+  q.Idc = q.C;
+  q.mean_s = c;
+  q.ss = q.C;
+  q.sz = q.C;
+  q.s_norm = std::sqrt(q.C);
+  q.consensus = 1;
+  q.certified = 1;
+}
+
+__global__ void k_copy_cols(int64_t n, int64_t k, int64_t c, const double* __restrict__ s, double* __restrict__ z) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    z[i * k + c] = s[i * k + c];
+}
+
+}  // namespace fj
+
+using namespace fj;
+
+extern "C" {
+
+fj_status fj_opinion_stats(const fj_graph* gc, int k, const double* s, double* stats_host, void* stream) {
+  if (!gc || !s || !stats_host) return fail(FJ_E_INVALID_ARG, "null argument");
+  if (k < 1 || k > MAXK) return fail(FJ_E_INVALID_ARG, "k must be in [1, 64]");
+  fj_graph* g = const_cast<fj_graph*>(gc);
+  cudaStream_t st = S(stream);
+  SolveWs* w = nullptr;
+  FJ_TRY(get_ws(g, st, &w));
+  std::vector<double> v;
+  FJ_TRY(stats_cols(g, w, k, s, v, st));
+  memcpy(stats_host, v.data(), sizeof(double) * 4 * k);
+  return FJ_OK;
+}
+
+fj_status fj_quantities(const fj_graph* gc, int k, const double* s, const double* z, fj_quantities_t* out,
+                        void* stream) {
+  if (!gc || !s || !z || !out) return fail(FJ_E_INVALID_ARG, "null argument");
+  if (k < 1 || k > MAXK) return fail(FJ_E_INVALID_ARG, "k must be in [1, 64]");
+  fj_graph* g = const_cast<fj_graph*>(gc);
+  cudaStream_t st = S(stream);
+  SolveWs* w = nullptr;
+  FJ_TRY(get_ws(g, st, &w));
+  std::vector<double> v;
+  FJ_TRY(stats_cols(g, w, k, s, v, st));
+  for (int c = 0; c < k; ++c) {
+    double t[10];
+    const double m = v[4 * c] / (double)g->n;
+    FJ_TRY(quant_pass(g, w, s, z, k, c, m, t, st));
+    memset(&out[c], 0, sizeof(fj_quantities_t));
+    fill_quantities(g, t, m, out[c]);
+  }
+  return FJ_OK;
+}
+
+fj_status fj_approxim(const fj_graph* gc, int k, const double* s, double* z_user, const fj_solve_opts* opts,
+                      fj_quantities_t* qout, fj_solve_report* rep, void* stream) {
+  if (!gc || !s || !qout) return fail(FJ_E_INVALID_ARG, "null argument");
+  if (k < 1 || k > MAXK) return fail(FJ_E_INVALID_ARG, "k must be in [1, 64]");
+  if (z_user == s) return fail(FJ_E_INVALID_ARG, "s and z must not alias");
+  fj_solve_opts o;
+  fj_default_solve_opts(&o);
+  if (opts) o = *opts;
+  if (!(o.rtol > 0.0) || o.max_iter < 0 || o.max_restarts < 0 || o.eps_target < 0)
+    return fail(FJ_E_INVALID_ARG, "bad solve options");
+  fj_graph* g = const_cast<fj_graph*>(gc);
+  cudaStream_t st = S(stream);
+  SolveWs* w = nullptr;
+  FJ_TRY(get_ws(g, st, &w));
+  double* z = z_user;
+  DevBuf<double> zbuf;
+  if (!z) {
+    FJ_TRY(zbuf.alloc(g->n * (int64_t)k, st));
+    z = zbuf.p;
+  }
+  FJ_CK(cudaEventRecord(w->ev0, st));
+  // Algorithm 1 line 2: mean of s, plus the consensus short-circuit
+  std::vector<double> v;
+  FJ_TRY(stats_cols(g, w, k, s, v, st));
+  fj_solve_report r{};
+  r.converged = 1;
+  r.rel_res_true = NAN;
+  const unsigned cb = (unsigned)std::min<int64_t>((g->n + 255) / 256, 4096);
+  fj_status worst = FJ_OK;
+  for (int c = 0; c < k; ++c) {
+    const double m = v[4 * c] / (double)g->n;
+    if (v[4 * c + 2] == v[4 * c + 3]) {   // s = c 1: z = s exactly (P:L129 Omega 1 = 1)
+      k_copy_cols<<<cb, 256, 0, st>>>(g->n, k, c, s, z);
+      FJ_CK_LAUNCH();
+      consensus_quantities(g, v[4 * c + 2], qout[c]);
+      r.rel_res_true = std::isnan(r.rel_res_true) ? 0.0 : r.rel_res_true;
+      continue;
+    }
+    fj_solve_opts oc = o;
+    int iters = 0, warm = 0, spent = 0;
+    double t[10];
+    for (int round = 0;; ++round) {
+      fj_solve_opts ob = oc;
+      ob.max_iter = std::max(0, o.max_iter - spent);
+      fj_status sc = solve_col(g, s, z, k, c, ob, warm, &r, st, &iters);   // Alg. 1 line 3
+      spent += iters;
+      if (sc != FJ_OK && sc != FJ_E_NO_CONVERGENCE) return sc;
+      FJ_TRY(quant_pass(g, w, s, z, k, c, m, t, st));                   // Alg. 1 lines 5-9
+      memset(&qout[c], 0, sizeof(fj_quantities_t));
+      fill_quantities(g, t, m, qout[c]);
+      if (sc != FJ_OK) { worst = sc; break; }
+      double emax = 0.0;
+      for (int j = 0; j < 6; ++j) emax = std::max(emax, qout[c].eps[j]);
+      if (o.eps_target <= 0.0 || emax <= o.eps_target || oc.rtol <= 1e-15 || spent >= o.max_iter) break;
+      oc.rtol = std::max(oc.rtol * 1e-2, 1e-15);   // tighten and continue from z (warm start)
+      warm = 1;
+    }
+    r.iterations = std::max(r.iterations, spent);
+  }
+  FJ_CK(cudaEventRecord(w->ev1, st));
+  FJ_CK(cudaEventSynchronize(w->ev1));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, w->ev0, w->ev1);
+  r.ms = ms;
+  if (worst != FJ_OK) r.converged = 0;
+  if (rep) *rep = r;
+  if (worst != FJ_OK) return fail(worst, "PCG did not reach rtol on the true residual");
+  return FJ_OK;
+}
+
+fj_status fj_approxim_host(int64_t n, int64_t m_in, const int32_t* u_h, const int32_t* v_h, const void* w_h,
+                           int wtype, int k, const double* s_h, double* z_h, const fj_solve_opts* opts,
+                           fj_quantities_t* q_h, fj_solve_report* rep, void* stream) {
+  if (n < 1 || m_in < 0 || !s_h || !q_h || (m_in > 0 && (!u_h || !v_h))) return fail(FJ_E_INVALID_ARG, "null argument");
+  if (k < 1 || k > MAXK) return fail(FJ_E_INVALID_ARG, "k must be in [1, 64]");
+  if (wtype < FJ_W_UNIT || wtype > FJ_W_F64) return fail(FJ_E_INVALID_ARG, "bad wtype");
+  const int wbytes = wtype == FJ_W_UNIT ? 0 : wtype == FJ_W_U8 ? 1 : wtype == FJ_W_F32 ? 4 : 8;
+  if (wbytes && m_in > 0 && !w_h) return fail(FJ_E_INVALID_ARG, "weights are NULL");
+  cudaStream_t st = S(stream);
+  DevBuf<int32_t> du, dv, dcol;
+  DevBuf<uint8_t> dw, dwo;
+  DevBuf<int64_t> drp;
+  DevBuf<double> ds, dz;
+  FJ_TRY(du.alloc(m_in, st)); FJ_TRY(dv.alloc(m_in, st));
+  FJ_TRY(ds.alloc(n * (int64_t)k, st)); FJ_TRY(dz.alloc(n * (int64_t)k, st));
+  FJ_TRY(drp.alloc(n + 1, st)); FJ_TRY(dcol.alloc(2 * m_in, st));
+  if (wbytes) { FJ_TRY(dw.alloc(m_in * wbytes, st)); FJ_TRY(dwo.alloc(2 * m_in * wbytes, st)); }
+  if (m_in > 0) {
+    FJ_CK(cudaMemcpyAsync(du.p, u_h, sizeof(int32_t) * m_in, cudaMemcpyHostToDevice, st));
+    FJ_CK(cudaMemcpyAsync(dv.p, v_h, sizeof(int32_t) * m_in, cudaMemcpyHostToDevice, st));
+    if (wbytes) FJ_CK(cudaMemcpyAsync(dw.p, w_h, (size_t)wbytes * m_in, cudaMemcpyHostToDevice, st));
+  }
+  FJ_CK(cudaMemcpyAsync(ds.p, s_h, sizeof(double) * n * k, cudaMemcpyHostToDevice, st));
+  int64_t nnz = 0;
+  FJ_TRY(fj_csr_from_edges(n, m_in, du.p, dv.p, wbytes ? dw.p : nullptr, wtype, drp.p, dcol.p,
+                           wbytes ? dwo.p : nullptr, &nnz, nullptr, nullptr, stream));
+  du.release(); dv.release(); dw.release();
+  fj_graph* g = nullptr;
+  FJ_TRY(fj_graph_create(n, nnz, drp.p, dcol.p, wbytes ? dwo.p : nullptr, wtype, 0, stream, &g));
+  fj_status s = fj_approxim(g, k, ds.p, dz.p, opts, q_h, rep, stream);
+  if ((s == FJ_OK || s == FJ_E_NO_CONVERGENCE) && z_h) {
+    cudaError_t e = cudaMemcpyAsync(z_h, dz.p, sizeof(double) * n * k, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) s = cuda_fail(e, "z readback", __FILE__, __LINE__);
+  }
+  fj_graph_destroy(g);
+  return s;
+}
+
+}  // extern "C"

@@ -1,0 +1,67 @@
+// workspace.cuh — stream-ordered device buffers and the few CUB calls used by setup code.
+#pragma once
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+
+namespace fj {
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  cudaStream_t st = nullptr;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  fj_status alloc(int64_t count, cudaStream_t s) {
+    st = s;
+    if (count <= 0) count = 1;
+    cudaError_t e = cudaMallocAsync(&p, sizeof(T) * (size_t)count, s);
+    if (e != cudaSuccess) { p = nullptr; return cuda_fail(e, "cudaMallocAsync", __FILE__, __LINE__); }
+    return FJ_OK;
+  }
+  void release() {
+    if (p) cudaFreeAsync(p, st);
+    p = nullptr;
+  }
+  ~DevBuf() { release(); }
+};
+
+// e[i] = sum_{j<i} c[j] for i in [0, count)
+inline fj_status cub_exclusive_sum(const int64_t* c, int64_t* e, int64_t count, cudaStream_t st) {
+  size_t bytes = 0;
+  FJ_CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, c, e, count, st));
+  DevBuf<uint8_t> tmp;
+  FJ_TRY(tmp.alloc((int64_t)bytes, st));
+  FJ_CK(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, c, e, count, st));
+  count_cub();
+  return FJ_OK;
+}
+
+inline fj_status cub_exclusive_sum_i32(const int32_t* c, int32_t* e, int64_t count, cudaStream_t st) {
+  size_t bytes = 0;
+  FJ_CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, c, e, count, st));
+  DevBuf<uint8_t> tmp;
+  FJ_TRY(tmp.alloc((int64_t)bytes, st));
+  FJ_CK(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, c, e, count, st));
+  count_cub();
+  return FJ_OK;
+}
+
+// out = { i in [0, count) : flags[i] != 0 } in increasing order; *num_out (device) = size.
+inline fj_status cub_select_index(const uint8_t* flags, int32_t* out, int32_t* num_out, int64_t count,
+                                  cudaStream_t st) {
+  cub::CountingInputIterator<int32_t> it(0);
+  size_t bytes = 0;
+  FJ_CK(cub::DeviceSelect::Flagged(nullptr, bytes, it, flags, out, num_out, (int)count, st));
+  DevBuf<uint8_t> tmp;
+  FJ_TRY(tmp.alloc((int64_t)bytes, st));
+  FJ_CK(cub::DeviceSelect::Flagged(tmp.p, bytes, it, flags, out, num_out, (int)count, st));
+  count_cub();
+  return FJ_OK;
+}
+
+void free_solve_ws(fj_graph* g);   // pcg.cu
+void free_quant_ws(fj_graph* g);   // quantities.cu
+
+}  // namespace fj

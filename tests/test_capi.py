@@ -1,0 +1,67 @@
+"""CPU checks of the boundary: libfj.so loads and exports every entry point include/fj.h declares
+(no compute calls: there is no GPU here)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_functions():
+    src = open(os.path.join(ROOT, "include", "fj.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(fj_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_header_declares_the_survey_boundary():
+    names = set(declared_functions())
+    for required in ["fj_csr_from_edges", "fj_graph_create", "fj_graph_info", "fj_graph_degrees", "fj_apply",
+                     "fj_solve", "fj_quantities", "fj_approxim", "fj_graph_destroy", "fj_status_str",
+                     "fj_last_error", "fj_opinion_stats", "fj_approxim_host"]:
+        assert required in names
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2101_08143_b200 import build as B
+    so = B.build()
+    lib = ctypes.CDLL(so)
+    missing = [f for f in declared_functions() if not hasattr(lib, f)]
+    assert not missing, missing
+    lib.fj_abi_version.restype = ctypes.c_int
+    assert lib.fj_abi_version() == 1
+    lib.fj_status_str.restype = ctypes.c_char_p
+    assert lib.fj_status_str(6) == b"FJ_E_NO_CONVERGENCE"
+
+
+def test_invalid_arguments_fail_without_gpu():
+    """Argument validation happens before any device call."""
+    import paper_2101_08143_b200 as fj
+    L = fj.lib()
+    h = ctypes.c_void_p()
+    st = L.fj_graph_create(0, 0, None, None, None, 0, 1, None, ctypes.byref(h))
+    assert st == 1 and not h.value
+    assert b"n must be" in L.fj_last_error()
+    assert L.fj_solve(None, 1, None, None, None, None, None) == 1
+
+
+def test_product_path_does_not_import_oracle():
+    pkg = os.path.join(ROOT, "paper_2101_08143_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                txt = open(os.path.join(dirpath, f)).read()
+                code = re.sub(r"#.*|//.*|/\*.*?\*/", "", txt, flags=re.S)
+                assert "oracle" not in code.lower(), f
+
+
+def test_missing_library_raises(tmp_path):
+    from paper_2101_08143_b200 import binding
+    with pytest.raises(ImportError):
+        binding._lib_backup = binding._lib
+        binding._lib = None
+        try:
+            binding.load_library(str(tmp_path / "nope.so"))
+        finally:
+            binding._lib = binding._lib_backup

@@ -1,0 +1,301 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same seeded inputs.
+
+Bars (BASELINE.json north_star): CSR and degrees bit-exact; relative residual <= 1e-10; each
+quantity within relative 1e-8 of the oracle.  Operator parity is checked against the oracle's
+(I+L)x within a rounding bound derived from the row sums."""
+import numpy as np
+import pytest
+
+import oracle as O
+import synth
+
+pytestmark = pytest.mark.gpu
+
+QKEYS = ["CI", "D", "P", "C", "Idc", "PDI"]
+
+
+@pytest.fixture(scope="module")
+def fj():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2101_08143_b200 as m
+    from paper_2101_08143_b200 import build as B
+    B.build()
+    return m
+
+
+def dev(a):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def host(t):
+    return t.cpu().numpy()
+
+
+def gpu_csr(fj, n, u, v, w=None):
+    rp, col, wo, stats = fj.csr_from_edges(n, dev(u.astype(np.int32)), dev(v.astype(np.int32)),
+                                           None if w is None else dev(w))
+    return rp, col, wo, stats
+
+
+def assert_csr_equal(fj, n, u, v, w=None):
+    g = O.canonical_csr(n, u, v, w)
+    rp, col, wo, stats = gpu_csr(fj, n, u, v, w)
+    assert np.array_equal(host(rp), g.row_ptr)
+    assert np.array_equal(host(col), g.col)
+    if w is not None:
+        assert np.array_equal(host(wo), g.w)
+    assert stats["selfloops"] == g.selfloops and stats["duplicates"] == g.duplicates
+    return g, (rp, col, wo)
+
+
+# ---------------------------------------------------------------- a1 / a2: bit-exact
+@pytest.mark.parametrize("seed", range(6))
+@pytest.mark.parametrize("wkind", ["unit", "u8", "f64"])
+def test_csr_bit_exact_random(fj, seed, wkind):
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(1, 3000))
+    m = int(rng.integers(0, 20000))
+    u = rng.integers(0, n, m).astype(np.int32)
+    v = rng.integers(0, n, m).astype(np.int32)
+    w = None if wkind == "unit" else (rng.integers(1, 6, m).astype(np.uint8) if wkind == "u8"
+                                      else rng.uniform(0.1, 4.0, m))
+    g, (rp, col, wo) = assert_csr_equal(fj, n, u, v, w)
+    G = fj.Graph(n, rp, col, wo, validate=True)
+    assert np.array_equal(host(G.degrees()), O.degrees(g))   # bit-exact, ascending-column sums
+    info = G.info()
+    assert info["nnz"] == g.nnz and info["n_isolated"] == int((np.diff(g.row_ptr) == 0).sum())
+
+
+def test_csr_edge_cases(fj):
+    assert_csr_equal(fj, 1, np.zeros(0, np.int32), np.zeros(0, np.int32))
+    assert_csr_equal(fj, 5, np.array([1, 2, 3], np.int32), np.array([1, 2, 3], np.int32))     # all self-loops
+    assert_csr_equal(fj, 4, np.array([0, 1, 0, 1], np.int32), np.array([1, 0, 1, 0], np.int32))  # duplicates
+    with pytest.raises(fj.FJError):
+        gpu_csr(fj, 4, np.array([0], np.int32), np.array([4], np.int32))
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3"])
+def test_csr_bit_exact_configs(fj, name):
+    wl = synth.make_config(name, k=1, kinds=["uniform"])
+    assert_csr_equal(fj, wl.n, wl.u, wl.v, wl.w)
+
+
+def test_csr_c4_scale16_bit_exact_and_full_size_sampled(fj):
+    wl = synth.make_config("c4", scale=16, k=1)
+    assert_csr_equal(fj, wl.n, wl.u, wl.v, wl.w)
+    big = synth.make_config("c4", k=1)                           # full scale 22, 67M raw edges
+    rp, col, wo, stats = gpu_csr(fj, big.n, big.u, big.v, big.w)
+    rp_h = host(rp)
+    rng = np.random.default_rng(0)
+    deg = np.diff(rp_h)
+    rows = list(rng.integers(0, big.n, 40)) + list(np.argsort(deg)[-5:]) + [0, big.n - 1]
+    want = O.csr_rows_from_edges(big.n, big.u, big.v, rows, big.w)
+    for i, (c_ref, w_ref) in want.items():
+        a, b = rp_h[i], rp_h[i + 1]
+        assert np.array_equal(host(col[a:b]), c_ref)
+        assert np.array_equal(host(wo[a:b]), w_ref)
+
+
+# ---------------------------------------------------------------- operator
+def hub_graph(rng, n, hubs, hub_deg, extra):
+    u = [rng.integers(0, n, extra)]
+    v = [rng.integers(0, n, extra)]
+    for h in range(hubs):
+        u.append(np.full(hub_deg, h))
+        v.append(rng.choice(n, hub_deg, replace=False))
+    return np.concatenate(u).astype(np.int32), np.concatenate(v).astype(np.int32)
+
+
+@pytest.mark.parametrize("wkind", ["unit", "u8", "f64"])
+@pytest.mark.parametrize("op", [0, 1])
+def test_apply_matches_oracle(fj, wkind, op):
+    rng = np.random.default_rng(7)
+    n = 40000
+    u, v = hub_graph(rng, n, hubs=3, hub_deg=20000, extra=150000)   # long rows -> multi-chunk path
+    m = len(u)
+    w = None if wkind == "unit" else (rng.integers(1, 6, m).astype(np.uint8) if wkind == "u8"
+                                      else rng.uniform(0.1, 4.0, m))
+    g, (rp, col, wo) = assert_csr_equal(fj, n, u, v, w)
+    G = fj.Graph(n, rp, col, wo)
+    assert G.info()["n_long_rows"] >= 3
+    X = rng.normal(size=(n, 3))
+    Y = host(G.apply(dev(X), op=op))
+    for c in range(3):
+        x = X[:, c]
+        ref = O.ipl_apply(g, x) - (x if op == 0 else 0.0)
+        d = O.degrees(g)
+        # rounding bound of a row sum: (len + 2) u ((1+d)|x_i| + sum_j w_ij |x_j|)
+        scale = (1 + d) * np.abs(x) + np.bincount(g.rows(), weights=g.wf() * np.abs(x[g.col]), minlength=n)
+        err = np.abs(Y[:, c] - ref)
+        assert np.all(err <= 2 * (np.diff(g.row_ptr) + 2) * 2.0 ** -53 * scale), c
+
+
+# ---------------------------------------------------------------- solve + quantities: pins
+def solve_quant(fj, n, u, v, w, S, **kw):
+    rp, col, wo, _ = gpu_csr(fj, n, np.asarray(u), np.asarray(v), w)
+    G = fj.Graph(n, rp, col, wo, validate=True)
+    z, q, rep = G.approxim(dev(S), opts=fj.SolveOpts.make(**kw))
+    return G, host(z), q, rep
+
+
+def test_p5_and_path2_golden(fj):
+    from conftest import read_golden
+    from fractions import Fraction
+    gold = {r[0]: Fraction(int(r[1]), int(r[2])) for r in read_golden("p5_e1_quantities.txt")}
+    u = np.arange(4); v = u + 1
+    _, z, q, rep = solve_quant(fj, 5, u, v, None, np.eye(5)[0], rtol=1e-14)
+    assert np.allclose(z * 55, [34, 13, 5, 2, 1], rtol=1e-12)
+    for k in QKEYS:
+        assert q[0][k] == pytest.approx(float(gold[k]), rel=1e-10), k
+    gold2 = {r[0]: Fraction(int(r[1]), int(r[2])) for r in read_golden("path2_quantities.txt")}
+    _, z, q, _ = solve_quant(fj, 2, [0], [1], None, np.array([1.0, 0.0]), rtol=1e-14)
+    for k in QKEYS:
+        assert q[0][k] == pytest.approx(float(gold2[k]), rel=1e-10), k
+
+
+@pytest.mark.parametrize("n", [300, 3000])
+def test_complete_graph_closed_form(fj, n):
+    iu, ju = np.triu_indices(n, 1)
+    s = np.random.default_rng(n).uniform(0, 1, n)
+    _, z, q, rep = solve_quant(fj, n, iu, ju, None, s)
+    m = s.mean(); S = ((s - m) ** 2).sum()
+    assert np.allclose(z, (s + n * m) / (n + 1), rtol=1e-9)
+    for k, ref in [("P", S / (n + 1) ** 2), ("D", n * S / (n + 1) ** 2), ("CI", n * n * S / (n + 1) ** 2),
+                   ("C", S / (n + 1) ** 2 + n * m * m), ("PDI", S / (n + 1))]:
+        assert q[0][k] == pytest.approx(ref, rel=1e-8), k
+
+
+def test_star_hub_closed_form(fj):
+    n = 200_000   # hub row of 199,999 nonzeros: 49 long-row chunks
+    s = np.random.default_rng(3).uniform(0, 1, n)
+    G, z, q, rep = solve_quant(fj, n, np.zeros(n - 1, np.int32), np.arange(1, n, dtype=np.int32), None, s)
+    assert G.info()["n_long_chunks"] == (n - 1 + 4095) // 4096
+    z0 = (2 * s[0] + s[1:].sum()) / (n + 1)
+    zc = np.concatenate([[z0], (s[1:] + z0) / 2])
+    assert np.allclose(z, zc, rtol=1e-9, atol=0)
+    qo = O.quantities(O.canonical_csr(n, np.zeros(n - 1), np.arange(1, n)), s, zc)
+    for k in QKEYS:
+        assert q[0][k] == pytest.approx(qo[k], rel=1e-8), k
+
+
+def test_consensus_zero_and_isolated(fj):
+    rng = np.random.default_rng(11)
+    u = rng.integers(0, 1000, 4000); v = rng.integers(0, 1000, 4000)
+    _, z, q, rep = solve_quant(fj, 1200, u, v, None, np.full(1200, 0.3))   # 200 isolated vertices too
+    assert np.array_equal(z, np.full(1200, 0.3)) and q[0]["consensus"] == 1
+    assert q[0]["C"] == pytest.approx(1200 * 0.09, rel=1e-15) and q[0]["D"] == 0 and q[0]["P"] == 0
+    _, z, q, rep = solve_quant(fj, 1200, u, v, None, np.zeros(1200))
+    assert not z.any() and q[0]["C"] == 0
+    s = rng.uniform(0, 1, 1200)
+    _, z, q, rep = solve_quant(fj, 1200, u, v, None, s)
+    iso = np.setdiff1d(np.arange(1200), np.concatenate([u, v]))
+    assert np.allclose(z[iso], s[iso], rtol=1e-12)
+
+
+# ---------------------------------------------------------------- solve + quantities: configs
+def check_against_oracle(q, qo, S_col, z, zo, cert=True):
+    for k in QKEYS:
+        rel = abs(q[k] - qo[k]) / abs(qo[k])
+        assert rel <= 1e-8, (k, rel)
+        if cert:
+            assert rel <= q["eps"][k] * (1 + 1e-9) + 1e-15, (k, rel, q["eps"][k])   # certificate holds
+    assert q["res_norm"] <= 1e-10 * q["s_norm"] * (1 + 1e-9)
+
+
+def test_c1_vs_dense_oracle(fj):
+    wl = synth.make_config("c1")
+    g = O.canonical_csr(wl.n, wl.u, wl.v)
+    zo = O.solve_dense(g, wl.S[:, 0])
+    qo = O.quantities(g, wl.S[:, 0], zo)
+    _, z, q, rep = solve_quant(fj, wl.n, wl.u, wl.v, None, wl.S[:, 0])
+    assert rep["converged"] == 1 and rep["rel_res_true"] <= 1e-10
+    check_against_oracle(q[0], qo, wl.S[:, 0], z, zo)
+    assert np.max(np.abs(z - zo)) < 1e-9
+
+
+@pytest.mark.parametrize("name", ["c2", "c3"])
+def test_full_config_vs_pcg_oracle(fj, name):
+    wl = synth.make_config(name)
+    g = O.canonical_csr(wl.n, wl.u, wl.v)
+    _, Z, Q, rep = solve_quant(fj, wl.n, wl.u, wl.v, None, wl.S)
+    assert rep["converged"] == 1 and rep["rel_res_true"] <= 1e-10
+    for c in range(wl.k):
+        zo, info = O.solve_pcg(g, wl.S[:, c], tol=1e-13)
+        assert info["converged"]
+        qo = O.quantities(g, wl.S[:, c], zo)
+        check_against_oracle(Q[c], qo, wl.S[:, c], Z[:, c], zo)
+
+
+def test_c4_small_weighted_batch(fj):
+    wl = synth.make_config("c4", scale=14, k=3)
+    g = O.canonical_csr(wl.n, wl.u, wl.v, wl.w)
+    _, Z, Q, rep = solve_quant(fj, wl.n, wl.u, wl.v, wl.w, wl.S)
+    for c in range(3):
+        zo, _ = O.solve_pcg(g, wl.S[:, c], tol=1e-13)
+        check_against_oracle(Q[c], O.quantities(g, wl.S[:, c], zo), wl.S[:, c], Z[:, c], zo)
+
+
+# ---------------------------------------------------------------- behaviour
+def test_determinism_and_graph_mode(fj):
+    wl = synth.make_config("c2", n=200_000)
+    rp, col, wo, _ = gpu_csr(fj, wl.n, wl.u, wl.v)
+    G = fj.Graph(wl.n, rp, col, wo)
+    s = dev(wl.S[:, 0])
+    z1, q1, r1 = G.approxim(s)
+    z2, q2, r2 = G.approxim(s)
+    z3, q3, r3 = G.approxim(s, opts=fj.SolveOpts.make(use_cuda_graph=False))
+    assert np.array_equal(host(z1), host(z2)) and np.array_equal(host(z1), host(z3))
+    assert q1[0]["D"] == q2[0]["D"] == q3[0]["D"] and r1["iterations"] == r3["iterations"]
+
+
+def test_solve_and_quantities_entry_points(fj):
+    wl = synth.make_config("c1", k=2)
+    rp, col, wo, _ = gpu_csr(fj, wl.n, wl.u, wl.v)
+    G = fj.Graph(wl.n, rp, col, wo)
+    S = dev(wl.S)
+    z, rep = G.solve(S)
+    assert rep["converged"] == 1 and rep["rel_res_true"] <= 1e-10
+    q = G.quantities(S, z)
+    _, qa, _ = G.approxim(S)
+    for c in range(2):
+        for k in QKEYS:
+            assert q[c][k] == pytest.approx(qa[c][k], rel=1e-9)
+    st = G.opinion_stats(S)
+    assert st[0][0] == pytest.approx(wl.S[:, 0].sum(), rel=1e-13) and st[1][3] == wl.S[:, 1].max()
+    with pytest.raises(fj.FJError):
+        G.approxim(dev(np.full(wl.n, np.nan)))
+
+
+def test_eps_target_tightens(fj):
+    wl = synth.make_config("c1")
+    rp, col, wo, _ = gpu_csr(fj, wl.n, wl.u, wl.v)
+    G = fj.Graph(wl.n, rp, col, wo)
+    _, q, rep = G.approxim(dev(wl.S[:, 0]), opts=fj.SolveOpts.make(rtol=1e-4, eps_target=1e-9))
+    assert max(q[0]["eps"].values()) <= 1e-9
+
+
+def test_validation_errors(fj):
+    import torch
+    rp = dev(np.array([0, 1, 1], np.int64)); col = dev(np.array([1], np.int32))
+    with pytest.raises(fj.FJError) as e:
+        fj.Graph(2, rp, col)                                  # (0,1) without (1,0)
+    assert e.value.status == 3
+    rp = dev(np.array([0, 1, 2], np.int64)); col = dev(np.array([0, 1], np.int32))
+    with pytest.raises(fj.FJError) as e:
+        fj.Graph(2, rp, col)                                  # self-loops
+    assert e.value.status == 2
+    rp = dev(np.array([0, 1, 2], np.int64)); col = dev(np.array([1, 0], np.int32))
+    with pytest.raises(fj.FJError) as e:
+        fj.Graph(2, rp, col, dev(np.array([-1.0, -1.0])))     # bad weight
+    assert e.value.status == 4
+
+
+def test_e2e_host_matches_device(fj):
+    wl = synth.make_config("c4", scale=12, k=2)
+    z_h, q_h, rep_h = fj.approxim_host(wl.n, wl.u, wl.v, wl.w, wl.S, want_z=True)
+    _, z_d, q_d, rep_d = solve_quant(fj, wl.n, wl.u, wl.v, wl.w, wl.S)
+    assert np.array_equal(z_h, z_d)
+    assert q_h[1]["D"] == q_d[1]["D"]
