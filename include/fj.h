@@ -58,7 +58,7 @@ typedef struct {
   int64_t deg_max;          /* largest row length                                            */
   double w_min, w_max;      /* extremal edge weights; 0 if nnz == 0                  */
   double d_max;             /* largest weighted degree                                       */
-  int64_t n_tiles, n_long_rows, n_long_chunks;  /* SpMV schedule       */
+  int64_t n_tiles, n_wrows, n_long_rows, n_long_chunks;  /* row-engine items    */
   int32_t wtype, reserved;
 } fj_graph_info_t;
 

@@ -17,7 +17,7 @@ _i64, _i32, _dbl, _vp = ctypes.c_int64, ctypes.c_int32, ctypes.c_double, ctypes.
 
 class GraphInfo(ctypes.Structure):
     _fields_ = [("n", _i64), ("nnz", _i64), ("m", _i64), ("n_isolated", _i64), ("deg_max", _i64),
-                ("w_min", _dbl), ("w_max", _dbl), ("d_max", _dbl), ("n_tiles", _i64),
+                ("w_min", _dbl), ("w_max", _dbl), ("d_max", _dbl), ("n_tiles", _i64), ("n_wrows", _i64),
                 ("n_long_rows", _i64), ("n_long_chunks", _i64), ("wtype", _i32), ("reserved", _i32)]
 
 

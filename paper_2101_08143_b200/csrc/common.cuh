@@ -39,13 +39,6 @@ extern thread_local bool g_capturing;
   } while (0)
 
 // ---------------------------------------------------------------- constants
-constexpr int TPB = 256;            // threads per block for the tile kernels
-constexpr int TILE_UNITS = 1024;    // merge-path units per tile: 4 per row + 1 per nonzero
-constexpr int ROW_COST = 4;         // -> at most 256 rows per tile (one thread per row)
-constexpr int LONG_ROW = 1024;      // rows with more nonzeros are processed in chunks
-constexpr int LONG_CHUNK = 4096;    // nonzeros per long-row chunk (16 per thread)
-constexpr int TILE_MAX_NNZ = TILE_UNITS + LONG_ROW;   // 2048
-constexpr int TILE_MAX_ROWS = TILE_UNITS / ROW_COST;  // 256
 constexpr int MAXK = 64;
 
 // ---------------------------------------------------------------- device workspace per solve
@@ -65,14 +58,11 @@ struct fj_graph {
   // derived (owned)
   double* deg = nullptr;        // weighted degree d_i            [n]
   double* dinv = nullptr;       // 1 / (1 + d_i)                  [n]
-  // schedule (owned): items [0, n_long_chunks) are long-row chunks, then n_tiles tiles
-  int64_t n_tiles = 0, n_long = 0, n_long_chunks = 0;
-  int32_t* tile_begin = nullptr;  // [n_tiles]
-  int32_t* tile_end = nullptr;    // [n_tiles]
-  int32_t* long_row = nullptr;    // [n_long]
-  int32_t* chunk_row = nullptr;   // [n_long_chunks] index into long_row
-  int32_t* chunk_idx = nullptr;   // [n_long_chunks] chunk index within its row
+  // schedule (owned): items [0, n_long_chunks) are long-row chunks, then W rows, then T tiles
+  int64_t n_items = 0, n_tiles = 0, n_wrows = 0, n_long = 0, n_long_chunks = 0;
+  void* items = nullptr;          // ItemMeta [n_items] (tiles.cuh)
   int32_t* long_nchunks = nullptr;// [n_long]
+  int32_t* long_item0 = nullptr;  // [n_long]
   fj_graph_info_t info{};
   int num_sms = 148;
   // caches

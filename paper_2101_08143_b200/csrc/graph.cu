@@ -129,139 +129,9 @@ __global__ void k_check_rowptr(int64_t n, int64_t nnz, const int64_t* rp, GStats
   if (bad) atomicOr(&st->bad_flags, 1u);
 }
 
-// ---------------------------------------------------------------- schedule kernels
-__global__ void k_units(int64_t n, const int64_t* __restrict__ rp, int64_t* __restrict__ c) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i > n) return;
-  if (i == n) { c[i] = 0; return; }
-  const int64_t len = rp[i + 1] - rp[i];
-  c[i] = len > LONG_ROW ? 0 : ROW_COST + len;
-}
-
-__device__ __forceinline__ bool is_long(const int64_t* rp, int64_t i) { return rp[i + 1] - rp[i] > LONG_ROW; }
-
-// boundary flags over i in [0, n]
-__global__ void k_bflags(int64_t n, const int64_t* __restrict__ rp, const int64_t* __restrict__ e,
-                         uint8_t* __restrict__ f) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i > n) return;
-  bool b = (i == 0) || (i == n);
-  if (!b) {
-    b = is_long(rp, i) || is_long(rp, i - 1) || (e[i] / TILE_UNITS != e[i - 1] / TILE_UNITS);
-  }
-  f[i] = b ? 1 : 0;
-}
-
-// per segment j (begin B[j], end B[j+1]): flag tile vs long
-__global__ void k_segflags(int64_t nseg, const int32_t* __restrict__ B, const int64_t* __restrict__ rp,
-                           uint8_t* __restrict__ ft, uint8_t* __restrict__ fl) {
-  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (j >= nseg) return;
-  const bool l = is_long(rp, B[j]);
-  ft[j] = l ? 0 : 1;
-  fl[j] = l ? 1 : 0;
-}
-
-__global__ void k_tiles_from_segs(int64_t nt, const int32_t* __restrict__ segs, const int32_t* __restrict__ B,
-                                  int32_t* __restrict__ tb, int32_t* __restrict__ te) {
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= nt) return;
-  const int32_t j = segs[t];
-  tb[t] = B[j];
-  te[t] = B[j + 1];
-}
-
-__global__ void k_long_from_segs(int64_t nl, const int32_t* __restrict__ segs, const int32_t* __restrict__ B,
-                                 const int64_t* __restrict__ rp, int32_t* __restrict__ lrow,
-                                 int32_t* __restrict__ lnch) {
-  const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (l >= nl) return;
-  const int32_t i = B[segs[l]];
-  lrow[l] = i;
-  const int64_t len = rp[i + 1] - rp[i];
-  lnch[l] = (int32_t)((len + LONG_CHUNK - 1) / LONG_CHUNK);
-}
-
-__global__ void k_chunks(int64_t nl, const int32_t* __restrict__ lnch, const int32_t* __restrict__ cstart,
-                         int32_t* __restrict__ crow, int32_t* __restrict__ cidx) {
-  const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (l >= nl) return;
-  const int32_t s = cstart[l];
-  for (int32_t c = 0; c < lnch[l]; ++c) { crow[s + c] = (int32_t)l; cidx[s + c] = c; }
-}
-
 static inline double bits2d(unsigned long long b) { double d; memcpy(&d, &b, sizeof d); return d; }
-
 static inline unsigned nblk(int64_t n, int t = 256) { return (unsigned)((n + t - 1) / t); }
-
-static fj_status build_schedule(fj_graph* g, cudaStream_t st) {
-  const int64_t n = g->n;
-  DevBuf<int64_t> c, e;
-  DevBuf<uint8_t> f;
-  DevBuf<int32_t> B, nsel;
-  FJ_TRY(c.alloc(n + 1, st));
-  FJ_TRY(e.alloc(n + 1, st));
-  FJ_TRY(f.alloc(n + 1, st));
-  FJ_TRY(B.alloc(n + 1, st));
-  FJ_TRY(nsel.alloc(1, st));
-  k_units<<<nblk(n + 1), 256, 0, st>>>(n, g->row_ptr, c.p);
-  FJ_CK_LAUNCH();
-  FJ_TRY(cub_exclusive_sum(c.p, e.p, n + 1, st));
-  k_bflags<<<nblk(n + 1), 256, 0, st>>>(n, g->row_ptr, e.p, f.p);
-  FJ_CK_LAUNCH();
-  FJ_TRY(cub_select_index(f.p, B.p, nsel.p, n + 1, st));
-  int32_t nb = 0;
-  FJ_CK(cudaMemcpyAsync(&nb, nsel.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-  FJ_CK(cudaStreamSynchronize(st));
-  const int64_t nseg = nb - 1;
-  int32_t nt = 0, nl = 0;
-  if (nseg > 0) {
-    DevBuf<uint8_t> ft, fl;
-    DevBuf<int32_t> segt, segl, ns2;
-    FJ_TRY(ft.alloc(nseg, st));
-    FJ_TRY(fl.alloc(nseg, st));
-    FJ_TRY(segt.alloc(nseg, st));
-    FJ_TRY(segl.alloc(nseg, st));
-    FJ_TRY(ns2.alloc(2, st));
-    k_segflags<<<nblk(nseg), 256, 0, st>>>(nseg, B.p, g->row_ptr, ft.p, fl.p);
-    FJ_CK_LAUNCH();
-    FJ_TRY(cub_select_index(ft.p, segt.p, ns2.p, nseg, st));
-    FJ_TRY(cub_select_index(fl.p, segl.p, ns2.p + 1, nseg, st));
-    int32_t cnt[2];
-    FJ_CK(cudaMemcpyAsync(cnt, ns2.p, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    FJ_CK(cudaStreamSynchronize(st));
-    nt = cnt[0];
-    nl = cnt[1];
-    if (nt > 0) {
-      FJ_CK(cudaMallocAsync(&g->tile_begin, sizeof(int32_t) * nt, st));
-      FJ_CK(cudaMallocAsync(&g->tile_end, sizeof(int32_t) * nt, st));
-      k_tiles_from_segs<<<nblk(nt), 256, 0, st>>>(nt, segt.p, B.p, g->tile_begin, g->tile_end);
-      FJ_CK_LAUNCH();
-    }
-    if (nl > 0) {
-      FJ_CK(cudaMallocAsync(&g->long_row, sizeof(int32_t) * nl, st));
-      FJ_CK(cudaMallocAsync(&g->long_nchunks, sizeof(int32_t) * nl, st));
-      k_long_from_segs<<<nblk(nl), 256, 0, st>>>(nl, segl.p, B.p, g->row_ptr, g->long_row, g->long_nchunks);
-      FJ_CK_LAUNCH();
-      DevBuf<int32_t> cs;
-      FJ_TRY(cs.alloc(nl + 1, st));
-      FJ_TRY(cub_exclusive_sum_i32(g->long_nchunks, cs.p, nl, st));
-      int32_t last_start = 0, last_n = 0;
-      FJ_CK(cudaMemcpyAsync(&last_start, cs.p + nl - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-      FJ_CK(cudaMemcpyAsync(&last_n, g->long_nchunks + nl - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-      FJ_CK(cudaStreamSynchronize(st));
-      const int64_t nch = (int64_t)last_start + last_n;
-      FJ_CK(cudaMallocAsync(&g->chunk_row, sizeof(int32_t) * nch, st));
-      FJ_CK(cudaMallocAsync(&g->chunk_idx, sizeof(int32_t) * nch, st));
-      k_chunks<<<nblk(nl), 256, 0, st>>>(nl, g->long_nchunks, cs.p, g->chunk_row, g->chunk_idx);
-      FJ_CK_LAUNCH();
-      g->n_long_chunks = nch;
-    }
-  }
-  g->n_tiles = nt;
-  g->n_long = nl;
-  return FJ_OK;
-}
+fj_status build_schedule(fj_graph* g, cudaStream_t st);   // schedule.cu
 
 template <int WT>
 static fj_status launch_degree(fj_graph* g, GStats* st_d, int validate, cudaStream_t st) {
@@ -378,7 +248,7 @@ fj_status fj_graph_create(int64_t n, int64_t nnz, const int64_t* row_ptr, const 
   I.d_max = bits2d(h.dmax_bits);
   I.w_min = nnz ? bits2d(h.wmin_bits) : 0.0;
   I.w_max = nnz ? bits2d(h.wmax_bits) : 0.0;
-  I.n_tiles = g->n_tiles; I.n_long_rows = g->n_long; I.n_long_chunks = g->n_long_chunks;
+  I.n_tiles = g->n_tiles; I.n_wrows = g->n_wrows; I.n_long_rows = g->n_long; I.n_long_chunks = g->n_long_chunks;
   I.wtype = wtype;
   ce = cudaStreamSynchronize(st);
   if (ce != cudaSuccess) return cleanup(cuda_fail(ce, "graph create", __FILE__, __LINE__));
@@ -404,9 +274,7 @@ fj_status fj_graph_destroy(fj_graph* g) {
   free_solve_ws(g);
   free_quant_ws(g);
   cudaFree(g->deg); cudaFree(g->dinv);
-  cudaFree(g->tile_begin); cudaFree(g->tile_end);
-  cudaFree(g->long_row); cudaFree(g->long_nchunks);
-  cudaFree(g->chunk_row); cudaFree(g->chunk_idx);
+  cudaFree(g->items); cudaFree(g->long_nchunks); cudaFree(g->long_item0);
   delete g;
   return FJ_OK;
 }

@@ -33,13 +33,13 @@ struct ApplyOp {
   double* dot_out;                  // optional: x^T y
   __device__ __forceinline__ bool skip() const { return sc && *(volatile int32_t*)&sc->done; }
   __device__ __forceinline__ double gather(int32_t j) const { return __ldg(x + (int64_t)j * ld + c); }
-  __device__ __forceinline__ double row_value(int64_t) const { return 0.0; }
+  __device__ __forceinline__ double row_value(int64_t i) const { return __ldg(x + i * ld + c); }
   __device__ __forceinline__ void add(double (&a)[NA], double w, double xj, double) const {
     if (WT == FJ_W_UNIT) a[0] += xj; else a[0] = fma(w, xj, a[0]);
   }
-  __device__ __forceinline__ void finish_row(int64_t i, int64_t len, const double (&a)[NA], double (&part)[NP]) const {
+  __device__ __forceinline__ void finish_row(int64_t i, int64_t len, double xi, const double (&a)[NA],
+                                             double (&part)[NP]) const {
     const double d = (WT == FJ_W_UNIT) ? (double)len : deg[i];
-    const double xi = x[i * ld + c];
     const double yi = opL ? fma(d, xi, -a[0]) : fma(1.0 + d, xi, -a[0]);
     y[i * ld + c] = yi;
     part[0] = fma(xi, yi, part[0]);
@@ -71,13 +71,13 @@ struct ResidOp {
   double* res2_out;
   __device__ __forceinline__ bool skip() const { return false; }
   __device__ __forceinline__ double gather(int32_t j) const { return __ldg(z + j); }
-  __device__ __forceinline__ double row_value(int64_t) const { return 0.0; }
+  __device__ __forceinline__ double row_value(int64_t i) const { return __ldg(z + i); }
   __device__ __forceinline__ void add(double (&a)[NA], double w, double xj, double) const {
     if (WT == FJ_W_UNIT) a[0] += xj; else a[0] = fma(w, xj, a[0]);
   }
-  __device__ __forceinline__ void finish_row(int64_t i, int64_t len, const double (&a)[NA], double (&part)[NP]) const {
+  __device__ __forceinline__ void finish_row(int64_t i, int64_t len, double zi, const double (&a)[NA],
+                                             double (&part)[NP]) const {
     const double d = (WT == FJ_W_UNIT) ? (double)len : deg[i];
-    const double zi = z[i];
     const double r = s[i * ld + c] - fma(1.0 + d, zi, -a[0]);
     part[0] = fma(r, r, part[0]);
   }
@@ -102,16 +102,17 @@ struct QuantOp {
   double* out;   // [NP]
   __device__ __forceinline__ bool skip() const { return false; }
   __device__ __forceinline__ double gather(int32_t j) const { return __ldg(z + (int64_t)j * ld + c); }
-  __device__ __forceinline__ double row_value(int64_t i) const { return z[i * ld + c]; }
+  __device__ __forceinline__ double row_value(int64_t i) const { return __ldg(z + i * ld + c); }
   __device__ __forceinline__ void add(double (&a)[NA], double w, double zj, double zi) const {
     const double df = zi - zj;
     a[0] = fma(w, zj, a[0]);
     a[1] = fma(w * df, df, a[1]);
     a[2] = fma(w, fabs(zj), a[2]);
   }
-  __device__ __forceinline__ void finish_row(int64_t i, int64_t len, const double (&a)[NA], double (&part)[NP]) const {
+  __device__ __forceinline__ void finish_row(int64_t i, int64_t len, double zi, const double (&a)[NA],
+                                             double (&part)[NP]) const {
     const double d = (WT == FJ_W_UNIT) ? (double)len : deg[i];
-    const double zi = z[i * ld + c], si = s[i * ld + c];
+    const double si = s[i * ld + c];
     const double t = fma(1.0 + d, zi, -a[0]);
     const double lz = fma(d, zi, -a[0]);
     const double r = si - t;
@@ -137,7 +138,7 @@ struct QuantOp {
 // Per-graph workspace shared by the solver and the quantities pass (stream-ordered use only).
 struct SolveWs {
   int64_t n = 0;
-  int grid_tile = 0, grid_elem = 0;
+  int grid_max = 0, grid_elem = 0;
   double *r = nullptr, *p = nullptr, *q = nullptr, *x = nullptr, *col_s = nullptr;
   PcgScalars* sc = nullptr;
   double* elem_part = nullptr;       // [grid_elem][4]
@@ -154,7 +155,22 @@ struct SolveWs {
 
 fj_status get_ws(fj_graph* g, cudaStream_t st, SolveWs** out);
 
-template <class Op>
-inline fj_status launch_tiles(const fj_graph* g, const SolveWs* ws, const Op& op, cudaStream_t st);
+// Launch the warp-item engine for one operator.  The grid is fixed per (graph, operator):
+// #SMs x occupancy of this instantiation, capped by the item count -> deterministic partials.
+template <int WT, class Op>
+inline cudaError_t launch_warp_items(const fj_graph* g, const SolveWs* ws, const Op& op, cudaStream_t st) {
+  static int occ = 0;   // per template instantiation
+  if (occ == 0) {
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, warp_kernel<WT, Op>, WTPB, 0);
+    if (e != cudaSuccess) return e;
+    if (occ < 1) occ = 1;
+  }
+  int64_t grid = (int64_t)g->num_sms * occ;
+  const int64_t need = (g->n_items + WPB - 1) / WPB;
+  if (grid > need) grid = need > 0 ? need : 1;
+  if (grid > ws->grid_max) grid = ws->grid_max;
+  warp_kernel<WT, Op><<<(unsigned)grid, WTPB, 0, st>>>(make_sched(g), op, ws->ts);
+  return cudaGetLastError();
+}
 
 }  // namespace fj

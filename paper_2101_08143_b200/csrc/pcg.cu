@@ -20,7 +20,7 @@ constexpr int ETPB = 256;
 
 template <int WT, class Op>
 inline fj_status launch_tiles_wt(const fj_graph* g, const SolveWs* ws, const Op& op, cudaStream_t st) {
-  tile_kernel<WT, Op><<<ws->grid_tile, TPB, 0, st>>>(make_sched(g), op, ws->ts);
+  FJ_CK(launch_warp_items<WT>(g, ws, op, st));
   FJ_CK_LAUNCH();
   return FJ_OK;
 }
@@ -57,14 +57,7 @@ fj_status get_ws(fj_graph* g, cudaStream_t st, SolveWs** out) {
   SolveWs* w = new SolveWs();
   g->solve_ws = w;
   w->n = g->n;
-  int occ = 0;
-  // all tile kernels share the same launch shape; occupancy of the largest instantiation
-  FJ_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tile_kernel<FJ_W_F64, QuantOp<FJ_W_F64>>, TPB, 0));
-  if (occ < 1) occ = 1;
-  const int64_t items = g->n_long_chunks + g->n_tiles;
-  int64_t gt = (int64_t)g->num_sms * occ;
-  if (gt > items) gt = items > 0 ? items : 1;
-  w->grid_tile = (int)gt;
+  w->grid_max = g->num_sms * (2048 / WTPB);   // upper bound of any warp-engine grid
   int64_t ge = (int64_t)g->num_sms * (2048 / ETPB);
   const int64_t need = (g->n + ETPB - 1) / ETPB;
   if (ge > need) ge = need > 0 ? need : 1;
@@ -78,7 +71,7 @@ fj_status get_ws(fj_graph* g, cudaStream_t st, SolveWs** out) {
   FJ_TRY(dalloc(&w->elem_part, (int64_t)w->grid_elem * 4, st));
   FJ_TRY(dalloc(&w->elem_ticket, 1, st, true));
   constexpr int NPMAX = 16, NAMAX = 4;
-  FJ_TRY(dalloc(&w->ts.block_part, (int64_t)w->grid_tile * NPMAX, st));
+  FJ_TRY(dalloc(&w->ts.block_part, (int64_t)w->grid_max * NPMAX, st));
   FJ_TRY(dalloc(&w->ts.long_part, g->n_long * NPMAX, st));
   FJ_TRY(dalloc(&w->ts.chunk_acc, g->n_long_chunks * NAMAX, st));
   FJ_TRY(dalloc(&w->ts.long_ticket, g->n_long, st, true));

@@ -91,7 +91,7 @@ template <int WT>
 static fj_status launch_quant_wt(const fj_graph* g, const SolveWs* w, const double* s, const double* z, int64_t ld,
                                  int64_t c, double m, cudaStream_t st) {
   QuantOp<WT> op{z, s, g->deg, ld, c, m, w->qout};
-  tile_kernel<WT, QuantOp<WT>><<<w->grid_tile, TPB, 0, st>>>(make_sched(g), op, w->ts);
+  FJ_CK(launch_warp_items<WT>(g, w, op, st));
   FJ_CK_LAUNCH();
   return FJ_OK;
 }

@@ -169,10 +169,10 @@ def test_complete_graph_closed_form(fj, n):
 
 
 def test_star_hub_closed_form(fj):
-    n = 200_000   # hub row of 199,999 nonzeros: 49 long-row chunks
+    n = 200_000   # hub row of 199,999 nonzeros: 98 long-row chunks
     s = np.random.default_rng(3).uniform(0, 1, n)
     G, z, q, rep = solve_quant(fj, n, np.zeros(n - 1, np.int32), np.arange(1, n, dtype=np.int32), None, s)
-    assert G.info()["n_long_chunks"] == (n - 1 + 4095) // 4096
+    assert G.info()["n_long_chunks"] == (n - 1 + 2047) // 2048
     z0 = (2 * s[0] + s[1:].sum()) / (n + 1)
     zc = np.concatenate([[z0], (s[1:] + z0) / 2])
     assert np.allclose(z, zc, rtol=1e-9, atol=0)
