@@ -27,6 +27,20 @@ fj_status cuda_fail(cudaError_t e, const char* what, const char* file, int line)
     if (_s != FJ_OK) return _s;                                                \
   } while (0)
 
+// Device memory: a library-owned stream-ordered pool per device whose release threshold is
+// unbounded, so repeated graph builds / solves reuse memory instead of re-mapping it.
+cudaMemPool_t lib_pool(int device);
+template <class T>
+inline cudaError_t dmalloc(T** p, size_t bytes, cudaStream_t st) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  return cudaMallocFromPoolAsync(reinterpret_cast<void**>(p), bytes, lib_pool(dev), st);
+}
+
+// FJ_TIMING=1: host-side phase timestamps on stderr (diagnostics; synchronises the stream)
+void phase_tick(const char* label, cudaStream_t st);
+
 // kernel launch accounting (fj_kernel_launches)
 void count_launch(int64_t n = 1);
 void count_cub(int64_t n = 1);

@@ -2,7 +2,10 @@
 // Jacobi diagonal 1/(1+d_i), statistics (P:L86 w_min/w_max) and the tile-engine schedule.
 #include <cub/cub.cuh>
 #include <atomic>
+#include <chrono>
+#include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -14,6 +17,37 @@ thread_local std::string g_last_error;
 thread_local bool g_capturing = false;
 static std::atomic<int64_t> g_launches{0}, g_cub{0};
 void count_launch(int64_t n) { g_launches += n; }
+
+void phase_tick(const char* label, cudaStream_t st) {
+  static const bool on = getenv("FJ_TIMING") != nullptr;
+  if (!on) return;
+  static std::chrono::steady_clock::time_point last = std::chrono::steady_clock::now();
+  cudaStreamSynchronize(st);
+  auto now = std::chrono::steady_clock::now();
+  fprintf(stderr, "[fj] %-28s %9.3f ms\n", label,
+          std::chrono::duration<double, std::milli>(now - last).count());
+  last = now;
+}
+
+cudaMemPool_t lib_pool(int device) {
+  static std::mutex mu;
+  static cudaMemPool_t pools[64] = {};
+  std::lock_guard<std::mutex> lk(mu);
+  if (device < 0 || device >= 64) device = 0;
+  if (!pools[device]) {
+    cudaMemPoolProps props;
+    memset(&props, 0, sizeof props);
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    if (cudaMemPoolCreate(&pools[device], &props) != cudaSuccess) {
+      cudaDeviceGetDefaultMemPool(&pools[device], device);
+    }
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pools[device], cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  return pools[device];
+}
 void count_cub(int64_t n) { g_cub += n; }
 
 void set_error(const std::string& msg) { g_last_error = msg; }
@@ -209,11 +243,11 @@ fj_status fj_graph_create(int64_t n, int64_t nnz, const int64_t* row_ptr, const 
   cudaError_t ce = cudaGetDevice(&g->device);
   if (ce != cudaSuccess) return cleanup(cuda_fail(ce, "cudaGetDevice", __FILE__, __LINE__));
   cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, g->device);
-  ce = cudaMallocAsync(&g->deg, sizeof(double) * n, st);
-  if (ce == cudaSuccess) ce = cudaMallocAsync(&g->dinv, sizeof(double) * n, st);
+  ce = dmalloc(&g->deg, sizeof(double) * n, st);
+  if (ce == cudaSuccess) ce = dmalloc(&g->dinv, sizeof(double) * n, st);
   if (ce != cudaSuccess) return cleanup(cuda_fail(ce, "cudaMallocAsync", __FILE__, __LINE__));
   GStats* st_d = nullptr;
-  ce = cudaMallocAsync(&st_d, sizeof(GStats), st);
+  ce = dmalloc(&st_d, sizeof(GStats), st);
   if (ce != cudaSuccess) return cleanup(cuda_fail(ce, "cudaMallocAsync", __FILE__, __LINE__));
   GStats init{};
   init.wmin_bits = (unsigned long long)0x7FF0000000000000ULL;  // +inf

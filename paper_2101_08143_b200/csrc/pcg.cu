@@ -47,7 +47,7 @@ void free_solve_ws(fj_graph* g) {
 template <class T>
 static fj_status dalloc(T** p, int64_t count, cudaStream_t st, bool zero = false) {
   if (count < 1) count = 1;
-  FJ_CK(cudaMallocAsync((void**)p, sizeof(T) * (size_t)count, st));
+  FJ_CK(dmalloc(p, sizeof(T) * (size_t)count, st));
   if (zero) FJ_CK(cudaMemsetAsync(*p, 0, sizeof(T) * (size_t)count, st));
   return FJ_OK;
 }

@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(STPB) k_stats(int64_t n, const double* __restr
 static fj_status stats_cols(fj_graph* g, SolveWs* w, int k, const double* s, std::vector<double>& st4,
                             cudaStream_t st) {
   int* d_bad = nullptr;
-  FJ_CK(cudaMallocAsync(&d_bad, sizeof(int), st));
+  FJ_CK(dmalloc(&d_bad, sizeof(int), st));
   FJ_CK(cudaMemsetAsync(d_bad, 0, sizeof(int), st));
   for (int c = 0; c < k; ++c) {
     k_stats<<<w->grid_elem, STPB, 0, st>>>(g->n, s, k, c, w->elem_part, w->elem_ticket, w->stat + 4 * c, d_bad);
@@ -260,10 +260,13 @@ fj_status fj_approxim(const fj_graph* gc, int k, const double* s, double* z_user
     for (int round = 0;; ++round) {
       fj_solve_opts ob = oc;
       ob.max_iter = std::max(0, o.max_iter - spent);
+      phase_tick("approxim: before solve", st);
       fj_status sc = solve_col(g, s, z, k, c, ob, warm, &r, st, &iters);   // Alg. 1 line 3
       spent += iters;
       if (sc != FJ_OK && sc != FJ_E_NO_CONVERGENCE) return sc;
+      phase_tick("approxim: solve", st);
       FJ_TRY(quant_pass(g, w, s, z, k, c, m, t, st));                   // Alg. 1 lines 5-9
+      phase_tick("approxim: quantities", st);
       memset(&qout[c], 0, sizeof(fj_quantities_t));
       fill_quantities(g, t, m, qout[c]);
       if (sc != FJ_OK) { worst = sc; break; }

@@ -131,9 +131,9 @@ fj_status build_schedule(fj_graph* g, cudaStream_t st) {
   g->n_tiles = tot[2];
   g->n_long = tot[3];
   g->n_items = tot[0] + tot[1] + tot[2];
-  FJ_CK(cudaMallocAsync(&g->items, sizeof(ItemMeta) * (size_t)std::max<int64_t>(g->n_items, 1), st));
-  FJ_CK(cudaMallocAsync(&g->long_nchunks, sizeof(int32_t) * (size_t)std::max<int64_t>(g->n_long, 1), st));
-  FJ_CK(cudaMallocAsync(&g->long_item0, sizeof(int32_t) * (size_t)std::max<int64_t>(g->n_long, 1), st));
+  FJ_CK(dmalloc(&g->items, sizeof(ItemMeta) * (size_t)std::max<int64_t>(g->n_items, 1), st));
+  FJ_CK(dmalloc(&g->long_nchunks, sizeof(int32_t) * (size_t)std::max<int64_t>(g->n_long, 1), st));
+  FJ_CK(dmalloc(&g->long_item0, sizeof(int32_t) * (size_t)std::max<int64_t>(g->n_long, 1), st));
   if (nseg > 0) {
     k_items<<<nb256(nseg), 256, 0, st>>>(nseg, B.p, g->row_ptr, pc.p, pw.p, pt.p, pl.p, tot[0], tot[1],
                                          reinterpret_cast<ItemMeta*>(g->items), g->long_nchunks, g->long_item0);

@@ -113,9 +113,12 @@ __device__ __forceinline__ void t_tile(const TileSched& sc, const Op& op, const 
   const int M = R + N;
   const int d0 = min(lane * ITEMS, M), d1 = min(d0 + ITEMS, M);
   const int row_s = merge_rows_before(d0, s_e, R, N);
-  const int row_e = merge_rows_before(d1, s_e, R, N);
+  const int row_n = __shfl_down_sync(0xffffffffu, row_s, 1);    // next lane's split = this lane's end
+  const int row_e = lane == 31 ? R : row_n;
   const int nz_s = d0 - row_s, nz_e = d1 - row_e;
-  double xv[ITEMS], wv[ITEMS];
+  using WS = typename std::conditional<WT == FJ_W_F64, double, float>::type;   // exact for u8 / f32
+  double xv[ITEMS];
+  WS wv[ITEMS];
 #pragma unroll
   for (int j = 0; j < ITEMS; ++j) {
     const int k = nz_s + j;
@@ -123,7 +126,7 @@ __device__ __forceinline__ void t_tile(const TileSched& sc, const Op& op, const 
     wv[j] = 1.0;
     if (k < nz_e) {
       xv[j] = op.gather(s_col[k]);
-      if (WEIGHTED) wv[j] = WeightT<WT>::get(sc.w, k0 + k);
+      if (WEIGHTED) wv[j] = (WS)WeightT<WT>::get(sc.w, k0 + k);
     }
   }
   double a[NA], a_first[NA];
@@ -155,7 +158,7 @@ __device__ __forceinline__ void t_tile(const TileSched& sc, const Op& op, const 
         re = row < R ? s_e[row] : INT_MAX;
         xi = row < R ? s_xi[row] : 0.0;
       }
-      op.add(a, wv[j], xv[j], xi);
+      op.add(a, (double)wv[j], xv[j], xi);
     }
   }
   while (row < row_e) {

@@ -16,7 +16,7 @@ struct DevBuf {
   fj_status alloc(int64_t count, cudaStream_t s) {
     st = s;
     if (count <= 0) count = 1;
-    cudaError_t e = cudaMallocAsync(&p, sizeof(T) * (size_t)count, s);
+    cudaError_t e = dmalloc(&p, sizeof(T) * (size_t)count, s);
     if (e != cudaSuccess) { p = nullptr; return cuda_fail(e, "cudaMallocAsync", __FILE__, __LINE__); }
     return FJ_OK;
   }
