@@ -167,6 +167,8 @@ def main():
     ap.add_argument("--spmv-reps", type=int, default=20)
     ap.add_argument("--ref-seconds", type=float, default=10.0)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cuda-graph", action="store_true",
+                    help="host-driven PCG loop (same kernels); ncu cannot see kernels inside conditional graphs")
     args = ap.parse_args()
     ws, rank, local = dist_init()
     if args.impl == "reference":
@@ -190,7 +192,7 @@ def main():
     w = None if wl.w is None else torch.from_numpy(wl.w).cuda()
     S = torch.from_numpy(wl.S).cuda()
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device="cuda")
-    opts = fj.SolveOpts.make(rtol=args.rtol)
+    opts = fj.SolveOpts.make(rtol=args.rtol, use_cuda_graph=not args.no_cuda_graph)
     stream = torch.cuda.current_stream()
 
     def step():
@@ -282,7 +284,7 @@ def main():
                    "bytes_per_iteration": B, "fraction_of_measured_hbm": value / peak},
         "time_to_quantities_ms": statistics.median(ttq_ms),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": "tile_kernel<ApplyOp> ((I+L)p SpMV)",
+                     "traffic": traffic, "kernel": "warp_kernel<ApplyOp> ((I+L)p SpMV, warp-item engine)",
                      "algorithmic_bytes_per_launch": Bs, "launch_ms": spmv_ms, "peak_source": peak_src},
         "clocks": clocks, "gpu_launches": launches1 - launches0,
         "cub_calls": cub1 - cub0, "wall_s_timed_region": wall,
