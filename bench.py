@@ -207,7 +207,8 @@ def main():
         q, rep, info, bst = step()
     torch.cuda.synchronize()
     nnz = info["nnz"]
-    B = canonical_bytes(n, nnz, wb, 1)
+    kb = k if rep["batch_k"] else 1
+    B = canonical_bytes(n, nnz, wb, kb)      # one PCG iteration (batched over kb columns)
 
     sampler = ClockSampler(local)
     launches0, cub0 = binding.kernel_launches()
@@ -226,7 +227,9 @@ def main():
         e1.synchronize()
         step_ms.append(e0.elapsed_time(e1))
         loop_ms += rep["ms_loop"]
-        iters += rep["iterations_total"]
+        # batched (row a9): B(k) per batch iteration; per-column solves: B(1) per column iteration
+        iters += rep["iterations"] if rep["batch_k"] else rep["iterations_total"]
+        batched = bool(rep["batch_k"])
         ttq_ms.append(rep["ms"])
         results.append((q, rep))
     torch.cuda.synchronize()
@@ -239,7 +242,7 @@ def main():
     # dominant kernel: the (I+L)p tile SpMV, timed live with CUDA events on the launching stream
     rp, col, wo, _ = fj.csr_from_edges(n, u, v, w)
     G = fj.Graph(n, rp, col, wo, validate=False)
-    x = S[:, 0].contiguous()
+    x = S.contiguous() if kb > 1 else S[:, 0].contiguous()
     for _ in range(3):
         G.apply(x)
     e0 = torch.cuda.Event(enable_timing=True)
@@ -266,7 +269,7 @@ def main():
     value = tot_bytes / (tot_loop_ms / 1e3) / 1e9
 
     peak, peak_src = load_peaks()
-    Bs = spmv_bytes(n, nnz, wb, 1)
+    Bs = spmv_bytes(n, nnz, wb, kb)
     achieved = Bs / (spmv_ms / 1e3) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -309,7 +312,7 @@ def main():
             t = time.perf_counter()
             zh, qh, reph = fj.approxim_host(n, uh, vh, wh, Sh, opts=opts, want_z=True)
             e_ms += (time.perf_counter() - t) * 1e3
-            e_iters += reph["iterations_total"]
+            e_iters += reph["iterations"] if reph["batch_k"] else reph["iterations_total"]
         e_bytes = B * e_iters
         if ws > 1:
             t = torch.tensor([e_ms], dtype=torch.float64, device="cuda")

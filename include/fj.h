@@ -76,7 +76,7 @@ typedef struct {
   int32_t iterations;       /* PCG iterations (max over the k columns)                       */
   int32_t converged;        /* 1 when every column met rtol on its TRUE residual             */
   int32_t restarts;
-  int32_t reserved;
+  int32_t batch_k;          /* k if the columns were solved as one batch (row a9), else 0     */
   double rel_res_recursive; /* max_j ||r_j|| / ||s_j|| of the recursion at exit               */
   double rel_res_true;      /* max_j ||s_j - (I+L) z_j|| / ||s_j||, recomputed (NaN if not)  */
   double ms;                /* device time of the whole call (CUDA events on `stream`)       */

@@ -31,7 +31,7 @@ class SolveOpts(ctypes.Structure):
 
 
 class SolveReport(ctypes.Structure):
-    _fields_ = [("iterations", _i32), ("converged", _i32), ("restarts", _i32), ("reserved", _i32),
+    _fields_ = [("iterations", _i32), ("converged", _i32), ("restarts", _i32), ("batch_k", _i32),
                 ("rel_res_recursive", _dbl), ("rel_res_true", _dbl), ("ms", _dbl), ("ms_loop", _dbl),
                 ("iterations_total", _i64)]
 

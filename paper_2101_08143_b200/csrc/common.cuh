@@ -54,10 +54,31 @@ extern thread_local bool g_capturing;
 
 // ---------------------------------------------------------------- constants
 constexpr int MAXK = 64;
+// k >= batch_min_k() columns are solved together (row a9, spmm.cu); fewer columns run the k = 1
+// path once per column (a small-k row of the batched layout wastes most lanes).  FJ_BATCH_MIN_K
+// overrides (tests).
+int batch_min_k();
 
 // ---------------------------------------------------------------- device workspace per solve
 struct SolveWs;   // pcg.cu
 struct QuantWs;   // quantities.cu
+
+// One work-item list of the row engine: items [0, n_long_chunks) are long-row chunks, then W rows,
+// then T tiles (schedule.cu).
+struct Sched {
+  int64_t n_items = 0, n_tiles = 0, n_wrows = 0, n_long = 0, n_long_chunks = 0;
+  void* items = nullptr;            // ItemMeta [n_items] (tiles.cuh)
+  int32_t* long_nchunks = nullptr;  // [n_long]
+  int32_t* long_item0 = nullptr;    // [n_long] item index of chunk 0
+  int chunk = 0;                    // nonzeros per long-row chunk (= max W row length)
+  bool built = false;
+};
+struct SchedParams {
+  int trow_max;     // rows with <= trow_max nonzeros go to T tiles
+  int t_units;      // merge-coordinate cut of T tiles
+  int t_min_cost;   // minimum merge units charged per T row (caps rows per tile)
+  int chunk;        // W rows up to chunk nonzeros; longer rows are cut in chunks of this size
+};
 
 }  // namespace fj
 
@@ -72,16 +93,15 @@ struct fj_graph {
   // derived (owned)
   double* deg = nullptr;        // weighted degree d_i            [n]
   double* dinv = nullptr;       // 1 / (1 + d_i)                  [n]
-  // schedule (owned): items [0, n_long_chunks) are long-row chunks, then W rows, then T tiles
-  int64_t n_items = 0, n_tiles = 0, n_wrows = 0, n_long = 0, n_long_chunks = 0;
-  void* items = nullptr;          // ItemMeta [n_items] (tiles.cuh)
-  int32_t* long_nchunks = nullptr;// [n_long]
-  int32_t* long_item0 = nullptr;  // [n_long]
+  // row-engine work-item lists (schedule.cu): s1 for k = 1 (tiles.cuh), sb for batched k (spmm.cu,
+  // built on first use)
+  fj::Sched s1, sb;
   fj_graph_info_t info{};
   int num_sms = 148;
   // caches
   fj::SolveWs* solve_ws = nullptr;
   fj::QuantWs* quant_ws = nullptr;
+  void* batch_ws = nullptr;       // spmm.cu BatchWs (k > 1)
 };
 
 namespace fj {
@@ -154,5 +174,12 @@ __device__ __forceinline__ bool last_block_ticket(unsigned int* counter, unsigne
 }
 
 __device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
+
+// gather of one fp64 through the plain (coherent) global path
+__device__ __forceinline__ double ld_plain(const double* p) {
+  double r;
+  asm volatile("ld.global.f64 %0, [%1];" : "=d"(r) : "l"(p));
+  return r;
+}
 
 }  // namespace fj

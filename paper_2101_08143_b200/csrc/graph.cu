@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "tiles.cuh"
 #include "workspace.cuh"
 
 namespace fj {
@@ -17,6 +18,14 @@ thread_local std::string g_last_error;
 thread_local bool g_capturing = false;
 static std::atomic<int64_t> g_launches{0}, g_cub{0};
 void count_launch(int64_t n) { g_launches += n; }
+
+int batch_min_k() {
+  static const int v = [] {
+    const char* e = getenv("FJ_BATCH_MIN_K");
+    return e ? std::max(2, atoi(e)) : 8;
+  }();
+  return v;
+}
 
 void phase_tick(const char* label, cudaStream_t st) {
   static const bool on = getenv("FJ_TIMING") != nullptr;
@@ -165,7 +174,6 @@ __global__ void k_check_rowptr(int64_t n, int64_t nnz, const int64_t* rp, GStats
 
 static inline double bits2d(unsigned long long b) { double d; memcpy(&d, &b, sizeof d); return d; }
 static inline unsigned nblk(int64_t n, int t = 256) { return (unsigned)((n + t - 1) / t); }
-fj_status build_schedule(fj_graph* g, cudaStream_t st);   // schedule.cu
 
 template <int WT>
 static fj_status launch_degree(fj_graph* g, GStats* st_d, int validate, cudaStream_t st) {
@@ -273,7 +281,7 @@ fj_status fj_graph_create(int64_t n, int64_t nnz, const int64_t* row_ptr, const 
     return cleanup(fail(FJ_E_ASYMMETRIC, "adjacency not symmetric: (i,j,w) without (j,i,w)"));
   }
   if (nnz % 2 != 0 && validate) return cleanup(fail(FJ_E_ASYMMETRIC, "odd nnz"));
-  s = build_schedule(g, st);
+  s = build_schedule(g, kSchedK1, g->s1, st);
   if (s != FJ_OK) return cleanup(s);
   fj_graph_info_t& I = g->info;
   I.n = n; I.nnz = nnz; I.m = nnz / 2;
@@ -282,7 +290,8 @@ fj_status fj_graph_create(int64_t n, int64_t nnz, const int64_t* row_ptr, const 
   I.d_max = bits2d(h.dmax_bits);
   I.w_min = nnz ? bits2d(h.wmin_bits) : 0.0;
   I.w_max = nnz ? bits2d(h.wmax_bits) : 0.0;
-  I.n_tiles = g->n_tiles; I.n_wrows = g->n_wrows; I.n_long_rows = g->n_long; I.n_long_chunks = g->n_long_chunks;
+  I.n_tiles = g->s1.n_tiles; I.n_wrows = g->s1.n_wrows; I.n_long_rows = g->s1.n_long;
+  I.n_long_chunks = g->s1.n_long_chunks;
   I.wtype = wtype;
   ce = cudaStreamSynchronize(st);
   if (ce != cudaSuccess) return cleanup(cuda_fail(ce, "graph create", __FILE__, __LINE__));
@@ -307,8 +316,10 @@ fj_status fj_graph_destroy(fj_graph* g) {
   cudaDeviceSynchronize();
   free_solve_ws(g);
   free_quant_ws(g);
+  free_batch_ws(g);
   cudaFree(g->deg); cudaFree(g->dinv);
-  cudaFree(g->items); cudaFree(g->long_nchunks); cudaFree(g->long_item0);
+  free_sched(g->s1);
+  free_sched(g->sb);
   delete g;
   return FJ_OK;
 }

@@ -32,7 +32,13 @@ struct ApplyOp {
   PcgScalars* sc;                   // PCG mode when non-null
   double* dot_out;                  // optional: x^T y
   __device__ __forceinline__ bool skip() const { return sc && *(volatile int32_t*)&sc->done; }
-  __device__ __forceinline__ double gather(int32_t j) const { return __ldg(x + (int64_t)j * ld + c); }
+  __device__ __forceinline__ double gather(int32_t j) const {
+#ifdef FJ_GATHER_NC
+    return __ldg(x + (int64_t)j * ld + c);
+#else
+    return ld_plain(x + (int64_t)j * ld + c);
+#endif
+  }
   __device__ __forceinline__ double row_value(int64_t i) const { return __ldg(x + i * ld + c); }
   __device__ __forceinline__ void add(double (&a)[NA], double w, double xj, double) const {
     if (WT == FJ_W_UNIT) a[0] += xj; else a[0] = fma(w, xj, a[0]);
@@ -166,10 +172,10 @@ inline cudaError_t launch_warp_items(const fj_graph* g, const SolveWs* ws, const
     if (occ < 1) occ = 1;
   }
   int64_t grid = (int64_t)g->num_sms * occ;
-  const int64_t need = (g->n_items + WPB - 1) / WPB;
+  const int64_t need = (g->s1.n_items + WPB - 1) / WPB;
   if (grid > need) grid = need > 0 ? need : 1;
   if (grid > ws->grid_max) grid = ws->grid_max;
-  warp_kernel<WT, Op><<<(unsigned)grid, WTPB, 0, st>>>(make_sched(g), op, ws->ts);
+  warp_kernel<WT, Op><<<(unsigned)grid, WTPB, 0, st>>>(make_sched(g, g->s1), op, ws->ts);
   return cudaGetLastError();
 }
 

@@ -72,9 +72,9 @@ fj_status get_ws(fj_graph* g, cudaStream_t st, SolveWs** out) {
   FJ_TRY(dalloc(&w->elem_ticket, 1, st, true));
   constexpr int NPMAX = 16, NAMAX = 4;
   FJ_TRY(dalloc(&w->ts.block_part, (int64_t)w->grid_max * NPMAX, st));
-  FJ_TRY(dalloc(&w->ts.long_part, g->n_long * NPMAX, st));
-  FJ_TRY(dalloc(&w->ts.chunk_acc, g->n_long_chunks * NAMAX, st));
-  FJ_TRY(dalloc(&w->ts.long_ticket, g->n_long, st, true));
+  FJ_TRY(dalloc(&w->ts.long_part, g->s1.n_long * NPMAX, st));
+  FJ_TRY(dalloc(&w->ts.chunk_acc, g->s1.n_long_chunks * NAMAX, st));
+  FJ_TRY(dalloc(&w->ts.long_ticket, g->s1.n_long, st, true));
   FJ_TRY(dalloc(&w->ts.grid_ticket, 1, st, true));
   FJ_TRY(dalloc(&w->qout, 16, st));
   FJ_TRY(dalloc(&w->stat, 4 * MAXK, st));
@@ -362,10 +362,10 @@ fj_status fj_apply(const fj_graph* gc, int op, int k, const double* x, double* y
   if (x == y) return fail(FJ_E_INVALID_ARG, "x and y must not alias");
   fj_graph* g = const_cast<fj_graph*>(gc);
   cudaStream_t st = S(stream);
+  if (k > 1) return apply_batch(g, k, x, y, op == FJ_OP_L ? 1 : 0, st);
   SolveWs* w = nullptr;
   FJ_TRY(get_ws(g, st, &w));
-  for (int c = 0; c < k; ++c) FJ_TRY(apply_col(g, w, x, y, k, c, op == FJ_OP_L ? 1 : 0, st));
-  return FJ_OK;
+  return apply_col(g, w, x, y, 1, 0, op == FJ_OP_L ? 1 : 0, st);
 }
 
 fj_status fj_solve(const fj_graph* gc, int k, const double* s, double* z, const fj_solve_opts* opts,
@@ -386,10 +386,16 @@ fj_status fj_solve(const fj_graph* gc, int k, const double* s, double* z, const 
   r.rel_res_true = NAN;
   FJ_CK(cudaEventRecord(w->ev0, st));
   fj_status worst = FJ_OK;
-  for (int c = 0; c < k; ++c) {
-    fj_status sc = solve_col(g, s, z, k, c, o, 0, &r, st, nullptr);
+  if (k >= batch_min_k()) {   // row a9: all columns together
+    fj_status sc = solve_batch(g, k, s, z, o, 0, &r, st);
     if (sc != FJ_OK && sc != FJ_E_NO_CONVERGENCE) return sc;
-    if (sc != FJ_OK) worst = sc;
+    worst = sc;
+  } else {
+    for (int c = 0; c < k; ++c) {
+      fj_status sc = solve_col(g, s, z, k, c, o, 0, &r, st, nullptr);
+      if (sc != FJ_OK && sc != FJ_E_NO_CONVERGENCE) return sc;
+      if (sc != FJ_OK) worst = sc;
+    }
   }
   FJ_CK(cudaEventRecord(w->ev1, st));
   FJ_CK(cudaEventSynchronize(w->ev1));

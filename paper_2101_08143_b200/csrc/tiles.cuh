@@ -46,17 +46,24 @@ struct TileSched {
   const int32_t* __restrict__ long_nchunks;   // [n_long]
   const int32_t* __restrict__ long_item0;     // [n_long] item index of chunk 0
   int64_t n_long, n_chunks;
+  int chunk;                                  // nonzeros per long-row chunk
 };
 
-inline TileSched make_sched(const fj_graph* g) {
+inline TileSched make_sched(const fj_graph* g, const Sched& S) {
   TileSched s;
   s.n = g->n; s.row_ptr = g->row_ptr; s.col = g->col; s.w = g->w;
-  s.items = reinterpret_cast<const ItemMeta*>(g->items);
-  s.n_items = g->n_items;
-  s.long_nchunks = g->long_nchunks; s.long_item0 = g->long_item0;
-  s.n_long = g->n_long; s.n_chunks = g->n_long_chunks;
+  s.items = reinterpret_cast<const ItemMeta*>(S.items);
+  s.n_items = S.n_items;
+  s.long_nchunks = S.long_nchunks; s.long_item0 = S.long_item0;
+  s.n_long = S.n_long; s.n_chunks = S.n_long_chunks;
+  s.chunk = S.chunk;
   return s;
 }
+
+// the k = 1 engine's schedule (ITEMS x 32 lanes = T_CAP merge items per tile)
+constexpr SchedParams kSchedK1{T_ROW_MAX, T_UNITS, T_ROW_MIN_COST, CHUNK};
+fj_status build_schedule(fj_graph* g, const SchedParams& P, Sched& out, cudaStream_t st);
+void free_sched(Sched& s);
 
 // Scratch for the cross-warp parts of a launch (device memory, owned by the workspace).
 struct TileScratch {
@@ -220,7 +227,7 @@ __global__ void __launch_bounds__(WTPB) warp_kernel(const TileSched sc, const Op
       const int64_t r = cur.r0;
       const int64_t rb = __ldg(sc.row_ptr + r), re = __ldg(sc.row_ptr + r + 1);
       const int64_t kb = cur.k0;
-      const int64_t ke = (type == IT_W) ? re : min(kb + (int64_t)CHUNK, re);
+      const int64_t ke = (type == IT_W) ? re : min(kb + (int64_t)sc.chunk, re);
       const double xi = op.row_value(r);
       double a[NA];
 #pragma unroll

@@ -63,5 +63,9 @@ inline fj_status cub_select_index(const uint8_t* flags, int32_t* out, int32_t* n
 
 void free_solve_ws(fj_graph* g);   // pcg.cu
 void free_quant_ws(fj_graph* g);   // quantities.cu
+void free_batch_ws(fj_graph* g);   // spmm.cu
+fj_status solve_batch(fj_graph* g, int k, const double* s, double* z, const fj_solve_opts& o, int warm,
+                      fj_solve_report* rep, cudaStream_t st);
+fj_status apply_batch(fj_graph* g, int k, const double* x, double* y, int opL, cudaStream_t st);
 
 }  // namespace fj

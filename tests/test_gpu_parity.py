@@ -299,3 +299,49 @@ def test_e2e_host_matches_device(fj):
     _, z_d, q_d, rep_d = solve_quant(fj, wl.n, wl.u, wl.v, wl.w, wl.S)
     assert np.array_equal(z_h, z_d)
     assert q_h[1]["D"] == q_d[1]["D"]
+
+
+# ---------------------------------------------------------------- a9: batched k-column PCG
+def test_batched_k_columns_vs_oracle(fj):
+    wl = synth.make_config("c4", scale=14, k=8)
+    S = wl.S.copy()
+    S[:, 3] = 0.25            # consensus column (exact z = s)
+    S[:, 5] = 0.0             # zero column
+    g = O.canonical_csr(wl.n, wl.u, wl.v, wl.w)
+    _, Z, Q, rep = solve_quant(fj, wl.n, wl.u, wl.v, wl.w, S)
+    assert rep["converged"] == 1 and rep["rel_res_true"] <= 1e-10
+    assert np.array_equal(Z[:, 3], S[:, 3]) and Q[3]["consensus"] == 1
+    assert not Z[:, 5].any()
+    for c in [0, 1, 2, 4, 6, 7]:
+        zo, _ = O.solve_pcg(g, S[:, c], tol=1e-13)
+        check_against_oracle(Q[c], O.quantities(g, S[:, c], zo), S[:, c], Z[:, c], zo)
+
+
+def test_batched_k64_deterministic_and_matches_single(fj):
+    wl = synth.make_config("c4", scale=13, k=64)
+    rp, col, wo, _ = gpu_csr(fj, wl.n, wl.u, wl.v, wl.w)
+    G = fj.Graph(wl.n, rp, col, wo)
+    S = dev(wl.S)
+    z1, q1, r1 = G.approxim(S)
+    z2, q2, r2 = G.approxim(S)
+    z3, q3, r3 = G.approxim(S, opts=fj.SolveOpts.make(use_cuda_graph=False))
+    assert np.array_equal(host(z1), host(z2)) and np.array_equal(host(z1), host(z3))
+    for c in [0, 17, 63]:                      # batched columns agree with the k = 1 path
+        zc, qc, rc = G.approxim(dev(wl.S[:, c].copy()))
+        for k in QKEYS:
+            assert q1[c][k] == pytest.approx(qc[0][k], rel=1e-8), (c, k)
+        assert np.max(np.abs(host(z1)[:, c] - host(zc))) < 1e-8
+
+
+def test_batched_apply_and_solve_entry(fj):
+    wl = synth.make_config("c1", k=5)
+    g = O.canonical_csr(wl.n, wl.u, wl.v)
+    rp, col, wo, _ = gpu_csr(fj, wl.n, wl.u, wl.v)
+    G = fj.Graph(wl.n, rp, col, wo)
+    Z, rep = G.solve(dev(wl.S))
+    Z = host(Z)
+    for c in range(5):
+        assert np.max(np.abs(Z[:, c] - O.solve_dense(g, wl.S[:, c]))) < 1e-9
+    Y = host(G.apply(dev(wl.S), op=0))
+    for c in range(5):
+        assert np.allclose(Y[:, c], O.ipl_apply(g, wl.S[:, c]) - wl.S[:, c], rtol=1e-12, atol=1e-12)
