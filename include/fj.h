@@ -196,6 +196,49 @@ fj_status fj_approxim_host(int64_t n, int64_t m_in, const int32_t* u_host, const
                            double* z_host, const fj_solve_opts* opts, fj_quantities_t* q_host,
                            fj_solve_report* rep, void* stream);
 
+/* ---------------------------------------------------------------- a8/e: row-partitioned multi-GPU
+ * The graph is split into contiguous row blocks balanced by nonzeros, one block per rank (one
+ * process per GPU).  Rank r owns rows [bounds[r], bounds[r+1]).  Its CSR first carries GLOBAL
+ * column ids; fj_graph_create_dist renumbers them (own columns -> [0, n_loc), off-rank "ghost"
+ * columns -> n_loc + their index in the sorted ghost list).  Each PCG iteration exchanges the ghost
+ * entries of the search direction (halo; grouped NCCL send/recv over NVLink) and allreduces the dot
+ * products; every rank takes identical decisions.  s / z passed to fj_solve / fj_approxim /
+ * fj_quantities on a distributed handle are the rank's LOCAL row slices [n_loc][k]; quantities are
+ * global and identical on every rank.  fj_apply is not available on a distributed handle.
+ * Every call on a distributed handle is collective: all ranks must make it, in the same order. */
+typedef struct fj_comm fj_comm;
+/* 128-byte NCCL unique id (rank 0 creates it; broadcast it to the other ranks out of band). */
+fj_status fj_comm_unique_id(unsigned char id_out[128]);
+/* NCCL communicator on the current CUDA device (libnccl.so.2 is loaded on first use). */
+fj_status fj_comm_init(int nranks, int rank, const unsigned char id[128], fj_comm** out);
+/* LOOPBACK transport: nranks virtual ranks inside ONE process on ONE device, one host thread per
+ * rank (each passes its rank to fj_graph_create_dist and uses its own stream).  Collectives become
+ * barrier-ordered device copies and host sums in rank order.  For testing the distributed path. */
+fj_status fj_comm_init_loopback(int nranks, fj_comm** out);
+fj_status fj_comm_destroy(fj_comm* comm);
+
+/* bounds_host[0..nranks]: contiguous row blocks with ~equal raw (pre-dedup) nonzero counts,
+ * computed from the raw edge list on the device (same result on every rank). */
+fj_status fj_partition_rows(int64_t n, int64_t m_in, const int32_t* u_dev, const int32_t* v_dev, int nranks,
+                            int64_t* bounds_host, void* stream);
+/* Row a1 restricted to rows [row_begin, row_end): local row_ptr [n_loc+1] (starting at 0), GLOBAL
+ * column ids (capacity 2*m_in), same simple-graph rules as fj_csr_from_edges. */
+fj_status fj_csr_rows_from_edges(int64_t n, int64_t m_in, const int32_t* u_dev, const int32_t* v_dev,
+                                 const void* w_dev, int wtype, int64_t row_begin, int64_t row_end,
+                                 int64_t* row_ptr_local_dev, int32_t* col_global_dev, void* w_out_dev,
+                                 int64_t* nnz_out, void* stream);
+/* Sorted unique columns outside [row_begin, row_end) (the halo), ghosts_out capacity nnz_local. */
+fj_status fj_dist_ghosts(int64_t nnz_local, const int32_t* col_global_dev, int64_t row_begin, int64_t row_end,
+                         int32_t* ghosts_out_dev, int64_t* n_ghost_out, void* stream);
+/* One rank's handle.  send_counts_host[q] = how many of MY rows rank q needs; send_idx_dev holds
+ * those local row indices, concatenated in peer order (obtained by exchanging ghost lists).  The
+ * CSR arrays are borrowed as in fj_graph_create (col_global is renumbered into an owned copy). */
+fj_status fj_graph_create_dist(fj_comm* comm, int rank, int64_t n_global, const int64_t* bounds_host,
+                               int64_t nnz_local, const int64_t* row_ptr_local_dev, const int32_t* col_global_dev,
+                               const void* w_dev, int wtype, int64_t n_ghost, const int32_t* ghosts_dev,
+                               const int64_t* send_counts_host, const int32_t* send_idx_dev, void* stream,
+                               fj_graph** out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -91,8 +91,20 @@ def load_library(path: str = SO):
     L.fj_approxim.argtypes = [_vp, ctypes.c_int, _vp, _vp, P(SolveOpts), P(Quantities), P(SolveReport), _vp]
     L.fj_approxim_host.argtypes = [_i64, _i64, _vp, _vp, _vp, ctypes.c_int, ctypes.c_int, _vp, _vp,
                                    P(SolveOpts), P(Quantities), P(SolveReport), _vp]
+    L.fj_comm_unique_id.argtypes = [_vp]
+    L.fj_comm_init.argtypes = [ctypes.c_int, ctypes.c_int, _vp, P(_vp)]
+    L.fj_comm_init_loopback.argtypes = [ctypes.c_int, P(_vp)]
+    L.fj_comm_destroy.argtypes = [_vp]
+    L.fj_partition_rows.argtypes = [_i64, _i64, _vp, _vp, ctypes.c_int, _vp, _vp]
+    L.fj_csr_rows_from_edges.argtypes = [_i64, _i64, _vp, _vp, _vp, ctypes.c_int, _i64, _i64, _vp, _vp, _vp,
+                                         P(_i64), _vp]
+    L.fj_dist_ghosts.argtypes = [_i64, _vp, _i64, _i64, _vp, P(_i64), _vp]
+    L.fj_graph_create_dist.argtypes = [_vp, ctypes.c_int, _i64, _vp, _i64, _vp, _vp, _vp, ctypes.c_int, _i64, _vp,
+                                       _vp, _vp, _vp, P(_vp)]
     for name in ["fj_csr_from_edges", "fj_graph_create", "fj_graph_info", "fj_graph_degrees", "fj_graph_destroy",
-                 "fj_apply", "fj_opinion_stats", "fj_solve", "fj_quantities", "fj_approxim", "fj_approxim_host"]:
+                 "fj_apply", "fj_opinion_stats", "fj_solve", "fj_quantities", "fj_approxim", "fj_approxim_host",
+                 "fj_comm_unique_id", "fj_comm_init", "fj_comm_init_loopback", "fj_comm_destroy",
+                 "fj_partition_rows", "fj_csr_rows_from_edges", "fj_dist_ghosts", "fj_graph_create_dist"]:
         getattr(L, name).restype = ctypes.c_int
     _lib = L
     return L
@@ -265,6 +277,93 @@ class Graph:
             self.close()
         except Exception:
             pass
+
+
+class Comm:
+    """Communicator of the row-partitioned path (rows a8/e): NCCL, or LOOPBACK for virtual ranks in one process."""
+
+    def __init__(self, handle, nranks, kind):
+        self._h, self.nranks, self.kind = handle, nranks, kind
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = ctypes.create_string_buffer(128)
+        _check(lib().fj_comm_unique_id(buf))
+        return buf.raw
+
+    @classmethod
+    def nccl(cls, nranks: int, rank: int, uid: bytes):
+        h = _vp()
+        buf = ctypes.create_string_buffer(bytes(uid), 128)
+        _check(lib().fj_comm_init(nranks, rank, buf, ctypes.byref(h)))
+        return cls(h, nranks, "nccl")
+
+    @classmethod
+    def loopback(cls, nranks: int):
+        h = _vp()
+        _check(lib().fj_comm_init_loopback(nranks, ctypes.byref(h)))
+        return cls(h, nranks, "loopback")
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and _lib is not None:
+            _lib.fj_comm_destroy(self._h)
+        self._h = None
+
+
+def partition_rows(n: int, u, v, nranks: int, stream=None):
+    import numpy as np
+    _need_cuda(u, v)
+    b = np.zeros(nranks + 1, dtype=np.int64)
+    _check(lib().fj_partition_rows(n, int(u.numel()), _ptr(u), _ptr(v), nranks, ctypes.c_void_p(b.ctypes.data),
+                                   _stream(stream)))
+    return [int(x) for x in b]
+
+
+def csr_rows_from_edges(n: int, u, v, w, r0: int, r1: int, stream=None):
+    """Row a1 for rows [r0, r1): (row_ptr_local, col_global, w_out, nnz)."""
+    import torch
+    _need_cuda(u, v, w)
+    m = int(u.numel())
+    dev = u.device
+    rp = torch.empty(r1 - r0 + 1, dtype=torch.int64, device=dev)
+    col = torch.empty(max(2 * m, 1), dtype=torch.int32, device=dev)
+    wo = None if w is None else torch.empty(max(2 * m, 1), dtype=w.dtype, device=dev)
+    nnz = _i64()
+    _check(lib().fj_csr_rows_from_edges(n, m, _ptr(u), _ptr(v), _ptr(w), _wtype(w), r0, r1, _ptr(rp), _ptr(col),
+                                        _ptr(wo), ctypes.byref(nnz), _stream(stream)))
+    k = nnz.value
+    return rp, col[:k], (None if wo is None else wo[:k]), k
+
+
+def dist_ghosts(col_global, r0: int, r1: int, stream=None):
+    import torch
+    _need_cuda(col_global)
+    nnz = int(col_global.numel())
+    out = torch.empty(max(nnz, 1), dtype=torch.int32, device=col_global.device)
+    ng = _i64()
+    _check(lib().fj_dist_ghosts(nnz, _ptr(col_global), r0, r1, _ptr(out), ctypes.byref(ng), _stream(stream)))
+    return out[:ng.value]
+
+
+class DistGraph(Graph):
+    """One rank's handle of a row-partitioned graph."""
+
+    def __init__(self, comm: Comm, rank: int, n_global: int, bounds, row_ptr, col_global, w, ghosts,
+                 send_counts, send_idx, stream=None):
+        import numpy as np
+        L = lib()
+        _need_cuda(row_ptr, col_global, w, ghosts, send_idx)
+        self.n = int(bounds[rank + 1] - bounds[rank])
+        self.rank, self.bounds, self.n_global = rank, list(bounds), n_global
+        self._keep = (row_ptr, col_global, w, ghosts, send_idx, comm)
+        b = np.asarray(bounds, dtype=np.int64)
+        sc = np.asarray(send_counts, dtype=np.int64)
+        h = _vp()
+        _check(L.fj_graph_create_dist(comm._h, rank, n_global, ctypes.c_void_p(b.ctypes.data), int(col_global.numel()),
+                                      _ptr(row_ptr), _ptr(col_global), _ptr(w), _wtype(w), int(ghosts.numel()),
+                                      _ptr(ghosts), ctypes.c_void_p(sc.ctypes.data), _ptr(send_idx), _stream(stream),
+                                      ctypes.byref(h)))
+        self._h = h
 
 
 def approxim_host(n, u, v, w, S, opts: SolveOpts | None = None, want_z=False, stream=None):

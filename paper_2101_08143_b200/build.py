@@ -12,6 +12,15 @@ CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libfj.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
+def _nccl_include():
+    """nccl.h for the TYPES only (libnccl.so.2 is dlopen'ed at fj_comm_init): torch's pip NCCL."""
+    try:
+        import nvidia.nccl
+        return os.path.join(list(nvidia.nccl.__path__)[0], "include")
+    except Exception:
+        return "/usr/include"
+
+
 FLAGS = [
     "-O3", "-std=c++17", "-lineinfo",
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -41,8 +50,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     procs = []
     for src in sources():
         obj = os.path.join(HERE, "build", os.path.basename(src) + ".o")
-        cmd = [NVCC, *[f for f in FLAGS if f != "-shared"], "-dc" if False else "-c", src, "-o", obj,
-               "-I", os.path.join(ROOT, "include")]
+        cmd = [NVCC, *[f for f in FLAGS if f != "-shared"], "-c", src, "-o", obj,
+               "-I", os.path.join(ROOT, "include"), "-I", _nccl_include()]
         if verbose:
             cmd += ["-Xptxas", "-v"]
         procs.append((subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT), src))
@@ -59,7 +68,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError("libfj build failed")
     tmp = SO + ".tmp"
     subprocess.check_call([NVCC, "-shared", "-cudart", "static", "-gencode", "arch=compute_100a,code=sm_100a",
-                           *objs, "-o", tmp])
+                           *objs, "-o", tmp, "-ldl"])
     os.replace(tmp, SO)
     return SO
 

@@ -102,6 +102,7 @@ struct fj_graph {
   fj::SolveWs* solve_ws = nullptr;
   fj::QuantWs* quant_ws = nullptr;
   void* batch_ws = nullptr;       // spmm.cu BatchWs (k > 1)
+  void* dist = nullptr;           // dist.cu DistInfo when this is one rank's row block
 };
 
 namespace fj {

@@ -188,3 +188,130 @@ extern "C" fj_status fj_csr_from_edges(int64_t n, int64_t m_in, const int32_t* u
   if (dups_out) *dups_out = m - (int64_t)hf.selfloops - nnz / 2;
   return FJ_OK;
 }
+
+// ---------------------------------------------------------------- a1 for a row block (row a8)
+namespace fj {
+
+// per raw edge: how many of its two orientations have their row in [r0, r1)
+__global__ void k_range_count(int64_t m, int64_t n, const int32_t* __restrict__ u, const int32_t* __restrict__ v,
+                              int64_t r0, int64_t r1, int64_t* __restrict__ cnt, BuildFlags* fl) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = u[e], c = v[e];
+    int64_t k = 0;
+    if (a < 0 || c < 0 || a >= n || c >= n) atomicOr(&fl->bad_range, 1u);
+    else if (a != c) k = (a >= r0 && a < r1) + (c >= r0 && c < r1);
+    cnt[e] = k;
+  }
+}
+
+// emit the in-range orientations in (edge, orientation) order: key = ((row - r0) << b) | col
+__global__ void k_range_emit(int64_t m, const int32_t* __restrict__ u, const int32_t* __restrict__ v, int64_t r0,
+                             int64_t r1, int b, const int64_t* __restrict__ pos, uint64_t* __restrict__ keys,
+                             int32_t* __restrict__ vals) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = u[e], c = v[e];
+    if (a == c || a < 0 || c < 0) continue;
+    int64_t p = pos[e];
+    if (a >= r0 && a < r1) {
+      keys[p] = ((uint64_t)(a - r0) << b) | (uint64_t)c;
+      if (vals) vals[p] = (int32_t)e;
+      ++p;
+    }
+    if (c >= r0 && c < r1) {
+      keys[p] = ((uint64_t)(c - r0) << b) | (uint64_t)a;
+      if (vals) vals[p] = (int32_t)e;
+    }
+  }
+}
+
+}  // namespace fj
+
+extern "C" fj_status fj_csr_rows_from_edges(int64_t n, int64_t m_in, const int32_t* u, const int32_t* v, const void* w,
+                                            int wtype, int64_t r0, int64_t r1, int64_t* row_ptr, int32_t* col,
+                                            void* w_out, int64_t* nnz_out, void* stream) {
+  if (n < 1 || n >= INT32_MAX) return fail(FJ_E_INVALID_ARG, "n must be in [1, 2^31-2]");
+  if (m_in < 0 || m_in >= INT32_MAX) return fail(FJ_E_INVALID_ARG, "m_in must be in [0, 2^31-2]");
+  if (r0 < 0 || r1 > n || r1 <= r0) return fail(FJ_E_INVALID_ARG, "bad row range");
+  if (!row_ptr || !nnz_out || (m_in > 0 && (!u || !v || !col))) return fail(FJ_E_INVALID_ARG, "null argument");
+  if (wtype < FJ_W_UNIT || wtype > FJ_W_F64) return fail(FJ_E_INVALID_ARG, "bad wtype");
+  if (wtype != FJ_W_UNIT && m_in > 0 && (!w || !w_out)) return fail(FJ_E_INVALID_ARG, "weights are NULL");
+  const int wbytes = wtype == FJ_W_UNIT ? 0 : wtype == FJ_W_U8 ? 1 : wtype == FJ_W_F32 ? 4 : 8;
+  cudaStream_t st = S(stream);
+  int dev = 0, sms = 148;
+  FJ_CK(cudaGetDevice(&dev));
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t nl = r1 - r0;
+  int b = 1;
+  while ((1LL << b) < n) ++b;
+  const uint64_t sent = (b == 32) ? ~0ULL : ((1ULL << (2 * b)) - 1ULL);
+  k_fill_empty<<<grid_for(nl + 1, sms), 256, 0, st>>>(nl, row_ptr);
+  FJ_CK_LAUNCH();
+  if (m_in == 0) {
+    FJ_CK(cudaStreamSynchronize(st));
+    *nnz_out = 0;
+    return FJ_OK;
+  }
+  const int64_t m = m_in;
+  DevBuf<int64_t> cnt, pos;
+  DevBuf<BuildFlags> fl;
+  FJ_TRY(cnt.alloc(m, st)); FJ_TRY(pos.alloc(m + 1, st)); FJ_TRY(fl.alloc(1, st));
+  FJ_CK(cudaMemsetAsync(fl.p, 0, sizeof(BuildFlags), st));
+  k_range_count<<<grid_for(m, sms), 256, 0, st>>>(m, n, u, v, r0, r1, cnt.p, fl.p);
+  FJ_CK_LAUNCH();
+  FJ_TRY(cub_exclusive_sum(cnt.p, pos.p, m, st));
+  int64_t last_pos = 0, last_cnt = 0;
+  BuildFlags hf{};
+  FJ_CK(cudaMemcpyAsync(&last_pos, pos.p + m - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  FJ_CK(cudaMemcpyAsync(&last_cnt, cnt.p + m - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  FJ_CK(cudaMemcpyAsync(&hf, fl.p, sizeof hf, cudaMemcpyDeviceToHost, st));
+  FJ_CK(cudaStreamSynchronize(st));
+  if (hf.bad_range) return fail(FJ_E_INVALID_ARG, "edge endpoint out of [0, n)");
+  const int64_t m2 = last_pos + last_cnt;
+  if (m2 == 0) { *nnz_out = 0; return FJ_OK; }
+  DevBuf<uint64_t> ka, kb;
+  DevBuf<int32_t> va, vb;
+  FJ_TRY(ka.alloc(m2, st)); FJ_TRY(kb.alloc(m2, st));
+  if (wbytes) { FJ_TRY(va.alloc(m2, st)); FJ_TRY(vb.alloc(m2, st)); }
+  k_range_emit<<<grid_for(m, sms), 256, 0, st>>>(m, u, v, r0, r1, b, pos.p, ka.p, wbytes ? va.p : nullptr);
+  FJ_CK_LAUNCH();
+  cnt.release();
+  pos.release();
+  cub::DoubleBuffer<uint64_t> dk(ka.p, kb.p);
+  cub::DoubleBuffer<int32_t> dv(va.p, vb.p);
+  size_t bytes = 0;
+  if (wbytes) FJ_CK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, dk, dv, m2, 0, 2 * b, st));
+  else FJ_CK(cub::DeviceRadixSort::SortKeys(nullptr, bytes, dk, m2, 0, 2 * b, st));
+  {
+    DevBuf<uint8_t> tmp;
+    FJ_TRY(tmp.alloc((int64_t)bytes, st));
+    if (wbytes) FJ_CK(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, dk, dv, m2, 0, 2 * b, st));
+    else FJ_CK(cub::DeviceRadixSort::SortKeys(tmp.p, bytes, dk, m2, 0, 2 * b, st));
+    count_cub();
+  }
+  const uint64_t* ks = dk.Current();
+  const int32_t* vs = wbytes ? dv.Current() : nullptr;
+  DevBuf<uint8_t> f;
+  DevBuf<int64_t> kp;
+  FJ_TRY(f.alloc(m2, st));
+  FJ_TRY(kp.alloc(m2, st));
+  k_kept<<<grid_for(m2, sms), 256, 0, st>>>(m2, ks, sent, f.p);
+  FJ_CK_LAUNCH();
+  cub::TransformInputIterator<int64_t, U8ToI64, const uint8_t*> fi(f.p, U8ToI64());
+  bytes = 0;
+  FJ_CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, fi, kp.p, m2, st));
+  {
+    DevBuf<uint8_t> tmp;
+    FJ_TRY(tmp.alloc((int64_t)bytes, st));
+    FJ_CK(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, fi, kp.p, m2, st));
+    count_cub();
+  }
+  k_scatter<<<grid_for(m2, sms), 256, 0, st>>>(m2, nl, ks, vs, f.p, kp.p, b, wbytes, w, col, w_out, row_ptr);
+  FJ_CK_LAUNCH();
+  int64_t lp = 0;
+  uint8_t lf = 0;
+  FJ_CK(cudaMemcpyAsync(&lp, kp.p + m2 - 1, sizeof lp, cudaMemcpyDeviceToHost, st));
+  FJ_CK(cudaMemcpyAsync(&lf, f.p + m2 - 1, 1, cudaMemcpyDeviceToHost, st));
+  FJ_CK(cudaStreamSynchronize(st));
+  *nnz_out = lp + lf;
+  return FJ_OK;
+}

@@ -317,6 +317,7 @@ fj_status fj_graph_destroy(fj_graph* g) {
   free_solve_ws(g);
   free_quant_ws(g);
   free_batch_ws(g);
+  free_dist(g);
   cudaFree(g->deg); cudaFree(g->dinv);
   free_sched(g->s1);
   free_sched(g->sb);

@@ -31,6 +31,7 @@ struct ApplyOp {
   int opL;                          // 1: L x, 0: (I + L) x
   PcgScalars* sc;                   // PCG mode when non-null
   double* dot_out;                  // optional: x^T y
+  int alpha_on_device = 1;          // 0 (distributed): leave alpha to the caller after the allreduce
   __device__ __forceinline__ bool skip() const { return sc && *(volatile int32_t*)&sc->done; }
   __device__ __forceinline__ double gather(int32_t j) const {
 #ifdef FJ_GATHER_NC
@@ -52,7 +53,7 @@ struct ApplyOp {
   }
   __device__ __forceinline__ void finalize(const double (&tot)[NP]) const {
     if (dot_out) *dot_out = tot[0];
-    if (sc) {
+    if (sc && alpha_on_device) {
       sc->pq = tot[0];
       if (!(tot[0] > 0.0) || !isfinite(tot[0])) {   // (I+L) is SPD: p^T q > 0 unless p = 0
         sc->alpha = 0.0;
@@ -106,9 +107,11 @@ struct QuantOp {
   int64_t ld, c;
   double m;
   double* out;   // [NP]
+  int64_t zld = -1, zc = 0;   // z layout if it differs from s (distributed: contiguous extended z)
   __device__ __forceinline__ bool skip() const { return false; }
-  __device__ __forceinline__ double gather(int32_t j) const { return __ldg(z + (int64_t)j * ld + c); }
-  __device__ __forceinline__ double row_value(int64_t i) const { return __ldg(z + i * ld + c); }
+  __device__ __forceinline__ int64_t zi(int64_t i) const { return zld < 0 ? i * ld + c : i * zld + zc; }
+  __device__ __forceinline__ double gather(int32_t j) const { return __ldg(z + zi(j)); }
+  __device__ __forceinline__ double row_value(int64_t i) const { return __ldg(z + zi(i)); }
   __device__ __forceinline__ void add(double (&a)[NA], double w, double zj, double zi) const {
     const double df = zi - zj;
     a[0] = fma(w, zj, a[0]);

@@ -362,6 +362,7 @@ fj_status fj_apply(const fj_graph* gc, int op, int k, const double* x, double* y
   if (x == y) return fail(FJ_E_INVALID_ARG, "x and y must not alias");
   fj_graph* g = const_cast<fj_graph*>(gc);
   cudaStream_t st = S(stream);
+  if (is_dist(g)) return fail(FJ_E_UNSUPPORTED, "fj_apply on a distributed graph (use fj_solve / fj_quantities)");
   if (k > 1) return apply_batch(g, k, x, y, op == FJ_OP_L ? 1 : 0, st);
   SolveWs* w = nullptr;
   FJ_TRY(get_ws(g, st, &w));
@@ -386,7 +387,13 @@ fj_status fj_solve(const fj_graph* gc, int k, const double* s, double* z, const 
   r.rel_res_true = NAN;
   FJ_CK(cudaEventRecord(w->ev0, st));
   fj_status worst = FJ_OK;
-  if (k >= batch_min_k()) {   // row a9: all columns together
+  if (is_dist(g)) {   // row a8: one rank's slice; halo exchange + allreduce inside
+    for (int c = 0; c < k; ++c) {
+      fj_status sc = dist_solve_col(g, s, z, k, c, o, 0, &r, st);
+      if (sc != FJ_OK && sc != FJ_E_NO_CONVERGENCE) return sc;
+      if (sc != FJ_OK) worst = sc;
+    }
+  } else if (k >= batch_min_k()) {   // row a9: all columns together
     fj_status sc = solve_batch(g, k, s, z, o, 0, &r, st);
     if (sc != FJ_OK && sc != FJ_E_NO_CONVERGENCE) return sc;
     worst = sc;

@@ -62,7 +62,8 @@ __global__ void __launch_bounds__(STPB) k_stats(int64_t n, const double* __restr
       lo = fmin(lo, __ldcg(part + q * 4 + 2));
       hi = fmax(hi, __ldcg(part + q * 4 + 3));
     }
-    out[0] = a; out[1] = b; out[2] = lo; out[3] = hi;
+    out[0] = *(volatile int*)nonfinite ? NAN : a;   // NaN marks a non-finite input (propagates over ranks)
+    out[1] = b; out[2] = lo; out[3] = hi;
     *ticket = 0u;
   }
 }
@@ -76,13 +77,13 @@ static fj_status stats_cols(fj_graph* g, SolveWs* w, int k, const double* s, std
     k_stats<<<w->grid_elem, STPB, 0, st>>>(g->n, s, k, c, w->elem_part, w->elem_ticket, w->stat + 4 * c, d_bad);
     FJ_CK_LAUNCH();
   }
+  if (is_dist(g)) FJ_TRY(dist_stats_combine(g, k, w->stat, st));   // global over the ranks' slices
   st4.assign(4 * k, 0.0);
-  int bad = 0;
   FJ_CK(cudaMemcpyAsync(st4.data(), w->stat, sizeof(double) * 4 * k, cudaMemcpyDeviceToHost, st));
-  FJ_CK(cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, st));
   FJ_CK(cudaFreeAsync(d_bad, st));
   FJ_CK(cudaStreamSynchronize(st));
-  if (bad) return fail(FJ_E_NONFINITE_INPUT, "opinion vector contains NaN or Inf");
+  for (int c = 0; c < k; ++c)   // k_stats poisons the sum with NaN when a slice held NaN / Inf
+    if (std::isnan(st4[4 * c])) return fail(FJ_E_NONFINITE_INPUT, "opinion vector contains NaN or Inf");
   return FJ_OK;
 }
 
@@ -98,6 +99,7 @@ static fj_status launch_quant_wt(const fj_graph* g, const SolveWs* w, const doub
 
 static fj_status quant_pass(const fj_graph* g, const SolveWs* w, const double* s, const double* z, int64_t ld,
                             int64_t c, double m, double* host10, cudaStream_t st) {
+  if (is_dist(g)) return dist_quant_pass(g, s, z, ld, c, m, host10, st);
   fj_status r;
   switch (g->wtype) {
     case FJ_W_UNIT: r = launch_quant_wt<FJ_W_UNIT>(g, w, s, z, ld, c, m, st); break;
@@ -125,7 +127,7 @@ static double cert_eps(double Qt, double R, double rel_sum) {
 }
 
 static void fill_quantities(const fj_graph* g, const double* t, double mean_s, fj_quantities_t& q) {
-  const double n = (double)g->n;
+  const double n = (double)global_n(g);
   q.CI = t[0];
   q.D = 0.5 * t[1];   // each undirected edge was visited from both ends
   q.P = t[2];
@@ -140,7 +142,7 @@ static void fill_quantities(const fj_graph* g, const double* t, double mean_s, f
   q.res_norm = std::sqrt(t[6]);
   q.s_norm = std::sqrt(t[9]);
   const double u = std::ldexp(1.0, -53);
-  const double lg = std::ceil(std::log2(g->info.d_max + 2.0));
+  const double lg = std::ceil(std::log2(global_dmax(g) + 2.0));
   const double gamma = (32.0 + lg + 4.0) * u;     // row sums: <= 32 sequential + tree levels
   q.fp_bound = gamma * std::sqrt(t[8]);
   const double R = q.res_norm * (1.0 + 1e-12) + q.fp_bound;
@@ -161,7 +163,7 @@ static void fill_quantities(const fj_graph* g, const double* t, double mean_s, f
 
 static void consensus_quantities(const fj_graph* g, double c, fj_quantities_t& q) {
   memset(&q, 0, sizeof q);
-  const double n = (double)g->n;
+  const double n = (double)global_n(g);
   q.C = n * c * c;          // z = s = c 1 exactly (Omega 1 = 1)
   q.Idc = q.C;
   q.mean_s = c;
@@ -208,7 +210,7 @@ fj_status fj_quantities(const fj_graph* gc, int k, const double* s, const double
   FJ_TRY(stats_cols(g, w, k, s, v, st));
   for (int c = 0; c < k; ++c) {
     double t[10];
-    const double m = v[4 * c] / (double)g->n;
+    const double m = v[4 * c] / (double)global_n(g);
     FJ_TRY(quant_pass(g, w, s, z, k, c, m, t, st));
     memset(&out[c], 0, sizeof(fj_quantities_t));
     fill_quantities(g, t, m, out[c]);
@@ -245,7 +247,7 @@ fj_status fj_approxim(const fj_graph* gc, int k, const double* s, double* z_user
   r.rel_res_true = NAN;
   const unsigned cb = (unsigned)std::min<int64_t>((g->n + 255) / 256, 4096);
   fj_status worst = FJ_OK;
-  if (k >= batch_min_k()) {
+  if (k >= batch_min_k() && !is_dist(g)) {
     // row a9: all k columns in ONE batched PCG (per-column alpha/beta, convergence mask)
     fj_solve_opts oc = o;
     int warm = 0, spent = 0;
@@ -269,7 +271,7 @@ fj_status fj_approxim(const fj_graph* gc, int k, const double* s, double* z_user
       r.batch_k = k;
       double emax = 0.0;
       for (int c = 0; c < k; ++c) {
-        const double m = v[4 * c] / (double)g->n;
+        const double m = v[4 * c] / (double)global_n(g);
         if (v[4 * c + 2] == v[4 * c + 3]) {   // s = c 1: z = s exactly (P:L129 Omega 1 = 1)
           k_copy_cols<<<cb, 256, 0, st>>>(g->n, k, c, s, z);
           FJ_CK_LAUNCH();
@@ -290,7 +292,7 @@ fj_status fj_approxim(const fj_graph* gc, int k, const double* s, double* z_user
     r.iterations = spent;
   } else {
   for (int c = 0; c < k; ++c) {
-    const double m = v[4 * c] / (double)g->n;
+    const double m = v[4 * c] / (double)global_n(g);
     if (v[4 * c + 2] == v[4 * c + 3]) {   // s = c 1: z = s exactly (P:L129 Omega 1 = 1)
       k_copy_cols<<<cb, 256, 0, st>>>(g->n, k, c, s, z);
       FJ_CK_LAUNCH();
@@ -305,7 +307,16 @@ fj_status fj_approxim(const fj_graph* gc, int k, const double* s, double* z_user
       fj_solve_opts ob = oc;
       ob.max_iter = std::max(0, o.max_iter - spent);
       phase_tick("approxim: before solve", st);
-      fj_status sc = solve_col(g, s, z, k, c, ob, warm, &r, st, &iters);   // Alg. 1 line 3
+      fj_status sc;
+      if (is_dist(g)) {   // row a8: this rank's slice, halo exchange + allreduce inside
+        const int before = r.iterations;
+        r.iterations = 0;
+        sc = dist_solve_col(g, s, z, k, c, ob, warm, &r, st);
+        iters = r.iterations;
+        r.iterations = std::max(before, iters);
+      } else {
+        sc = solve_col(g, s, z, k, c, ob, warm, &r, st, &iters);   // Alg. 1 line 3
+      }
       spent += iters;
       if (sc != FJ_OK && sc != FJ_E_NO_CONVERGENCE) return sc;
       phase_tick("approxim: solve", st);

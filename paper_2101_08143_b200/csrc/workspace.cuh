@@ -67,5 +67,15 @@ void free_batch_ws(fj_graph* g);   // spmm.cu
 fj_status solve_batch(fj_graph* g, int k, const double* s, double* z, const fj_solve_opts& o, int warm,
                       fj_solve_report* rep, cudaStream_t st);
 fj_status apply_batch(fj_graph* g, int k, const double* x, double* y, int opL, cudaStream_t st);
+// dist.cu
+void free_dist(fj_graph* g);
+bool is_dist(const fj_graph* g);
+int64_t global_n(const fj_graph* g);
+double global_dmax(const fj_graph* g);
+fj_status dist_solve_col(fj_graph* g, const double* s, double* z, int64_t ld, int64_t c, const fj_solve_opts& o,
+                         int warm, fj_solve_report* rep, cudaStream_t st);
+fj_status dist_quant_pass(const fj_graph* g, const double* s, const double* z, int64_t ld, int64_t c, double m,
+                          double* host10, cudaStream_t st);
+fj_status dist_stats_combine(const fj_graph* g, int k, double* dev4k, cudaStream_t st);
 
 }  // namespace fj

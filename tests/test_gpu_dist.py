@@ -1,0 +1,113 @@
+"""GPU tests of the row-partitioned path (rows a8/e) with the LOOPBACK transport: P virtual ranks
+as host threads of one process on one B200, each with its own stream and its own row block, the
+halo exchange and allreduces done by the library (barrier-ordered device copies / host sums; no
+kernel ever waits on another).  Results must match the single-GPU path and the oracle."""
+import threading
+
+import numpy as np
+import pytest
+
+import oracle as O
+import synth
+
+pytestmark = pytest.mark.gpu
+QKEYS = ["CI", "D", "P", "C", "Idc", "PDI"]
+
+
+@pytest.fixture(scope="module")
+def fj():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2101_08143_b200 as m
+    from paper_2101_08143_b200 import build as B
+    B.build()
+    return m
+
+
+def run_ranks(fj, P, wl, S, opts=None):
+    import torch
+    from paper_2101_08143_b200 import dist as D
+    comm = fj.Comm.loopback(P)
+    world = D.ThreadWorld(P)
+    u = torch.from_numpy(wl.u).cuda()
+    v = torch.from_numpy(wl.v).cuda()
+    w = None if wl.w is None else torch.from_numpy(wl.w).cuda()
+    bounds = fj.partition_rows(wl.n, u, v, P)
+    out, errs = [None] * P, []
+
+    def rank_main(r):
+        try:
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                G, _ = D.build_dist_graph(comm, r, wl.n, u, v, w, D.ThreadGroup(world, r), bounds=bounds, stream=st)
+                Sl = torch.from_numpy(np.ascontiguousarray(S[bounds[r]:bounds[r + 1]])).cuda()
+                z, q, rep = G.approxim(Sl, opts=opts, stream=st)
+                st.synchronize()
+                out[r] = (z.cpu().numpy(), q, rep, G.plan)
+                G.close()
+        except Exception as e:  # surface in the main thread
+            errs.append(e)
+            raise
+
+    ts = [threading.Thread(target=rank_main, args=(r,)) for r in range(P)]
+    [t.start() for t in ts]
+    [t.join(300) for t in ts]
+    comm.close()
+    assert not errs, errs
+    Z = np.concatenate([o[0] for o in out])
+    return Z, [o[1] for o in out], [o[2] for o in out], bounds, [o[3] for o in out]
+
+
+@pytest.mark.parametrize("P", [2, 3, 4])
+def test_loopback_c1_matches_dense_oracle(fj, P):
+    wl = synth.make_config("c1", k=2)
+    Z, Q, R, bounds, plans = run_ranks(fj, P, wl, wl.S)
+    g = O.canonical_csr(wl.n, wl.u, wl.v)
+    for c in range(2):
+        zo = O.solve_dense(g, wl.S[:, c])
+        qo = O.quantities(g, wl.S[:, c], zo)
+        assert np.max(np.abs(Z[:, c] - zo)) < 1e-9
+        for r in range(P):                      # identical global quantities on every rank
+            for k in QKEYS:
+                assert Q[r][c][k] == Q[0][c][k]
+                assert abs(Q[r][c][k] - qo[k]) / qo[k] <= 1e-8, (r, c, k)
+    assert all(R[r]["iterations"] == R[0]["iterations"] for r in range(P))
+    assert sum(p["nnz_local"] for p in plans) == g.nnz
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_loopback_weighted_rmat_vs_single(fj, P):
+    import torch
+    wl = synth.make_config("c4", scale=14, k=1)
+    Z, Q, R, bounds, plans = run_ranks(fj, P, wl, wl.S)
+    G = fj.Graph.from_edges(wl.n, torch.from_numpy(wl.u).cuda(), torch.from_numpy(wl.v).cuda(),
+                            torch.from_numpy(wl.w).cuda())
+    z1, q1, r1 = G.approxim(torch.from_numpy(wl.S.copy()).cuda())
+    assert np.max(np.abs(Z - z1.cpu().numpy())) < 1e-8
+    g = O.canonical_csr(wl.n, wl.u, wl.v, wl.w)
+    zo, _ = O.solve_pcg(g, wl.S[:, 0], tol=1e-13)
+    qo = O.quantities(g, wl.S[:, 0], zo)
+    for k in QKEYS:
+        assert abs(Q[0][0][k] - qo[k]) / qo[k] <= 1e-8, k
+        assert Q[0][0][k] == pytest.approx(q1[0][k], rel=1e-9)
+    assert R[0]["rel_res_true"] <= 1e-10
+
+
+def test_loopback_rows_build_bit_exact(fj):
+    """Row-block CSR (a1 per rank) concatenates to the oracle's canonical CSR."""
+    import torch
+    wl = synth.make_config("c4", scale=12, k=1)
+    u, v, w = (torch.from_numpy(a).cuda() for a in (wl.u, wl.v, wl.w))
+    g = O.canonical_csr(wl.n, wl.u, wl.v, wl.w)
+    bounds = fj.partition_rows(wl.n, u, v, 3)
+    assert bounds[0] == 0 and bounds[-1] == wl.n
+    cols, ws, rps = [], [], [np.zeros(1, np.int64)]
+    for r in range(3):
+        rp, cg, wo, nnz = fj.csr_rows_from_edges(wl.n, u, v, w, bounds[r], bounds[r + 1])
+        cols.append(cg.cpu().numpy())
+        ws.append(wo.cpu().numpy())
+        rps.append(rp.cpu().numpy()[1:] + rps[-1][-1])
+    assert np.array_equal(np.concatenate(rps), g.row_ptr)
+    assert np.array_equal(np.concatenate(cols), g.col)
+    assert np.array_equal(np.concatenate(ws), g.w)
