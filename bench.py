@@ -195,7 +195,22 @@ def main():
     opts = fj.SolveOpts.make(rtol=args.rtol, use_cuda_graph=not args.no_cuda_graph)
     stream = torch.cuda.current_stream()
 
+    dist_mode = ws > 1
+    if dist_mode:   # rows a8/e: the graph row-partitioned over the ranks, NCCL halo + allreduce
+        from paper_2101_08143_b200 import dist as FD
+        uid = [fj.Comm.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = fj.Comm.nccl(ws, rank, uid[0])
+        grp = FD.TorchGroup(None, device=f"cuda:{local}")
+
     def step():
+        if dist_mode:
+            G, b = FD.build_dist_graph(comm, rank, n, u, v, w, grp)   # partition + a1 + ghosts + plan + a2
+            Sl = S[b[rank]:b[rank + 1]].contiguous()
+            z, q, rep = G.approxim(Sl, opts=opts)
+            info = {"nnz": G.plan["nnz_local"], "bounds": b}
+            G.close()
+            return q, rep, info, G.plan
         rp, col, wo, st = fj.csr_from_edges(n, u, v, w)
         G = fj.Graph(n, rp, col, wo, validate=False)
         z, q, rep = G.approxim(S, opts=opts)
@@ -207,6 +222,10 @@ def main():
         q, rep, info, bst = step()
     torch.cuda.synchronize()
     nnz = info["nnz"]
+    if dist_mode:   # global nonzeros = sum of the ranks' blocks
+        t = torch.tensor([float(nnz)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t)
+        nnz = int(t[0])
     kb = k if rep["batch_k"] else 1
     B = canonical_bytes(n, nnz, wb, kb)      # one PCG iteration (batched over kb columns)
 
@@ -240,37 +259,43 @@ def main():
     clocks = sampler.stop()
 
     # dominant kernel: the (I+L)p tile SpMV, timed live with CUDA events on the launching stream
-    rp, col, wo, _ = fj.csr_from_edges(n, u, v, w)
-    G = fj.Graph(n, rp, col, wo, validate=False)
-    x = S.contiguous() if kb > 1 else S[:, 0].contiguous()
-    for _ in range(3):
-        G.apply(x)
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    flush.fill_(1)
-    e0.record(stream)
-    for _ in range(args.spmv_reps):
-        y = G.apply(x)
-    e1.record(stream)
-    e1.synchronize()
-    spmv_ms = e0.elapsed_time(e1) / args.spmv_reps
-    G.close()
+    spmv_ms = None
+    if not dist_mode:
+        rp, col, wo, _ = fj.csr_from_edges(n, u, v, w)
+        G = fj.Graph(n, rp, col, wo, validate=False)
+        x = S.contiguous() if kb > 1 else S[:, 0].contiguous()
+        for _ in range(3):
+            G.apply(x)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        flush.fill_(1)
+        e0.record(stream)
+        for _ in range(args.spmv_reps):
+            y = G.apply(x)
+        e1.record(stream)
+        e1.synchronize()
+        spmv_ms = e0.elapsed_time(e1) / args.spmv_reps
+        G.close()
 
     # aggregate over ranks: time = max over ranks, bytes = sum over ranks
     tot_loop_ms = loop_ms
     tot_bytes = B * iters
     max_step_ms = sum(step_ms)
-    if ws > 1:
+    if ws > 1:   # B is already the GLOBAL per-iteration traffic (all ranks iterate together)
         t = torch.tensor([loop_ms, sum(step_ms)], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        tb = torch.tensor([float(tot_bytes)], dtype=torch.float64, device="cuda")
-        dist.all_reduce(tb, op=dist.ReduceOp.SUM)
-        tot_loop_ms, max_step_ms, tot_bytes = float(t[0]), float(t[1]), float(tb[0])
+        tot_loop_ms, max_step_ms = float(t[0]), float(t[1])
     value = tot_bytes / (tot_loop_ms / 1e3) / 1e9
 
     peak, peak_src = load_peaks()
     Bs = spmv_bytes(n, nnz, wb, kb)
-    achieved = Bs / (spmv_ms / 1e3) / 1e9
+    if dist_mode:   # fj_apply is not available on a distributed handle: per-rank whole iteration
+        t_iter_ms = tot_loop_ms / max(iters, 1)
+        Bs = B / ws
+        achieved = Bs / (t_iter_ms / 1e3) / 1e9
+        spmv_ms = t_iter_ms
+    else:
+        achieved = Bs / (spmv_ms / 1e3) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
@@ -279,15 +304,18 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": max_step_ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong" if dist_mode else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{wl.name}: {wl.desc}", "n": n, "nnz": nnz, "k": k, "rtol": args.rtol,
-                   "opinions": wl.kinds, "parallelism": f"replicas{ws}" if ws > 1 else "1 GPU",
+                   "opinions": wl.kinds,
+                   "parallelism": f"row-partition x{ws} (NCCL halo + allreduce)" if dist_mode else "1 GPU",
                    "l2": "flushed between steps (512 MiB write, outside the timed events)",
                    "pcg_iterations_per_step": iters / args.steps,
                    "bytes_per_iteration": B, "fraction_of_measured_hbm": value / peak},
         "time_to_quantities_ms": statistics.median(ttq_ms),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": "warp_kernel<ApplyOp> ((I+L)p SpMV, warp-item engine)",
+                     "traffic": None if dist_mode else traffic,
+                     "kernel": ("whole distributed PCG iteration per rank (B(k)/N per iteration time)" if dist_mode
+                                else "warp_kernel<ApplyOp> ((I+L)p SpMV, warp-item engine)"),
                      "algorithmic_bytes_per_launch": Bs, "launch_ms": spmv_ms, "peak_source": peak_src},
         "clocks": clocks, "gpu_launches": launches1 - launches0,
         "cub_calls": cub1 - cub0, "wall_s_timed_region": wall,
@@ -296,7 +324,37 @@ def main():
     }
 
     # e2e: the public host-buffer call; H2D of the inputs and D2H of z + quantities inside the timing
-    if not args.no_e2e:
+    if not args.no_e2e and dist_mode:
+        # distributed e2e: every step copies the raw edge list and this rank's opinion slice from
+        # pinned host memory, runs the row-partitioned path and reads z + quantities back
+        uh, vh = torch.from_numpy(wl.u).pin_memory(), torch.from_numpy(wl.v).pin_memory()
+        wh = None if wl.w is None else torch.from_numpy(wl.w).pin_memory()
+        b = info["bounds"]
+        Sh = torch.from_numpy(np.ascontiguousarray(wl.S[b[rank]:b[rank + 1]])).pin_memory()
+        h2d = uh.nbytes + vh.nbytes + (0 if wh is None else wh.nbytes) + Sh.nbytes
+        d2h = Sh.nbytes + k * 200
+        e_ms, e_iters, reps = 0.0, 0, max(1, min(args.steps, 3))
+        for _ in range(reps):
+            torch.cuda.synchronize()
+            dist.barrier()
+            t = time.perf_counter()
+            ud, vd = uh.cuda(non_blocking=True), vh.cuda(non_blocking=True)
+            wd = None if wh is None else wh.cuda(non_blocking=True)
+            Sd = Sh.cuda(non_blocking=True)
+            G, _ = FD.build_dist_graph(comm, rank, n, ud, vd, wd, grp)
+            zd, qh, reph = G.approxim(Sd, opts=opts)
+            zh = zd.cpu()
+            G.close()
+            e_ms += (time.perf_counter() - t) * 1e3
+            e_iters += reph["iterations_total"]
+        t = torch.tensor([e_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e_ms = float(t[0])
+        line["e2e"] = {"value": B * e_iters / (e_ms / 1e3) / 1e9, "unit": "GB/s", "h2d_bytes_per_step": h2d,
+                       "d2h_bytes_per_step": d2h, "ms_per_step": e_ms / reps,
+                       "note": "per rank: pinned H2D of the raw edges + opinion slice, partition, row-block CSR, "
+                               "halo plan, distributed Algorithm 1, D2H z; host wall clock, max over ranks"}
+    if not args.no_e2e and not dist_mode:
         uh = torch.from_numpy(wl.u).pin_memory().numpy()
         vh = torch.from_numpy(wl.v).pin_memory().numpy()
         wh = None if wl.w is None else torch.from_numpy(wl.w).pin_memory().numpy()

@@ -141,7 +141,7 @@ static DistInfo* D(const fj_graph* g) { return reinterpret_cast<DistInfo*>(g->di
 // ---------------------------------------------------------------- collectives
 static fj_status allreduce(DistInfo* d, double* buf, int count, RedOp op, cudaStream_t st) {
   fj_comm* c = d->comm;
-  if (c->nranks == 1) return FJ_OK;
+  if (c->nranks == 1 && !c->nccl) return FJ_OK;
   if (c->kind == 0) {
     NcclApi* api = nullptr;
     FJ_TRY(nccl_api(&api));
@@ -648,7 +648,8 @@ fj_status fj_comm_init(int nranks, int rank, const unsigned char id[128], fj_com
   c->kind = 0;
   c->nranks = nranks;
   c->rank = rank;
-  if (nranks > 1) {
+  // a 1-rank communicator skips NCCL unless FJ_NCCL_FORCE is set (exercises the NCCL calls on one GPU)
+  if (nranks > 1 || getenv("FJ_NCCL_FORCE")) {
     NcclApi* api = nullptr;
     fj_status s = nccl_api(&api);
     if (s != FJ_OK) { delete c; return s; }

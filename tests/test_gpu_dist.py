@@ -111,3 +111,27 @@ def test_loopback_rows_build_bit_exact(fj):
     assert np.array_equal(np.concatenate(rps), g.row_ptr)
     assert np.array_equal(np.concatenate(cols), g.col)
     assert np.array_equal(np.concatenate(ws), g.w)
+
+
+def test_nccl_single_rank_comm(fj, monkeypatch):
+    """The NCCL transport on a 1-rank communicator (dlopen, ncclCommInitRank, ncclAllReduce on the
+    device scalars) gives the single-GPU result.  Multi-rank NCCL needs several GPUs (bench.py under
+    torchrun); its plan / exchange logic is covered by the gloo and loopback tests."""
+    import torch
+    from paper_2101_08143_b200 import dist as D
+    monkeypatch.setenv("FJ_NCCL_FORCE", "1")
+    uid = fj.Comm.unique_id()
+    assert len(uid) == 128
+    comm = fj.Comm.nccl(1, 0, uid)
+    wl = synth.make_config("c1", k=1)
+    u, v = torch.from_numpy(wl.u).cuda(), torch.from_numpy(wl.v).cuda()
+    G, b = D.build_dist_graph(comm, 0, wl.n, u, v, None, D.ThreadGroup(D.ThreadWorld(1), 0))
+    assert b == [0, wl.n]
+    z, q, rep = G.approxim(torch.from_numpy(wl.S.copy()).cuda())
+    G1 = fj.Graph.from_edges(wl.n, u, v)
+    z1, q1, rep1 = G1.approxim(torch.from_numpy(wl.S.copy()).cuda())
+    assert np.max(np.abs(z.cpu().numpy() - z1.cpu().numpy())) < 1e-12
+    for k in QKEYS:
+        assert q[0][k] == pytest.approx(q1[0][k], rel=1e-12)
+    G.close()
+    comm.close()
