@@ -38,6 +38,12 @@ inline cudaError_t dmalloc(T** p, size_t bytes, cudaStream_t st) {
   return cudaMallocFromPoolAsync(reinterpret_cast<void**>(p), bytes, lib_pool(dev), st);
 }
 
+// Return pool memory stream-ordered on the legacy stream (callers synchronise the device first);
+// plain cudaFree on pool memory would hand it back to the OS and the next graph would re-map it.
+inline void dfree(void* p) {
+  if (p) cudaFreeAsync(p, 0);
+}
+
 // FJ_TIMING=1: host-side phase timestamps on stderr (diagnostics; synchronises the stream)
 void phase_tick(const char* label, cudaStream_t st);
 

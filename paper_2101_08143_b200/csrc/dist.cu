@@ -616,9 +616,9 @@ void free_dist(fj_graph* g) {
   if (d->comm && d->comm->kind == 1 && d->comm->world) {
     d->comm->world->send_buf[d->rank] = nullptr;
   }
-  cudaFree(d->col_local); cudaFree(d->send_idx); cudaFree(d->send_buf);
-  cudaFree(d->x); cudaFree(d->r); cudaFree(d->p); cudaFree(d->q); cudaFree(d->red); cudaFree(d->sc);
-  cudaFree(d->elem_part); cudaFree(d->elem_ticket);
+  dfree(d->col_local); dfree(d->send_idx); dfree(d->send_buf);
+  dfree(d->x); dfree(d->r); dfree(d->p); dfree(d->q); dfree(d->red); dfree(d->sc);
+  dfree(d->elem_part); dfree(d->elem_ticket);
   if (d->ev0) cudaEventDestroy(d->ev0);
   if (d->ev1) cudaEventDestroy(d->ev1);
   delete d;
@@ -780,7 +780,7 @@ fj_status fj_graph_create_dist(fj_comm* comm, int rank, int64_t n_global, const 
   d->n_loc = nl;
   d->n_ghost = n_ghost;
   d->bounds.assign(bounds, bounds + P + 1);
-  auto bail = [&](fj_status s) { cudaFree(d->col_local); cudaFree(d->send_idx); cudaFree(d->send_buf); delete d; return s; };
+  auto bail = [&](fj_status s) { dfree(d->col_local); dfree(d->send_idx); dfree(d->send_buf); delete d; return s; };
   cudaError_t ce = dmalloc(&d->col_local, sizeof(int32_t) * std::max<int64_t>(nnz_local, 1), st);
   if (ce != cudaSuccess) return bail(cuda_fail(ce, "dmalloc", __FILE__, __LINE__));
   if (nnz_local > 0) {

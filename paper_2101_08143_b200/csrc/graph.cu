@@ -318,7 +318,7 @@ fj_status fj_graph_destroy(fj_graph* g) {
   free_quant_ws(g);
   free_batch_ws(g);
   free_dist(g);
-  cudaFree(g->deg); cudaFree(g->dinv);
+  dfree(g->deg); dfree(g->dinv);
   free_sched(g->s1);
   free_sched(g->sb);
   delete g;

@@ -35,11 +35,11 @@ void free_solve_ws(fj_graph* g) {
   if (w->ev1) cudaEventDestroy(w->ev1);
   if (w->ev2) cudaEventDestroy(w->ev2);
   if (w->ev3) cudaEventDestroy(w->ev3);
-  cudaFree(w->r); cudaFree(w->p); cudaFree(w->q); cudaFree(w->x); cudaFree(w->col_s);
-  cudaFree(w->sc); cudaFree(w->elem_part); cudaFree(w->elem_ticket);
-  cudaFree(w->ts.block_part); cudaFree(w->ts.long_part); cudaFree(w->ts.chunk_acc);
-  cudaFree(w->ts.long_ticket); cudaFree(w->ts.grid_ticket);
-  cudaFree(w->qout); cudaFree(w->stat);
+  dfree(w->r); dfree(w->p); dfree(w->q); dfree(w->x); dfree(w->col_s);
+  dfree(w->sc); dfree(w->elem_part); dfree(w->elem_ticket);
+  dfree(w->ts.block_part); dfree(w->ts.long_part); dfree(w->ts.chunk_acc);
+  dfree(w->ts.long_ticket); dfree(w->ts.grid_ticket);
+  dfree(w->qout); dfree(w->stat);
   delete w;
   g->solve_ws = nullptr;
 }

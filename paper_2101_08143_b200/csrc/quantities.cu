@@ -208,6 +208,16 @@ fj_status fj_quantities(const fj_graph* gc, int k, const double* s, const double
   FJ_TRY(get_ws(g, st, &w));
   std::vector<double> v;
   FJ_TRY(stats_cols(g, w, k, s, v, st));
+  if (k >= batch_min_k() && !is_dist(g)) {   // all columns in one pass
+    std::vector<double> means(k), sums(10 * (size_t)k);
+    for (int c = 0; c < k; ++c) means[c] = v[4 * c] / (double)global_n(g);
+    FJ_TRY(quant_batch(g, k, s, z, means.data(), sums.data(), st));
+    for (int c = 0; c < k; ++c) {
+      memset(&out[c], 0, sizeof(fj_quantities_t));
+      fill_quantities(g, &sums[10 * (size_t)c], means[c], out[c]);
+    }
+    return FJ_OK;
+  }
   for (int c = 0; c < k; ++c) {
     double t[10];
     const double m = v[4 * c] / (double)global_n(g);
@@ -251,7 +261,6 @@ fj_status fj_approxim(const fj_graph* gc, int k, const double* s, double* z_user
     // row a9: all k columns in ONE batched PCG (per-column alpha/beta, convergence mask)
     fj_solve_opts oc = o;
     int warm = 0, spent = 0;
-    double t[10];
     for (;;) {
       fj_solve_opts ob = oc;
       ob.max_iter = std::max(0, o.max_iter - spent);
@@ -270,17 +279,22 @@ fj_status fj_approxim(const fj_graph* gc, int k, const double* s, double* z_user
       r.rel_res_recursive = rb.rel_res_recursive;
       r.batch_k = k;
       double emax = 0.0;
+      std::vector<double> means(k), sums(10 * (size_t)k);
       for (int c = 0; c < k; ++c) {
-        const double m = v[4 * c] / (double)global_n(g);
+        means[c] = v[4 * c] / (double)global_n(g);
         if (v[4 * c + 2] == v[4 * c + 3]) {   // s = c 1: z = s exactly (P:L129 Omega 1 = 1)
           k_copy_cols<<<cb, 256, 0, st>>>(g->n, k, c, s, z);
           FJ_CK_LAUNCH();
+        }
+      }
+      FJ_TRY(quant_batch(g, k, s, z, means.data(), sums.data(), st));   // Alg. 1 lines 5-9, all columns
+      for (int c = 0; c < k; ++c) {
+        if (v[4 * c + 2] == v[4 * c + 3]) {
           consensus_quantities(g, v[4 * c + 2], qout[c]);
           continue;
         }
-        FJ_TRY(quant_pass(g, w, s, z, k, c, m, t, st));                 // Alg. 1 lines 5-9
         memset(&qout[c], 0, sizeof(fj_quantities_t));
-        fill_quantities(g, t, m, qout[c]);
+        fill_quantities(g, &sums[10 * (size_t)c], means[c], qout[c]);
         for (int j = 0; j < 6; ++j) emax = std::max(emax, qout[c].eps[j]);
       }
       phase_tick("approxim: quantities", st);

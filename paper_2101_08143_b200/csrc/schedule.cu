@@ -94,7 +94,7 @@ __global__ void k_items(int64_t nseg, const int32_t* __restrict__ B, const int64
 static inline unsigned nb256(int64_t n) { return (unsigned)((n + 255) / 256); }
 
 void free_sched(Sched& s) {
-  cudaFree(s.items); cudaFree(s.long_nchunks); cudaFree(s.long_item0);
+  dfree(s.items); dfree(s.long_nchunks); dfree(s.long_item0);
   s = Sched();
 }
 

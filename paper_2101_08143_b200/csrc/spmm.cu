@@ -6,6 +6,7 @@
 // per-column dot products are per-lane (columns never mix), reduced over warps and blocks in a
 // fixed order, so results are bitwise reproducible.
 #include <cstring>
+#include <vector>
 
 #include "ops.cuh"
 #include "workspace.cuh"
@@ -422,6 +423,7 @@ struct BatchWs {
   BatchScalars* bs = nullptr;
   double *chunk_acc = nullptr, *long_part = nullptr, *block_part = nullptr, *elem_part = nullptr;
   unsigned int *long_ticket = nullptr, *grid_ticket = nullptr, *elem_ticket = nullptr;
+  double *q_chunk = nullptr, *q_long = nullptr, *q_block = nullptr, *q_out = nullptr;   // quant_batch
   cudaGraphExec_t exec = nullptr;
   cudaGraph_t graph = nullptr;
   cudaStream_t cap_stream = nullptr;
@@ -438,9 +440,10 @@ void free_batch_ws(fj_graph* g) {
   if (w->cap_stream) cudaStreamDestroy(w->cap_stream);
   if (w->ev2) cudaEventDestroy(w->ev2);
   if (w->ev3) cudaEventDestroy(w->ev3);
-  cudaFree(w->r); cudaFree(w->p); cudaFree(w->q); cudaFree(w->x); cudaFree(w->bs);
-  cudaFree(w->chunk_acc); cudaFree(w->long_part); cudaFree(w->block_part); cudaFree(w->elem_part);
-  cudaFree(w->long_ticket); cudaFree(w->grid_ticket); cudaFree(w->elem_ticket);
+  dfree(w->r); dfree(w->p); dfree(w->q); dfree(w->x); dfree(w->bs);
+  dfree(w->chunk_acc); dfree(w->long_part); dfree(w->block_part); dfree(w->elem_part);
+  dfree(w->long_ticket); dfree(w->grid_ticket); dfree(w->elem_ticket);
+  dfree(w->q_chunk); dfree(w->q_long); dfree(w->q_block); dfree(w->q_out);
   delete w;
   g->batch_ws = nullptr;
 }
@@ -456,7 +459,10 @@ static fj_status balloc(T** p, int64_t count, cudaStream_t st, bool zero = false
 static fj_status get_batch_ws(fj_graph* g, int k, cudaStream_t st, BatchWs** out) {
   BatchWs* w = g_batch_cache(g);
   if (w && w->k == k) { *out = w; return FJ_OK; }
-  if (w) free_batch_ws(g);
+  if (w) {
+    FJ_CK(cudaStreamSynchronize(st));   // the old buffers may still be in use on st
+    free_batch_ws(g);
+  }
   w = new BatchWs();
   g->batch_ws = w;
   w->k = k;
@@ -646,6 +652,261 @@ fj_status apply_batch(fj_graph* g, int k, const double* x, double* y, int opL, c
   BatchWs* w = nullptr;
   FJ_TRY(get_batch_ws(g, k, st, &w));
   return launch_spmm<BM_APPLY>(g, w, make_args(g, w, k, x, y, nullptr, opL), st);
+}
+
+// ---------------------------------------------------------------- batched fused quantities (a6, k cols)
+// Same traversal as spmm_kernel; per row and column: A = sum w z_j, Dd = sum w (z_i - z_j)^2,
+// Aa = sum w |z_j|, then the 10 per-row contributions of QuantOp (ops.cuh) for each column.
+constexpr int QNP = 10;
+
+struct QuantArgs {
+  int k;
+  const double* __restrict__ z;    // [n][k]
+  const double* __restrict__ s;    // [n][k]
+  const double* __restrict__ deg;
+  const double* __restrict__ mean; // [k] mean of s per column
+  double* chunk_acc;               // [n_chunks][3][64]
+  double* long_part;               // [n_long][10][64]
+  unsigned int* long_ticket;
+  double* block_part;              // [grid][10][64]
+  unsigned int* grid_ticket;
+  double* out;                     // [10][64]
+};
+
+template <int WT, bool PAIR>
+__device__ __forceinline__ void q_accumulate(const TileSched& sc, const QuantArgs& a, int64_t kb, int64_t ke, int lane,
+                                             double zi0, double zi1, double (&acc)[6]) {
+  constexpr int NB = 8;
+  const int k = a.k;
+  const int c0 = col0<PAIR>(lane), c1 = col1<PAIR>(lane);
+  const bool h0 = c0 < k, h1 = c1 < k;
+  for (int64_t kk = kb; kk < ke; kk += NB) {
+    const int nb = (int)min((int64_t)NB, ke - kk);
+    int32_t cl = 0;
+    double wl = 1.0;
+    if (lane < nb) {
+      cl = __ldg(sc.col + kk + lane);
+      if (WT != FJ_W_UNIT) wl = WeightT<WT>::get(sc.w, kk + lane);
+    }
+    double v0[NB], v1[NB];
+#pragma unroll
+    for (int u = 0; u < NB; ++u) {
+      const int64_t j = __shfl_sync(0xffffffffu, cl, u);
+      v0[u] = 0.0;
+      v1[u] = 0.0;
+      if (u < nb) {
+        if (PAIR) {
+          if (h0) { const double2 t = ld_gather2(a.z + j * k + c0, 1); v0[u] = t.x; v1[u] = t.y; }
+        } else {
+          if (h0) v0[u] = ld_plain(a.z + j * k + c0);
+          if (h1) v1[u] = ld_plain(a.z + j * k + c1);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < NB; ++u) {
+      const double wu = (WT == FJ_W_UNIT) ? 1.0 : __shfl_sync(0xffffffffu, wl, u);
+      if (u < nb) {
+        const double d0 = zi0 - v0[u], d1 = zi1 - v1[u];
+        acc[0] = fma(wu, v0[u], acc[0]);
+        acc[1] = fma(wu * d0, d0, acc[1]);
+        acc[2] = fma(wu, fabs(v0[u]), acc[2]);
+        acc[3] = fma(wu, v1[u], acc[3]);
+        acc[4] = fma(wu * d1, d1, acc[4]);
+        acc[5] = fma(wu, fabs(v1[u]), acc[5]);
+      }
+    }
+  }
+}
+
+template <int WT>
+__device__ __forceinline__ void q_finish_col(const QuantArgs& a, int64_t i, int c, double d, double zi, double A,
+                                             double Dd, double Aa, double (&p)[QNP]) {
+  const double si = a.s[i * a.k + c], m = a.mean[c];
+  const double t = fma(1.0 + d, zi, -A);
+  const double lz = fma(d, zi, -A);
+  const double r = si - t;
+  const double e1 = zi - si, e2 = zi - m, e3 = si - m;
+  const double ab = fabs(si) + fma(1.0 + d, fabs(zi), Aa);
+  p[0] = fma(e1, e1, p[0]);
+  p[1] += Dd;
+  p[2] = fma(e2, e2, p[2]);
+  p[3] = fma(zi, zi, p[3]);
+  p[4] = fma(si, zi, p[4]);
+  p[5] = fma(e3, e2, p[5]);
+  p[6] = fma(r, r, p[6]);
+  p[7] = fma(lz, lz, p[7]);
+  p[8] = fma(ab, ab, p[8]);
+  p[9] = fma(si, si, p[9]);
+}
+
+template <int WT, bool PAIR>
+__device__ __forceinline__ void q_row(const QuantArgs& a, int64_t i, int64_t len, int lane, double zi0, double zi1,
+                                      const double (&acc)[6], double (&p0)[QNP], double (&p1)[QNP]) {
+  const double d = (WT == FJ_W_UNIT) ? (double)len : a.deg[i];
+  const int c0 = col0<PAIR>(lane), c1 = col1<PAIR>(lane);
+  if (c0 < a.k) q_finish_col<WT>(a, i, c0, d, zi0, acc[0], acc[1], acc[2], p0);
+  if (c1 < a.k) q_finish_col<WT>(a, i, c1, d, zi1, acc[3], acc[4], acc[5], p1);
+}
+
+template <int WT, bool PAIR>
+__global__ void __launch_bounds__(BTPB) quant_batch_kernel(const TileSched sc, const QuantArgs a) {
+  __shared__ double s_red[BWPB][MAXK];
+  __shared__ bool s_last;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int k = a.k;
+  const int c0 = col0<PAIR>(lane), c1 = col1<PAIR>(lane);
+  double p0[QNP], p1[QNP];
+#pragma unroll
+  for (int j = 0; j < QNP; ++j) { p0[j] = 0.0; p1[j] = 0.0; }
+  auto zrow = [&](int64_t i, double& z0, double& z1) {
+    z0 = c0 < k ? a.z[i * k + c0] : 0.0;
+    z1 = c1 < k ? a.z[i * k + c1] : 0.0;
+  };
+  const int64_t nwarps = (int64_t)gridDim.x * BWPB;
+  for (int64_t it = (int64_t)blockIdx.x * BWPB + wib; it < sc.n_items; it += nwarps) {
+    const ItemMeta cur = sc.items[it];
+    const uint32_t type = cur.info >> 30;
+    if (type == IT_T) {
+      const int R = cur.info & 63;
+      const int64_t r0 = cur.r0;
+      int64_t rb = cur.k0;
+      for (int t = 0; t < R; ++t) {
+        const int64_t re = __ldg(sc.row_ptr + r0 + t + 1);
+        double z0, z1, acc[6] = {0, 0, 0, 0, 0, 0};
+        zrow(r0 + t, z0, z1);
+        q_accumulate<WT, PAIR>(sc, a, rb, re, lane, z0, z1, acc);
+        q_row<WT, PAIR>(a, r0 + t, re - rb, lane, z0, z1, acc, p0, p1);
+        rb = re;
+      }
+    } else {
+      const int64_t r = cur.r0;
+      const int64_t rb = __ldg(sc.row_ptr + r), re = __ldg(sc.row_ptr + r + 1);
+      const int64_t kb = cur.k0;
+      const int64_t ke = (type == IT_W) ? re : min(kb + (int64_t)sc.chunk, re);
+      double z0, z1, acc[6] = {0, 0, 0, 0, 0, 0};
+      zrow(r, z0, z1);
+      q_accumulate<WT, PAIR>(sc, a, kb, ke, lane, z0, z1, acc);
+      if (type == IT_W) {
+        q_row<WT, PAIR>(a, r, re - rb, lane, z0, z1, acc, p0, p1);
+      } else {
+        const uint32_t l = cur.info & 0x3FFFFFFFu;
+        const int64_t first = sc.long_item0[l];
+        const int32_t nch = sc.long_nchunks[l];
+#pragma unroll
+        for (int f = 0; f < 3; ++f) {
+          if (c0 < MAXK) a.chunk_acc[(it * 3 + f) * MAXK + c0] = acc[f];
+          if (c1 < MAXK) a.chunk_acc[(it * 3 + f) * MAXK + c1] = acc[3 + f];
+        }
+        __threadfence();
+        __syncwarp();
+        unsigned last = 0;
+        if (lane == 0) last = atomicAdd(a.long_ticket + l, 1u) == (unsigned)nch - 1u;
+        last = __shfl_sync(0xffffffffu, last, 0);
+        if (last) {
+          __threadfence();
+          double m[6] = {0, 0, 0, 0, 0, 0};
+          for (int32_t c = 0; c < nch; ++c) {   // chunk order
+#pragma unroll
+            for (int f = 0; f < 3; ++f) {
+              if (c0 < MAXK) m[f] += __ldcg(a.chunk_acc + ((first + c) * 3 + f) * MAXK + c0);
+              if (c1 < MAXK) m[3 + f] += __ldcg(a.chunk_acc + ((first + c) * 3 + f) * MAXK + c1);
+            }
+          }
+          double l0[QNP], l1[QNP];
+#pragma unroll
+          for (int j = 0; j < QNP; ++j) { l0[j] = 0.0; l1[j] = 0.0; }
+          q_row<WT, PAIR>(a, r, re - rb, lane, z0, z1, m, l0, l1);
+#pragma unroll
+          for (int j = 0; j < QNP; ++j) {
+            if (c0 < MAXK) a.long_part[((int64_t)l * QNP + j) * MAXK + c0] = l0[j];
+            if (c1 < MAXK) a.long_part[((int64_t)l * QNP + j) * MAXK + c1] = l1[j];
+          }
+          if (lane == 0) a.long_ticket[l] = 0u;
+        }
+      }
+    }
+  }
+  // per-column partials, one quantity at a time: warps in order, then blocks in order
+#pragma unroll
+  for (int j = 0; j < QNP; ++j) {
+    if (c0 < MAXK) s_red[wib][c0] = p0[j];
+    if (c1 < MAXK) s_red[wib][c1] = p1[j];
+    __syncthreads();
+    if (threadIdx.x < MAXK) {
+      double t = 0.0;
+      for (int w = 0; w < BWPB; ++w) t += s_red[w][threadIdx.x];
+      a.block_part[((int64_t)blockIdx.x * QNP + j) * MAXK + threadIdx.x] = t;
+    }
+    __syncthreads();
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(a.grid_ticket, 1u) == gridDim.x - 1u;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (threadIdx.x < MAXK) {
+    const int c = threadIdx.x;
+    for (int j = 0; j < QNP; ++j) {
+      double t = 0.0;
+      for (unsigned b = 0; b < gridDim.x; ++b) t += __ldcg(a.block_part + ((int64_t)b * QNP + j) * MAXK + c);
+      for (int64_t l = 0; l < sc.n_long; ++l) t += __ldcg(a.long_part + (l * QNP + j) * MAXK + c);
+      a.out[j * MAXK + c] = t;
+    }
+  }
+  if (threadIdx.x == 0) *a.grid_ticket = 0u;
+}
+
+template <int WT, bool PAIR>
+static fj_status launch_quant_batch_p(const fj_graph* g, const QuantArgs& a, cudaStream_t st) {
+  static int occ = 0;
+  if (occ == 0) {
+    FJ_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, quant_batch_kernel<WT, PAIR>, BTPB, 0));
+    if (occ < 1) occ = 1;
+  }
+  int64_t grid = (int64_t)g->num_sms * occ;
+  const int64_t need = (g->sb.n_items + BWPB - 1) / BWPB;
+  if (grid > need) grid = need > 0 ? need : 1;
+  quant_batch_kernel<WT, PAIR><<<(unsigned)grid, BTPB, 0, st>>>(make_sched(g, g->sb), a);
+  FJ_CK_LAUNCH();
+  return FJ_OK;
+}
+
+template <int WT>
+static fj_status launch_quant_batch_wt(const fj_graph* g, const QuantArgs& a, cudaStream_t st) {
+  const bool pair = (a.k % 2 == 0) && ((reinterpret_cast<uintptr_t>(a.z) & 15) == 0);
+  return pair ? launch_quant_batch_p<WT, true>(g, a, st) : launch_quant_batch_p<WT, false>(g, a, st);
+}
+
+// All k columns' 10 sums in one pass: host_out[c * 10 + j] (same order as QuantOp's partials).
+fj_status quant_batch(fj_graph* g, int k, const double* s, const double* z, const double* mean_host,
+                      double* host_out, cudaStream_t st) {
+  BatchWs* w = nullptr;
+  FJ_TRY(get_batch_ws(g, k, st, &w));
+  if (!w->q_chunk) {
+    FJ_TRY(balloc(&w->q_chunk, g->sb.n_long_chunks * 3 * MAXK, st));
+    FJ_TRY(balloc(&w->q_long, g->sb.n_long * QNP * MAXK, st));
+    FJ_TRY(balloc(&w->q_block, (int64_t)g->num_sms * (2048 / BTPB) * QNP * MAXK, st));
+    FJ_TRY(balloc(&w->q_out, QNP * MAXK + MAXK, st));
+  }
+  FJ_CK(cudaMemcpyAsync(w->q_out + QNP * MAXK, mean_host, sizeof(double) * k, cudaMemcpyHostToDevice, st));
+  QuantArgs a;
+  a.k = k; a.z = z; a.s = s; a.deg = g->deg; a.mean = w->q_out + QNP * MAXK;
+  a.chunk_acc = w->q_chunk; a.long_part = w->q_long; a.long_ticket = w->long_ticket;
+  a.block_part = w->q_block; a.grid_ticket = w->grid_ticket; a.out = w->q_out;
+  switch (g->wtype) {
+    case FJ_W_UNIT: FJ_TRY(launch_quant_batch_wt<FJ_W_UNIT>(g, a, st)); break;
+    case FJ_W_U8: FJ_TRY(launch_quant_batch_wt<FJ_W_U8>(g, a, st)); break;
+    case FJ_W_F32: FJ_TRY(launch_quant_batch_wt<FJ_W_F32>(g, a, st)); break;
+    default: FJ_TRY(launch_quant_batch_wt<FJ_W_F64>(g, a, st)); break;
+  }
+  std::vector<double> h(QNP * MAXK);
+  FJ_CK(cudaMemcpyAsync(h.data(), w->q_out, sizeof(double) * QNP * MAXK, cudaMemcpyDeviceToHost, st));
+  FJ_CK(cudaStreamSynchronize(st));
+  for (int c = 0; c < k; ++c)
+    for (int j = 0; j < QNP; ++j) host_out[c * QNP + j] = h[j * MAXK + c];
+  return FJ_OK;
 }
 
 }  // namespace fj

@@ -67,6 +67,8 @@ void free_batch_ws(fj_graph* g);   // spmm.cu
 fj_status solve_batch(fj_graph* g, int k, const double* s, double* z, const fj_solve_opts& o, int warm,
                       fj_solve_report* rep, cudaStream_t st);
 fj_status apply_batch(fj_graph* g, int k, const double* x, double* y, int opL, cudaStream_t st);
+fj_status quant_batch(fj_graph* g, int k, const double* s, const double* z, const double* mean_host,
+                      double* host_out /* [k][10] */, cudaStream_t st);
 // dist.cu
 void free_dist(fj_graph* g);
 bool is_dist(const fj_graph* g);
