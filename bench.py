@@ -41,6 +41,14 @@ def spmv_bytes(n, nnz, wb, k):
     return (4 + wb) * nnz + 8 * (n + 1) + 16 * n * k
 
 
+def spmv_kernel_name(k):
+    if k == 1:
+        return "warp_kernel<ApplyOp> ((I+L)p SpMV, warp-item engine, k = 1)"
+    if k <= 4:
+        return f"warp_kernel<ApplyOpV<KP={2 if k <= 2 else 4}>> ((I+L)P SpMM, warp-item engine, k = {k} padded)"
+    return f"spmm_kernel<BM_APPLY> ((I+L)P SpMM, warp per row, k = {k})"
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -258,23 +266,15 @@ def main():
     launches1, cub1 = binding.kernel_launches()
     clocks = sampler.stop()
 
-    # dominant kernel: the (I+L)p tile SpMV, timed live with CUDA events on the launching stream
+    # dominant kernel: the PCG's (I+L)p product exactly as the solve loop launches it (k columns,
+    # solver buffers), timed live inside the library with CUDA events on the launching stream
     spmv_ms = None
     if not dist_mode:
         rp, col, wo, _ = fj.csr_from_edges(n, u, v, w)
         G = fj.Graph(n, rp, col, wo, validate=False)
-        x = S.contiguous() if kb > 1 else S[:, 0].contiguous()
-        for _ in range(3):
-            G.apply(x)
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
+        G.approxim(S, opts=opts)          # fills the solver buffers with a real search direction
         flush.fill_(1)
-        e0.record(stream)
-        for _ in range(args.spmv_reps):
-            y = G.apply(x)
-        e1.record(stream)
-        e1.synchronize()
-        spmv_ms = e0.elapsed_time(e1) / args.spmv_reps
+        spmv_ms = G.time_spmv(k=kb, reps=args.spmv_reps)
         G.close()
 
     # aggregate over ranks: time = max over ranks, bytes = sum over ranks
@@ -296,6 +296,18 @@ def main():
         spmv_ms = t_iter_ms
     else:
         achieved = Bs / (spmv_ms / 1e3) / 1e9
+    # the SpMV's real bound: random gathers (one L2 sector request per nonzero), measured live by
+    # fj_probe_gather on the same vector size, index count and gather width
+    gather_roof = None
+    if not dist_mode:
+        width = 1 if kb == 1 else (2 if kb == 2 else 4)
+        probe = binding.probe_gather(n, nnz, width=width, reps=5)
+        ach = nnz / (spmv_ms / 1e3)
+        gather_roof = {"achieved_gathers_per_s": ach, "peak_gathers_per_s": probe, "frac": ach / probe,
+                       "width_doubles": width,
+                       "note": "peak = fj_probe_gather: nnz uniform random int32 indices streamed once, one "
+                               f"{8 * width}-byte gather each from an n-row vector, no row logic; achieved = "
+                               "nnz / SpMV launch time"}
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
@@ -315,8 +327,9 @@ def main():
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": None if dist_mode else traffic,
                      "kernel": ("whole distributed PCG iteration per rank (B(k)/N per iteration time)" if dist_mode
-                                else "warp_kernel<ApplyOp> ((I+L)p SpMV, warp-item engine)"),
+                                else spmv_kernel_name(kb)),
                      "algorithmic_bytes_per_launch": Bs, "launch_ms": spmv_ms, "peak_source": peak_src},
+        "gather_roofline": gather_roof,
         "clocks": clocks, "gpu_launches": launches1 - launches0,
         "cub_calls": cub1 - cub0, "wall_s_timed_region": wall,
         "quantities_step0": {kk: results[0][0][0][kk] for kk in ["CI", "D", "P", "C", "Idc", "PDI"]},

@@ -156,6 +156,21 @@ fj_status fj_graph_destroy(fj_graph* g);
  * (device).  x and y must not alias. */
 fj_status fj_apply(const fj_graph* g, int op, int k, const double* x_dev, double* y_dev, void* stream);
 
+/* Diagnostic (bench roofline): average device time in ms of ONE search-direction product
+ * q = (I + L) p exactly as the k-column PCG loop launches it (same kernel, same schedule, the
+ * library's own workspace buffers; their contents are left undefined), over `reps` back-to-back
+ * launches timed with CUDA events on `stream`.  Synchronises.  FJ_E_UNSUPPORTED on a distributed
+ * handle. */
+fj_status fj_time_spmv(const fj_graph* g, int k, int reps, float* ms_host, void* stream);
+
+/* Diagnostic (bench "gather roofline"): the random-gather rate this GPU sustains for the SpMV's
+ * access pattern without any row logic: m int32 indices uniform in [0, n_vec) streamed once, one
+ * gather of `width` (1, 2 or 4) contiguous doubles per index from an n_vec-row device vector
+ * (L2-resident when it fits), 8 gathers in flight per thread.  *gathers_per_s (host) receives
+ * indices processed per second over `reps` timed launches (CUDA events on `stream`; one warm-up
+ * launch).  Allocates and frees its own buffers.  Synchronises. */
+fj_status fj_probe_gather(int64_t n_vec, int64_t m, int width, int reps, double* gathers_per_s, void* stream);
+
 /* ---------------------------------------------------------------- a3: opinion statistics
  * stats_host[4*j + 0..3] = (sum s_j, sum s_j^2, min s_j, max s_j) for each column j of the
  * row-major [n][k] s_dev.  FJ_E_NONFINITE_INPUT if any entry is NaN/Inf.  Synchronises. */

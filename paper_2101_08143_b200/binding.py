@@ -85,6 +85,8 @@ def load_library(path: str = SO):
     L.fj_graph_degrees.argtypes = [_vp, _vp, _vp]
     L.fj_graph_destroy.argtypes = [_vp]
     L.fj_apply.argtypes = [_vp, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp]
+    L.fj_time_spmv.argtypes = [_vp, ctypes.c_int, ctypes.c_int, P(ctypes.c_float), _vp]
+    L.fj_probe_gather.argtypes = [_i64, _i64, ctypes.c_int, ctypes.c_int, P(ctypes.c_double), _vp]
     L.fj_opinion_stats.argtypes = [_vp, ctypes.c_int, _vp, _vp, _vp]
     L.fj_solve.argtypes = [_vp, ctypes.c_int, _vp, _vp, P(SolveOpts), P(SolveReport), _vp]
     L.fj_quantities.argtypes = [_vp, ctypes.c_int, _vp, _vp, P(Quantities), _vp]
@@ -102,7 +104,7 @@ def load_library(path: str = SO):
     L.fj_graph_create_dist.argtypes = [_vp, ctypes.c_int, _i64, _vp, _i64, _vp, _vp, _vp, ctypes.c_int, _i64, _vp,
                                        _vp, _vp, _vp, P(_vp)]
     for name in ["fj_csr_from_edges", "fj_graph_create", "fj_graph_info", "fj_graph_degrees", "fj_graph_destroy",
-                 "fj_apply", "fj_opinion_stats", "fj_solve", "fj_quantities", "fj_approxim", "fj_approxim_host",
+                 "fj_apply", "fj_time_spmv", "fj_probe_gather", "fj_opinion_stats", "fj_solve", "fj_quantities", "fj_approxim", "fj_approxim_host",
                  "fj_comm_unique_id", "fj_comm_init", "fj_comm_init_loopback", "fj_comm_destroy",
                  "fj_partition_rows", "fj_csr_rows_from_edges", "fj_dist_ghosts", "fj_graph_create_dist"]:
         getattr(L, name).restype = ctypes.c_int
@@ -119,6 +121,13 @@ def kernel_launches():
     c = _i64()
     n = lib().fj_kernel_launches(ctypes.byref(c))
     return int(n), int(c.value)
+
+
+def probe_gather(n_vec: int, m: int, width: int = 1, reps: int = 10, stream=None) -> float:
+    """Random-gather rate (indices / s) of fj_probe_gather: the SpMV's measured gather bound."""
+    r = ctypes.c_double()
+    _check(lib().fj_probe_gather(int(n_vec), int(m), int(width), int(reps), ctypes.byref(r), _stream(stream)))
+    return float(r.value)
 
 
 def _check(st: int, allow=()):
@@ -227,6 +236,12 @@ class Graph:
         y = torch.empty_like(x)
         _check(lib().fj_apply(self.handle, op, k, _ptr(x), _ptr(y), _stream(stream)))
         return y
+
+    def time_spmv(self, k: int = 1, reps: int = 20, stream=None) -> float:
+        """ms per launch of the k-column PCG product q = (I+L)p (fj_time_spmv; CUDA events)."""
+        ms = ctypes.c_float()
+        _check(lib().fj_time_spmv(self.handle, int(k), int(reps), ctypes.byref(ms), _stream(stream)))
+        return float(ms.value)
 
     def opinion_stats(self, s, stream=None):
         import numpy as np

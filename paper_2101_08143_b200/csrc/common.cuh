@@ -60,10 +60,14 @@ extern thread_local bool g_capturing;
 
 // ---------------------------------------------------------------- constants
 constexpr int MAXK = 64;
-// k >= batch_min_k() columns are solved together (row a9, spmm.cu); fewer columns run the k = 1
-// path once per column (a small-k row of the batched layout wastes most lanes).  FJ_BATCH_MIN_K
-// overrides (tests).
+// k >= batch_min_k() columns are solved together (row a9): 2 <= k <= 4 on the warp-item engine with
+// vector values (spmv_vec.cu), k > 4 on the warp-per-row engine (spmm.cu); fewer columns run the
+// k = 1 path once per column.  FJ_BATCH_MIN_K overrides (tests).
 int batch_min_k();
+// L2 policy bits of the row engine's stream loads (FJ_L2_HINT, default 1; tiles.cuh ld_col/ld_rp)
+int l2_hint();
+// padded row width of the small-k engine for k = 3 (default 4; FJ_VEC_PAD=0: unpadded 3; spmv_vec.cu)
+int vec_pad3();
 
 // ---------------------------------------------------------------- device workspace per solve
 struct SolveWs;   // pcg.cu
@@ -107,7 +111,8 @@ struct fj_graph {
   // caches
   fj::SolveWs* solve_ws = nullptr;
   fj::QuantWs* quant_ws = nullptr;
-  void* batch_ws = nullptr;       // spmm.cu BatchWs (k > 1)
+  void* batch_ws = nullptr;       // spmm.cu BatchWs (k > 4)
+  void* vec_ws = nullptr;         // spmv_vec.cu VecWs (2 <= k <= 4)
   void* dist = nullptr;           // dist.cu DistInfo when this is one rank's row block
 };
 

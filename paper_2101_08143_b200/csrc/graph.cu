@@ -22,7 +22,23 @@ void count_launch(int64_t n) { g_launches += n; }
 int batch_min_k() {
   static const int v = [] {
     const char* e = getenv("FJ_BATCH_MIN_K");
-    return e ? std::max(2, atoi(e)) : 8;
+    return e ? std::max(2, atoi(e)) : 2;
+  }();
+  return v;
+}
+
+int l2_hint() {
+  static const int v = [] {
+    const char* e = getenv("FJ_L2_HINT");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
+}
+
+int vec_pad3() {
+  static const int v = [] {
+    const char* e = getenv("FJ_VEC_PAD");
+    return (e && atoi(e) == 0) ? 3 : 4;
   }();
   return v;
 }
@@ -317,6 +333,7 @@ fj_status fj_graph_destroy(fj_graph* g) {
   free_solve_ws(g);
   free_quant_ws(g);
   free_batch_ws(g);
+  free_vec_ws(g);
   free_dist(g);
   dfree(g->deg); dfree(g->dinv);
   free_sched(g->s1);

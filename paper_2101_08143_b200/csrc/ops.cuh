@@ -24,6 +24,8 @@ template <int WT>
 struct ApplyOp {
   static constexpr int NA = 1, NP = 1;
   static constexpr bool NEEDS_XI = false;
+  using V = double;
+  static __device__ __forceinline__ V vzero() { return 0.0; }
   const double* __restrict__ x;
   double* __restrict__ y;
   const double* __restrict__ deg;   // weighted degree (unused for unit weights)
@@ -41,6 +43,7 @@ struct ApplyOp {
 #endif
   }
   __device__ __forceinline__ double row_value(int64_t i) const { return __ldg(x + i * ld + c); }
+  __device__ __forceinline__ const double* xi_base() const { return ld == 1 ? x : nullptr; }
   __device__ __forceinline__ void add(double (&a)[NA], double w, double xj, double) const {
     if (WT == FJ_W_UNIT) a[0] += xj; else a[0] = fma(w, xj, a[0]);
   }
@@ -71,6 +74,8 @@ template <int WT>
 struct ResidOp {
   static constexpr int NA = 1, NP = 1;
   static constexpr bool NEEDS_XI = false;
+  using V = double;
+  static __device__ __forceinline__ V vzero() { return 0.0; }
   const double* __restrict__ z;     // contiguous [n]
   const double* __restrict__ s;     // column c of row-major [n][ld]
   const double* __restrict__ deg;
@@ -79,6 +84,7 @@ struct ResidOp {
   __device__ __forceinline__ bool skip() const { return false; }
   __device__ __forceinline__ double gather(int32_t j) const { return __ldg(z + j); }
   __device__ __forceinline__ double row_value(int64_t i) const { return __ldg(z + i); }
+  __device__ __forceinline__ const double* xi_base() const { return z; }
   __device__ __forceinline__ void add(double (&a)[NA], double w, double xj, double) const {
     if (WT == FJ_W_UNIT) a[0] += xj; else a[0] = fma(w, xj, a[0]);
   }
@@ -101,6 +107,8 @@ template <int WT>
 struct QuantOp {
   static constexpr int NA = 3, NP = 10;
   static constexpr bool NEEDS_XI = true;
+  using V = double;
+  static __device__ __forceinline__ V vzero() { return 0.0; }
   const double* __restrict__ z;
   const double* __restrict__ s;
   const double* __restrict__ deg;
@@ -112,6 +120,9 @@ struct QuantOp {
   __device__ __forceinline__ int64_t zi(int64_t i) const { return zld < 0 ? i * ld + c : i * zld + zc; }
   __device__ __forceinline__ double gather(int32_t j) const { return __ldg(z + zi(j)); }
   __device__ __forceinline__ double row_value(int64_t i) const { return __ldg(z + zi(i)); }
+  __device__ __forceinline__ const double* xi_base() const {
+    return (zld < 0 ? (ld == 1 && c == 0) : (zld == 1 && zc == 0)) ? z : nullptr;
+  }
   __device__ __forceinline__ void add(double (&a)[NA], double w, double zj, double zi) const {
     const double df = zi - zj;
     a[0] = fma(w, zj, a[0]);

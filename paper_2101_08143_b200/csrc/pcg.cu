@@ -369,6 +369,26 @@ fj_status fj_apply(const fj_graph* gc, int op, int k, const double* x, double* y
   return apply_col(g, w, x, y, 1, 0, op == FJ_OP_L ? 1 : 0, st);
 }
 
+fj_status fj_time_spmv(const fj_graph* gc, int k, int reps, float* ms_host, void* stream) {
+  if (!gc || !ms_host) return fail(FJ_E_INVALID_ARG, "null argument");
+  if (k < 1 || k > MAXK || reps < 1) return fail(FJ_E_INVALID_ARG, "k must be in [1, 64], reps >= 1");
+  fj_graph* g = const_cast<fj_graph*>(gc);
+  cudaStream_t st = S(stream);
+  if (is_dist(g)) return fail(FJ_E_UNSUPPORTED, "fj_time_spmv on a distributed graph");
+  if (k >= batch_min_k()) return time_batch_spmv(g, k, reps, ms_host, st);
+  SolveWs* w = nullptr;
+  FJ_TRY(get_ws(g, st, &w));
+  FJ_TRY(apply_col(g, w, w->p, w->q, 1, 0, 0, st));
+  FJ_CK(cudaEventRecord(w->ev2, st));
+  for (int i = 0; i < reps; ++i) FJ_TRY(apply_col(g, w, w->p, w->q, 1, 0, 0, st));
+  FJ_CK(cudaEventRecord(w->ev3, st));
+  FJ_CK(cudaEventSynchronize(w->ev3));
+  float ms = 0.f;
+  FJ_CK(cudaEventElapsedTime(&ms, w->ev2, w->ev3));
+  *ms_host = ms / (float)reps;
+  return FJ_OK;
+}
+
 fj_status fj_solve(const fj_graph* gc, int k, const double* s, double* z, const fj_solve_opts* opts,
                    fj_solve_report* rep, void* stream) {
   if (!gc || !s || !z) return fail(FJ_E_INVALID_ARG, "null argument");

@@ -280,14 +280,16 @@ fj_status fj_approxim(const fj_graph* gc, int k, const double* s, double* z_user
       r.batch_k = k;
       double emax = 0.0;
       std::vector<double> means(k), sums(10 * (size_t)k);
+      bool z_is_solve = true;   // z untouched since the solve: its padded solver copy may be gathered
       for (int c = 0; c < k; ++c) {
         means[c] = v[4 * c] / (double)global_n(g);
         if (v[4 * c + 2] == v[4 * c + 3]) {   // s = c 1: z = s exactly (P:L129 Omega 1 = 1)
           k_copy_cols<<<cb, 256, 0, st>>>(g->n, k, c, s, z);
           FJ_CK_LAUNCH();
+          z_is_solve = false;
         }
       }
-      FJ_TRY(quant_batch(g, k, s, z, means.data(), sums.data(), st));   // Alg. 1 lines 5-9, all columns
+      FJ_TRY(quant_batch(g, k, s, z, means.data(), sums.data(), st, z_is_solve));   // Alg. 1 lines 5-9
       for (int c = 0; c < k; ++c) {
         if (v[4 * c + 2] == v[4 * c + 3]) {
           consensus_quantities(g, v[4 * c + 2], qout[c]);

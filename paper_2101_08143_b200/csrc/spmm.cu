@@ -578,6 +578,7 @@ static fj_status build_batch_graph(fj_graph* g, BatchWs* w) {
 // columns together, warm) up to max_restarts times.
 fj_status solve_batch(fj_graph* g, int k, const double* s, double* z, const fj_solve_opts& o, int warm,
                       fj_solve_report* rep, cudaStream_t st) {
+  if (vec_supported(k)) return solve_vec(g, k, s, z, o, warm, rep, st);
   BatchWs* w = nullptr;
   FJ_TRY(get_batch_ws(g, k, st, &w));
   const int64_t nk = g->n * (int64_t)k;
@@ -649,9 +650,27 @@ fj_status solve_batch(fj_graph* g, int k, const double* s, double* z, const fj_s
 }
 
 fj_status apply_batch(fj_graph* g, int k, const double* x, double* y, int opL, cudaStream_t st) {
+  if (vec_supported(k)) return apply_vec(g, k, x, y, opL, st);
   BatchWs* w = nullptr;
   FJ_TRY(get_batch_ws(g, k, st, &w));
   return launch_spmm<BM_APPLY>(g, w, make_args(g, w, k, x, y, nullptr, opL), st);
+}
+
+// Device time of one batched product q = (I+L) p on the solver's own buffers (bench roofline).
+fj_status time_batch_spmv(fj_graph* g, int k, int reps, float* ms_out, cudaStream_t st) {
+  if (vec_supported(k)) return time_vec_spmv(g, k, reps, ms_out, st);
+  BatchWs* w = nullptr;
+  FJ_TRY(get_batch_ws(g, k, st, &w));
+  const BatchArgs a = make_args(g, w, k, w->p, w->q, nullptr, 0);
+  FJ_TRY(launch_spmm<BM_APPLY>(g, w, a, st));
+  FJ_CK(cudaEventRecord(w->ev2, st));
+  for (int i = 0; i < reps; ++i) FJ_TRY(launch_spmm<BM_APPLY>(g, w, a, st));
+  FJ_CK(cudaEventRecord(w->ev3, st));
+  FJ_CK(cudaEventSynchronize(w->ev3));
+  float ms = 0.f;
+  FJ_CK(cudaEventElapsedTime(&ms, w->ev2, w->ev3));
+  *ms_out = ms / (float)std::max(reps, 1);
+  return FJ_OK;
 }
 
 // ---------------------------------------------------------------- batched fused quantities (a6, k cols)
@@ -881,7 +900,8 @@ static fj_status launch_quant_batch_wt(const fj_graph* g, const QuantArgs& a, cu
 
 // All k columns' 10 sums in one pass: host_out[c * 10 + j] (same order as QuantOp's partials).
 fj_status quant_batch(fj_graph* g, int k, const double* s, const double* z, const double* mean_host,
-                      double* host_out, cudaStream_t st) {
+                      double* host_out, cudaStream_t st, bool z_from_solve) {
+  if (vec_supported(k)) return quant_vec(g, k, s, z, mean_host, host_out, z_from_solve, st);
   BatchWs* w = nullptr;
   FJ_TRY(get_batch_ws(g, k, st, &w));
   if (!w->q_chunk) {

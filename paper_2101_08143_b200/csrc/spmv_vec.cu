@@ -1,0 +1,747 @@
+// spmv_vec.cu — row a9 for SMALL k (2 <= k <= 4): the k opinion columns are solved together on
+// the k = 1 warp-item engine (tiles.cuh) with a VECTOR value per nonzero.
+//
+// Why: the SpMV on these graphs is bound by the random 8-byte gathers (one L2 sector request per
+// nonzero), not by HBM.  Solving the columns one by one pays that request cost k
+// times.  Here the solver's vectors are row-major [n][KP] with KP = 2 (k = 2) or KP = 4 (k = 3, 4),
+// zero-padded, 32-byte aligned, so one neighbour row is ONE aligned 16/32-byte load (LDG.128 /
+// LDG.E.ENL2.256) = one L2 sector for all k columns.  The warp-per-row batched engine (spmm.cu)
+// would leave 32 - k lanes idle at this k.
+//
+// Per PCG iteration (same algebra as pcg.cu, per column):
+//   K_A warp_kernel<ApplyOpV>  q = (I+L) p (all columns), pq_c = p_c^T q_c -> alpha_c   (last block)
+//   K_B k_v_update             x += alpha p, r -= alpha q, rho'_c, ||r_c||^2 -> beta_c,
+//                              per-column convergence mask, loop condition             (last block)
+//   K_C k_v_dir                p = dinv o r + beta p
+// in one CUDA graph with a device-driven conditional WHILE node.  Columns that converged keep
+// alpha_c = 0 (x_c, r_c frozen).  All partial sums are formed and combined in a fixed order:
+// results are bitwise reproducible.
+#include <cstring>
+#include <vector>
+
+#include "ops.cuh"
+#include "workspace.cuh"
+
+namespace fj {
+
+constexpr int KVMAX = 4;     // widest padded row handled here
+constexpr int VETB = 256;    // elementwise kernels: one thread per row
+
+template <int KP>
+struct alignas(KP == 3 ? 8 : KP * 8) DVec {
+  double v[KP];
+};
+
+template <int KP> __device__ __forceinline__ DVec<KP> ld_vec(const double* p);
+template <> __device__ __forceinline__ DVec<2> ld_vec<2>(const double* p) {
+  DVec<2> r;
+  asm volatile("ld.global.v2.f64 {%0, %1}, [%2];" : "=d"(r.v[0]), "=d"(r.v[1]) : "l"(p));
+  return r;
+}
+template <> __device__ __forceinline__ DVec<4> ld_vec<4>(const double* p) {   // 256-bit LDG (sm_100)
+  DVec<4> r;
+  asm volatile("ld.global.v4.f64 {%0, %1, %2, %3}, [%4];"
+               : "=d"(r.v[0]), "=d"(r.v[1]), "=d"(r.v[2]), "=d"(r.v[3]) : "l"(p));
+  return r;
+}
+// KP = 3 (unpadded [n][3], 24-byte rows, base 16-byte aligned): one 16-byte pair + one 8-byte load.
+// Even rows start 16-byte aligned (pair = columns 0,1); odd rows end 16-byte aligned (pair = 1,2).
+// A row touches 1.5 sectors on average (vs 1 padded to 32 bytes, which no longer fits in L2 at C3).
+template <> __device__ __forceinline__ DVec<3> ld_vec<3>(const double* p) {
+  const bool odd = (reinterpret_cast<uintptr_t>(p) & 8) != 0;
+  const double* pp = p + (odd ? 1 : 0);
+  const double* ps = p + (odd ? 0 : 2);
+  double a, b, c;
+  asm volatile("ld.global.v2.f64 {%0, %1}, [%2];" : "=d"(a), "=d"(b) : "l"(pp));
+  asm volatile("ld.global.f64 %0, [%1];" : "=d"(c) : "l"(ps));
+  DVec<3> r;
+  r.v[0] = odd ? c : a;
+  r.v[1] = odd ? a : b;
+  r.v[2] = odd ? b : c;
+  return r;
+}
+template <int KP> __device__ __forceinline__ void st_vec(double* p, const DVec<KP>& v);
+template <> __device__ __forceinline__ void st_vec<3>(double* p, const DVec<3>& v) {
+  const bool odd = (reinterpret_cast<uintptr_t>(p) & 8) != 0;
+  const double a = odd ? v.v[1] : v.v[0], b = odd ? v.v[2] : v.v[1], c = odd ? v.v[0] : v.v[2];
+  asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(p + (odd ? 1 : 0)), "d"(a), "d"(b) : "memory");
+  asm volatile("st.global.f64 [%0], %1;" ::"l"(p + (odd ? 0 : 2)), "d"(c) : "memory");
+}
+template <> __device__ __forceinline__ void st_vec<2>(double* p, const DVec<2>& v) {
+  asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.v[0]), "d"(v.v[1]) : "memory");
+}
+template <> __device__ __forceinline__ void st_vec<4>(double* p, const DVec<4>& v) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(v.v[0]), "d"(v.v[1]), "d"(v.v[2]),
+               "d"(v.v[3]) : "memory");
+}
+template <int KP> __device__ __forceinline__ DVec<KP> vzero_kp() {
+  DVec<KP> r;
+#pragma unroll
+  for (int c = 0; c < KP; ++c) r.v[c] = 0.0;
+  return r;
+}
+
+// Device scalars of one small-k batched solve (per column), written only by last-block finalisers.
+struct VecScalars {
+  double rho[KVMAX], alpha[KVMAX], beta[KVMAX], pq[KVMAX], rr[KVMAX], ss[KVMAX], tol2[KVMAX], res2[KVMAX];
+  int32_t active[KVMAX], conv[KVMAX], breakdown[KVMAX];
+  int32_t iter, max_iter, done, k;
+};
+
+// ---------------------------------------------------------------- row operators (tiles.cuh Op)
+// q = (I+L) p or L p for all KP columns of a padded [n][KP] block (P:L88 L = D - A).
+template <int WT, int KP>
+struct ApplyOpV {
+  using V = DVec<KP>;
+  static constexpr int NA = KP, NP = KP;
+  static constexpr bool NEEDS_XI = false;
+  static __device__ __forceinline__ V vzero() { return vzero_kp<KP>(); }
+  const double* __restrict__ x;
+  double* __restrict__ y;
+  const double* __restrict__ deg;
+  int opL;
+  VecScalars* sc;   // PCG mode when non-null: alpha_c = rho_c / p_c^T q_c on device
+  int k;
+  __device__ __forceinline__ bool skip() const { return sc && *(volatile int32_t*)&sc->done; }
+  __device__ __forceinline__ V gather(int32_t j) const { return ld_vec<KP>(x + (int64_t)j * KP); }
+  __device__ __forceinline__ V row_value(int64_t i) const { return ld_vec<KP>(x + i * KP); }
+  __device__ __forceinline__ const V* xi_base() const { return reinterpret_cast<const V*>(x); }
+  __device__ __forceinline__ void add(double (&a)[NA], double w, const V& xj, const V&) const {
+#pragma unroll
+    for (int c = 0; c < KP; ++c) a[c] = (WT == FJ_W_UNIT) ? a[c] + xj.v[c] : fma(w, xj.v[c], a[c]);
+  }
+  __device__ __forceinline__ void finish_row(int64_t i, int64_t len, const V& xi, const double (&a)[NA],
+                                             double (&part)[NP]) const {
+    const double d = (WT == FJ_W_UNIT) ? (double)len : deg[i];
+    const double dd = opL ? d : 1.0 + d;
+    V yv;
+#pragma unroll
+    for (int c = 0; c < KP; ++c) {
+      yv.v[c] = fma(dd, xi.v[c], -a[c]);
+      part[c] = fma(xi.v[c], yv.v[c], part[c]);
+    }
+    st_vec<KP>(y + i * KP, yv);
+  }
+  __device__ __forceinline__ void finalize(const double (&tot)[NP]) const {
+    if (!sc) return;
+#pragma unroll
+    for (int c = 0; c < KP; ++c) {
+      if (c >= k) break;
+      sc->pq[c] = tot[c];
+      if (sc->active[c]) {
+        if (!(tot[c] > 0.0) || !isfinite(tot[c])) {   // I+L is SPD: p^T q > 0 unless p = 0
+          sc->alpha[c] = 0.0;
+          sc->active[c] = 0;
+          sc->breakdown[c] = 1;
+        } else {
+          sc->alpha[c] = sc->rho[c] / tot[c];
+        }
+      } else {
+        sc->alpha[c] = 0.0;
+      }
+    }
+  }
+};
+
+// ||s_c - (I+L) z_c||^2 per column: z padded [n][KP], s the caller's [n][k].
+template <int WT, int KP>
+struct ResidOpV {
+  using V = DVec<KP>;
+  static constexpr int NA = KP, NP = KP;
+  static constexpr bool NEEDS_XI = false;
+  static __device__ __forceinline__ V vzero() { return vzero_kp<KP>(); }
+  const double* __restrict__ z;
+  const double* __restrict__ s;
+  const double* __restrict__ deg;
+  int k;
+  VecScalars* sc;
+  __device__ __forceinline__ bool skip() const { return false; }
+  __device__ __forceinline__ V gather(int32_t j) const { return ld_vec<KP>(z + (int64_t)j * KP); }
+  __device__ __forceinline__ V row_value(int64_t i) const { return ld_vec<KP>(z + i * KP); }
+  __device__ __forceinline__ const V* xi_base() const { return reinterpret_cast<const V*>(z); }
+  __device__ __forceinline__ void add(double (&a)[NA], double w, const V& xj, const V&) const {
+#pragma unroll
+    for (int c = 0; c < KP; ++c) a[c] = (WT == FJ_W_UNIT) ? a[c] + xj.v[c] : fma(w, xj.v[c], a[c]);
+  }
+  __device__ __forceinline__ void finish_row(int64_t i, int64_t len, const V& zi, const double (&a)[NA],
+                                             double (&part)[NP]) const {
+    const double d = (WT == FJ_W_UNIT) ? (double)len : deg[i];
+#pragma unroll
+    for (int c = 0; c < KP; ++c) {
+      if (c < k) {
+        const double r = s[i * k + c] - fma(1.0 + d, zi.v[c], -a[c]);
+        part[c] = fma(r, r, part[c]);
+      }
+    }
+  }
+  __device__ __forceinline__ void finalize(const double (&tot)[NP]) const {
+#pragma unroll
+    for (int c = 0; c < KP; ++c)
+      if (c < k) sc->res2[c] = tot[c];
+  }
+};
+
+// Fused quantities pass (rows a5-a7) for all columns at once; the 10 per-row contributions of
+// QuantOp (ops.cuh) per column, part[j * KP + c].
+template <int WT, int KP>
+struct QuantOpV {
+  using V = DVec<KP>;
+  static constexpr int NA = 3 * KP, NP = 10 * KP;
+  static constexpr bool NEEDS_XI = true;
+  static __device__ __forceinline__ V vzero() { return vzero_kp<KP>(); }
+  const double* __restrict__ z;   // padded [n][KP]
+  const double* __restrict__ s;   // [n][k]
+  const double* __restrict__ deg;
+  int k;
+  double m[KP];                   // mean of s per column
+  double* out;                    // [10][KP]
+  __device__ __forceinline__ bool skip() const { return false; }
+  __device__ __forceinline__ V gather(int32_t j) const { return ld_vec<KP>(z + (int64_t)j * KP); }
+  __device__ __forceinline__ V row_value(int64_t i) const { return ld_vec<KP>(z + i * KP); }
+  __device__ __forceinline__ const V* xi_base() const { return reinterpret_cast<const V*>(z); }
+  __device__ __forceinline__ void add(double (&a)[NA], double w, const V& zj, const V& zi) const {
+#pragma unroll
+    for (int c = 0; c < KP; ++c) {
+      const double df = zi.v[c] - zj.v[c];
+      a[c] = fma(w, zj.v[c], a[c]);
+      a[KP + c] = fma(w * df, df, a[KP + c]);
+      a[2 * KP + c] = fma(w, fabs(zj.v[c]), a[2 * KP + c]);
+    }
+  }
+  __device__ __forceinline__ void finish_row(int64_t i, int64_t len, const V& zv, const double (&a)[NA],
+                                             double (&part)[NP]) const {
+    const double d = (WT == FJ_W_UNIT) ? (double)len : deg[i];
+#pragma unroll
+    for (int c = 0; c < KP; ++c) {
+      if (c >= k) break;
+      const double zi = zv.v[c];
+      const double si = s[i * k + c];
+      const double t = fma(1.0 + d, zi, -a[c]);
+      const double lz = fma(d, zi, -a[c]);
+      const double r = si - t;
+      const double e1 = zi - si, e2 = zi - m[c], e3 = si - m[c];
+      const double ab = fabs(si) + fma(1.0 + d, fabs(zi), a[2 * KP + c]);
+      part[0 * KP + c] = fma(e1, e1, part[0 * KP + c]);
+      part[1 * KP + c] += a[KP + c];
+      part[2 * KP + c] = fma(e2, e2, part[2 * KP + c]);
+      part[3 * KP + c] = fma(zi, zi, part[3 * KP + c]);
+      part[4 * KP + c] = fma(si, zi, part[4 * KP + c]);
+      part[5 * KP + c] = fma(e3, e2, part[5 * KP + c]);
+      part[6 * KP + c] = fma(r, r, part[6 * KP + c]);
+      part[7 * KP + c] = fma(lz, lz, part[7 * KP + c]);
+      part[8 * KP + c] = fma(ab, ab, part[8 * KP + c]);
+      part[9 * KP + c] = fma(si, si, part[9 * KP + c]);
+    }
+  }
+  __device__ __forceinline__ void finalize(const double (&tot)[NP]) const {
+#pragma unroll
+    for (int j = 0; j < NP; ++j) out[j] = tot[j];
+  }
+};
+
+// ---------------------------------------------------------------- elementwise kernels
+// One thread per row (KP values, one aligned vector load per array); fixed grid, per-column
+// partials reduced block -> last block in block order (deterministic).
+template <int NPART>
+__device__ __forceinline__ bool vec_reduce(double (&v)[NPART], double* part, unsigned int* ticket, double* s_red) {
+  block_sum<NPART, VETB>(v, s_red);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int j = 0; j < NPART; ++j) part[(int64_t)blockIdx.x * NPART + j] = v[j];
+  }
+  if (!last_block_ticket(ticket, gridDim.x)) return false;
+  double t[NPART];
+#pragma unroll
+  for (int j = 0; j < NPART; ++j) t[j] = 0.0;
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += VETB) {
+#pragma unroll
+    for (int j = 0; j < NPART; ++j) t[j] += __ldcg(part + (int64_t)b * NPART + j);
+  }
+  block_sum<NPART, VETB>(t, s_red);
+#pragma unroll
+  for (int j = 0; j < NPART; ++j) v[j] = t[j];
+  return true;
+}
+
+// fresh start (x = 0, r = s) or restart (r = s - q, q = (I+L) x precomputed); p = dinv o r.
+template <int KP>
+__global__ void __launch_bounds__(VETB) k_v_init(int64_t n, int k, const double* __restrict__ s,
+                                                 const double* __restrict__ dinv, const double* __restrict__ q,
+                                                 int restart, double* __restrict__ x, double* __restrict__ r,
+                                                 double* __restrict__ p, VecScalars* sc, double rtol, int max_iter,
+                                                 double* part, unsigned int* ticket) {
+  __shared__ double s_red[3 * KP * VETB / 32];
+  double v[3 * KP];
+#pragma unroll
+  for (int j = 0; j < 3 * KP; ++j) v[j] = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)VETB + threadIdx.x; i < n; i += (int64_t)gridDim.x * VETB) {
+    DVec<KP> sv, rv, pv;
+#pragma unroll
+    for (int c = 0; c < KP; ++c) sv.v[c] = c < k ? s[i * k + c] : 0.0;
+    if (restart) {
+      const DVec<KP> qv = ld_vec<KP>(q + i * KP);
+#pragma unroll
+      for (int c = 0; c < KP; ++c) rv.v[c] = c < k ? sv.v[c] - qv.v[c] : 0.0;
+    } else {
+      rv = sv;
+      st_vec<KP>(x + i * KP, vzero_kp<KP>());
+    }
+    const double di = dinv[i];
+#pragma unroll
+    for (int c = 0; c < KP; ++c) {
+      pv.v[c] = di * rv.v[c];
+      v[c] = fma(rv.v[c], pv.v[c], v[c]);
+      v[KP + c] = fma(rv.v[c], rv.v[c], v[KP + c]);
+      v[2 * KP + c] = fma(sv.v[c], sv.v[c], v[2 * KP + c]);
+    }
+    st_vec<KP>(r + i * KP, rv);
+    st_vec<KP>(p + i * KP, pv);
+  }
+  if (vec_reduce<3 * KP>(v, part, ticket, s_red) && threadIdx.x == 0) {
+    int any = 0;
+    for (int c = 0; c < k; ++c) {
+      sc->rho[c] = v[c];
+      sc->rr[c] = v[KP + c];
+      sc->ss[c] = v[2 * KP + c];
+      sc->tol2[c] = rtol * rtol * v[2 * KP + c];
+      const int conv = v[KP + c] <= sc->tol2[c];
+      sc->conv[c] = conv;
+      sc->active[c] = conv ? 0 : 1;
+      sc->breakdown[c] = 0;
+      sc->alpha[c] = sc->beta[c] = 0.0;
+      any |= sc->active[c];
+    }
+    sc->iter = 0;
+    sc->max_iter = max_iter;
+    sc->k = k;
+    sc->done = (!any || max_iter <= 0) ? 1 : 0;
+    *ticket = 0u;
+  }
+}
+
+template <int KP>
+__global__ void __launch_bounds__(VETB) k_v_update(int64_t n, int k, const double* __restrict__ dinv,
+                                                   const double* __restrict__ p, const double* __restrict__ q,
+                                                   double* __restrict__ x, double* __restrict__ r, VecScalars* sc,
+                                                   double* part, unsigned int* ticket, cudaGraphConditionalHandle h,
+                                                   int use_h) {
+  __shared__ double s_red[2 * KP * VETB / 32];
+  if (*(volatile int32_t*)&sc->done) {
+    if (use_h && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(h, 0);
+    return;
+  }
+  double al[KP];
+#pragma unroll
+  for (int c = 0; c < KP; ++c) al[c] = (c < k && sc->active[c]) ? sc->alpha[c] : 0.0;
+  double v[2 * KP];
+#pragma unroll
+  for (int j = 0; j < 2 * KP; ++j) v[j] = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)VETB + threadIdx.x; i < n; i += (int64_t)gridDim.x * VETB) {
+    const DVec<KP> pv = ld_vec<KP>(p + i * KP), qv = ld_vec<KP>(q + i * KP);
+    DVec<KP> xv = ld_vec<KP>(x + i * KP), rv = ld_vec<KP>(r + i * KP);
+    const double di = dinv[i];
+#pragma unroll
+    for (int c = 0; c < KP; ++c) {
+      xv.v[c] = fma(al[c], pv.v[c], xv.v[c]);
+      rv.v[c] = fma(-al[c], qv.v[c], rv.v[c]);
+      v[c] = fma(rv.v[c], di * rv.v[c], v[c]);
+      v[KP + c] = fma(rv.v[c], rv.v[c], v[KP + c]);
+    }
+    st_vec<KP>(x + i * KP, xv);
+    st_vec<KP>(r + i * KP, rv);
+  }
+  if (vec_reduce<2 * KP>(v, part, ticket, s_red) && threadIdx.x == 0) {
+    int any = 0;
+    for (int c = 0; c < k; ++c) {
+      if (sc->active[c]) {
+        sc->beta[c] = v[c] / sc->rho[c];
+        sc->rho[c] = v[c];
+        sc->rr[c] = v[KP + c];
+        const bool conv = v[KP + c] <= sc->tol2[c];
+        if (conv || !isfinite(v[KP + c])) { sc->active[c] = 0; sc->conv[c] = conv ? 1 : 0; }
+      }
+      any |= sc->active[c];
+    }
+    const int it = sc->iter + 1;
+    sc->iter = it;
+    if (!any || it >= sc->max_iter) {
+      sc->done = 1;
+      if (use_h) cudaGraphSetConditional(h, 0);
+    }
+    *ticket = 0u;
+  }
+}
+
+template <int KP>
+__global__ void __launch_bounds__(VETB) k_v_dir(int64_t n, int k, const double* __restrict__ dinv,
+                                                const double* __restrict__ r, double* __restrict__ p,
+                                                const VecScalars* sc) {
+  if (*(volatile const int32_t*)&sc->done) return;
+  double be[KP];
+#pragma unroll
+  for (int c = 0; c < KP; ++c) be[c] = (c < k && sc->active[c]) ? sc->beta[c] : 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)VETB + threadIdx.x; i < n; i += (int64_t)gridDim.x * VETB) {
+    const DVec<KP> rv = ld_vec<KP>(r + i * KP);
+    DVec<KP> pv = ld_vec<KP>(p + i * KP);
+    const double di = dinv[i];
+#pragma unroll
+    for (int c = 0; c < KP; ++c) pv.v[c] = fma(be[c], pv.v[c], di * rv.v[c]);
+    st_vec<KP>(p + i * KP, pv);
+  }
+}
+
+// [n][k] <-> padded [n][KP]
+template <int KP>
+__global__ void k_v_pack(int64_t n, int k, const double* __restrict__ src, double* __restrict__ dst) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    DVec<KP> v;
+#pragma unroll
+    for (int c = 0; c < KP; ++c) v.v[c] = c < k ? src[i * k + c] : 0.0;
+    st_vec<KP>(dst + i * KP, v);
+  }
+}
+template <int KP>
+__global__ void k_v_unpack(int64_t n, int k, const double* __restrict__ src, double* __restrict__ dst) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const DVec<KP> v = ld_vec<KP>(src + i * KP);
+#pragma unroll
+    for (int c = 0; c < KP; ++c)
+      if (c < k) dst[i * k + c] = v.v[c];
+  }
+}
+
+// ---------------------------------------------------------------- workspace
+constexpr int VNP_MAX = 10 * KVMAX, VNA_MAX = 3 * KVMAX;
+
+struct VecWs {
+  int k = 0, kp = 0;
+  int grid_elem = 0, grid_max = 0;
+  double *r = nullptr, *p = nullptr, *q = nullptr, *x = nullptr;
+  bool x_is_solution = false;        // x holds the padded z of the last solve_vec (for quant_vec)
+  VecScalars* sc = nullptr;
+  double* elem_part = nullptr;       // [grid_elem][3 * KVMAX]
+  unsigned int* elem_ticket = nullptr;
+  TileScratch ts{};
+  double* qout = nullptr;            // [VNP_MAX]
+  cudaGraphExec_t exec = nullptr;
+  cudaGraph_t graph = nullptr;
+  cudaStream_t cap_stream = nullptr;
+  cudaEvent_t ev2 = nullptr, ev3 = nullptr, ev4 = nullptr;
+};
+
+static VecWs* vec_cache(fj_graph* g) { return reinterpret_cast<VecWs*>(g->vec_ws); }
+
+void free_vec_ws(fj_graph* g) {
+  VecWs* w = vec_cache(g);
+  if (!w) return;
+  if (w->exec) cudaGraphExecDestroy(w->exec);
+  if (w->graph) cudaGraphDestroy(w->graph);
+  if (w->cap_stream) cudaStreamDestroy(w->cap_stream);
+  if (w->ev2) cudaEventDestroy(w->ev2);
+  if (w->ev3) cudaEventDestroy(w->ev3);
+  if (w->ev4) cudaEventDestroy(w->ev4);
+  dfree(w->r); dfree(w->p); dfree(w->q); dfree(w->x); dfree(w->sc);
+  dfree(w->elem_part); dfree(w->elem_ticket);
+  dfree(w->ts.block_part); dfree(w->ts.long_part); dfree(w->ts.chunk_acc);
+  dfree(w->ts.long_ticket); dfree(w->ts.grid_ticket); dfree(w->qout);
+  delete w;
+  g->vec_ws = nullptr;
+}
+
+template <class T>
+static fj_status valloc(T** p, int64_t count, cudaStream_t st, bool zero = false) {
+  if (count < 1) count = 1;
+  FJ_CK(dmalloc(p, sizeof(T) * (size_t)count, st));
+  if (zero) FJ_CK(cudaMemsetAsync(*p, 0, sizeof(T) * (size_t)count, st));
+  return FJ_OK;
+}
+
+static int kp_of(int k) { return k <= 2 ? 2 : k == 3 ? vec_pad3() : 4; }
+
+static fj_status get_vec_ws(fj_graph* g, int k, cudaStream_t st, VecWs** out) {
+  VecWs* w = vec_cache(g);
+  const int kp = kp_of(k);
+  if (w && w->kp == kp) { w->k = k; *out = w; return FJ_OK; }
+  if (w) {
+    FJ_CK(cudaStreamSynchronize(st));   // old buffers may still be in use on st
+    free_vec_ws(g);
+  }
+  w = new VecWs();
+  g->vec_ws = w;
+  w->k = k;
+  w->kp = kp;
+  const int64_t nk = g->n * (int64_t)kp;
+  FJ_TRY(valloc(&w->r, nk, st)); FJ_TRY(valloc(&w->p, nk, st));
+  FJ_TRY(valloc(&w->q, nk, st)); FJ_TRY(valloc(&w->x, nk, st));
+  FJ_TRY(valloc(&w->sc, 1, st, true));
+  int64_t ge = (int64_t)g->num_sms * (2048 / VETB);
+  const int64_t need = (g->n + VETB - 1) / VETB;
+  if (ge > need) ge = need > 0 ? need : 1;
+  w->grid_elem = (int)ge;
+  FJ_TRY(valloc(&w->elem_part, ge * 3 * KVMAX, st));
+  FJ_TRY(valloc(&w->elem_ticket, 1, st, true));
+  w->grid_max = g->num_sms * (2048 / WTPB);
+  FJ_TRY(valloc(&w->ts.block_part, (int64_t)w->grid_max * VNP_MAX, st));
+  FJ_TRY(valloc(&w->ts.long_part, g->s1.n_long * VNP_MAX, st));
+  FJ_TRY(valloc(&w->ts.chunk_acc, g->s1.n_long_chunks * VNA_MAX, st));
+  FJ_TRY(valloc(&w->ts.long_ticket, g->s1.n_long, st, true));
+  FJ_TRY(valloc(&w->ts.grid_ticket, 1, st, true));
+  FJ_TRY(valloc(&w->qout, VNP_MAX, st));
+  FJ_CK(cudaEventCreate(&w->ev2));
+  FJ_CK(cudaEventCreate(&w->ev3));
+  FJ_CK(cudaEventCreate(&w->ev4));
+  *out = w;
+  return FJ_OK;
+}
+
+// The warp-item engine on the k = 1 schedule (s1): same tiles, vector values.
+template <int WT, class Op>
+static fj_status launch_vec_items(const fj_graph* g, const VecWs* w, const Op& op, cudaStream_t st) {
+  static int occ = 0;   // per instantiation
+  if (occ == 0) {
+    FJ_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, warp_kernel<WT, Op>, WTPB, 0));
+    if (occ < 1) occ = 1;
+  }
+  int64_t grid = (int64_t)g->num_sms * occ;
+  const int64_t need = (g->s1.n_items + WPB - 1) / WPB;
+  if (grid > need) grid = need > 0 ? need : 1;
+  if (grid > w->grid_max) grid = w->grid_max;
+  warp_kernel<WT, Op><<<(unsigned)grid, WTPB, 0, st>>>(make_sched(g, g->s1), op, w->ts);
+  FJ_CK_LAUNCH();
+  return FJ_OK;
+}
+
+template <int KP, class F>
+static fj_status by_wtype(const fj_graph* g, F&& f) {
+  switch (g->wtype) {
+    case FJ_W_UNIT: return f(std::integral_constant<int, FJ_W_UNIT>());
+    case FJ_W_U8: return f(std::integral_constant<int, FJ_W_U8>());
+    case FJ_W_F32: return f(std::integral_constant<int, FJ_W_F32>());
+    default: return f(std::integral_constant<int, FJ_W_F64>());
+  }
+}
+
+template <int KP>
+static fj_status vec_apply_padded(const fj_graph* g, const VecWs* w, const double* x, double* y, int opL,
+                                  VecScalars* sc, cudaStream_t st) {
+  return by_wtype<KP>(g, [&](auto wt) {
+    constexpr int WT = decltype(wt)::value;
+    ApplyOpV<WT, KP> op{x, y, g->deg, opL, sc, w->k};
+    return launch_vec_items<WT>(g, w, op, st);
+  });
+}
+
+template <int KP>
+static fj_status vec_iteration(const fj_graph* g, VecWs* w, cudaStream_t st, cudaGraphConditionalHandle h, int use_h) {
+  FJ_TRY(vec_apply_padded<KP>(g, w, w->p, w->q, 0, w->sc, st));
+  k_v_update<KP><<<w->grid_elem, VETB, 0, st>>>(g->n, w->k, g->dinv, w->p, w->q, w->x, w->r, w->sc, w->elem_part,
+                                                w->elem_ticket, h, use_h);
+  FJ_CK_LAUNCH();
+  k_v_dir<KP><<<w->grid_elem, VETB, 0, st>>>(g->n, w->k, g->dinv, w->r, w->p, w->sc);
+  FJ_CK_LAUNCH();
+  return FJ_OK;
+}
+
+template <int KP>
+static fj_status build_vec_graph(fj_graph* g, VecWs* w) {
+  if (w->exec) return FJ_OK;
+  FJ_CK(cudaStreamCreateWithFlags(&w->cap_stream, cudaStreamNonBlocking));
+  FJ_CK(cudaGraphCreate(&w->graph, 0));
+  cudaGraphConditionalHandle h;
+  FJ_CK(cudaGraphConditionalHandleCreate(&h, w->graph, 1, cudaGraphCondAssignDefault));
+  alignas(cudaGraphNodeParams) unsigned char raw[sizeof(cudaGraphNodeParams)];
+  memset(raw, 0, sizeof raw);
+  cudaGraphNodeParams& cp = *reinterpret_cast<cudaGraphNodeParams*>(raw);
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  FJ_CK(cudaGraphAddNode(&node, w->graph, nullptr, 0, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  FJ_CK(cudaStreamBeginCaptureToGraph(w->cap_stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+  g_capturing = true;
+  fj_status s = vec_iteration<KP>(g, w, w->cap_stream, h, 1);
+  g_capturing = false;
+  cudaGraph_t captured = nullptr;
+  cudaError_t e = cudaStreamEndCapture(w->cap_stream, &captured);
+  FJ_TRY(s);
+  FJ_CK(e);
+  FJ_CK(cudaGraphInstantiate(&w->exec, w->graph, 0));
+  return FJ_OK;
+}
+
+template <int KP>
+static fj_status solve_vec_t(fj_graph* g, VecWs* w, int k, const double* s, double* z, const fj_solve_opts& o,
+                             int warm, fj_solve_report* rep, cudaStream_t st) {
+  const int64_t n = g->n;
+  const unsigned cb = (unsigned)std::min<int64_t>((n + 255) / 256, 8192);
+  w->x_is_solution = false;
+  if (o.use_cuda_graph) FJ_TRY(build_vec_graph<KP>(g, w));
+  VecScalars h{};
+  int restarts = 0, total_iter = 0;
+  bool first = true;
+  for (;;) {
+    const bool restart = !first || warm;
+    if (restart) {
+      if (first) { k_v_pack<KP><<<cb, 256, 0, st>>>(n, k, z, w->x); FJ_CK_LAUNCH(); }
+      FJ_TRY(vec_apply_padded<KP>(g, w, w->x, w->q, 0, nullptr, st));
+    }
+    const int budget = std::max(0, o.max_iter - total_iter);
+    FJ_CK(cudaEventRecord(w->ev2, st));
+    k_v_init<KP><<<w->grid_elem, VETB, 0, st>>>(n, k, s, g->dinv, w->q, restart ? 1 : 0, w->x, w->r, w->p, w->sc,
+                                                o.rtol, budget, w->elem_part, w->elem_ticket);
+    FJ_CK_LAUNCH();
+    first = false;
+    if (o.use_cuda_graph) {
+      FJ_CK(cudaGraphLaunch(w->exec, st));
+    } else {
+      for (;;) {
+        for (int u = 0; u < 8; ++u) FJ_TRY(vec_iteration<KP>(g, w, st, 0, 0));
+        int32_t done = 0;
+        FJ_CK(cudaMemcpyAsync(&done, &w->sc->done, sizeof done, cudaMemcpyDeviceToHost, st));
+        FJ_CK(cudaStreamSynchronize(st));
+        if (done) break;
+      }
+    }
+    FJ_CK(cudaEventRecord(w->ev3, st));
+    FJ_TRY(by_wtype<KP>(g, [&](auto wt) {   // true residual per column
+      constexpr int WT = decltype(wt)::value;
+      ResidOpV<WT, KP> op{w->x, s, g->deg, k, w->sc};
+      return launch_vec_items<WT>(g, w, op, st);
+    }));
+    FJ_CK(cudaMemcpyAsync(&h, w->sc, sizeof h, cudaMemcpyDeviceToHost, st));
+    FJ_CK(cudaStreamSynchronize(st));
+    total_iter += h.iter;
+    if (o.use_cuda_graph) count_launch(3 * std::max(h.iter, 1));
+    float lms = 0.f;
+    cudaEventElapsedTime(&lms, w->ev2, w->ev3);
+    if (rep) { rep->ms_loop += lms; rep->iterations_total += (int64_t)h.iter * k; }
+    bool ok = true, brk = false;
+    for (int c = 0; c < k; ++c) {
+      if (h.res2[c] > h.tol2[c]) ok = false;
+      if (h.breakdown[c]) brk = true;
+    }
+    if (ok || restarts >= o.max_restarts || total_iter >= o.max_iter || brk) break;
+    ++restarts;
+  }
+  k_v_unpack<KP><<<cb, 256, 0, st>>>(n, k, w->x, z);
+  FJ_CK_LAUNCH();
+  w->x_is_solution = true;
+  bool converged = true;
+  double worst_true = 0.0, worst_rec = 0.0;
+  for (int c = 0; c < k; ++c) {
+    if (h.res2[c] > h.tol2[c]) converged = false;
+    if (h.ss[c] > 0) {
+      worst_true = std::max(worst_true, std::sqrt(h.res2[c] / h.ss[c]));
+      worst_rec = std::max(worst_rec, std::sqrt(h.rr[c] / h.ss[c]));
+    }
+  }
+  if (rep) {
+    rep->iterations = std::max(rep->iterations, total_iter);
+    rep->restarts = std::max(rep->restarts, restarts);
+    rep->batch_k = k;
+    rep->rel_res_recursive = std::max(rep->rel_res_recursive, worst_rec);
+    rep->rel_res_true = std::isnan(rep->rel_res_true) ? worst_true : std::max(rep->rel_res_true, worst_true);
+    if (!converged) rep->converged = 0;
+  }
+  return converged ? FJ_OK : fail(FJ_E_NO_CONVERGENCE, "batched PCG did not reach rtol on the true residual");
+}
+
+// ---------------------------------------------------------------- entry points (workspace.cuh)
+bool vec_supported(int k) { return k >= 2 && k <= KVMAX; }
+
+fj_status solve_vec(fj_graph* g, int k, const double* s, double* z, const fj_solve_opts& o, int warm,
+                    fj_solve_report* rep, cudaStream_t st) {
+  VecWs* w = nullptr;
+  FJ_TRY(get_vec_ws(g, k, st, &w));
+  switch (w->kp) {
+    case 2: return solve_vec_t<2>(g, w, k, s, z, o, warm, rep, st);
+    case 3: return solve_vec_t<3>(g, w, k, s, z, o, warm, rep, st);
+    default: return solve_vec_t<4>(g, w, k, s, z, o, warm, rep, st);
+  }
+}
+
+fj_status apply_vec(fj_graph* g, int k, const double* x, double* y, int opL, cudaStream_t st) {
+  VecWs* w = nullptr;
+  FJ_TRY(get_vec_ws(g, k, st, &w));
+  w->x_is_solution = false;
+  const unsigned cb = (unsigned)std::min<int64_t>((g->n + 255) / 256, 8192);
+  auto run = [&](auto kpc) -> fj_status {
+    constexpr int KP = decltype(kpc)::value;
+    k_v_pack<KP><<<cb, 256, 0, st>>>(g->n, k, x, w->p);
+    FJ_CK_LAUNCH();
+    FJ_TRY(vec_apply_padded<KP>(g, w, w->p, w->q, opL, nullptr, st));
+    k_v_unpack<KP><<<cb, 256, 0, st>>>(g->n, k, w->q, y);
+    FJ_CK_LAUNCH();
+    return FJ_OK;
+  };
+  switch (w->kp) {
+    case 2: return run(std::integral_constant<int, 2>());
+    case 3: return run(std::integral_constant<int, 3>());
+    default: return run(std::integral_constant<int, 4>());
+  }
+}
+
+// Time `reps` launches of the PCG-mode product q = (I+L) p on the solver's own padded buffers
+// (the kernel the solve loop runs), CUDA events on st.  Diagnostic for the bench roofline.
+fj_status time_vec_spmv(fj_graph* g, int k, int reps, float* ms_out, cudaStream_t st) {
+  VecWs* w = nullptr;
+  FJ_TRY(get_vec_ws(g, k, st, &w));
+  w->x_is_solution = false;
+  auto run = [&]() -> fj_status {
+    switch (w->kp) {
+      case 2: return vec_apply_padded<2>(g, w, w->p, w->q, 0, nullptr, st);
+      case 3: return vec_apply_padded<3>(g, w, w->p, w->q, 0, nullptr, st);
+      default: return vec_apply_padded<4>(g, w, w->p, w->q, 0, nullptr, st);
+    }
+  };
+  FJ_TRY(run());
+  FJ_CK(cudaEventRecord(w->ev2, st));
+  for (int i = 0; i < reps; ++i) FJ_TRY(run());
+  FJ_CK(cudaEventRecord(w->ev3, st));
+  FJ_CK(cudaEventSynchronize(w->ev3));
+  float ms = 0.f;
+  FJ_CK(cudaEventElapsedTime(&ms, w->ev2, w->ev3));
+  *ms_out = ms / (float)std::max(reps, 1);
+  return FJ_OK;
+}
+
+// All k columns' 10 sums in one pass: host_out[c * 10 + j] (same order as QuantOp's partials).
+// If the last solve_vec on this graph produced z, its padded copy is gathered directly.
+fj_status quant_vec(fj_graph* g, int k, const double* s, const double* z, const double* mean_host,
+                    double* host_out, bool z_from_solve, cudaStream_t st) {
+  VecWs* w = nullptr;
+  FJ_TRY(get_vec_ws(g, k, st, &w));
+  const int kp = w->kp;
+  const unsigned cb = (unsigned)std::min<int64_t>((g->n + 255) / 256, 8192);
+  const double* zp = w->x;
+  if (!(z_from_solve && w->x_is_solution && w->k == k)) {
+    if (kp == 2) k_v_pack<2><<<cb, 256, 0, st>>>(g->n, k, z, w->q);
+    else if (kp == 3) k_v_pack<3><<<cb, 256, 0, st>>>(g->n, k, z, w->q);
+    else k_v_pack<4><<<cb, 256, 0, st>>>(g->n, k, z, w->q);
+    FJ_CK_LAUNCH();
+    zp = w->q;
+  }
+  auto launch = [&](auto kpc) -> fj_status {
+    constexpr int KP = decltype(kpc)::value;
+    return by_wtype<KP>(g, [&](auto wt) {
+      constexpr int WT = decltype(wt)::value;
+      QuantOpV<WT, KP> op;
+      op.z = zp; op.s = s; op.deg = g->deg; op.k = k; op.out = w->qout;
+      for (int c = 0; c < KP; ++c) op.m[c] = c < k ? mean_host[c] : 0.0;
+      return launch_vec_items<WT>(g, w, op, st);
+    });
+  };
+  if (kp == 2) FJ_TRY(launch(std::integral_constant<int, 2>()));
+  else if (kp == 3) FJ_TRY(launch(std::integral_constant<int, 3>()));
+  else FJ_TRY(launch(std::integral_constant<int, 4>()));
+  std::vector<double> h(10 * kp);
+  FJ_CK(cudaMemcpyAsync(h.data(), w->qout, sizeof(double) * 10 * kp, cudaMemcpyDeviceToHost, st));
+  FJ_CK(cudaStreamSynchronize(st));
+  for (int c = 0; c < k; ++c)
+    for (int j = 0; j < 10; ++j) host_out[c * 10 + j] = h[j * kp + c];
+  return FJ_OK;
+}
+
+}  // namespace fj

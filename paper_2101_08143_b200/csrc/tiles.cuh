@@ -37,7 +37,7 @@ struct ItemMeta {   // 16 bytes
 };
 
 struct TileSched {
-  int64_t n;
+  int64_t n, nnz;
   const int64_t* __restrict__ row_ptr;
   const int32_t* __restrict__ col;
   const void* __restrict__ w;
@@ -47,16 +47,38 @@ struct TileSched {
   const int32_t* __restrict__ long_item0;     // [n_long] item index of chunk 0
   int64_t n_long, n_chunks;
   int chunk;                                  // nonzeros per long-row chunk
+  int hint;                                   // bit 0: stream col / row_ptr with ld.global.cs (L2 evict-first);
+                                              // bit 1: disable the TMA tile prefetch
 };
+
+// Loads of the CSR streams (read once per product): with hint bit 0 they are marked evict-first so
+// they do not push the gathered vector out of L2.
+__device__ __forceinline__ int32_t ld_col(const TileSched& sc, int64_t p) {
+  if (sc.hint & 1) {
+    int32_t r;
+    asm volatile("ld.global.cs.s32 %0, [%1];" : "=r"(r) : "l"(sc.col + p));
+    return r;
+  }
+  return __ldg(sc.col + p);
+}
+__device__ __forceinline__ int64_t ld_rp(const TileSched& sc, int64_t i) {
+  if (sc.hint & 1) {
+    int64_t r;
+    asm volatile("ld.global.cs.s64 %0, [%1];" : "=l"(r) : "l"(sc.row_ptr + i));
+    return r;
+  }
+  return __ldg(sc.row_ptr + i);
+}
 
 inline TileSched make_sched(const fj_graph* g, const Sched& S) {
   TileSched s;
-  s.n = g->n; s.row_ptr = g->row_ptr; s.col = g->col; s.w = g->w;
+  s.n = g->n; s.nnz = g->nnz; s.row_ptr = g->row_ptr; s.col = g->col; s.w = g->w;
   s.items = reinterpret_cast<const ItemMeta*>(S.items);
   s.n_items = S.n_items;
   s.long_nchunks = S.long_nchunks; s.long_item0 = S.long_item0;
   s.n_long = S.n_long; s.n_chunks = S.n_long_chunks;
   s.chunk = S.chunk;
+  s.hint = l2_hint();
   return s;
 }
 
@@ -75,12 +97,15 @@ struct TileScratch {
 };
 
 // Op interface:
+//   using V;                                       // gathered value: double (k = 1) or DVec<KP> (k <= 4)
 //   static constexpr int NA, NP; static constexpr bool NEEDS_XI;
+//   static __device__ V vzero();
 //   __device__ bool skip() const;                  // uniform early exit (solver finished)
-//   __device__ double gather(int32_t j) const;     // x_j for a nonzero (i, j)
-//   __device__ double row_value(int64_t i) const;  // x_i
-//   __device__ void add(double (&a)[NA], double w, double xj, double xi) const;
-//   __device__ void finish_row(int64_t i, int64_t len, double xi, const double (&a)[NA], double (&part)[NP]) const;
+//   __device__ V gather(int32_t j) const;          // x_j for a nonzero (i, j)
+//   __device__ V row_value(int64_t i) const;       // x_i
+//   __device__ const V* xi_base() const;           // x_i = xi_base()[i] (contiguous), or nullptr
+//   __device__ void add(double (&a)[NA], double w, V xj, V xi) const;
+//   __device__ void finish_row(int64_t i, int64_t len, V xi, const double (&a)[NA], double (&part)[NP]) const;
 //   __device__ void finalize(const double (&tot)[NP]) const;   // single thread of the last block
 
 // Merge-path split (Merrill & Garland): on the merge of the row-end offsets A[0..R) with the nonzero
@@ -98,23 +123,37 @@ __device__ __forceinline__ int merge_rows_before(int d, const int32_t* A, int R,
 // the tile: it gathers its <= ITEMS values with independent loads, walks them finishing every row
 // that ends inside its range, and hands the partial of the row it ends inside to the next lanes
 // (warp segmented scan).  No shared-memory reduction, no idle lanes on ragged rows.
+// Tile inputs staged by the TMA bulk-copy prefetch (warp_kernel): the tile's col indices, row_ptr
+// entries and row values already sit in shared memory (null members: load them here).
+template <class V>
+struct TilePre {
+  const int32_t* col;     // col[k0 .. k0+N)
+  const int64_t* rp;      // row_ptr[r0+1 .. r0+R]
+  const V* xi;            // x[r0 .. r0+R)
+};
+
 template <int WT, class Op>
 __device__ __forceinline__ void t_tile(const TileSched& sc, const Op& op, const ItemMeta& cur, int lane,
-                                       int32_t* s_e, int32_t* s_col, double* s_xi,
-                                       double (&part)[Op::NP]) {
+                                       int32_t* s_e, int32_t* s_col_own, typename Op::V* s_xi_own,
+                                       double (&part)[Op::NP], const TilePre<typename Op::V>& pre) {
+  using V = typename Op::V;
   constexpr int NA = Op::NA;
   constexpr bool WEIGHTED = (WT != FJ_W_UNIT);
   const int R = cur.info & 63;
   const int N = (cur.info >> 6) & 0xFFFFF;
   const int64_t r0 = cur.r0, k0 = cur.k0;
+  const int32_t* s_col = pre.col ? pre.col : s_col_own;
+  const V* s_xi = pre.xi ? pre.xi : s_xi_own;
   if (lane < R) {
-    s_e[lane] = (int32_t)(__ldg(sc.row_ptr + r0 + lane + 1) - k0);
-    s_xi[lane] = op.row_value(r0 + lane);
+    s_e[lane] = (int32_t)((pre.rp ? pre.rp[lane] : ld_rp(sc, r0 + lane + 1)) - k0);
+    if (!pre.xi) s_xi_own[lane] = op.row_value(r0 + lane);
   }
+  if (!pre.col) {
 #pragma unroll
-  for (int u = 0; u < ITEMS; ++u) {
-    const int k = lane + 32 * u;
-    if (k < N) s_col[k] = __ldg(sc.col + k0 + k);
+    for (int u = 0; u < ITEMS; ++u) {
+      const int k = lane + 32 * u;
+      if (k < N) s_col_own[k] = ld_col(sc, k0 + k);
+    }
   }
   __syncwarp();
   const int M = R + N;
@@ -124,12 +163,12 @@ __device__ __forceinline__ void t_tile(const TileSched& sc, const Op& op, const 
   const int row_e = lane == 31 ? R : row_n;
   const int nz_s = d0 - row_s, nz_e = d1 - row_e;
   using WS = typename std::conditional<WT == FJ_W_F64, double, float>::type;   // exact for u8 / f32
-  double xv[ITEMS];
+  V xv[ITEMS];
   WS wv[ITEMS];
 #pragma unroll
   for (int j = 0; j < ITEMS; ++j) {
     const int k = nz_s + j;
-    xv[j] = 0.0;
+    xv[j] = Op::vzero();
     wv[j] = 1.0;
     if (k < nz_e) {
       xv[j] = op.gather(s_col[k]);
@@ -142,7 +181,7 @@ __device__ __forceinline__ void t_tile(const TileSched& sc, const Op& op, const 
   bool has_first = false;
   int row = row_s;
   int re = row < R ? s_e[row] : INT_MAX;
-  double xi = row < R ? s_xi[row] : 0.0;
+  V xi = row < R ? s_xi[row] : Op::vzero();
   auto close_row = [&](int r) {
     if (r == row_s) {           // may have started in earlier lanes: finish after the carry scan
       has_first = true;
@@ -163,7 +202,7 @@ __device__ __forceinline__ void t_tile(const TileSched& sc, const Op& op, const 
         close_row(row);
         ++row;
         re = row < R ? s_e[row] : INT_MAX;
-        xi = row < R ? s_xi[row] : 0.0;
+        xi = row < R ? s_xi[row] : Op::vzero();
       }
       op.add(a, (double)wv[j], xv[j], xi);
     }
@@ -196,15 +235,111 @@ __device__ __forceinline__ void t_tile(const TileSched& sc, const Op& op, const 
   __syncwarp();
 }
 
+// ---------------------------------------------------------------- TMA bulk-copy tile prefetch
+// While a warp works on one T tile, the TMA engine copies the NEXT tile's three contiguous input
+// ranges (col indices, row_ptr entries, row values) global -> shared (cp.async.bulk, completion on
+// a per-warp mbarrier, two slots).  The CSR stream latency then overlaps the current tile's gathers
+// instead of stalling the warp at the start of every tile.  Copies are 16-byte granular: each range
+// is widened to 16-byte boundaries (never past the array's last full 16-byte unit; such a tile,
+// and any tile whose base pointers are not 16-byte aligned, takes the plain-load path).
+constexpr int PF_COL_BYTES = T_CAP * 4 + 32;
+constexpr int PF_RP_BYTES = 32 * 8 + 32;
+template <class V>
+struct PfSlot {
+  static constexpr int XI_BYTES = 32 * (int)sizeof(V) + 32;
+  static constexpr int BYTES = ((PF_COL_BYTES + PF_RP_BYTES + XI_BYTES) + 15) & ~15;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile("{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+               " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+
+struct PfRange {   // one widened 16-byte-granular copy [b0, b1) of an array, in bytes from its base
+  int64_t b0, b1;
+};
+__device__ __forceinline__ PfRange pf_range(int64_t byte_begin, int64_t byte_end) {
+  return PfRange{byte_begin & ~(int64_t)15, (byte_end + 15) & ~(int64_t)15};
+}
+
+// Per-kernel limits (uniform): last full 16-byte unit of each array, or -1 if its base is unaligned.
+struct PfLimits {
+  int64_t col, rp, xi;
+};
+
+template <class Op>
+__device__ __forceinline__ bool pf_ok(const TileSched& sc, const Op& op, const ItemMeta& m, const PfLimits& L) {
+  using V = typename Op::V;
+  if ((m.info >> 30) != IT_T || L.col < 0 || L.rp < 0) return false;
+  const int R = m.info & 63, N = (m.info >> 6) & 0xFFFFF;
+  const PfRange c = pf_range(4 * m.k0, 4 * (m.k0 + N));
+  const PfRange r = pf_range(8 * ((int64_t)m.r0 + 1), 8 * ((int64_t)m.r0 + R + 1));
+  if (c.b1 > L.col || r.b1 > L.rp) return false;
+  if (L.xi >= 0) {
+    const PfRange x = pf_range((int64_t)sizeof(V) * m.r0, (int64_t)sizeof(V) * (m.r0 + R));
+    if (x.b1 > L.xi) return false;
+  }
+  return true;
+}
+
+// lane 0 only: arm the slot's barrier and issue the (up to) three bulk copies of tile m.
+template <class Op>
+__device__ __forceinline__ void pf_issue(const TileSched& sc, const Op& op, const ItemMeta& m, const PfLimits& L,
+                                         unsigned char* slot, uint64_t* bar) {
+  using V = typename Op::V;
+  const int R = m.info & 63, N = (m.info >> 6) & 0xFFFFF;
+  const PfRange c = pf_range(4 * m.k0, 4 * (m.k0 + N));
+  const PfRange r = pf_range(8 * ((int64_t)m.r0 + 1), 8 * ((int64_t)m.r0 + R + 1));
+  PfRange x{0, 0};
+  if (L.xi >= 0) x = pf_range((int64_t)sizeof(V) * m.r0, (int64_t)sizeof(V) * (m.r0 + R));
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic reads of the slot are done
+  mbar_expect_tx(bar, (uint32_t)((c.b1 - c.b0) + (r.b1 - r.b0) + (x.b1 - x.b0)));
+  if (c.b1 > c.b0)
+    bulk_g2s(slot, reinterpret_cast<const unsigned char*>(sc.col) + c.b0, (uint32_t)(c.b1 - c.b0), bar);
+  bulk_g2s(slot + PF_COL_BYTES, reinterpret_cast<const unsigned char*>(sc.row_ptr) + r.b0, (uint32_t)(r.b1 - r.b0),
+           bar);
+  if (x.b1 > x.b0)
+    bulk_g2s(slot + PF_COL_BYTES + PF_RP_BYTES, reinterpret_cast<const unsigned char*>(op.xi_base()) + x.b0,
+             (uint32_t)(x.b1 - x.b0), bar);
+}
+
+// Pointers into a filled slot for tile m (byte shifts undo the 16-byte widening).
+template <class Op>
+__device__ __forceinline__ TilePre<typename Op::V> pf_view(const ItemMeta& m, const PfLimits& L,
+                                                          unsigned char* slot) {
+  using V = typename Op::V;
+  TilePre<V> p;
+  p.col = reinterpret_cast<const int32_t*>(slot + ((4 * m.k0) & 15));
+  p.rp = reinterpret_cast<const int64_t*>(slot + PF_COL_BYTES + ((8 * ((int64_t)m.r0 + 1)) & 15));
+  p.xi = L.xi >= 0 ? reinterpret_cast<const V*>(slot + PF_COL_BYTES + PF_RP_BYTES +
+                                                 (((int64_t)sizeof(V) * m.r0) & 15))
+                   : nullptr;
+  return p;
+}
+
 template <int WT, class Op>
 __global__ void __launch_bounds__(WTPB) warp_kernel(const TileSched sc, const Op op, const TileScratch ws) {
+  using V = typename Op::V;
   constexpr int NA = Op::NA, NP = Op::NP;
   constexpr bool WEIGHTED = (WT != FJ_W_UNIT);
   __shared__ int32_t s_col[WPB][T_CAP];
   __shared__ int32_t s_e[WPB][32];
-  __shared__ double s_xi[WPB][32];
+  __shared__ V s_xi[WPB][32];
   __shared__ double s_red[(NP > NA ? NP : NA) * WPB];
   __shared__ bool s_last;
+  __shared__ __align__(128) unsigned char s_pf[WPB][2][PfSlot<V>::BYTES];
+  __shared__ uint64_t s_bar[WPB][2];
 
   if (op.skip()) return;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -212,23 +347,55 @@ __global__ void __launch_bounds__(WTPB) warp_kernel(const TileSched sc, const Op
 #pragma unroll
   for (int j = 0; j < NP; ++j) part[j] = 0.0;
 
+  PfLimits L;
+  L.col = (sc.hint & 2) || (reinterpret_cast<uintptr_t>(sc.col) & 15) ? -1 : ((4 * sc.nnz) & ~(int64_t)15);
+  L.rp = (reinterpret_cast<uintptr_t>(sc.row_ptr) & 15) ? -1 : ((8 * (sc.n + 1)) & ~(int64_t)15);
+  const V* xb = op.xi_base();
+  L.xi = (!xb || (reinterpret_cast<uintptr_t>(xb) & 15)) ? -1 : (((int64_t)sizeof(V) * sc.n) & ~(int64_t)15);
+  if (lane == 0) {
+    mbar_init(&s_bar[wib][0]);
+    mbar_init(&s_bar[wib][1]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+
   const int64_t nwarps = (int64_t)gridDim.x * WPB;
   int64_t it = (int64_t)blockIdx.x * WPB + wib;
-  ItemMeta m{};
+  ItemMeta m{}, m1{};   // current and next item
   if (it < sc.n_items) m = sc.items[it];
+  if (it + nwarps < sc.n_items) m1 = sc.items[it + nwarps];
+  uint32_t pend = 0, par = 0;   // per slot: copy in flight / barrier phase parity
+  int slot = 0;
+  if (it < sc.n_items && pf_ok(sc, op, m, L)) {
+    if (lane == 0) pf_issue(sc, op, m, L, s_pf[wib][0], &s_bar[wib][0]);
+    pend = 1;
+  }
   for (; it < sc.n_items; it += nwarps) {
     const ItemMeta cur = m;
-    if (it + nwarps < sc.n_items) m = sc.items[it + nwarps];   // prefetch the next item's meta
+    ItemMeta m2{};
+    if (it + 2 * nwarps < sc.n_items) m2 = sc.items[it + 2 * nwarps];   // meta two items ahead
+    if (it + nwarps < sc.n_items && pf_ok(sc, op, m1, L)) {              // stage the next tile
+      __syncwarp();
+      if (lane == 0) pf_issue(sc, op, m1, L, s_pf[wib][slot ^ 1], &s_bar[wib][slot ^ 1]);
+      pend |= 1u << (slot ^ 1);
+    }
     const uint32_t type = cur.info >> 30;
     if (type == IT_T) {
-      t_tile<WT, Op>(sc, op, cur, lane, s_e[wib], s_col[wib], s_xi[wib], part);
+      TilePre<V> pre{nullptr, nullptr, nullptr};
+      if (pend & (1u << slot)) {
+        mbar_wait(&s_bar[wib][slot], (par >> slot) & 1u);
+        par ^= 1u << slot;
+        pend &= ~(1u << slot);
+        pre = pf_view<Op>(cur, L, s_pf[wib][slot]);
+      }
+      t_tile<WT, Op>(sc, op, cur, lane, s_e[wib], s_col[wib], s_xi[wib], part, pre);
     } else {
       // ------------------------------------------------ W row or C chunk: lanes stride
       const int64_t r = cur.r0;
-      const int64_t rb = __ldg(sc.row_ptr + r), re = __ldg(sc.row_ptr + r + 1);
+      const int64_t rb = ld_rp(sc, r), re = ld_rp(sc, r + 1);
       const int64_t kb = cur.k0;
       const int64_t ke = (type == IT_W) ? re : min(kb + (int64_t)sc.chunk, re);
-      const double xi = op.row_value(r);
+      const V xi = op.row_value(r);
       double a[NA];
 #pragma unroll
       for (int f = 0; f < NA; ++f) a[f] = 0.0;
@@ -238,7 +405,7 @@ __global__ void __launch_bounds__(WTPB) warp_kernel(const TileSched sc, const Op
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const int64_t kk = k + 32 * u;
-          c8[u] = kk < ke ? __ldg(sc.col + kk) : -1;
+          c8[u] = kk < ke ? ld_col(sc, kk) : -1;
           w8[u] = (WEIGHTED && kk < ke) ? WeightT<WT>::get(sc.w, kk) : 1.0;
         }
 #pragma unroll
@@ -279,6 +446,9 @@ __global__ void __launch_bounds__(WTPB) warp_kernel(const TileSched sc, const Op
         }
       }
     }
+    m = m1;
+    m1 = m2;
+    slot ^= 1;
   }
 
   // ---------------------------------------------------- grid-level deterministic reduction

@@ -68,7 +68,17 @@ fj_status solve_batch(fj_graph* g, int k, const double* s, double* z, const fj_s
                       fj_solve_report* rep, cudaStream_t st);
 fj_status apply_batch(fj_graph* g, int k, const double* x, double* y, int opL, cudaStream_t st);
 fj_status quant_batch(fj_graph* g, int k, const double* s, const double* z, const double* mean_host,
-                      double* host_out /* [k][10] */, cudaStream_t st);
+                      double* host_out /* [k][10] */, cudaStream_t st, bool z_from_solve = false);
+fj_status time_batch_spmv(fj_graph* g, int k, int reps, float* ms_out, cudaStream_t st);
+// spmv_vec.cu (2 <= k <= 4)
+void free_vec_ws(fj_graph* g);
+bool vec_supported(int k);
+fj_status solve_vec(fj_graph* g, int k, const double* s, double* z, const fj_solve_opts& o, int warm,
+                    fj_solve_report* rep, cudaStream_t st);
+fj_status apply_vec(fj_graph* g, int k, const double* x, double* y, int opL, cudaStream_t st);
+fj_status quant_vec(fj_graph* g, int k, const double* s, const double* z, const double* mean_host,
+                    double* host_out, bool z_from_solve, cudaStream_t st);
+fj_status time_vec_spmv(fj_graph* g, int k, int reps, float* ms_out, cudaStream_t st);
 // dist.cu
 void free_dist(fj_graph* g);
 bool is_dist(const fj_graph* g);

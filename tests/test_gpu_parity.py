@@ -345,3 +345,52 @@ def test_batched_apply_and_solve_entry(fj):
     Y = host(G.apply(dev(wl.S), op=0))
     for c in range(5):
         assert np.allclose(Y[:, c], O.ipl_apply(g, wl.S[:, c]) - wl.S[:, c], rtol=1e-12, atol=1e-12)
+
+
+# ---------------------------------------------------------------- a9, small k: vector warp-item engine
+@pytest.mark.parametrize("k,wkind", [(2, "unit"), (3, "u8"), (4, "f64"), (3, "unit")])
+def test_small_k_vector_engine_vs_oracle(fj, k, wkind):
+    """2 <= k <= 4 columns solved together on padded [n][KP] blocks (spmv_vec.cu): every column
+    against the oracle, a consensus column exact, bitwise graph / host-loop agreement."""
+    rng = np.random.default_rng(20 + k)
+    n = 30000
+    u, v = hub_graph(rng, n, hubs=2, hub_deg=9000, extra=120000)   # T tiles + W rows + long chunks
+    m = len(u)
+    w = None if wkind == "unit" else (rng.integers(1, 6, m).astype(np.uint8) if wkind == "u8"
+                                      else rng.uniform(0.1, 4.0, m))
+    S = rng.uniform(0, 1, (n, k))
+    S[:, k - 1] = 0.375                    # consensus column: z = s exactly
+    g = O.canonical_csr(n, u, v, w)
+    G, Z, Q, rep = solve_quant(fj, n, u, v, w, S)
+    assert rep["batch_k"] == k and rep["converged"] == 1 and rep["rel_res_true"] <= 1e-10
+    assert np.array_equal(Z[:, k - 1], S[:, k - 1]) and Q[k - 1]["consensus"] == 1
+    for c in range(k - 1):
+        zo, _ = O.solve_pcg(g, S[:, c], tol=1e-13)
+        check_against_oracle(Q[c], O.quantities(g, S[:, c], zo), S[:, c], Z[:, c], zo)
+    Sd = dev(S)
+    z1, q1, r1 = G.approxim(Sd)
+    z2, q2, r2 = G.approxim(Sd, opts=fj.SolveOpts.make(use_cuda_graph=False))
+    assert np.array_equal(host(z1), host(z2)) and r1["iterations"] == r2["iterations"]
+    qs = G.quantities(Sd, z1)                  # stand-alone entry packs z itself
+    for c in range(k):
+        for key in QKEYS:
+            assert qs[c][key] == q1[c][key], (c, key)
+    assert G.time_spmv(k=k, reps=2) > 0
+
+
+def test_small_k_solve_entry_and_ragged(fj):
+    """fj_solve with k = 3 on a graph with isolated vertices and a single edge component."""
+    n = 5000
+    rng = np.random.default_rng(5)
+    u = rng.integers(0, 4000, 12000); v = rng.integers(0, 4000, 12000)     # 1000 isolated rows
+    g = O.canonical_csr(n, u, v)
+    rp, col, wo, _ = gpu_csr(fj, n, u.astype(np.int32), v.astype(np.int32))
+    G = fj.Graph(n, rp, col, wo)
+    S = rng.uniform(0, 1, (n, 3))
+    Z, rep = G.solve(dev(S))
+    Z = host(Z)
+    assert rep["batch_k"] == 3 and rep["converged"] == 1
+    for c in range(3):
+        assert np.max(np.abs(Z[:, c] - O.solve_dense(g, S[:, c]) if n <= 4096 else
+                             Z[:, c] - O.solve_pcg(g, S[:, c], tol=1e-13)[0])) < 1e-9
+    assert np.allclose(Z[4000:], S[4000:], rtol=1e-12)
