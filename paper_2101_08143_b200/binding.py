@@ -6,7 +6,7 @@ import math
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SO = os.path.join(HERE, "libfj.so")
+SO = os.environ.get("FJ_LIBRARY") or os.path.join(HERE, "libfj.so")   # FJ_LIBRARY: A/B builds (tools/)
 
 FJ_W_UNIT, FJ_W_U8, FJ_W_F32, FJ_W_F64 = 0, 1, 2, 3
 FJ_OP_L, FJ_OP_IPL = 0, 1

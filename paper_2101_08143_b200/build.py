@@ -42,15 +42,19 @@ def needs_build() -> bool:
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, so: str = SO, defines=()) -> str:
+    """Compile every csrc/*.cu and link `so`.  `defines` (e.g. ["FJ_ITEMS=16"]) are tuning-knob
+    variants for A/B builds (tools/build_variant.py); the default build uses none."""
+    if not force and so == SO and not needs_build():
         return SO
     objs = []
-    os.makedirs(os.path.join(HERE, "build"), exist_ok=True)
+    tag = "" if not defines else "_" + "_".join(d.replace("=", "") for d in defines)
+    bdir = os.path.join(HERE, "build" + tag)
+    os.makedirs(bdir, exist_ok=True)
     procs = []
     for src in sources():
-        obj = os.path.join(HERE, "build", os.path.basename(src) + ".o")
-        cmd = [NVCC, *[f for f in FLAGS if f != "-shared"], "-c", src, "-o", obj,
+        obj = os.path.join(bdir, os.path.basename(src) + ".o")
+        cmd = [NVCC, *[f for f in FLAGS if f != "-shared"], *[f"-D{d}" for d in defines], "-c", src, "-o", obj,
                "-I", os.path.join(ROOT, "include"), "-I", _nccl_include()]
         if verbose:
             cmd += ["-Xptxas", "-v"]
@@ -66,11 +70,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
             sys.stderr.write(f"nvcc failed on {src}\n")
     if failed:
         raise RuntimeError("libfj build failed")
-    tmp = SO + ".tmp"
+    tmp = so + ".tmp"
     subprocess.check_call([NVCC, "-shared", "-cudart", "static", "-gencode", "arch=compute_100a,code=sm_100a",
                            *objs, "-o", tmp, "-ldl"])
-    os.replace(tmp, SO)
-    return SO
+    os.replace(tmp, so)
+    return so
 
 
 if __name__ == "__main__":

@@ -34,7 +34,9 @@ struct ApplyOp {
   PcgScalars* sc;                   // PCG mode when non-null
   double* dot_out;                  // optional: x^T y
   int alpha_on_device = 1;          // 0 (distributed): leave alpha to the caller after the allreduce
+  int seg = SEG_WHOLE;              // role in a segmented product (segments.cu)
   __device__ __forceinline__ bool skip() const { return sc && *(volatile int32_t*)&sc->done; }
+  __device__ __forceinline__ bool wants_xi() const { return seg != SEG_MID; }
   __device__ __forceinline__ double gather(int32_t j) const {
 #ifdef FJ_GATHER_NC
     return __ldg(x + (int64_t)j * ld + c);
@@ -49,12 +51,18 @@ struct ApplyOp {
   }
   __device__ __forceinline__ void finish_row(int64_t i, int64_t len, double xi, const double (&a)[NA],
                                              double (&part)[NP]) const {
-    const double d = (WT == FJ_W_UNIT) ? (double)len : deg[i];
-    const double yi = opL ? fma(d, xi, -a[0]) : fma(1.0 + d, xi, -a[0]);
+    double yi;
+    if (seg <= SEG_FIRST) {
+      const double d = (WT == FJ_W_UNIT && seg == SEG_WHOLE) ? (double)len : deg[i];
+      yi = opL ? fma(d, xi, -a[0]) : fma(1.0 + d, xi, -a[0]);
+    } else {
+      yi = y[i * ld + c] - a[0];
+    }
     y[i * ld + c] = yi;
-    part[0] = fma(xi, yi, part[0]);
+    if (seg == SEG_WHOLE || seg == SEG_LAST) part[0] = fma(xi, yi, part[0]);
   }
   __device__ __forceinline__ void finalize(const double (&tot)[NP]) const {
+    if (seg == SEG_FIRST || seg == SEG_MID) return;
     if (dot_out) *dot_out = tot[0];
     if (sc && alpha_on_device) {
       sc->pq = tot[0];
@@ -82,6 +90,7 @@ struct ResidOp {
   int64_t ld, c;
   double* res2_out;
   __device__ __forceinline__ bool skip() const { return false; }
+  __device__ __forceinline__ bool wants_xi() const { return true; }
   __device__ __forceinline__ double gather(int32_t j) const { return __ldg(z + j); }
   __device__ __forceinline__ double row_value(int64_t i) const { return __ldg(z + i); }
   __device__ __forceinline__ const double* xi_base() const { return z; }
@@ -117,6 +126,7 @@ struct QuantOp {
   double* out;   // [NP]
   int64_t zld = -1, zc = 0;   // z layout if it differs from s (distributed: contiguous extended z)
   __device__ __forceinline__ bool skip() const { return false; }
+  __device__ __forceinline__ bool wants_xi() const { return true; }
   __device__ __forceinline__ int64_t zi(int64_t i) const { return zld < 0 ? i * ld + c : i * zld + zc; }
   __device__ __forceinline__ double gather(int32_t j) const { return __ldg(z + zi(j)); }
   __device__ __forceinline__ double row_value(int64_t i) const { return __ldg(z + zi(i)); }
@@ -191,6 +201,50 @@ inline cudaError_t launch_warp_items(const fj_graph* g, const SolveWs* ws, const
   if (grid > ws->grid_max) grid = ws->grid_max;
   warp_kernel<WT, Op><<<(unsigned)grid, WTPB, 0, st>>>(make_sched(g, g->s1), op, ws->ts);
   return cudaGetLastError();
+}
+
+// The engine on an explicit schedule / CSR view / scratch (segment passes).
+template <int WT, class Op>
+inline cudaError_t launch_items_on(const fj_graph* g, const Sched& S, const TileSched& ts, const Op& op,
+                                   const TileScratch& scr, int grid_max, cudaStream_t st) {
+  static int occ = 0;   // per template instantiation
+  if (occ == 0) {
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, warp_kernel<WT, Op>, WTPB, 0);
+    if (e != cudaSuccess) return e;
+    if (occ < 1) occ = 1;
+  }
+  int64_t grid = (int64_t)g->num_sms * occ;
+  const int64_t need = (S.n_items + WPB - 1) / WPB;
+  if (grid > need) grid = need > 0 ? need : 1;
+  if (grid > grid_max) grid = grid_max;
+  warp_kernel<WT, Op><<<(unsigned)grid, WTPB, 0, st>>>(ts, op, scr);
+  return cudaGetLastError();
+}
+
+// The segment layout built for gathered width kp, if the graph uses one (segments.cu); nullptr:
+// one whole-row pass.  Never builds (safe inside stream capture): get_segments() builds it first.
+inline const SegLayout* seg_for(const fj_graph* g, int kp) {
+  return (kp >= 1 && kp <= 4) ? reinterpret_cast<const SegLayout*>(g->seg[kp]) : nullptr;
+}
+
+// A product of the ApplyOp family (ApplyOp / ApplyOpV): one launch per column segment when the
+// graph has a segment layout for this width, else one whole-row launch with the workspace scratch.
+// Returns the number of kernel launches (for accounting) through *launches.
+template <int WT, class Op>
+inline cudaError_t launch_product(const fj_graph* g, const SegLayout* L, const TileScratch& scr, int grid_max, Op op,
+                                  cudaStream_t st, int* launches) {
+  if (!L) {
+    *launches = 1;
+    op.seg = SEG_WHOLE;
+    return launch_items_on<WT>(g, g->s1, make_sched(g, g->s1), op, scr, grid_max, st);
+  }
+  *launches = L->nseg;
+  for (int s = 0; s < L->nseg; ++s) {
+    op.seg = s == 0 ? SEG_FIRST : (s == L->nseg - 1 ? SEG_LAST : SEG_MID);
+    cudaError_t e = launch_items_on<WT>(g, L->sched[s], make_sched_seg(g, *L, s), op, L->ts, L->grid_max, st);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 }  // namespace fj

@@ -102,7 +102,9 @@ struct ApplyOpV {
   int opL;
   VecScalars* sc;   // PCG mode when non-null: alpha_c = rho_c / p_c^T q_c on device
   int k;
+  int seg = SEG_WHOLE;   // role in a segmented product (segments.cu)
   __device__ __forceinline__ bool skip() const { return sc && *(volatile int32_t*)&sc->done; }
+  __device__ __forceinline__ bool wants_xi() const { return seg != SEG_MID; }
   __device__ __forceinline__ V gather(int32_t j) const { return ld_vec<KP>(x + (int64_t)j * KP); }
   __device__ __forceinline__ V row_value(int64_t i) const { return ld_vec<KP>(x + i * KP); }
   __device__ __forceinline__ const V* xi_base() const { return reinterpret_cast<const V*>(x); }
@@ -112,18 +114,25 @@ struct ApplyOpV {
   }
   __device__ __forceinline__ void finish_row(int64_t i, int64_t len, const V& xi, const double (&a)[NA],
                                              double (&part)[NP]) const {
-    const double d = (WT == FJ_W_UNIT) ? (double)len : deg[i];
-    const double dd = opL ? d : 1.0 + d;
     V yv;
+    if (seg <= SEG_FIRST) {
+      const double d = (WT == FJ_W_UNIT && seg == SEG_WHOLE) ? (double)len : deg[i];
+      const double dd = opL ? d : 1.0 + d;
 #pragma unroll
-    for (int c = 0; c < KP; ++c) {
-      yv.v[c] = fma(dd, xi.v[c], -a[c]);
-      part[c] = fma(xi.v[c], yv.v[c], part[c]);
+      for (int c = 0; c < KP; ++c) yv.v[c] = fma(dd, xi.v[c], -a[c]);
+    } else {
+      yv = ld_vec<KP>(y + i * KP);
+#pragma unroll
+      for (int c = 0; c < KP; ++c) yv.v[c] -= a[c];
+    }
+    if (seg == SEG_WHOLE || seg == SEG_LAST) {
+#pragma unroll
+      for (int c = 0; c < KP; ++c) part[c] = fma(xi.v[c], yv.v[c], part[c]);
     }
     st_vec<KP>(y + i * KP, yv);
   }
   __device__ __forceinline__ void finalize(const double (&tot)[NP]) const {
-    if (!sc) return;
+    if (!sc || seg == SEG_FIRST || seg == SEG_MID) return;
 #pragma unroll
     for (int c = 0; c < KP; ++c) {
       if (c >= k) break;
@@ -156,6 +165,7 @@ struct ResidOpV {
   int k;
   VecScalars* sc;
   __device__ __forceinline__ bool skip() const { return false; }
+  __device__ __forceinline__ bool wants_xi() const { return true; }
   __device__ __forceinline__ V gather(int32_t j) const { return ld_vec<KP>(z + (int64_t)j * KP); }
   __device__ __forceinline__ V row_value(int64_t i) const { return ld_vec<KP>(z + i * KP); }
   __device__ __forceinline__ const V* xi_base() const { return reinterpret_cast<const V*>(z); }
@@ -196,6 +206,7 @@ struct QuantOpV {
   double m[KP];                   // mean of s per column
   double* out;                    // [10][KP]
   __device__ __forceinline__ bool skip() const { return false; }
+  __device__ __forceinline__ bool wants_xi() const { return true; }
   __device__ __forceinline__ V gather(int32_t j) const { return ld_vec<KP>(z + (int64_t)j * KP); }
   __device__ __forceinline__ V row_value(int64_t i) const { return ld_vec<KP>(z + i * KP); }
   __device__ __forceinline__ const V* xi_base() const { return reinterpret_cast<const V*>(z); }
@@ -527,7 +538,10 @@ static fj_status vec_apply_padded(const fj_graph* g, const VecWs* w, const doubl
   return by_wtype<KP>(g, [&](auto wt) {
     constexpr int WT = decltype(wt)::value;
     ApplyOpV<WT, KP> op{x, y, g->deg, opL, sc, w->k};
-    return launch_vec_items<WT>(g, w, op, st);
+    int nl = 0;
+    FJ_CK(launch_product<WT>(g, seg_for(g, KP), w->ts, w->grid_max, op, st, &nl));   // L2 segments
+    if (!g_capturing) count_launch(nl);
+    return FJ_OK;
   });
 }
 
@@ -577,6 +591,8 @@ static fj_status solve_vec_t(fj_graph* g, VecWs* w, int k, const double* s, doub
   const int64_t n = g->n;
   const unsigned cb = (unsigned)std::min<int64_t>((n + 255) / 256, 8192);
   w->x_is_solution = false;
+  const SegLayout* L = nullptr;
+  FJ_TRY(get_segments(g, KP, st, &L));   // before capture: the loop graph launches its passes
   if (o.use_cuda_graph) FJ_TRY(build_vec_graph<KP>(g, w));
   VecScalars h{};
   int restarts = 0, total_iter = 0;
@@ -613,7 +629,7 @@ static fj_status solve_vec_t(fj_graph* g, VecWs* w, int k, const double* s, doub
     FJ_CK(cudaMemcpyAsync(&h, w->sc, sizeof h, cudaMemcpyDeviceToHost, st));
     FJ_CK(cudaStreamSynchronize(st));
     total_iter += h.iter;
-    if (o.use_cuda_graph) count_launch(3 * std::max(h.iter, 1));
+    if (o.use_cuda_graph) count_launch((2 + (L ? L->nseg : 1)) * std::max(h.iter, 1));
     float lms = 0.f;
     cudaEventElapsedTime(&lms, w->ev2, w->ev3);
     if (rep) { rep->ms_loop += lms; rep->iterations_total += (int64_t)h.iter * k; }
@@ -665,6 +681,8 @@ fj_status solve_vec(fj_graph* g, int k, const double* s, double* z, const fj_sol
 fj_status apply_vec(fj_graph* g, int k, const double* x, double* y, int opL, cudaStream_t st) {
   VecWs* w = nullptr;
   FJ_TRY(get_vec_ws(g, k, st, &w));
+  const SegLayout* L = nullptr;
+  FJ_TRY(get_segments(g, w->kp, st, &L));
   w->x_is_solution = false;
   const unsigned cb = (unsigned)std::min<int64_t>((g->n + 255) / 256, 8192);
   auto run = [&](auto kpc) -> fj_status {
@@ -688,6 +706,8 @@ fj_status apply_vec(fj_graph* g, int k, const double* x, double* y, int opL, cud
 fj_status time_vec_spmv(fj_graph* g, int k, int reps, float* ms_out, cudaStream_t st) {
   VecWs* w = nullptr;
   FJ_TRY(get_vec_ws(g, k, st, &w));
+  const SegLayout* L = nullptr;
+  FJ_TRY(get_segments(g, w->kp, st, &L));
   w->x_is_solution = false;
   auto run = [&]() -> fj_status {
     switch (w->kp) {

@@ -22,7 +22,13 @@ namespace fj {
 
 constexpr int WTPB = 128;                 // 4 warps per block
 constexpr int WPB = WTPB / 32;
-constexpr int ITEMS = 12;                 // merge items (row ends + nonzeros) per lane in a T tile
+#ifndef FJ_ITEMS
+#define FJ_ITEMS 12
+#endif
+#ifndef FJ_K1_MIN_BLOCKS
+#define FJ_K1_MIN_BLOCKS 1
+#endif
+constexpr int ITEMS = FJ_ITEMS;           // merge items (row ends + nonzeros) per lane in a T tile
 constexpr int T_CAP = 32 * ITEMS;         // 384 merge items per tile
 constexpr int T_ROW_MAX = 64;             // rows longer than this are W rows or chunked
 constexpr int T_ROW_MIN_COST = 12;        // schedule units per row are max(1 + len, 12): <= 32 rows
@@ -96,6 +102,30 @@ struct TileScratch {
   unsigned int* grid_ticket;   // [1], zero-initialised, self-resetting
 };
 
+// L2-sized column segments of the CSR (segments.cu): segment s holds, for every row, the nonzeros
+// whose column lies in [bounds[s], bounds[s+1]), ascending, with its own row_ptr and schedule.
+constexpr int MAXSEG = 64;
+struct SegLayout {
+  int nseg = 0, kp = 0, grid_max = 0;
+  int64_t bounds[MAXSEG + 1] = {};
+  int64_t* rp[MAXSEG] = {};
+  int32_t* col[MAXSEG] = {};
+  void* w[MAXSEG] = {};
+  int64_t nnz[MAXSEG] = {};
+  Sched sched[MAXSEG];
+  TileScratch ts{};
+};
+// pass roles of a segmented product (Op::seg): whole row / first / middle / last segment
+enum { SEG_WHOLE = 0, SEG_FIRST = 1, SEG_MID = 2, SEG_LAST = 3 };
+int seg_count(const fj_graph* g, int kp);
+inline TileSched make_sched_seg(const fj_graph* g, const SegLayout& L, int s) {
+  TileSched t = make_sched(g, L.sched[s]);
+  t.nnz = L.nnz[s]; t.row_ptr = L.rp[s]; t.col = L.col[s]; t.w = L.w[s];
+  return t;
+}
+fj_status get_segments(fj_graph* g, int kp, cudaStream_t st, const SegLayout** out);
+void free_segments(fj_graph* g);
+
 // Op interface:
 //   using V;                                       // gathered value: double (k = 1) or DVec<KP> (k <= 4)
 //   static constexpr int NA, NP; static constexpr bool NEEDS_XI;
@@ -104,6 +134,7 @@ struct TileScratch {
 //   __device__ V gather(int32_t j) const;          // x_j for a nonzero (i, j)
 //   __device__ V row_value(int64_t i) const;       // x_i
 //   __device__ const V* xi_base() const;           // x_i = xi_base()[i] (contiguous), or nullptr
+//   __device__ bool wants_xi() const;              // false: x_i unused by finish_row (not loaded)
 //   __device__ void add(double (&a)[NA], double w, V xj, V xi) const;
 //   __device__ void finish_row(int64_t i, int64_t len, V xi, const double (&a)[NA], double (&part)[NP]) const;
 //   __device__ void finalize(const double (&tot)[NP]) const;   // single thread of the last block
@@ -146,7 +177,7 @@ __device__ __forceinline__ void t_tile(const TileSched& sc, const Op& op, const 
   const V* s_xi = pre.xi ? pre.xi : s_xi_own;
   if (lane < R) {
     s_e[lane] = (int32_t)((pre.rp ? pre.rp[lane] : ld_rp(sc, r0 + lane + 1)) - k0);
-    if (!pre.xi) s_xi_own[lane] = op.row_value(r0 + lane);
+    if (!pre.xi && op.wants_xi()) s_xi_own[lane] = op.row_value(r0 + lane);
   }
   if (!pre.col) {
 #pragma unroll
@@ -329,7 +360,7 @@ __device__ __forceinline__ TilePre<typename Op::V> pf_view(const ItemMeta& m, co
 }
 
 template <int WT, class Op>
-__global__ void __launch_bounds__(WTPB) warp_kernel(const TileSched sc, const Op op, const TileScratch ws) {
+__global__ void __launch_bounds__(WTPB, sizeof(typename Op::V) == 8 ? FJ_K1_MIN_BLOCKS : 1) warp_kernel(const TileSched sc, const Op op, const TileScratch ws) {
   using V = typename Op::V;
   constexpr int NA = Op::NA, NP = Op::NP;
   constexpr bool WEIGHTED = (WT != FJ_W_UNIT);
@@ -351,7 +382,8 @@ __global__ void __launch_bounds__(WTPB) warp_kernel(const TileSched sc, const Op
   L.col = (sc.hint & 2) || (reinterpret_cast<uintptr_t>(sc.col) & 15) ? -1 : ((4 * sc.nnz) & ~(int64_t)15);
   L.rp = (reinterpret_cast<uintptr_t>(sc.row_ptr) & 15) ? -1 : ((8 * (sc.n + 1)) & ~(int64_t)15);
   const V* xb = op.xi_base();
-  L.xi = (!xb || (reinterpret_cast<uintptr_t>(xb) & 15)) ? -1 : (((int64_t)sizeof(V) * sc.n) & ~(int64_t)15);
+  L.xi = (!xb || !op.wants_xi() || (reinterpret_cast<uintptr_t>(xb) & 15)) ? -1
+                                                                         : (((int64_t)sizeof(V) * sc.n) & ~(int64_t)15);
   if (lane == 0) {
     mbar_init(&s_bar[wib][0]);
     mbar_init(&s_bar[wib][1]);
@@ -395,7 +427,7 @@ __global__ void __launch_bounds__(WTPB) warp_kernel(const TileSched sc, const Op
       const int64_t rb = ld_rp(sc, r), re = ld_rp(sc, r + 1);
       const int64_t kb = cur.k0;
       const int64_t ke = (type == IT_W) ? re : min(kb + (int64_t)sc.chunk, re);
-      const V xi = op.row_value(r);
+      const V xi = op.wants_xi() ? op.row_value(r) : Op::vzero();
       double a[NA];
 #pragma unroll
       for (int f = 0; f < NA; ++f) a[f] = 0.0;
