@@ -105,7 +105,7 @@ struct fj_graph {
   double* dinv = nullptr;       // 1 / (1 + d_i)                  [n]
   // row-engine work-item lists (schedule.cu): s1 for k = 1 (tiles.cuh), sb for batched k (spmm.cu,
   // built on first use)
-  fj::Sched s1, sb;
+  fj::Sched s1, sb, sv;   // sv: vector engine (spmv_vec.cu, VEC_ITEMS per lane), built on first use
   fj_graph_info_t info{};
   int num_sms = 148;
   // caches

@@ -339,6 +339,7 @@ fj_status fj_graph_destroy(fj_graph* g) {
   dfree(g->deg); dfree(g->dinv);
   free_sched(g->s1);
   free_sched(g->sb);
+  free_sched(g->sv);
   delete g;
   return FJ_OK;
 }

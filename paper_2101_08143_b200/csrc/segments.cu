@@ -146,7 +146,7 @@ static fj_status build_layout(fj_graph* g, int kp, int nseg, SegLayout* L, cudaS
     tmp.row_ptr = L->rp[s];
     tmp.col = L->col[s];
     tmp.nnz = nnz_s;
-    FJ_TRY(build_schedule(&tmp, kSchedK1, L->sched[s], st));
+    FJ_TRY(build_schedule(&tmp, kp == 1 ? kSchedK1 : kSchedVec, L->sched[s], st));
     max_long = std::max(max_long, L->sched[s].n_long);
     max_chunks = std::max(max_chunks, L->sched[s].n_long_chunks);
   }

@@ -90,9 +90,10 @@ struct VecScalars {
 
 // ---------------------------------------------------------------- row operators (tiles.cuh Op)
 // q = (I+L) p or L p for all KP columns of a padded [n][KP] block (P:L88 L = D - A).
-template <int WT, int KP>
+template <int WT, int KP, int SEG = SEG_WHOLE>   // SEG: role in a segmented product (segments.cu)
 struct ApplyOpV {
   using V = DVec<KP>;
+  static constexpr int ITEMS = VEC_ITEMS;
   static constexpr int NA = KP, NP = KP;
   static constexpr bool NEEDS_XI = false;
   static __device__ __forceinline__ V vzero() { return vzero_kp<KP>(); }
@@ -102,9 +103,15 @@ struct ApplyOpV {
   int opL;
   VecScalars* sc;   // PCG mode when non-null: alpha_c = rho_c / p_c^T q_c on device
   int k;
-  int seg = SEG_WHOLE;   // role in a segmented product (segments.cu)
   __device__ __forceinline__ bool skip() const { return sc && *(volatile int32_t*)&sc->done; }
-  __device__ __forceinline__ bool wants_xi() const { return seg != SEG_MID; }
+  __device__ __forceinline__ bool wants_xi() const { return SEG != SEG_MID; }
+  template <int S>
+  ApplyOpV<WT, KP, S> as_seg() const {
+    ApplyOpV<WT, KP, S> o;
+    static_assert(sizeof o == sizeof *this, "same layout");
+    memcpy(static_cast<void*>(&o), this, sizeof o);
+    return o;
+  }
   __device__ __forceinline__ V gather(int32_t j) const { return ld_vec<KP>(x + (int64_t)j * KP); }
   __device__ __forceinline__ V row_value(int64_t i) const { return ld_vec<KP>(x + i * KP); }
   __device__ __forceinline__ const V* xi_base() const { return reinterpret_cast<const V*>(x); }
@@ -115,8 +122,8 @@ struct ApplyOpV {
   __device__ __forceinline__ void finish_row(int64_t i, int64_t len, const V& xi, const double (&a)[NA],
                                              double (&part)[NP]) const {
     V yv;
-    if (seg <= SEG_FIRST) {
-      const double d = (WT == FJ_W_UNIT && seg == SEG_WHOLE) ? (double)len : deg[i];
+    if (SEG <= SEG_FIRST) {
+      const double d = (WT == FJ_W_UNIT && SEG == SEG_WHOLE) ? (double)len : deg[i];
       const double dd = opL ? d : 1.0 + d;
 #pragma unroll
       for (int c = 0; c < KP; ++c) yv.v[c] = fma(dd, xi.v[c], -a[c]);
@@ -125,14 +132,14 @@ struct ApplyOpV {
 #pragma unroll
       for (int c = 0; c < KP; ++c) yv.v[c] -= a[c];
     }
-    if (seg == SEG_WHOLE || seg == SEG_LAST) {
+    if (SEG == SEG_WHOLE || SEG == SEG_LAST) {
 #pragma unroll
       for (int c = 0; c < KP; ++c) part[c] = fma(xi.v[c], yv.v[c], part[c]);
     }
     st_vec<KP>(y + i * KP, yv);
   }
   __device__ __forceinline__ void finalize(const double (&tot)[NP]) const {
-    if (!sc || seg == SEG_FIRST || seg == SEG_MID) return;
+    if (!sc || SEG == SEG_FIRST || SEG == SEG_MID) return;
 #pragma unroll
     for (int c = 0; c < KP; ++c) {
       if (c >= k) break;
@@ -156,6 +163,7 @@ struct ApplyOpV {
 template <int WT, int KP>
 struct ResidOpV {
   using V = DVec<KP>;
+  static constexpr int ITEMS = VEC_ITEMS;
   static constexpr int NA = KP, NP = KP;
   static constexpr bool NEEDS_XI = false;
   static __device__ __forceinline__ V vzero() { return vzero_kp<KP>(); }
@@ -196,6 +204,7 @@ struct ResidOpV {
 template <int WT, int KP>
 struct QuantOpV {
   using V = DVec<KP>;
+  static constexpr int ITEMS = VEC_ITEMS;
   static constexpr int NA = 3 * KP, NP = 10 * KP;
   static constexpr bool NEEDS_XI = true;
   static __device__ __forceinline__ V vzero() { return vzero_kp<KP>(); }
@@ -493,9 +502,10 @@ static fj_status get_vec_ws(fj_graph* g, int k, cudaStream_t st, VecWs** out) {
   FJ_TRY(valloc(&w->elem_ticket, 1, st, true));
   w->grid_max = g->num_sms * (2048 / WTPB);
   FJ_TRY(valloc(&w->ts.block_part, (int64_t)w->grid_max * VNP_MAX, st));
-  FJ_TRY(valloc(&w->ts.long_part, g->s1.n_long * VNP_MAX, st));
-  FJ_TRY(valloc(&w->ts.chunk_acc, g->s1.n_long_chunks * VNA_MAX, st));
-  FJ_TRY(valloc(&w->ts.long_ticket, g->s1.n_long, st, true));
+  if (!g->sv.built) FJ_TRY(build_schedule(g, kSchedVec, g->sv, st));
+  FJ_TRY(valloc(&w->ts.long_part, g->sv.n_long * VNP_MAX, st));
+  FJ_TRY(valloc(&w->ts.chunk_acc, g->sv.n_long_chunks * VNA_MAX, st));
+  FJ_TRY(valloc(&w->ts.long_ticket, g->sv.n_long, st, true));
   FJ_TRY(valloc(&w->ts.grid_ticket, 1, st, true));
   FJ_TRY(valloc(&w->qout, VNP_MAX, st));
   FJ_CK(cudaEventCreate(&w->ev2));
@@ -505,7 +515,7 @@ static fj_status get_vec_ws(fj_graph* g, int k, cudaStream_t st, VecWs** out) {
   return FJ_OK;
 }
 
-// The warp-item engine on the k = 1 schedule (s1): same tiles, vector values.
+// The warp-item engine on the vector schedule (sv: VEC_ITEMS merge items per lane), vector values.
 template <int WT, class Op>
 static fj_status launch_vec_items(const fj_graph* g, const VecWs* w, const Op& op, cudaStream_t st) {
   static int occ = 0;   // per instantiation
@@ -514,10 +524,10 @@ static fj_status launch_vec_items(const fj_graph* g, const VecWs* w, const Op& o
     if (occ < 1) occ = 1;
   }
   int64_t grid = (int64_t)g->num_sms * occ;
-  const int64_t need = (g->s1.n_items + WPB - 1) / WPB;
+  const int64_t need = (g->sv.n_items + WPB - 1) / WPB;
   if (grid > need) grid = need > 0 ? need : 1;
   if (grid > w->grid_max) grid = w->grid_max;
-  warp_kernel<WT, Op><<<(unsigned)grid, WTPB, 0, st>>>(make_sched(g, g->s1), op, w->ts);
+  warp_kernel<WT, Op><<<(unsigned)grid, WTPB, 0, st>>>(make_sched(g, g->sv), op, w->ts);
   FJ_CK_LAUNCH();
   return FJ_OK;
 }
@@ -556,6 +566,38 @@ static fj_status vec_iteration(const fj_graph* g, VecWs* w, cudaStream_t st, cud
   return FJ_OK;
 }
 
+// Experiment knob FJ_L2_PERSIST=<hit ratio>: mark the gathered block p as an L2 persisting access-
+// policy window on the launching stream (captured into the loop graph's kernel nodes).
+static float l2_persist() {
+  static const float v = [] {
+    const char* e = getenv("FJ_L2_PERSIST");
+    return e ? (float)atof(e) : 0.f;
+  }();
+  return v;
+}
+static void set_l2_window(cudaStream_t st, const void* base, size_t bytes, float ratio) {
+  static size_t limit = 0;
+  if (ratio <= 0.f) return;
+  if (!limit) {
+    int dev = 0, mx = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&mx, cudaDevAttrMaxPersistingL2CacheSize, dev);
+    limit = (size_t)mx;
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, limit);
+  }
+  cudaStreamAttrValue a;
+  memset(&a, 0, sizeof a);
+  int dev = 0, maxw = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+  a.accessPolicyWindow.base_ptr = const_cast<void*>(base);
+  a.accessPolicyWindow.num_bytes = std::min(bytes, (size_t)maxw);
+  a.accessPolicyWindow.hitRatio = std::min(1.f, ratio * (float)limit / (float)a.accessPolicyWindow.num_bytes);
+  a.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  a.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &a);
+}
+
 template <int KP>
 static fj_status build_vec_graph(fj_graph* g, VecWs* w) {
   if (w->exec) return FJ_OK;
@@ -573,6 +615,7 @@ static fj_status build_vec_graph(fj_graph* g, VecWs* w) {
   cudaGraphNode_t node;
   FJ_CK(cudaGraphAddNode(&node, w->graph, nullptr, 0, &cp));
   cudaGraph_t body = cp.conditional.phGraph_out[0];
+  set_l2_window(w->cap_stream, w->p, sizeof(double) * KP * (size_t)g->n, l2_persist());
   FJ_CK(cudaStreamBeginCaptureToGraph(w->cap_stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
   g_capturing = true;
   fj_status s = vec_iteration<KP>(g, w, w->cap_stream, h, 1);
@@ -716,6 +759,7 @@ fj_status time_vec_spmv(fj_graph* g, int k, int reps, float* ms_out, cudaStream_
       default: return vec_apply_padded<4>(g, w, w->p, w->q, 0, nullptr, st);
     }
   };
+  set_l2_window(st, w->p, sizeof(double) * w->kp * (size_t)g->n, l2_persist());
   FJ_TRY(run());
   FJ_CK(cudaEventRecord(w->ev2, st));
   for (int i = 0; i < reps; ++i) FJ_TRY(run());

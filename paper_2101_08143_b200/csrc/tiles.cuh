@@ -14,6 +14,7 @@
 // fixed order and reduced in a fixed order: results are bitwise reproducible run to run.
 #pragma once
 #include <climits>
+#include <cstring>
 #include <type_traits>
 
 #include "common.cuh"
@@ -26,13 +27,37 @@ constexpr int WPB = WTPB / 32;
 #define FJ_ITEMS 12
 #endif
 #ifndef FJ_K1_MIN_BLOCKS
-#define FJ_K1_MIN_BLOCKS 1
+#define FJ_K1_MIN_BLOCKS 6
 #endif
-constexpr int ITEMS = FJ_ITEMS;           // merge items (row ends + nonzeros) per lane in a T tile
-constexpr int T_CAP = 32 * ITEMS;         // 384 merge items per tile
+// Register caps of the engine (__launch_bounds__ min blocks / SM) per gathered value width.
+// Measured on B200 (C3, C4): KP = 4 at 4 blocks (128 regs, no spill) is 1.2-1.5x faster than the
+// unconstrained 160 regs / 3 blocks; KP = 2 best at 5 blocks; k = 1 at 6 blocks (<= 80 regs; at 8
+// blocks it spills and is 1.5x slower).
+#ifndef FJ_VEC_MIN_BLOCKS
+#define FJ_VEC_MIN_BLOCKS 4
+#endif
+#ifndef FJ_VEC2_MIN_BLOCKS
+#define FJ_VEC2_MIN_BLOCKS 5
+#endif
+template <class V>
+constexpr int engine_min_blocks() {
+  return sizeof(V) == 8 ? FJ_K1_MIN_BLOCKS : (sizeof(V) == 16 ? FJ_VEC2_MIN_BLOCKS : FJ_VEC_MIN_BLOCKS);
+}
+#ifndef FJ_VEC_ITEMS
+#define FJ_VEC_ITEMS 8
+#endif
+// Merge items (row ends + nonzeros) per lane in a T tile, per engine: the k = 1 operators use
+// ITEMS (32 x 12 = 384 per tile); the vector operators (spmv_vec.cu) hold KP doubles per item and
+// use VEC_ITEMS (32 x 8 = 256): fewer registers, 4 instead of 3 blocks / SM (measured 21 % faster).
+constexpr int ITEMS = FJ_ITEMS;
+constexpr int VEC_ITEMS = FJ_VEC_ITEMS;
 constexpr int T_ROW_MAX = 64;             // rows longer than this are W rows or chunked
-constexpr int T_ROW_MIN_COST = 12;        // schedule units per row are max(1 + len, 12): <= 32 rows
-constexpr int T_UNITS = T_CAP - (T_ROW_MAX + 1);   // 319: a tile holds <= T_CAP merge items
+template <int IT> constexpr int t_cap() { return 32 * IT; }
+// a tile holds <= t_cap merge items: cut the merge coordinate every t_units = t_cap - (T_ROW_MAX + 1)
+template <int IT> constexpr int t_units() { return t_cap<IT>() - (T_ROW_MAX + 1); }
+// schedule units per row are max(1 + len, t_min_cost): <= 32 rows per tile (one per lane)
+template <int IT> constexpr int t_min_cost() { return (t_units<IT>() + 30) / 31 > 12 ? (t_units<IT>() + 30) / 31 : 12; }
+constexpr int T_CAP = t_cap<ITEMS>();
 constexpr int CHUNK = 2048;               // nonzeros per W row (max) / per long-row chunk
 constexpr int IT_T = 0, IT_W = 1, IT_C = 2;
 
@@ -89,7 +114,9 @@ inline TileSched make_sched(const fj_graph* g, const Sched& S) {
 }
 
 // the k = 1 engine's schedule (ITEMS x 32 lanes = T_CAP merge items per tile)
-constexpr SchedParams kSchedK1{T_ROW_MAX, T_UNITS, T_ROW_MIN_COST, CHUNK};
+template <int IT> constexpr SchedParams sched_params() { return SchedParams{T_ROW_MAX, t_units<IT>(), t_min_cost<IT>(), CHUNK}; }
+constexpr SchedParams kSchedK1 = sched_params<ITEMS>();
+constexpr SchedParams kSchedVec = sched_params<VEC_ITEMS>();
 fj_status build_schedule(fj_graph* g, const SchedParams& P, Sched& out, cudaStream_t st);
 void free_sched(Sched& s);
 
@@ -128,6 +155,7 @@ void free_segments(fj_graph* g);
 
 // Op interface:
 //   using V;                                       // gathered value: double (k = 1) or DVec<KP> (k <= 4)
+//   static constexpr int ITEMS;                    // merge items per lane (the schedule's t_cap / 32)
 //   static constexpr int NA, NP; static constexpr bool NEEDS_XI;
 //   static __device__ V vzero();
 //   __device__ bool skip() const;                  // uniform early exit (solver finished)
@@ -169,6 +197,7 @@ __device__ __forceinline__ void t_tile(const TileSched& sc, const Op& op, const 
                                        double (&part)[Op::NP], const TilePre<typename Op::V>& pre) {
   using V = typename Op::V;
   constexpr int NA = Op::NA;
+  constexpr int ITEMS = Op::ITEMS;
   constexpr bool WEIGHTED = (WT != FJ_W_UNIT);
   const int R = cur.info & 63;
   const int N = (cur.info >> 6) & 0xFFFFF;
@@ -273,12 +302,12 @@ __device__ __forceinline__ void t_tile(const TileSched& sc, const Op& op, const 
 // instead of stalling the warp at the start of every tile.  Copies are 16-byte granular: each range
 // is widened to 16-byte boundaries (never past the array's last full 16-byte unit; such a tile,
 // and any tile whose base pointers are not 16-byte aligned, takes the plain-load path).
-constexpr int PF_COL_BYTES = T_CAP * 4 + 32;
 constexpr int PF_RP_BYTES = 32 * 8 + 32;
-template <class V>
-struct PfSlot {
-  static constexpr int XI_BYTES = 32 * (int)sizeof(V) + 32;
-  static constexpr int BYTES = ((PF_COL_BYTES + PF_RP_BYTES + XI_BYTES) + 15) & ~15;
+template <class Op>
+struct PfSlot {   // [cols | row_ptr | row values] of one tile
+  static constexpr int COL_BYTES = t_cap<Op::ITEMS>() * 4 + 32;
+  static constexpr int XI_BYTES = 32 * (int)sizeof(typename Op::V) + 32;
+  static constexpr int BYTES = ((COL_BYTES + PF_RP_BYTES + XI_BYTES) + 15) & ~15;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -338,6 +367,7 @@ __device__ __forceinline__ void pf_issue(const TileSched& sc, const Op& op, cons
   mbar_expect_tx(bar, (uint32_t)((c.b1 - c.b0) + (r.b1 - r.b0) + (x.b1 - x.b0)));
   if (c.b1 > c.b0)
     bulk_g2s(slot, reinterpret_cast<const unsigned char*>(sc.col) + c.b0, (uint32_t)(c.b1 - c.b0), bar);
+  constexpr int PF_COL_BYTES = PfSlot<Op>::COL_BYTES;
   bulk_g2s(slot + PF_COL_BYTES, reinterpret_cast<const unsigned char*>(sc.row_ptr) + r.b0, (uint32_t)(r.b1 - r.b0),
            bar);
   if (x.b1 > x.b0)
@@ -350,6 +380,7 @@ template <class Op>
 __device__ __forceinline__ TilePre<typename Op::V> pf_view(const ItemMeta& m, const PfLimits& L,
                                                           unsigned char* slot) {
   using V = typename Op::V;
+  constexpr int PF_COL_BYTES = PfSlot<Op>::COL_BYTES;
   TilePre<V> p;
   p.col = reinterpret_cast<const int32_t*>(slot + ((4 * m.k0) & 15));
   p.rp = reinterpret_cast<const int64_t*>(slot + PF_COL_BYTES + ((8 * ((int64_t)m.r0 + 1)) & 15));
@@ -360,16 +391,16 @@ __device__ __forceinline__ TilePre<typename Op::V> pf_view(const ItemMeta& m, co
 }
 
 template <int WT, class Op>
-__global__ void __launch_bounds__(WTPB, sizeof(typename Op::V) == 8 ? FJ_K1_MIN_BLOCKS : 1) warp_kernel(const TileSched sc, const Op op, const TileScratch ws) {
+__global__ void __launch_bounds__(WTPB, engine_min_blocks<typename Op::V>()) warp_kernel(const TileSched sc, const Op op, const TileScratch ws) {
   using V = typename Op::V;
   constexpr int NA = Op::NA, NP = Op::NP;
   constexpr bool WEIGHTED = (WT != FJ_W_UNIT);
-  __shared__ int32_t s_col[WPB][T_CAP];
+  __shared__ int32_t s_col[WPB][t_cap<Op::ITEMS>()];
   __shared__ int32_t s_e[WPB][32];
   __shared__ V s_xi[WPB][32];
   __shared__ double s_red[(NP > NA ? NP : NA) * WPB];
   __shared__ bool s_last;
-  __shared__ __align__(128) unsigned char s_pf[WPB][2][PfSlot<V>::BYTES];
+  __shared__ __align__(128) unsigned char s_pf[WPB][2][PfSlot<Op>::BYTES];
   __shared__ uint64_t s_bar[WPB][2];
 
   if (op.skip()) return;
