@@ -381,9 +381,10 @@ class DistGraph(Graph):
         self._h = h
 
 
-def approxim_host(n, u, v, w, S, opts: SolveOpts | None = None, want_z=False, stream=None):
+def approxim_host(n, u, v, w, S, opts: SolveOpts | None = None, want_z=False, stream=None, z_out=None):
     """End-to-end from HOST numpy buffers (pinned memory recommended): H2D copies, CSR build, handle,
-    Algorithm 1, D2H.  Returns (z or None, [quantities], report)."""
+    Algorithm 1, D2H.  Returns (z or None, [quantities], report).  z_out: optional caller-owned host
+    float64 array shaped like S (pinned for full link speed) that receives z."""
     import numpy as np
     L = lib()
     S = np.ascontiguousarray(S, dtype=np.float64)
@@ -392,7 +393,14 @@ def approxim_host(n, u, v, w, S, opts: SolveOpts | None = None, want_z=False, st
     v = np.ascontiguousarray(v, dtype=np.int32)
     wt = FJ_W_UNIT if w is None else {np.dtype(np.uint8): FJ_W_U8, np.dtype(np.float32): FJ_W_F32,
                                       np.dtype(np.float64): FJ_W_F64}[np.asarray(w).dtype]
-    z = np.empty_like(S) if want_z else None
+    z = None
+    if z_out is not None:
+        if z_out.shape != S.shape or z_out.dtype != np.float64 or not z_out.flags.c_contiguous:
+            raise ValueError("z_out must be a C-contiguous float64 array shaped like S")
+        z = z_out
+    elif want_z:   # pinned, so the D2H of z runs at full link speed
+        import torch
+        z = torch.empty(S.shape, dtype=torch.float64, pin_memory=True).numpy()
     q = (Quantities * k)()
     rep = SolveReport()
     o = opts or SolveOpts.make()

@@ -26,6 +26,7 @@ struct ApplyOp {
   static constexpr bool NEEDS_XI = false;
   using V = double;
   static constexpr int ITEMS = fj::ITEMS;
+  static constexpr int MIN_BLOCKS = engine_min_blocks<double>();
   static __device__ __forceinline__ V vzero() { return 0.0; }
   const double* __restrict__ x;
   double* __restrict__ y;
@@ -91,6 +92,7 @@ struct ResidOp {
   static constexpr bool NEEDS_XI = false;
   using V = double;
   static constexpr int ITEMS = fj::ITEMS;
+  static constexpr int MIN_BLOCKS = engine_min_blocks<double>();
   static __device__ __forceinline__ V vzero() { return 0.0; }
   const double* __restrict__ z;     // contiguous [n]
   const double* __restrict__ s;     // column c of row-major [n][ld]
@@ -126,6 +128,7 @@ struct QuantOp {
   static constexpr bool NEEDS_XI = true;
   using V = double;
   static constexpr int ITEMS = fj::ITEMS;
+  static constexpr int MIN_BLOCKS = engine_min_blocks<double>();
   static __device__ __forceinline__ V vzero() { return 0.0; }
   const double* __restrict__ z;
   const double* __restrict__ s;

@@ -383,13 +383,21 @@ fj_status fj_approxim_host(int64_t n, int64_t m_in, const int32_t* u_h, const in
     FJ_CK(cudaMemcpyAsync(dv.p, v_h, sizeof(int32_t) * m_in, cudaMemcpyHostToDevice, st));
     if (wbytes) FJ_CK(cudaMemcpyAsync(dw.p, w_h, (size_t)wbytes * m_in, cudaMemcpyHostToDevice, st));
   }
-  FJ_CK(cudaMemcpyAsync(ds.p, s_h, sizeof(double) * n * k, cudaMemcpyHostToDevice, st));
+  // the opinions are not needed before the solve: their H2D runs on a side stream after the edge
+  // copies, overlapping the CSR build and the graph setup (a1, a2) on `st`
+  SideStream side;
+  FJ_TRY(side.init());
+  FJ_CK(cudaEventRecord(side.ev_in, st));
+  FJ_CK(cudaStreamWaitEvent(side.s, side.ev_in, 0));
+  FJ_CK(cudaMemcpyAsync(ds.p, s_h, sizeof(double) * n * k, cudaMemcpyHostToDevice, side.s));
+  FJ_CK(cudaEventRecord(side.ev_out, side.s));
   int64_t nnz = 0;
   FJ_TRY(fj_csr_from_edges(n, m_in, du.p, dv.p, wbytes ? dw.p : nullptr, wtype, drp.p, dcol.p,
                            wbytes ? dwo.p : nullptr, &nnz, nullptr, nullptr, stream));
   du.release(); dv.release(); dw.release();
   fj_graph* g = nullptr;
   FJ_TRY(fj_graph_create(n, nnz, drp.p, dcol.p, wbytes ? dwo.p : nullptr, wtype, 0, stream, &g));
+  FJ_CK(cudaStreamWaitEvent(st, side.ev_out, 0));
   fj_status s = fj_approxim(g, k, ds.p, dz.p, opts, q_h, rep, stream);
   if ((s == FJ_OK || s == FJ_E_NO_CONVERGENCE) && z_h) {
     cudaError_t e = cudaMemcpyAsync(z_h, dz.p, sizeof(double) * n * k, cudaMemcpyDeviceToHost, st);

@@ -94,6 +94,7 @@ template <int WT, int KP, int SEG = SEG_WHOLE>   // SEG: role in a segmented pro
 struct ApplyOpV {
   using V = DVec<KP>;
   static constexpr int ITEMS = VEC_ITEMS;
+  static constexpr int MIN_BLOCKS = engine_min_blocks<V>();
   static constexpr int NA = KP, NP = KP;
   static constexpr bool NEEDS_XI = false;
   static __device__ __forceinline__ V vzero() { return vzero_kp<KP>(); }
@@ -164,6 +165,7 @@ template <int WT, int KP>
 struct ResidOpV {
   using V = DVec<KP>;
   static constexpr int ITEMS = VEC_ITEMS;
+  static constexpr int MIN_BLOCKS = engine_min_blocks<V>();
   static constexpr int NA = KP, NP = KP;
   static constexpr bool NEEDS_XI = false;
   static __device__ __forceinline__ V vzero() { return vzero_kp<KP>(); }
@@ -205,6 +207,7 @@ template <int WT, int KP>
 struct QuantOpV {
   using V = DVec<KP>;
   static constexpr int ITEMS = VEC_ITEMS;
+  static constexpr int MIN_BLOCKS = FJ_QUANTV_MIN_BLOCKS;   // 40 per-thread partial sums
   static constexpr int NA = 3 * KP, NP = 10 * KP;
   static constexpr bool NEEDS_XI = true;
   static __device__ __forceinline__ V vzero() { return vzero_kp<KP>(); }

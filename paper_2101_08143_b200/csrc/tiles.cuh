@@ -36,6 +36,9 @@ constexpr int WPB = WTPB / 32;
 #ifndef FJ_VEC_MIN_BLOCKS
 #define FJ_VEC_MIN_BLOCKS 4
 #endif
+#ifndef FJ_QUANTV_MIN_BLOCKS
+#define FJ_QUANTV_MIN_BLOCKS 1
+#endif
 #ifndef FJ_VEC2_MIN_BLOCKS
 #define FJ_VEC2_MIN_BLOCKS 5
 #endif
@@ -156,6 +159,7 @@ void free_segments(fj_graph* g);
 // Op interface:
 //   using V;                                       // gathered value: double (k = 1) or DVec<KP> (k <= 4)
 //   static constexpr int ITEMS;                    // merge items per lane (the schedule's t_cap / 32)
+//   static constexpr int MIN_BLOCKS;               // __launch_bounds__ min blocks / SM (register cap)
 //   static constexpr int NA, NP; static constexpr bool NEEDS_XI;
 //   static __device__ V vzero();
 //   __device__ bool skip() const;                  // uniform early exit (solver finished)
@@ -391,7 +395,7 @@ __device__ __forceinline__ TilePre<typename Op::V> pf_view(const ItemMeta& m, co
 }
 
 template <int WT, class Op>
-__global__ void __launch_bounds__(WTPB, engine_min_blocks<typename Op::V>()) warp_kernel(const TileSched sc, const Op op, const TileScratch ws) {
+__global__ void __launch_bounds__(WTPB, Op::MIN_BLOCKS) warp_kernel(const TileSched sc, const Op op, const TileScratch ws) {
   using V = typename Op::V;
   constexpr int NA = Op::NA, NP = Op::NP;
   constexpr bool WEIGHTED = (WT != FJ_W_UNIT);

@@ -27,6 +27,23 @@ struct DevBuf {
   ~DevBuf() { release(); }
 };
 
+// A non-blocking side stream with two events (host-buffer entry points overlap copies with compute).
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  fj_status init() {
+    FJ_CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    FJ_CK(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
+    FJ_CK(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));
+    return FJ_OK;
+  }
+  ~SideStream() {
+    if (s) { cudaStreamSynchronize(s); cudaStreamDestroy(s); }
+    if (ev_in) cudaEventDestroy(ev_in);
+    if (ev_out) cudaEventDestroy(ev_out);
+  }
+};
+
 // e[i] = sum_{j<i} c[j] for i in [0, count)
 inline fj_status cub_exclusive_sum(const int64_t* c, int64_t* e, int64_t count, cudaStream_t st) {
   size_t bytes = 0;

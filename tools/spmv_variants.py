@@ -29,7 +29,15 @@ G = fj.Graph.from_edges(wl.n, u, v, w)
 z, q, rep = G.approxim(S if a.k > 1 else S[:, 0].contiguous())
 z, q, rep = G.approxim(S if a.k > 1 else S[:, 0].contiguous())
 ms = G.time_spmv(k=a.k, reps=a.reps)
+Sq = S if a.k > 1 else S[:, 0].contiguous()
+G.quantities(Sq, z)
+torch.cuda.synchronize()
+import time  # noqa: E402
+t0 = time.perf_counter()
+for _ in range(3):
+    G.quantities(Sq, z)
+quant_ms = (time.perf_counter() - t0) / 3 * 1e3
 env = {k: v for k, v in os.environ.items() if k.startswith("FJ_")}
 print(json.dumps({"env": env, "config": a.config, "n": wl.n, "k": a.k, "spmv_ms": ms, "loop_ms": rep["ms_loop"],
-                  "ms": rep["ms"], "iters": rep["iterations"], "rel_res": rep["rel_res_true"],
+                  "ms": rep["ms"], "quant_ms": quant_ms, "iters": rep["iterations"], "rel_res": rep["rel_res_true"],
                   "D0": q[0]["D"]}), flush=True)
