@@ -569,38 +569,6 @@ static fj_status vec_iteration(const fj_graph* g, VecWs* w, cudaStream_t st, cud
   return FJ_OK;
 }
 
-// Experiment knob FJ_L2_PERSIST=<hit ratio>: mark the gathered block p as an L2 persisting access-
-// policy window on the launching stream (captured into the loop graph's kernel nodes).
-static float l2_persist() {
-  static const float v = [] {
-    const char* e = getenv("FJ_L2_PERSIST");
-    return e ? (float)atof(e) : 0.f;
-  }();
-  return v;
-}
-static void set_l2_window(cudaStream_t st, const void* base, size_t bytes, float ratio) {
-  static size_t limit = 0;
-  if (ratio <= 0.f) return;
-  if (!limit) {
-    int dev = 0, mx = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&mx, cudaDevAttrMaxPersistingL2CacheSize, dev);
-    limit = (size_t)mx;
-    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, limit);
-  }
-  cudaStreamAttrValue a;
-  memset(&a, 0, sizeof a);
-  int dev = 0, maxw = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, dev);
-  a.accessPolicyWindow.base_ptr = const_cast<void*>(base);
-  a.accessPolicyWindow.num_bytes = std::min(bytes, (size_t)maxw);
-  a.accessPolicyWindow.hitRatio = std::min(1.f, ratio * (float)limit / (float)a.accessPolicyWindow.num_bytes);
-  a.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-  a.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-  cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &a);
-}
-
 template <int KP>
 static fj_status build_vec_graph(fj_graph* g, VecWs* w) {
   if (w->exec) return FJ_OK;
@@ -618,7 +586,6 @@ static fj_status build_vec_graph(fj_graph* g, VecWs* w) {
   cudaGraphNode_t node;
   FJ_CK(cudaGraphAddNode(&node, w->graph, nullptr, 0, &cp));
   cudaGraph_t body = cp.conditional.phGraph_out[0];
-  set_l2_window(w->cap_stream, w->p, sizeof(double) * KP * (size_t)g->n, l2_persist());
   FJ_CK(cudaStreamBeginCaptureToGraph(w->cap_stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
   g_capturing = true;
   fj_status s = vec_iteration<KP>(g, w, w->cap_stream, h, 1);
@@ -762,7 +729,6 @@ fj_status time_vec_spmv(fj_graph* g, int k, int reps, float* ms_out, cudaStream_
       default: return vec_apply_padded<4>(g, w, w->p, w->q, 0, nullptr, st);
     }
   };
-  set_l2_window(st, w->p, sizeof(double) * w->kp * (size_t)g->n, l2_persist());
   FJ_TRY(run());
   FJ_CK(cudaEventRecord(w->ev2, st));
   for (int i = 0; i < reps; ++i) FJ_TRY(run());
