@@ -211,6 +211,39 @@ fj_status fj_approxim_host(int64_t n, int64_t m_in, const int32_t* u_host, const
                            double* z_host, const fj_solve_opts* opts, fj_quantities_t* q_host,
                            fj_solve_report* rep, void* stream);
 
+/* ---------------------------------------------------------------- f2: Algorithm 1 verbatim
+ * Both solves of Approxim(G, s, eps): z~ = Solve(I+L, s, delta), q = Solve(I+L, s_bar, delta)
+ * (lines 3-4, run as one 2-column batch), then C_I = ||L z~||^2, D = ||W^{1/2} B q||^2,
+ * P = ||q||^2, C = ||z~||^2, I_dc = D + C (lines 5-9).  delta is line 1's formula; delta_eff clamps
+ * it to 1e-12 when it is below 1e-14 (SPEC's solver decision); the solve stops on the relative
+ * residual rtol = delta_eff / sqrt(1 + 2 d_max), which implies Lemma 4.2's (I+L)-norm bound since
+ * lambda(I+L) lies in [1, 1 + 2 d_max] (Gershgorin); rtol is floored at 1e-14 (fp64), recorded. */
+typedef struct {
+  double CI, D, P, C, Idc, PDI;   /* lines 5-9 (+ PDI = P + D)                                  */
+  double delta;                   /* line 1                                                      */
+  double delta_eff;               /* after the clamp                                             */
+  double rtol;                    /* relative-residual stop used for both solves                 */
+  double D_from_z;                /* ||W^{1/2} B z~||^2: equals D at solver tolerance */
+  double CI_def;                  /* sum (z~ - s)^2, Def. 3.1 form of C_I                        */
+  double mean_s, sbar_norm;       /* 1^T s / n and ||s_bar|| (line 2)                            */
+  int32_t clamped, rtol_floored;
+} fj_alg1_t;
+/* Host-only arithmetic of line 1 + clamp + residual map (no device work; any thread). */
+fj_status fj_alg1_delta(int64_t n, double w_min, double w_max, double d_max, double sbar_norm, double eps,
+                        double* delta, double* delta_eff, double* rtol, int* clamped, int* floored);
+/* s_dev: fp64 [n] device (one opinion vector); eps in (0, 1/2).  opts: max_iter / restarts / graph
+ * mode are honoured, rtol is replaced by the mapped one.  Synchronises. */
+fj_status fj_approxim_alg1(const fj_graph* g, const double* s_dev, double eps, const fj_solve_opts* opts,
+                           fj_alg1_t* out_host, fj_solve_report* rep, void* stream);
+
+/* ---------------------------------------------------------------- f4: forest-matrix entries
+ * omega_dev (row-major [n][m], device) receives columns cols_host[0..m) of Omega = (I + L)^{-1}:
+ * omega_dev[i*m + t] = omega_{i, cols[t]} = eps(Gamma_{i cols[t]}) / eps(Gamma), the forest-based
+ * proximity of P:L103/L132 (Omega is symmetric, so these are rows as well).  Each column solves
+ * (I+L) x = e_c; the columns are batched (<= 64 per batch).  rep aggregates the batches. */
+fj_status fj_forest_columns(const fj_graph* g, int64_t m, const int32_t* cols_host, double* omega_dev,
+                            const fj_solve_opts* opts, fj_solve_report* rep, void* stream);
+
 /* ---------------------------------------------------------------- a8/e: row-partitioned multi-GPU
  * The graph is split into contiguous row blocks balanced by nonzeros, one block per rank (one
  * process per GPU).  Rank r owns rows [bounds[r], bounds[r+1]).  Its CSR first carries GLOBAL

@@ -28,6 +28,11 @@ quantities        C_I, D, P, C, I_dc by Definitions 3.1-3.5 (P:L167, L183, L206,
                   PDI = P + D (BASELINE.json north_star), cross-checks s^T z.
 fj_iterate        synchronous iteration of the FJ update rule, Eq. (1).
 forest_census     spanning rooted forest weights eps(Gamma), eps(Gamma_ij).
+alg1_delta        Algorithm 1 line 1 delta, SPEC's clamp and the residual map.
+alg1              Algorithm 1 Approxim step by step, both solves.
+                  Pinned: SPEC's residual-map examples and a hand-computed delta (alg1_delta);
+                  the 2-node path example (golden path2), consensus, and equality with
+                  Definitions 3.1-3.4 on exact solves (Lemma 4.1).
 """
 from __future__ import annotations
 
@@ -355,3 +360,57 @@ def csr_rows_from_edges(n: int, u, v, rows_wanted, w=None):
         o = np.argsort(nbk, kind="stable")
         out[int(i)] = (nbk[o].astype(np.int32), None if w is None else np.asarray(w)[keep][o])
     return out
+
+
+# --------------------------------------------------------------------------- Algorithm 1 (row f2)
+def alg1_delta(n: int, w_min: float, w_max: float, d_max: float, sbar_norm: float, eps: float):
+    """Algorithm 1 line 1:
+        delta = eps * w_min * ||s_bar|| / (3 * w_max * n^3 * (n * w_max + 1) * sqrt(n)),
+    then SPEC's solver decision: used verbatim when delta >= 1e-14, else delta_eff = 1e-12
+    (clamped).  Residual stop implying Lemma 4.2's T-norm bound with T = I + L: every eigenvalue of T
+    lies in [1, 1 + 2 d_max] (Gershgorin; SPEC's S:L139 map uses the looser 1 + n w_max), so
+    ||y - y*||_T / ||y*||_T <= sqrt(1 + 2 d_max) * ||x - T y|| / ||x||  =>  rtol = delta_eff / sqrt(1 + 2 d_max),
+    floored at 1e-14 (fp64-attainable; reading R14).  Edgeless graphs (w_max = 0) use
+    w_min = w_max = 1 in the formula (their solve is exact at any tolerance).
+    Returns (delta, delta_eff, rtol, clamped, floored)."""
+    if w_max > 0:
+        delta = eps * w_min * sbar_norm / (3.0 * w_max * n ** 3 * (n * w_max + 1.0) * math.sqrt(n))
+    else:
+        delta = eps * sbar_norm / (3.0 * n ** 3 * math.sqrt(n))
+    clamped = delta < 1e-14
+    delta_eff = 1e-12 if clamped else delta
+    rtol = delta_eff / math.sqrt(1.0 + 2.0 * d_max)
+    floored = rtol < 1e-14
+    return delta, delta_eff, (1e-14 if floored else rtol), clamped, floored
+
+
+def alg1(g: CSR, s: np.ndarray, eps: float, tol: float = 1e-13) -> dict:
+    """Approxim(G, s, eps), Algorithm 1, line by line; the two Solve calls are the
+    oracle's own exact solves (dense Cholesky for n <= 4096, else Jacobi-PCG at rtol 1e-13, which
+    meets any delta the clamp admits):
+      1  delta                 (alg1_delta)
+      2  s_bar = s - (1^T s / n) 1
+      3  z = Solve(I + L, s, delta)
+      4  q = Solve(I + L, s_bar, delta)
+      5  C_I = ||L z||^2
+      6  D   = ||W^{1/2} B q||^2
+      7  P   = ||q||^2
+      8  C   = ||z||^2
+      9  I_dc = D + C"""
+    s = np.asarray(s, dtype=np.float64)
+    n = g.n
+    wf = g.wf()
+    w_min = float(wf.min()) if g.nnz else 0.0
+    w_max = float(wf.max()) if g.nnz else 0.0
+    d = degrees(g)
+    sbar = s - _fsum(s) / n                                          # line 2
+    delta = alg1_delta(n, w_min, w_max, float(d.max(initial=0.0)), math.sqrt(_fsum(sbar * sbar)), eps)
+    z = solve(g, s, tol=tol)                                         # line 3
+    q = solve(g, sbar, tol=tol)                                      # line 4
+    CI = _fsum(laplacian_apply(g, z) ** 2)                           # line 5
+    D = _fsum(incidence_apply(g, q) ** 2)                            # line 6
+    P = _fsum(q * q)                                                 # line 7
+    C = _fsum(z * z)                                                 # line 8
+    return {"CI": CI, "D": D, "P": P, "C": C, "Idc": D + C, "PDI": P + D,   # line 9
+            "delta": delta[0], "delta_eff": delta[1], "rtol": delta[2], "clamped": delta[3],
+            "floored": delta[4], "z": z, "q": q}

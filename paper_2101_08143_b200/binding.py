@@ -51,6 +51,15 @@ class Quantities(ctypes.Structure):
         return d
 
 
+class Alg1Result(ctypes.Structure):
+    _fields_ = [("CI", _dbl), ("D", _dbl), ("P", _dbl), ("C", _dbl), ("Idc", _dbl), ("PDI", _dbl),
+                ("delta", _dbl), ("delta_eff", _dbl), ("rtol", _dbl), ("D_from_z", _dbl), ("CI_def", _dbl),
+                ("mean_s", _dbl), ("sbar_norm", _dbl), ("clamped", _i32), ("rtol_floored", _i32)]
+
+    def to_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
 class FJError(RuntimeError):
     def __init__(self, status: int, msg: str):
         super().__init__(f"{_lib.fj_status_str(status).decode()}: {msg}")
@@ -87,6 +96,10 @@ def load_library(path: str = SO):
     L.fj_apply.argtypes = [_vp, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp]
     L.fj_time_spmv.argtypes = [_vp, ctypes.c_int, ctypes.c_int, P(ctypes.c_float), _vp]
     L.fj_probe_gather.argtypes = [_i64, _i64, ctypes.c_int, ctypes.c_int, P(ctypes.c_double), _vp]
+    L.fj_alg1_delta.argtypes = [_i64, _dbl, _dbl, _dbl, _dbl, _dbl, P(_dbl), P(_dbl), P(_dbl),
+                                P(ctypes.c_int), P(ctypes.c_int)]
+    L.fj_approxim_alg1.argtypes = [_vp, _vp, _dbl, P(SolveOpts), P(Alg1Result), P(SolveReport), _vp]
+    L.fj_forest_columns.argtypes = [_vp, _i64, _vp, _vp, P(SolveOpts), P(SolveReport), _vp]
     L.fj_opinion_stats.argtypes = [_vp, ctypes.c_int, _vp, _vp, _vp]
     L.fj_solve.argtypes = [_vp, ctypes.c_int, _vp, _vp, P(SolveOpts), P(SolveReport), _vp]
     L.fj_quantities.argtypes = [_vp, ctypes.c_int, _vp, _vp, P(Quantities), _vp]
@@ -104,7 +117,8 @@ def load_library(path: str = SO):
     L.fj_graph_create_dist.argtypes = [_vp, ctypes.c_int, _i64, _vp, _i64, _vp, _vp, _vp, ctypes.c_int, _i64, _vp,
                                        _vp, _vp, _vp, P(_vp)]
     for name in ["fj_csr_from_edges", "fj_graph_create", "fj_graph_info", "fj_graph_degrees", "fj_graph_destroy",
-                 "fj_apply", "fj_time_spmv", "fj_probe_gather", "fj_opinion_stats", "fj_solve", "fj_quantities", "fj_approxim", "fj_approxim_host",
+                 "fj_apply", "fj_time_spmv", "fj_probe_gather",
+                 "fj_alg1_delta", "fj_approxim_alg1", "fj_forest_columns", "fj_opinion_stats", "fj_solve", "fj_quantities", "fj_approxim", "fj_approxim_host",
                  "fj_comm_unique_id", "fj_comm_init", "fj_comm_init_loopback", "fj_comm_destroy",
                  "fj_partition_rows", "fj_csr_rows_from_edges", "fj_dist_ghosts", "fj_graph_create_dist"]:
         getattr(L, name).restype = ctypes.c_int
@@ -128,6 +142,16 @@ def probe_gather(n_vec: int, m: int, width: int = 1, reps: int = 10, stream=None
     r = ctypes.c_double()
     _check(lib().fj_probe_gather(int(n_vec), int(m), int(width), int(reps), ctypes.byref(r), _stream(stream)))
     return float(r.value)
+
+
+def alg1_delta(n, w_min, w_max, d_max, sbar_norm, eps):
+    """Host arithmetic of Algorithm 1 line 1 + clamp + residual map (fj_alg1_delta; no device work)."""
+    d, de, rt = _dbl(), _dbl(), _dbl()
+    cl, fl = ctypes.c_int(), ctypes.c_int()
+    _check(lib().fj_alg1_delta(int(n), float(w_min), float(w_max), float(d_max), float(sbar_norm), float(eps),
+                               ctypes.byref(d), ctypes.byref(de), ctypes.byref(rt), ctypes.byref(cl),
+                               ctypes.byref(fl)))
+    return d.value, de.value, rt.value, bool(cl.value), bool(fl.value)
 
 
 def _check(st: int, allow=()):
@@ -281,6 +305,30 @@ class Graph:
         _check(lib().fj_approxim(self.handle, k, _ptr(s), _ptr(z), ctypes.byref(o), q, ctypes.byref(rep),
                                  _stream(stream)))
         return z, [x.to_dict() for x in q], rep.to_dict()
+
+    def approxim_alg1(self, s, eps: float = 1e-6, opts: SolveOpts | None = None, stream=None):
+        """Algorithm 1 verbatim (row f2): both solves, lines 5-9 norms.  Returns (dict, report)."""
+        _need_cuda(s)
+        if _cols(s, self.n) != 1:
+            raise ValueError("approxim_alg1 takes one opinion vector")
+        r = Alg1Result()
+        rep = SolveReport()
+        o = opts or SolveOpts.make()
+        _check(lib().fj_approxim_alg1(self.handle, _ptr(s), float(eps), ctypes.byref(o), ctypes.byref(r),
+                                      ctypes.byref(rep), _stream(stream)))
+        return r.to_dict(), rep.to_dict()
+
+    def forest_columns(self, cols, opts: SolveOpts | None = None, stream=None):
+        """Columns `cols` of Omega = (I+L)^{-1} (row f4): a [n][len(cols)] fp64 CUDA tensor + report."""
+        import numpy as np
+        import torch
+        c = np.ascontiguousarray(cols, dtype=np.int32)
+        out = torch.empty((self.n, len(c)), dtype=torch.float64, device=self._keep[0].device)
+        rep = SolveReport()
+        o = opts or SolveOpts.make()
+        _check(lib().fj_forest_columns(self.handle, len(c), ctypes.c_void_p(c.ctypes.data), _ptr(out),
+                                       ctypes.byref(o), ctypes.byref(rep), _stream(stream)))
+        return out, rep.to_dict()
 
     def close(self):
         if getattr(self, "_h", None) is not None and _lib is not None:

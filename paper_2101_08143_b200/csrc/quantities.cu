@@ -409,3 +409,115 @@ fj_status fj_approxim_host(int64_t n, int64_t m_in, const int32_t* u_h, const in
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- Algorithm 1 verbatim
+// Approxim(G, s, eps) with BOTH solves: z~ = Solve(I+L, s, delta) (line 3) and
+// q = Solve(I+L, s_bar, delta) (line 4), run together as one k = 2 batch [s, s_bar]; then
+// C_I = ||L z~||^2 (line 5), D = ||W^{1/2} B q||^2 (line 6), P = ||q||^2 (line 7), C = ||z~||^2 (line 8),
+// I_dc = D + C (line 9).  delta per line 1, clamped as SPEC's solver decision, mapped to a
+// relative-residual stop by the Gershgorin form of SPEC's map (R14).
+namespace fj {
+
+constexpr int ATPB = 256;
+
+// S2[i] = (s_i, s_i - m); part[b] = this block's sum of (s_i - m)^2 (host sums the blocks in order)
+__global__ void __launch_bounds__(ATPB) k_alg1_rhs(int64_t n, const double* __restrict__ s, double m,
+                                                   double* __restrict__ S2, double* __restrict__ part) {
+  __shared__ double s_red[ATPB / 32];
+  double acc = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)ATPB + threadIdx.x; i < n; i += (int64_t)gridDim.x * ATPB) {
+    const double si = s[i], b = si - m;
+    S2[2 * i] = si;
+    S2[2 * i + 1] = b;
+    acc = fma(b, b, acc);
+  }
+  double v[1] = {acc};
+  block_sum<1, ATPB>(v, s_red);
+  if (threadIdx.x == 0) part[blockIdx.x] = v[0];
+}
+
+}  // namespace fj
+
+extern "C" {
+
+fj_status fj_alg1_delta(int64_t n, double w_min, double w_max, double d_max, double sbar_norm, double eps,
+                        double* delta, double* delta_eff, double* rtol, int* clamped, int* floored) {
+  if (n < 1 || !(w_min >= 0.0) || !(w_max >= w_min) || !(d_max >= 0.0) || !(sbar_norm >= 0.0) || !(eps > 0.0) ||
+      !(eps < 0.5) || !delta || !delta_eff || !rtol || !clamped || !floored)
+    return fail(FJ_E_INVALID_ARG, "fj_alg1_delta: n >= 1, 0 <= w_min <= w_max, d_max >= 0, eps in (0, 1/2)");
+  const double nn = (double)n;
+  // line 1: delta = eps w_min ||s_bar|| / (3 w_max n^3 (n w_max + 1) sqrt(n))   (w_max = 0: no edges)
+  const double den = 3.0 * (w_max > 0.0 ? w_max : 1.0) * nn * nn * nn * (nn * w_max + 1.0) * std::sqrt(nn);
+  *delta = eps * (w_max > 0.0 ? w_min : 1.0) * sbar_norm / den;
+  // the theoretical delta is used verbatim when >= 1e-14, else clamped to 1e-12 (recorded)
+  *clamped = *delta >= 1e-14 ? 0 : 1;
+  *delta_eff = *clamped ? 1e-12 : *delta;
+  // Residual stop that implies the Lemma 4.2 T-norm contract: lambda(I+L) in [1, 1 + 2 d_max]
+  // (Gershgorin), so ||y - y*||_T / ||y*||_T <= sqrt(1 + 2 d_max) ||r|| / ||x||.
+  *rtol = *delta_eff / std::sqrt(1.0 + 2.0 * d_max);
+  // fp64 floor of an attainable relative residual; recorded when it binds
+  *floored = *rtol < 1e-14 ? 1 : 0;
+  if (*floored) *rtol = 1e-14;
+  return FJ_OK;
+}
+
+fj_status fj_approxim_alg1(const fj_graph* gc, const double* s, double eps, const fj_solve_opts* opts,
+                           fj_alg1_t* out, fj_solve_report* rep, void* stream) {
+  if (!gc || !s || !out) return fail(FJ_E_INVALID_ARG, "null argument");
+  fj_graph* g = const_cast<fj_graph*>(gc);
+  if (is_dist(g)) return fail(FJ_E_UNSUPPORTED, "fj_approxim_alg1 on a distributed graph");
+  if (!(eps > 0.0) || !(eps < 0.5)) return fail(FJ_E_INVALID_ARG, "eps must lie in (0, 1/2) (Algorithm 1 input)");
+  cudaStream_t st = S(stream);
+  SolveWs* w = nullptr;
+  FJ_TRY(get_ws(g, st, &w));
+  std::vector<double> v;
+  FJ_TRY(stats_cols(g, w, 1, s, v, st));   // line 2: 1^T s / n
+  const int64_t n = g->n;
+  const double m = v[0] / (double)n;
+  DevBuf<double> S2, Z2, part;
+  FJ_TRY(S2.alloc(2 * n, st));
+  FJ_TRY(Z2.alloc(2 * n, st));
+  const int grid = (int)std::min<int64_t>((n + ATPB - 1) / ATPB, (int64_t)g->num_sms * 8);
+  FJ_TRY(part.alloc(grid, st));
+  k_alg1_rhs<<<grid, ATPB, 0, st>>>(n, s, m, S2.p, part.p);   // line 2: s_bar = s - (1^T s / n) 1
+  FJ_CK_LAUNCH();
+  std::vector<double> hp(grid);
+  FJ_CK(cudaMemcpyAsync(hp.data(), part.p, sizeof(double) * grid, cudaMemcpyDeviceToHost, st));
+  FJ_CK(cudaStreamSynchronize(st));
+  double sb2 = 0.0;
+  for (int b = 0; b < grid; ++b) sb2 += hp[b];   // block order: deterministic
+  fj_alg1_t r;
+  memset(&r, 0, sizeof r);
+  const fj_graph_info_t& I = g->info;
+  FJ_TRY(fj_alg1_delta(n, I.w_min, I.w_max, I.d_max, std::sqrt(sb2), eps, &r.delta, &r.delta_eff, &r.rtol,
+                       &r.clamped, &r.rtol_floored));   // line 1
+  fj_solve_opts o;
+  fj_default_solve_opts(&o);
+  if (opts) o = *opts;
+  o.rtol = r.rtol;
+  fj_solve_report sr{};
+  sr.converged = 1;
+  sr.rel_res_true = NAN;
+  const fj_status ss = solve_batch(g, 2, S2.p, Z2.p, o, 0, &sr, st);   // lines 3-4, one k = 2 batch
+  if (ss != FJ_OK && ss != FJ_E_NO_CONVERGENCE) return ss;
+  const double means[2] = {m, 0.0};
+  double sums[20];
+  FJ_TRY(quant_batch(g, 2, S2.p, Z2.p, means, sums, st, true));
+  // QuantOp sums per column: [0] (z-s)^2 [1] sum_i sum_j w (z_i - z_j)^2 [3] z^2 [7] ||L z||^2 ...
+  r.CI = sums[7];               // line 5: ||L z~||^2
+  r.D = 0.5 * sums[10 + 1];     // line 6: ||W^{1/2} B q||^2 (each edge once)
+  r.P = sums[10 + 3];           // line 7: ||q||^2
+  r.C = sums[3];                // line 8: ||z~||^2
+  r.Idc = r.D + r.C;            // line 9
+  r.PDI = r.P + r.D;
+  r.D_from_z = 0.5 * sums[1];   // SPEC note: D from the s-solve agrees at solver tolerance
+  r.CI_def = sums[0];           // Def. 3.1 form sum (z~ - s)^2
+  r.mean_s = m;
+  r.sbar_norm = std::sqrt(sb2);
+  *out = r;
+  if (rep) *rep = sr;
+  if (ss != FJ_OK) return fail(ss, "PCG did not reach the Algorithm 1 tolerance on the true residual");
+  return FJ_OK;
+}
+
+}  // extern "C"

@@ -65,3 +65,17 @@ def test_missing_library_raises(tmp_path):
             binding.load_library(str(tmp_path / "nope.so"))
         finally:
             binding._lib = binding._lib_backup
+
+
+def test_alg1_delta_host_arithmetic_matches_oracle():
+    """fj_alg1_delta is host-only arithmetic (Algorithm 1 line 1; clamp S:L153; residual map):
+    it must agree with the oracle's independent transcription on a range of graph sizes."""
+    import oracle as O
+    import paper_2101_08143_b200 as fj
+    cases = [(1, 0.0, 0.0, 0.0, 1.0, 0.1), (2, 1.0, 1.0, 1.0, 0.5 ** 0.5, 1e-6), (2000, 1.0, 1.0, 90.0, 12.9, 1e-6),
+             (300, 0.2, 3.0, 40.0, 5.0, 0.25), (4_000_000, 1.0, 1.0, 9507.0, 577.0, 1e-6)]
+    for c in cases:
+        got = fj.alg1_delta(*c)
+        want = O.alg1_delta(*c)
+        for a, b in zip(got, want):
+            assert a == pytest.approx(b, rel=1e-14), (c, got, want)

@@ -415,3 +415,73 @@ def test_segmented_product_vs_oracle(fj, wkind):
         assert d["converged"] == 1 and d["rel_res"] <= 1e-10, (k, d)
         assert d["err"] <= 1e-8 and d["apply_err"] <= 1e-13, (k, d)
         assert d["bitwise_graph_vs_loop"], (k, d)
+
+
+# ---------------------------------------------------------------- f2: Algorithm 1 verbatim
+@pytest.mark.parametrize("name", ["c1", "c4s"])
+def test_alg1_verbatim_vs_oracle(fj, name):
+    """fj_approxim_alg1 (both solves as one k = 2 batch, lines 5-9 norms) against the oracle's
+    line-by-line Algorithm 1 with exact solves; delta / clamp / rtol equal the oracle's transcription."""
+    if name == "c1":
+        wl = synth.make_config("c1")
+        w = None
+    else:
+        wl = synth.make_config("c4", scale=11, k=1)
+        w = wl.w
+    s = wl.S[:, 0].copy()
+    g = O.canonical_csr(wl.n, wl.u, wl.v, w)
+    rp, col, wo, _ = gpu_csr(fj, wl.n, wl.u, wl.v, w)
+    G = fj.Graph(wl.n, rp, col, wo)
+    r, rep = G.approxim_alg1(dev(s), eps=1e-6)
+    o = O.alg1(g, s, 1e-6)
+    assert rep["converged"] == 1 and rep["batch_k"] == 2 and rep["rel_res_true"] <= r["rtol"] * (1 + 1e-9)
+    for k in ["CI", "D", "P", "C", "Idc", "PDI"]:
+        assert r[k] == pytest.approx(o[k], rel=1e-8), k
+    assert r["D_from_z"] == pytest.approx(r["D"], rel=1e-9)        # D from s or s_bar (P:L250-253)
+    assert r["CI_def"] == pytest.approx(r["CI"], rel=1e-8)         # ||Lz||^2 = sum (z - s)^2 (Lemma 4.1)
+    for a, b in [("delta", "delta"), ("delta_eff", "delta_eff"), ("rtol", "rtol")]:
+        assert r[a] == pytest.approx(o[b], rel=1e-12), a
+    assert bool(r["clamped"]) == o["clamped"] and bool(r["rtol_floored"]) == o["floored"]
+
+
+def test_alg1_path2_and_consensus(fj):
+    gold = {"CI": 2 / 9, "D": 1 / 9, "P": 1 / 18, "C": 5 / 9, "Idc": 2 / 3}      # S:L311 example (golden path2)
+    rp, col, wo, _ = gpu_csr(fj, 2, np.array([0], np.int32), np.array([1], np.int32))
+    G = fj.Graph(2, rp, col, wo)
+    r, rep = G.approxim_alg1(dev(np.array([1.0, 0.0])), eps=1e-6)
+    for k, v in gold.items():
+        assert r[k] == pytest.approx(v, rel=1e-12), k
+    wl = synth.make_config("c1")
+    rp, col, wo, _ = gpu_csr(fj, wl.n, wl.u, wl.v)
+    G = fj.Graph(wl.n, rp, col, wo)
+    r, rep = G.approxim_alg1(dev(np.full(wl.n, 0.4)), eps=1e-6)        # S:L314: consensus
+    assert r["D"] == 0 and r["P"] == 0 and r["CI"] < 1e-20 and r["C"] == pytest.approx(wl.n * 0.16, rel=1e-12)
+
+
+# ---------------------------------------------------------------- f4: forest-matrix entries
+@pytest.mark.parametrize("m", [1, 3, 5, 70])
+def test_forest_columns_vs_dense_inverse(fj, m):
+    """Columns of Omega = (I+L)^{-1} against the oracle's dense inverse on C1 (k = 1, vector
+    engine, warp-per-row engine, and two batches 64 + 6)."""
+    wl = synth.make_config("c1")
+    g = O.canonical_csr(wl.n, wl.u, wl.v)
+    rp, col, wo, _ = gpu_csr(fj, wl.n, wl.u, wl.v)
+    G = fj.Graph(wl.n, rp, col, wo)
+    cols = np.random.default_rng(m).choice(wl.n, m, replace=False)
+    Om, rep = G.forest_columns(cols, opts=fj.SolveOpts.make(rtol=1e-12))
+    Om = host(Om)
+    inv = np.linalg.inv(O.dense_ipl(g))
+    assert rep["converged"] == 1
+    assert np.max(np.abs(Om - inv[:, cols])) < 1e-11
+    assert np.allclose(Om.sum(axis=0), 1.0, atol=1e-10)              # Omega 1 = 1 (P:L129), symmetric
+
+
+def test_forest_columns_p5_golden(fj):
+    """P5: 55 * Omega is the paper's integer matrix (golden p5_forest_matrix)."""
+    from conftest import read_golden
+    M = np.array([[int(x) for x in r] for r in read_golden("p5_forest_matrix.txt")], dtype=float)
+    u = np.arange(4, dtype=np.int32)
+    rp, col, wo, _ = gpu_csr(fj, 5, u, u + 1)
+    G = fj.Graph(5, rp, col, wo)
+    Om, _ = G.forest_columns(np.arange(5), opts=fj.SolveOpts.make(rtol=1e-14))
+    assert np.allclose(host(Om) * 55, M, rtol=0, atol=1e-10)

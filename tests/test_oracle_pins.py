@@ -311,3 +311,49 @@ def test_csr_sampled_rows_match_full():
         a, b = g.row_ptr[i], g.row_ptr[i + 1]
         assert np.array_equal(got[i][0], g.col[a:b])
         assert np.array_equal(got[i][1], g.w[a:b])
+
+
+# ---------------------------------------------------------------- Algorithm 1 (row f2)
+def test_alg1_delta_spec_examples_and_hand_value():
+    """SPEC S:L139 examples of the residual map (single node: tau = delta; n = 2, w_max = 1:
+    tau = delta / sqrt(3) -- the Gershgorin form 1 + 2 d_max equals SPEC's 1 + n w_max there),
+    and line 1's delta for the 2-node path by hand:
+    eps w_min ||s_bar|| / (3 w_max n^3 (n w_max + 1) sqrt n) = 1e-6 * sqrt(1/2) / (3 * 8 * 3 * sqrt 2)
+    = 1e-6 / 144."""
+    d, de, tau, cl, fl = O.alg1_delta(1, 0.0, 0.0, 0.0, 1.0, 0.1)          # L = 0
+    assert tau == pytest.approx(de) and not fl
+    d, de, tau, cl, fl = O.alg1_delta(2, 1.0, 1.0, 1.0, np.sqrt(0.5), 1e-6)
+    assert d == pytest.approx(1e-6 / 144, rel=1e-15) and not cl and de == d
+    assert tau == pytest.approx(d / np.sqrt(3), rel=1e-15)
+    d, de, tau, cl, fl = O.alg1_delta(4_000_000, 1.0, 1.0, 9507.0, 577.0, 1e-6)   # C3-sized: clamped
+    assert d < 1e-14 and cl and de == 1e-12 and fl and tau == 1e-14
+
+
+def test_alg1_path2_matches_spec_example():
+    """SPEC S:L311 example: 2-node path, s = (1, 0), eps = 1e-6 -> (C_I, D, P, C, I_dc) =
+    (2/9, 1/9, 1/18, 5/9, 2/3) (golden path2); q = z - mean(s)."""
+    gold = _golden_fracs("path2_quantities.txt")
+    r = O.alg1(path_graph(2), np.array([1.0, 0.0]), 1e-6)
+    for k in ["CI", "D", "P", "C", "Idc", "PDI"]:
+        assert r[k] == pytest.approx(float(gold[k]), rel=1e-14), k
+    assert r["q"] == pytest.approx(r["z"] - 0.5, abs=1e-15)
+
+
+def test_alg1_equals_definitions_random_weighted():
+    """For exact solves Algorithm 1's norms equal Definitions 3.1-3.4 (Lemma 4.1):
+    ||L z||^2 = sum (z - s)^2, ||W^{1/2} B q||^2 = D (shift invariance), ||q||^2 = P."""
+    rng = np.random.default_rng(9)
+    g = random_graph(300, 1500, rng, weighted=True, connected=True)
+    s = rng.uniform(0, 1, 300)
+    r = O.alg1(g, s, 1e-3)
+    qd = O.quantities(g, s, O.solve_dense(g, s))
+    for k in ["CI", "D", "P", "C", "Idc", "PDI"]:
+        assert r[k] == pytest.approx(qd[k], rel=1e-10), k
+
+
+def test_alg1_consensus():
+    """s = c 1 -> C_I = D = P = 0, C = n c^2 (s_bar = 0 makes the second solve trivial)."""
+    g = random_graph(50, 200, np.random.default_rng(1), connected=True)
+    r = O.alg1(g, np.full(50, 0.4), 1e-6)
+    assert r["D"] == 0 and r["P"] == 0 and r["CI"] < 1e-28
+    assert r["C"] == pytest.approx(50 * 0.16, rel=1e-13)
