@@ -244,6 +244,26 @@ fj_status fj_approxim_alg1(const fj_graph* g, const double* s_dev, double eps, c
 fj_status fj_forest_columns(const fj_graph* g, int64_t m, const int32_t* cols_host, double* omega_dev,
                             const fj_solve_opts* opts, fj_solve_report* rep, void* stream);
 
+/* ---------------------------------------------------------------- f1: preprocessing on the device
+ * Opinion vectors of P:L637-639 drawn on the device by the synthetic workloads' counter-based
+ * generator: U_i = (rand64(seed, 1, i) >> 11) 2^-53 with rand64 = sm(sm(sm(seed) ^ 1) ^ i), sm the
+ * splitmix64 finaliser; kind 0: s_i = U_i; kind 1 (exponential, rate 1, x_min 1): x = 1 - ln(1 - U);
+ * kind 2 (power law, alpha 2.5, x_min 1): x = (1 - U)^(-1/1.5); kinds 1, 2 divided by max x.
+ * s_dev: fp64 [n] device output.  Synchronises. */
+fj_status fj_opinions_generate(int64_t n, int kind, uint64_t seed, double* s_dev, void* stream);
+/* Connected components of the raw edge list (self-loops / duplicates allowed): label_dev [n]
+ * receives the smallest vertex id of each vertex's component; *n_comp (may be NULL) the count.
+ * FJ_E_INVALID_ARG on a vertex id outside [0, n).  Synchronises. */
+fj_status fj_connected_components(int64_t n, int64_t m_in, const int32_t* u_dev, const int32_t* v_dev,
+                                  int32_t* label_dev, int64_t* n_comp, void* stream);
+/* Largest connected component (ties -> the component with the smallest vertex id):
+ * vmap_dev [n] = new id (LCC vertices renumbered 0.. in increasing old id) or -1; u_out/v_out/w_out
+ * (capacity m_in) receive the LCC's raw edges relabelled, in input order (self-loops and duplicates
+ * kept: fj_csr_from_edges applies a1's rules afterwards).  *n_lcc, *m_lcc: vertex / edge counts. */
+fj_status fj_lcc(int64_t n, int64_t m_in, const int32_t* u_dev, const int32_t* v_dev, const void* w_dev, int wtype,
+                 int32_t* vmap_dev, int32_t* u_out, int32_t* v_out, void* w_out, int64_t* n_lcc, int64_t* m_lcc,
+                 void* stream);
+
 /* ---------------------------------------------------------------- a8/e: row-partitioned multi-GPU
  * The graph is split into contiguous row blocks balanced by nonzeros, one block per rank (one
  * process per GPU).  Rank r owns rows [bounds[r], bounds[r+1]).  Its CSR first carries GLOBAL

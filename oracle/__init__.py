@@ -29,6 +29,9 @@ quantities        C_I, D, P, C, I_dc by Definitions 3.1-3.5 (P:L167, L183, L206,
 fj_iterate        synchronous iteration of the FJ update rule, Eq. (1).
 forest_census     spanning rooted forest weights eps(Gamma), eps(Gamma_ij).
 alg1_delta        Algorithm 1 line 1 delta, SPEC's clamp and the residual map.
+components / lcc  connected components by union-find and the largest component's relabelled edge
+                  list ("largest connected components"; row f1).  Pinned against
+                  scipy.sparse.csgraph.connected_components and hand-built graphs.
 alg1              Algorithm 1 Approxim step by step, both solves.
                   Pinned: SPEC's residual-map examples and a hand-computed delta (alg1_delta);
                   the 2-node path example (golden path2), consensus, and equality with
@@ -414,3 +417,42 @@ def alg1(g: CSR, s: np.ndarray, eps: float, tol: float = 1e-13) -> dict:
     return {"CI": CI, "D": D, "P": P, "C": C, "Idc": D + C, "PDI": P + D,   # line 9
             "delta": delta[0], "delta_eff": delta[1], "rtol": delta[2], "clamped": delta[3],
             "floored": delta[4], "z": z, "q": q}
+
+
+# --------------------------------------------------------------------------- ingest (row f1)
+def components(n: int, u, v) -> np.ndarray:
+    """Connected components of the raw edge list by union-find (path halving, union by smaller
+    id): label[i] = smallest vertex id in i's component."""
+    parent = list(range(n))
+
+    def find(x):
+        while parent[x] != x:
+            parent[x] = parent[parent[x]]
+            x = parent[x]
+        return x
+    for a, b in zip(np.asarray(u).tolist(), np.asarray(v).tolist()):
+        ra, rb = find(a), find(b)
+        if ra != rb:
+            if ra < rb:
+                parent[rb] = ra
+            else:
+                parent[ra] = rb
+    return np.array([find(i) for i in range(n)], dtype=np.int64)
+
+
+def lcc(n: int, u, v, w=None):
+    """Largest connected component, ties -> the component holding the smallest vertex id.
+    Returns (vmap, u2, v2, w2, n_lcc): vmap[i] = new id (increasing old id) or -1; the LCC's raw
+    edges relabelled in input order (self-loops / duplicates kept for the CSR rules of a1)."""
+    lab = components(n, u, v)
+    sizes = np.bincount(lab, minlength=n)
+    roots = np.flatnonzero(lab == np.arange(n))
+    best = roots[np.lexsort((roots, -sizes[roots]))[0]]
+    inside = lab == best
+    vmap = np.full(n, -1, dtype=np.int64)
+    vmap[inside] = np.arange(int(inside.sum()))
+    u = np.asarray(u)
+    v = np.asarray(v)
+    keep = inside[u]
+    w2 = None if w is None else np.asarray(w)[keep]
+    return vmap, vmap[u[keep]], vmap[v[keep]], w2, int(inside.sum())

@@ -100,6 +100,9 @@ def load_library(path: str = SO):
                                 P(ctypes.c_int), P(ctypes.c_int)]
     L.fj_approxim_alg1.argtypes = [_vp, _vp, _dbl, P(SolveOpts), P(Alg1Result), P(SolveReport), _vp]
     L.fj_forest_columns.argtypes = [_vp, _i64, _vp, _vp, P(SolveOpts), P(SolveReport), _vp]
+    L.fj_opinions_generate.argtypes = [_i64, ctypes.c_int, ctypes.c_uint64, _vp, _vp]
+    L.fj_connected_components.argtypes = [_i64, _i64, _vp, _vp, _vp, P(_i64), _vp]
+    L.fj_lcc.argtypes = [_i64, _i64, _vp, _vp, _vp, ctypes.c_int, _vp, _vp, _vp, _vp, P(_i64), P(_i64), _vp]
     L.fj_opinion_stats.argtypes = [_vp, ctypes.c_int, _vp, _vp, _vp]
     L.fj_solve.argtypes = [_vp, ctypes.c_int, _vp, _vp, P(SolveOpts), P(SolveReport), _vp]
     L.fj_quantities.argtypes = [_vp, ctypes.c_int, _vp, _vp, P(Quantities), _vp]
@@ -118,7 +121,8 @@ def load_library(path: str = SO):
                                        _vp, _vp, _vp, P(_vp)]
     for name in ["fj_csr_from_edges", "fj_graph_create", "fj_graph_info", "fj_graph_degrees", "fj_graph_destroy",
                  "fj_apply", "fj_time_spmv", "fj_probe_gather",
-                 "fj_alg1_delta", "fj_approxim_alg1", "fj_forest_columns", "fj_opinion_stats", "fj_solve", "fj_quantities", "fj_approxim", "fj_approxim_host",
+                 "fj_alg1_delta", "fj_approxim_alg1", "fj_forest_columns", "fj_opinions_generate",
+                 "fj_connected_components", "fj_lcc", "fj_opinion_stats", "fj_solve", "fj_quantities", "fj_approxim", "fj_approxim_host",
                  "fj_comm_unique_id", "fj_comm_init", "fj_comm_init_loopback", "fj_comm_destroy",
                  "fj_partition_rows", "fj_csr_rows_from_edges", "fj_dist_ghosts", "fj_graph_create_dist"]:
         getattr(L, name).restype = ctypes.c_int
@@ -142,6 +146,45 @@ def probe_gather(n_vec: int, m: int, width: int = 1, reps: int = 10, stream=None
     r = ctypes.c_double()
     _check(lib().fj_probe_gather(int(n_vec), int(m), int(width), int(reps), ctypes.byref(r), _stream(stream)))
     return float(r.value)
+
+
+OPINION_KINDS = {"uniform": 0, "exponential": 1, "powerlaw": 2}
+
+
+def opinions_generate(n: int, kind: str, seed: int, device=None, stream=None):
+    """Row f1: an opinion vector drawn on the device (fj_opinions_generate) -> fp64 CUDA tensor [n]."""
+    import torch
+    s = torch.empty(n, dtype=torch.float64, device=device or "cuda")
+    _check(lib().fj_opinions_generate(int(n), OPINION_KINDS[kind], int(seed), _ptr(s), _stream(stream)))
+    return s
+
+
+def connected_components(n: int, u, v, stream=None):
+    """Row f1: (labels int32 CUDA tensor [n] = smallest vertex id of the component, count)."""
+    import torch
+    _need_cuda(u, v)
+    lab = torch.empty(n, dtype=torch.int32, device=u.device)
+    nc = _i64()
+    _check(lib().fj_connected_components(int(n), u.numel(), _ptr(u), _ptr(v), _ptr(lab), ctypes.byref(nc),
+                                         _stream(stream)))
+    return lab, int(nc.value)
+
+
+def lcc(n: int, u, v, w=None, stream=None):
+    """Row f1: largest connected component -> (vmap [n], u', v', w' or None, n_lcc); edges in input order."""
+    import torch
+    _need_cuda(u, v)
+    m = u.numel()
+    vmap = torch.empty(n, dtype=torch.int32, device=u.device)
+    u2 = torch.empty(max(m, 1), dtype=torch.int32, device=u.device)
+    v2 = torch.empty(max(m, 1), dtype=torch.int32, device=u.device)
+    w2 = None if w is None else torch.empty(max(m, 1), dtype=w.dtype, device=u.device)
+    nl, ml = _i64(), _i64()
+    _check(lib().fj_lcc(int(n), m, _ptr(u), _ptr(v), None if w is None else _ptr(w), _wtype(w), _ptr(vmap),
+                        _ptr(u2), _ptr(v2), None if w2 is None else _ptr(w2), ctypes.byref(nl), ctypes.byref(ml),
+                        _stream(stream)))
+    k = int(ml.value)
+    return vmap, u2[:k], v2[:k], (None if w2 is None else w2[:k]), int(nl.value)
 
 
 def alg1_delta(n, w_min, w_max, d_max, sbar_norm, eps):

@@ -485,3 +485,55 @@ def test_forest_columns_p5_golden(fj):
     G = fj.Graph(5, rp, col, wo)
     Om, _ = G.forest_columns(np.arange(5), opts=fj.SolveOpts.make(rtol=1e-14))
     assert np.allclose(host(Om) * 55, M, rtol=0, atol=1e-10)
+
+
+# ---------------------------------------------------------------- f1: ingest on the device
+@pytest.mark.parametrize("kind", ["uniform", "exponential", "powerlaw"])
+def test_device_opinions_match_generator(fj, kind):
+    """fj_opinions_generate re-implements the workloads' counter-based generator (DESIGN.md §5,
+    R10): uniform bit-exact; exponential / power law within 4 ulp (device log1p / pow vs libm),
+    max s = 1 exactly after the rescale."""
+    n = 1_000_003
+    g = host(fj.opinions_generate(n, kind, 7))
+    ref = synth.opinions(kind, n, 7)
+    if kind == "uniform":
+        assert np.array_equal(g, ref)
+    else:
+        assert np.max(np.abs(g - ref) / ref) <= 4 * 2.0 ** -52
+        assert g.max() == 1.0
+
+
+def test_components_and_lcc_vs_oracle(fj):
+    rng = np.random.default_rng(12)
+    n, m = 20000, 16000                         # below the giant-component threshold: many pieces
+    u = rng.integers(0, n, m).astype(np.int32)
+    v = rng.integers(0, n, m).astype(np.int32)
+    u[:50] = v[:50]                             # self-loops
+    u[50:60] = u[60:70]; v[50:60] = v[60:70]    # duplicates
+    w = rng.integers(1, 6, m).astype(np.uint8)
+    lab, nc = fj.connected_components(n, dev(u), dev(v))
+    ref = O.components(n, u, v)
+    assert np.array_equal(host(lab), ref) and nc == len(np.unique(ref))
+    vmap, u2, v2, w2, nl = fj.lcc(n, dev(u), dev(v), dev(w))
+    rv, ru2, rv2, rw2, rnl = O.lcc(n, u, v, w)
+    assert nl == rnl and np.array_equal(host(vmap), rv)
+    assert np.array_equal(host(u2), ru2) and np.array_equal(host(v2), rv2) and np.array_equal(host(w2), rw2)
+    # the LCC through the rest of the path: CSR bit-exact, quantities vs the oracle
+    g = O.canonical_csr(nl, ru2, rv2, rw2)
+    rp, col, wo, _ = fj.csr_from_edges(nl, u2.contiguous(), v2.contiguous(), w2.contiguous())
+    assert np.array_equal(host(rp), g.row_ptr) and np.array_equal(host(col), g.col)
+    G = fj.Graph(nl, rp, col, wo)
+    s = host(fj.opinions_generate(nl, "exponential", 3))
+    z, q, rep = G.approxim(dev(s))
+    qo = O.quantities(g, s, O.solve(g, s))
+    for k in QKEYS:
+        assert q[0][k] == pytest.approx(qo[k], rel=1e-8), k
+
+
+def test_components_long_path_and_errors(fj):
+    n = 300000                                   # one path in shuffled id order: many hook rounds
+    perm = np.random.default_rng(2).permutation(n).astype(np.int32)
+    lab, nc = fj.connected_components(n, dev(perm[:-1]), dev(perm[1:]))
+    assert nc == 1 and not host(lab).any()
+    with pytest.raises(fj.FJError):
+        fj.connected_components(10, dev(np.array([0], np.int32)), dev(np.array([10], np.int32)))

@@ -357,3 +357,27 @@ def test_alg1_consensus():
     r = O.alg1(g, np.full(50, 0.4), 1e-6)
     assert r["D"] == 0 and r["P"] == 0 and r["CI"] < 1e-28
     assert r["C"] == pytest.approx(50 * 0.16, rel=1e-13)
+
+
+# ---------------------------------------------------------------- ingest (row f1)
+def test_components_vs_scipy_and_lcc_by_hand():
+    from scipy.sparse import coo_matrix
+    from scipy.sparse.csgraph import connected_components
+    rng = np.random.default_rng(4)
+    n, m = 3000, 2500            # sparse: many components
+    u = rng.integers(0, n, m)
+    v = rng.integers(0, n, m)
+    lab = O.components(n, u, v)
+    nc, sl = connected_components(coo_matrix((np.ones(m), (u, v)), shape=(n, n)), directed=False)
+    assert len(np.unique(lab)) == nc
+    for c in range(nc):                       # same partition, label = smallest member
+        members = np.flatnonzero(sl == c)
+        assert np.all(lab[members] == members.min())
+    # hand-built: triangle {5,6,7}, path 0-1-2-3, isolated 4, triangle {8,9,10} (ties with {5,6,7})
+    u = np.array([5, 6, 7, 0, 1, 2, 8, 9, 10, 3])
+    v = np.array([6, 7, 5, 1, 2, 3, 9, 10, 8, 3])
+    vmap, u2, v2, w2, nl = O.lcc(11, u, v)
+    assert nl == 4 and list(vmap[:5]) == [0, 1, 2, 3, -1] and np.all(vmap[5:] == -1)
+    assert list(u2) == [0, 1, 2, 3] and list(v2) == [1, 2, 3, 3]            # input order, self-loop kept
+    vmap, u2, v2, w2, nl = O.lcc(11, u[[0, 1, 2, 6, 7, 8]], v[[0, 1, 2, 6, 7, 8]], np.arange(6))
+    assert nl == 3 and list(np.flatnonzero(vmap >= 0)) == [5, 6, 7] and list(w2) == [0, 1, 2]   # tie -> smaller ids
