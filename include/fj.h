@@ -236,6 +236,15 @@ fj_status fj_alg1_delta(int64_t n, double w_min, double w_max, double d_max, dou
 fj_status fj_approxim_alg1(const fj_graph* g, const double* s_dev, double eps, const fj_solve_opts* opts,
                            fj_alg1_t* out_host, fj_solve_report* rep, void* stream);
 
+/* ---------------------------------------------------------------- f3: the paper's "Exact" on the device
+ * z = (I + L)^{-1} s by a dense fp64 Cholesky of I + L ("Exact"; cuSOLVER potrf / potrs,
+ * libcusolver.so.11 loaded on first use) for n <= 50000, then (q_host non-NULL) the fused
+ * quantities pass on that z (fj_quantities).  A mid-size checker for fj_approxim (Table 2's
+ * relative-error protocol, tools/table2.py).  FJ_E_UNSUPPORTED above n = 50000 or without
+ * libcusolver.  The n x n matrix is allocated and freed inside the call.  Synchronises. */
+fj_status fj_exact_dense(const fj_graph* g, int k, const double* s_dev, double* z_dev, fj_quantities_t* q_host,
+                         void* stream);
+
 /* ---------------------------------------------------------------- f4: forest-matrix entries
  * omega_dev (row-major [n][m], device) receives columns cols_host[0..m) of Omega = (I + L)^{-1}:
  * omega_dev[i*m + t] = omega_{i, cols[t]} = eps(Gamma_{i cols[t]}) / eps(Gamma), the forest-based

@@ -101,6 +101,7 @@ def load_library(path: str = SO):
     L.fj_approxim_alg1.argtypes = [_vp, _vp, _dbl, P(SolveOpts), P(Alg1Result), P(SolveReport), _vp]
     L.fj_forest_columns.argtypes = [_vp, _i64, _vp, _vp, P(SolveOpts), P(SolveReport), _vp]
     L.fj_opinions_generate.argtypes = [_i64, ctypes.c_int, ctypes.c_uint64, _vp, _vp]
+    L.fj_exact_dense.argtypes = [_vp, ctypes.c_int, _vp, _vp, _vp, _vp]
     L.fj_connected_components.argtypes = [_i64, _i64, _vp, _vp, _vp, P(_i64), _vp]
     L.fj_lcc.argtypes = [_i64, _i64, _vp, _vp, _vp, ctypes.c_int, _vp, _vp, _vp, _vp, P(_i64), P(_i64), _vp]
     L.fj_opinion_stats.argtypes = [_vp, ctypes.c_int, _vp, _vp, _vp]
@@ -122,7 +123,7 @@ def load_library(path: str = SO):
     for name in ["fj_csr_from_edges", "fj_graph_create", "fj_graph_info", "fj_graph_degrees", "fj_graph_destroy",
                  "fj_apply", "fj_time_spmv", "fj_probe_gather",
                  "fj_alg1_delta", "fj_approxim_alg1", "fj_forest_columns", "fj_opinions_generate",
-                 "fj_connected_components", "fj_lcc", "fj_opinion_stats", "fj_solve", "fj_quantities", "fj_approxim", "fj_approxim_host",
+                 "fj_connected_components", "fj_lcc", "fj_exact_dense", "fj_opinion_stats", "fj_solve", "fj_quantities", "fj_approxim", "fj_approxim_host",
                  "fj_comm_unique_id", "fj_comm_init", "fj_comm_init_loopback", "fj_comm_destroy",
                  "fj_partition_rows", "fj_csr_rows_from_edges", "fj_dist_ghosts", "fj_graph_create_dist"]:
         getattr(L, name).restype = ctypes.c_int
@@ -360,6 +361,16 @@ class Graph:
         _check(lib().fj_approxim_alg1(self.handle, _ptr(s), float(eps), ctypes.byref(o), ctypes.byref(r),
                                       ctypes.byref(rep), _stream(stream)))
         return r.to_dict(), rep.to_dict()
+
+    def exact_dense(self, s, stream=None):
+        """Row f3: the paper's Exact (dense Cholesky of I+L on the device) -> (z, [quantities])."""
+        import torch
+        _need_cuda(s)
+        k = _cols(s, self.n)
+        z = torch.empty_like(s)
+        q = (Quantities * k)()
+        _check(lib().fj_exact_dense(self.handle, k, _ptr(s), _ptr(z), q, _stream(stream)))
+        return z, [x.to_dict() for x in q]
 
     def forest_columns(self, cols, opts: SolveOpts | None = None, stream=None):
         """Columns `cols` of Omega = (I+L)^{-1} (row f4): a [n][len(cols)] fp64 CUDA tensor + report."""

@@ -537,3 +537,31 @@ def test_components_long_path_and_errors(fj):
     assert nc == 1 and not host(lab).any()
     with pytest.raises(fj.FJError):
         fj.connected_components(10, dev(np.array([0], np.int32)), dev(np.array([10], np.int32)))
+
+
+# ---------------------------------------------------------------- f3: Exact on the device + Table 2 protocol
+def test_exact_dense_vs_oracle_and_table2_protocol(fj):
+    """fj_exact_dense (dense Cholesky) on C1 against the oracle's LAPACK solve, then Table 2's
+    error protocol (sigma = |rho - rho~| / rho) for fj_approxim against it on a 12000-node BA
+    graph with the three opinion distributions: every sigma <= 1e-8 and within its certificate."""
+    wl = synth.make_config("c1")
+    g = O.canonical_csr(wl.n, wl.u, wl.v)
+    rp, col, wo, _ = gpu_csr(fj, wl.n, wl.u, wl.v)
+    G = fj.Graph(wl.n, rp, col, wo)
+    s = wl.S[:, 0].copy()
+    z, q = G.exact_dense(dev(s))
+    zo = O.solve_dense(g, s)
+    assert np.max(np.abs(host(z) - zo)) < 1e-13
+    qo = O.quantities(g, s, zo)
+    for k in QKEYS:
+        assert q[0][k] == pytest.approx(qo[k], rel=1e-12), k
+    wl = synth.make_config("c3", n=12000)
+    rp, col, wo, _ = gpu_csr(fj, wl.n, wl.u, wl.v)
+    G = fj.Graph(wl.n, rp, col, wo)
+    S = dev(wl.S)
+    ze, qe = G.exact_dense(S)
+    za, qa, rep = G.approxim(S)
+    for c in range(3):
+        for k in QKEYS:
+            sigma = abs(qe[c][k] - qa[c][k]) / qe[c][k]
+            assert sigma <= 1e-8 and sigma <= qa[c]["eps"][k] * (1 + 1e-9) + 1e-15, (c, k, sigma)
