@@ -297,7 +297,9 @@ fj_status fj_graph_create(int64_t n, int64_t nnz, const int64_t* row_ptr, const 
     return cleanup(fail(FJ_E_ASYMMETRIC, "adjacency not symmetric: (i,j,w) without (j,i,w)"));
   }
   if (nnz % 2 != 0 && validate) return cleanup(fail(FJ_E_ASYMMETRIC, "odd nnz"));
+  phase_tick("graph: degrees + stats", st);
   s = build_schedule(g, kSchedK1, g->s1, st);
+  phase_tick("graph: k=1 schedule", st);
   if (s != FJ_OK) return cleanup(s);
   fj_graph_info_t& I = g->info;
   I.n = n; I.nnz = nnz; I.m = nnz / 2;

@@ -259,8 +259,10 @@ fj_status fj_approxim(const fj_graph* gc, int k, const double* s, double* z_user
   fj_status worst = FJ_OK;
   if (k >= batch_min_k() && !is_dist(g)) {
     // row a9: all k columns in ONE batched PCG (per-column alpha/beta, convergence mask)
+    // The solve defers its true-residual pass: the fused quantities pass computes ||s - (I+L)z||^2
+    // per column anyway (QuantOp sum 6), so the restart decision is taken on it (one CSR pass less).
     fj_solve_opts oc = o;
-    int warm = 0, spent = 0;
+    int warm = 0, spent = 0, restarts = 0;
     for (;;) {
       fj_solve_opts ob = oc;
       ob.max_iter = std::max(0, o.max_iter - spent);
@@ -268,14 +270,13 @@ fj_status fj_approxim(const fj_graph* gc, int k, const double* s, double* z_user
       rb.converged = 1;
       rb.rel_res_true = NAN;
       phase_tick("approxim: before solve", st);
-      fj_status sc = solve_batch(g, k, s, z, ob, warm, &rb, st);      // Alg. 1 line 3
+      fj_status sc = solve_batch(g, k, s, z, ob, warm, &rb, st, /*defer_true_residual=*/true);   // Alg. 1 l.3
       if (sc != FJ_OK && sc != FJ_E_NO_CONVERGENCE) return sc;
       phase_tick("approxim: batched solve", st);
       spent += rb.iterations;
       r.ms_loop += rb.ms_loop;
       r.iterations_total += rb.iterations_total;
       r.restarts += rb.restarts;
-      r.rel_res_true = rb.rel_res_true;
       r.rel_res_recursive = rb.rel_res_recursive;
       r.batch_k = k;
       double emax = 0.0;
@@ -290,6 +291,8 @@ fj_status fj_approxim(const fj_graph* gc, int k, const double* s, double* z_user
         }
       }
       FJ_TRY(quant_batch(g, k, s, z, means.data(), sums.data(), st, z_is_solve));   // Alg. 1 lines 5-9
+      bool res_ok = true;
+      double worst_true = 0.0;
       for (int c = 0; c < k; ++c) {
         if (v[4 * c + 2] == v[4 * c + 3]) {
           consensus_quantities(g, v[4 * c + 2], qout[c]);
@@ -298,8 +301,21 @@ fj_status fj_approxim(const fj_graph* gc, int k, const double* s, double* z_user
         memset(&qout[c], 0, sizeof(fj_quantities_t));
         fill_quantities(g, &sums[10 * (size_t)c], means[c], qout[c]);
         for (int j = 0; j < 6; ++j) emax = std::max(emax, qout[c].eps[j]);
+        const double res2 = sums[10 * (size_t)c + 6], ss = sums[10 * (size_t)c + 9];
+        if (res2 > oc.rtol * oc.rtol * ss) res_ok = false;
+        if (ss > 0) worst_true = std::max(worst_true, std::sqrt(res2 / ss));
       }
+      r.rel_res_true = worst_true;
       phase_tick("approxim: quantities", st);
+      if (sc == FJ_OK && !res_ok) {   // true residual missed rtol: restart from z (warm)
+        if (restarts < o.max_restarts && spent < o.max_iter) {
+          ++restarts;
+          ++r.restarts;
+          warm = 1;
+          continue;
+        }
+        sc = FJ_E_NO_CONVERGENCE;
+      }
       if (sc != FJ_OK) { worst = sc; break; }
       if (o.eps_target <= 0.0 || emax <= o.eps_target || oc.rtol <= 1e-15 || spent >= o.max_iter) break;
       oc.rtol = std::max(oc.rtol * 1e-2, 1e-15);   // tighten and continue from z (warm start)

@@ -577,8 +577,8 @@ static fj_status build_batch_graph(fj_graph* g, BatchWs* w) {
 // Per-column true residuals are recomputed after the loop; columns missing rtol restart (all
 // columns together, warm) up to max_restarts times.
 fj_status solve_batch(fj_graph* g, int k, const double* s, double* z, const fj_solve_opts& o, int warm,
-                      fj_solve_report* rep, cudaStream_t st) {
-  if (vec_supported(k)) return solve_vec(g, k, s, z, o, warm, rep, st);
+                      fj_solve_report* rep, cudaStream_t st, bool defer_true_residual) {
+  if (vec_supported(k)) return solve_vec(g, k, s, z, o, warm, rep, st, defer_true_residual);
   BatchWs* w = nullptr;
   FJ_TRY(get_batch_ws(g, k, st, &w));
   const int64_t nk = g->n * (int64_t)k;

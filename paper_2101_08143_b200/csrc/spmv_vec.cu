@@ -600,13 +600,14 @@ static fj_status build_vec_graph(fj_graph* g, VecWs* w) {
 
 template <int KP>
 static fj_status solve_vec_t(fj_graph* g, VecWs* w, int k, const double* s, double* z, const fj_solve_opts& o,
-                             int warm, fj_solve_report* rep, cudaStream_t st) {
+                             int warm, fj_solve_report* rep, cudaStream_t st, bool defer) {
   const int64_t n = g->n;
   const unsigned cb = (unsigned)std::min<int64_t>((n + 255) / 256, 8192);
   w->x_is_solution = false;
   const SegLayout* L = nullptr;
   FJ_TRY(get_segments(g, KP, st, &L));   // before capture: the loop graph launches its passes
   if (o.use_cuda_graph) FJ_TRY(build_vec_graph<KP>(g, w));
+  phase_tick("vec: loop graph capture", st);
   VecScalars h{};
   int restarts = 0, total_iter = 0;
   bool first = true;
@@ -634,6 +635,18 @@ static fj_status solve_vec_t(fj_graph* g, VecWs* w, int k, const double* s, doub
       }
     }
     FJ_CK(cudaEventRecord(w->ev3, st));
+    phase_tick("vec: init + PCG loop", st);
+    if (defer) {   // the caller checks the true residual (fused quantities pass)
+      FJ_CK(cudaMemcpyAsync(&h, w->sc, sizeof h, cudaMemcpyDeviceToHost, st));
+      FJ_CK(cudaStreamSynchronize(st));
+      total_iter += h.iter;
+      if (o.use_cuda_graph) count_launch((2 + (L ? L->nseg : 1)) * std::max(h.iter, 1));
+      float lms = 0.f;
+      cudaEventElapsedTime(&lms, w->ev2, w->ev3);
+      if (rep) { rep->ms_loop += lms; rep->iterations_total += (int64_t)h.iter * k; }
+      for (int c = 0; c < k; ++c) h.res2[c] = h.rr[c];   // recursive residual stands in
+      break;
+    }
     FJ_TRY(by_wtype<KP>(g, [&](auto wt) {   // true residual per column
       constexpr int WT = decltype(wt)::value;
       ResidOpV<WT, KP> op{w->x, s, g->deg, k, w->sc};
@@ -641,6 +654,7 @@ static fj_status solve_vec_t(fj_graph* g, VecWs* w, int k, const double* s, doub
     }));
     FJ_CK(cudaMemcpyAsync(&h, w->sc, sizeof h, cudaMemcpyDeviceToHost, st));
     FJ_CK(cudaStreamSynchronize(st));
+    phase_tick("vec: true residual", st);
     total_iter += h.iter;
     if (o.use_cuda_graph) count_launch((2 + (L ? L->nseg : 1)) * std::max(h.iter, 1));
     float lms = 0.f;
@@ -660,7 +674,7 @@ static fj_status solve_vec_t(fj_graph* g, VecWs* w, int k, const double* s, doub
   bool converged = true;
   double worst_true = 0.0, worst_rec = 0.0;
   for (int c = 0; c < k; ++c) {
-    if (h.res2[c] > h.tol2[c]) converged = false;
+    if (h.res2[c] > h.tol2[c] && !(defer && h.conv[c])) converged = false;
     if (h.ss[c] > 0) {
       worst_true = std::max(worst_true, std::sqrt(h.res2[c] / h.ss[c]));
       worst_rec = std::max(worst_rec, std::sqrt(h.rr[c] / h.ss[c]));
@@ -671,7 +685,8 @@ static fj_status solve_vec_t(fj_graph* g, VecWs* w, int k, const double* s, doub
     rep->restarts = std::max(rep->restarts, restarts);
     rep->batch_k = k;
     rep->rel_res_recursive = std::max(rep->rel_res_recursive, worst_rec);
-    rep->rel_res_true = std::isnan(rep->rel_res_true) ? worst_true : std::max(rep->rel_res_true, worst_true);
+    if (!defer)
+      rep->rel_res_true = std::isnan(rep->rel_res_true) ? worst_true : std::max(rep->rel_res_true, worst_true);
     if (!converged) rep->converged = 0;
   }
   return converged ? FJ_OK : fail(FJ_E_NO_CONVERGENCE, "batched PCG did not reach rtol on the true residual");
@@ -681,13 +696,15 @@ static fj_status solve_vec_t(fj_graph* g, VecWs* w, int k, const double* s, doub
 bool vec_supported(int k) { return k >= 2 && k <= KVMAX; }
 
 fj_status solve_vec(fj_graph* g, int k, const double* s, double* z, const fj_solve_opts& o, int warm,
-                    fj_solve_report* rep, cudaStream_t st) {
+                    fj_solve_report* rep, cudaStream_t st, bool defer) {
   VecWs* w = nullptr;
+  phase_tick("vec: enter", st);
   FJ_TRY(get_vec_ws(g, k, st, &w));
+  phase_tick("vec: workspace + schedule", st);
   switch (w->kp) {
-    case 2: return solve_vec_t<2>(g, w, k, s, z, o, warm, rep, st);
-    case 3: return solve_vec_t<3>(g, w, k, s, z, o, warm, rep, st);
-    default: return solve_vec_t<4>(g, w, k, s, z, o, warm, rep, st);
+    case 2: return solve_vec_t<2>(g, w, k, s, z, o, warm, rep, st, defer);
+    case 3: return solve_vec_t<3>(g, w, k, s, z, o, warm, rep, st, defer);
+    default: return solve_vec_t<4>(g, w, k, s, z, o, warm, rep, st, defer);
   }
 }
 

@@ -81,8 +81,11 @@ inline fj_status cub_select_index(const uint8_t* flags, int32_t* out, int32_t* n
 void free_solve_ws(fj_graph* g);   // pcg.cu
 void free_quant_ws(fj_graph* g);   // quantities.cu
 void free_batch_ws(fj_graph* g);   // spmm.cu
+// defer_true_residual: stop on the recursive residual and leave the true-residual check (and any
+// restart) to the caller, which gets ||s - (I+L)z||^2 from the fused quantities pass; honoured by
+// the small-k vector engine (other engines check it themselves as usual).
 fj_status solve_batch(fj_graph* g, int k, const double* s, double* z, const fj_solve_opts& o, int warm,
-                      fj_solve_report* rep, cudaStream_t st);
+                      fj_solve_report* rep, cudaStream_t st, bool defer_true_residual = false);
 fj_status apply_batch(fj_graph* g, int k, const double* x, double* y, int opL, cudaStream_t st);
 fj_status quant_batch(fj_graph* g, int k, const double* s, const double* z, const double* mean_host,
                       double* host_out /* [k][10] */, cudaStream_t st, bool z_from_solve = false);
@@ -91,7 +94,7 @@ fj_status time_batch_spmv(fj_graph* g, int k, int reps, float* ms_out, cudaStrea
 void free_vec_ws(fj_graph* g);
 bool vec_supported(int k);
 fj_status solve_vec(fj_graph* g, int k, const double* s, double* z, const fj_solve_opts& o, int warm,
-                    fj_solve_report* rep, cudaStream_t st);
+                    fj_solve_report* rep, cudaStream_t st, bool defer_true_residual = false);
 fj_status apply_vec(fj_graph* g, int k, const double* x, double* y, int opL, cudaStream_t st);
 fj_status quant_vec(fj_graph* g, int k, const double* s, const double* z, const double* mean_host,
                     double* host_out, bool z_from_solve, cudaStream_t st);
