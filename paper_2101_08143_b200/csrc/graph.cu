@@ -105,6 +105,48 @@ __device__ __forceinline__ unsigned long long dbits(double x) {
   return (unsigned long long)__double_as_longlong(x);
 }
 
+constexpr int64_t kDegLong = 32;   // u8 rows longer than this are summed by a whole warp
+
+// Long rows of an integer-weighted graph: one warp per row; the integer sum is exact in any order,
+// so the degree is bit-identical to the ascending-column sum of k_degree and of the oracle.
+__global__ void k_degree_long_u8(int64_t n, const int64_t* __restrict__ rp, const uint8_t* __restrict__ w,
+                                 double* __restrict__ deg, double* __restrict__ dinv, GStats* st) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t r0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; r0 < n; r0 += nw * 32) {
+    const int64_t i = r0 + lane;
+    const int64_t len = i < n ? rp[i + 1] - rp[i] : 0;
+    unsigned longs = __ballot_sync(0xffffffffu, len > kDegLong);
+    while (longs) {
+      const int t = __ffs(longs) - 1;
+      longs &= longs - 1;
+      const int64_t row = r0 + t;
+      const int64_t b = rp[row], e = rp[row + 1];
+      unsigned long long s = 0;
+      unsigned mn = 255, mx = 0;
+      for (int64_t p = b + lane; p < e; p += 32) {
+        const unsigned x = w[p];
+        s += x;
+        mn = min(mn, x);
+        mx = max(mx, x);
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        s += __shfl_xor_sync(0xffffffffu, s, o);
+        mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      }
+      if (lane == 0) {
+        const double d = (double)s;
+        deg[row] = d;
+        dinv[row] = 1.0 / (1.0 + d);
+        atomicMax(&st->dmax_bits, dbits(d));
+        atomicMin(&st->wmin_bits, dbits((double)mn));
+        atomicMax(&st->wmax_bits, dbits((double)mx));
+      }
+    }
+  }
+}
+
 template <int WT>
 __global__ void k_degree(int64_t n, const int64_t* __restrict__ rp, const void* __restrict__ w,
                          double* __restrict__ deg, double* __restrict__ dinv, GStats* st) {
@@ -117,6 +159,8 @@ __global__ void k_degree(int64_t n, const int64_t* __restrict__ rp, const void* 
     if (WT == FJ_W_UNIT) {
       d = (double)len;
       if (len) { wmn = 1.0; wmx = 1.0; }
+    } else if (WT == FJ_W_U8 && len > kDegLong) {
+      // integer weights: the sum is exact in any order -> long rows go to k_degree_long (a warp each)
     } else {
       for (int64_t p = b; p < e; ++p) {   // ascending column order: bit-exact with the oracle
         const double x = WeightT<WT>::get(w, p);
@@ -125,8 +169,10 @@ __global__ void k_degree(int64_t n, const int64_t* __restrict__ rp, const void* 
         wmx = fmax(wmx, x);
       }
     }
-    deg[i] = d;
-    dinv[i] = 1.0 / (1.0 + d);   // IEEE division (no fast-math)
+    if (!(WT == FJ_W_U8 && len > kDegLong)) {
+      deg[i] = d;
+      dinv[i] = 1.0 / (1.0 + d);   // IEEE division (no fast-math)
+    }
   }
   // warp-aggregated statistics
   const unsigned iso = __ballot_sync(0xffffffffu, i < n && len == 0);
@@ -205,6 +251,11 @@ static fj_status launch_degree(fj_graph* g, GStats* st_d, int validate, cudaStre
   }
   k_degree<WT><<<nblk(g->n), 256, 0, st>>>(g->n, g->row_ptr, g->w, g->deg, g->dinv, st_d);
   FJ_CK_LAUNCH();
+  if (WT == FJ_W_U8) {
+    k_degree_long_u8<<<g->num_sms * 8, 256, 0, st>>>(g->n, g->row_ptr, reinterpret_cast<const uint8_t*>(g->w),
+                                                     g->deg, g->dinv, st_d);
+    FJ_CK_LAUNCH();
+  }
   return FJ_OK;
 }
 

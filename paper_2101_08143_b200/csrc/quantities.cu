@@ -228,8 +228,14 @@ fj_status fj_quantities(const fj_graph* gc, int k, const double* s, const double
   return FJ_OK;
 }
 
-fj_status fj_approxim(const fj_graph* gc, int k, const double* s, double* z_user, const fj_solve_opts* opts,
-                      fj_quantities_t* qout, fj_solve_report* rep, void* stream) {
+}  // extern "C"
+
+// Algorithm 1 (fj_approxim).  z_host (host-buffer entry point only): after the batched solve the
+// D2H of z runs on a side stream while the fused quantities pass runs on `stream`.
+static fj_status approxim_impl(const fj_graph* gc, int k, const double* s, double* z_user, const fj_solve_opts* opts,
+                               fj_quantities_t* qout, fj_solve_report* rep, void* stream, double* z_host,
+                               bool* z_host_done) {
+  if (z_host_done) *z_host_done = false;
   if (!gc || !s || !qout) return fail(FJ_E_INVALID_ARG, "null argument");
   if (k < 1 || k > MAXK) return fail(FJ_E_INVALID_ARG, "k must be in [1, 64]");
   if (z_user == s) return fail(FJ_E_INVALID_ARG, "s and z must not alias");
@@ -257,6 +263,8 @@ fj_status fj_approxim(const fj_graph* gc, int k, const double* s, double* z_user
   r.rel_res_true = NAN;
   const unsigned cb = (unsigned)std::min<int64_t>((g->n + 255) / 256, 4096);
   fj_status worst = FJ_OK;
+  SideStream side;            // z_host: D2H of z overlapping the quantities pass
+  bool d2h_issued = false;
   if (k >= batch_min_k() && !is_dist(g)) {
     // row a9: all k columns in ONE batched PCG (per-column alpha/beta, convergence mask)
     // The solve defers its true-residual pass: the fused quantities pass computes ||s - (I+L)z||^2
@@ -290,6 +298,14 @@ fj_status fj_approxim(const fj_graph* gc, int k, const double* s, double* z_user
           z_is_solve = false;
         }
       }
+      if (z_host) {   // z is final unless the residual check below restarts: copy it out meanwhile
+        if (!side.s) FJ_TRY(side.init());
+        FJ_CK(cudaEventRecord(side.ev_in, st));
+        FJ_CK(cudaStreamWaitEvent(side.s, side.ev_in, 0));
+        FJ_CK(cudaMemcpyAsync(z_host, z, sizeof(double) * g->n * k, cudaMemcpyDeviceToHost, side.s));
+        FJ_CK(cudaEventRecord(side.ev_out, side.s));
+        d2h_issued = true;
+      }
       FJ_TRY(quant_batch(g, k, s, z, means.data(), sums.data(), st, z_is_solve));   // Alg. 1 lines 5-9
       bool res_ok = true;
       double worst_true = 0.0;
@@ -312,6 +328,8 @@ fj_status fj_approxim(const fj_graph* gc, int k, const double* s, double* z_user
           ++restarts;
           ++r.restarts;
           warm = 1;
+          if (d2h_issued) FJ_CK(cudaStreamWaitEvent(st, side.ev_out, 0));   // z is read by the copy
+          d2h_issued = false;
           continue;
         }
         sc = FJ_E_NO_CONVERGENCE;
@@ -320,6 +338,8 @@ fj_status fj_approxim(const fj_graph* gc, int k, const double* s, double* z_user
       if (o.eps_target <= 0.0 || emax <= o.eps_target || oc.rtol <= 1e-15 || spent >= o.max_iter) break;
       oc.rtol = std::max(oc.rtol * 1e-2, 1e-15);   // tighten and continue from z (warm start)
       warm = 1;
+      if (d2h_issued) FJ_CK(cudaStreamWaitEvent(st, side.ev_out, 0));
+      d2h_issued = false;
     }
     r.iterations = spent;
   } else {
@@ -373,8 +393,19 @@ fj_status fj_approxim(const fj_graph* gc, int k, const double* s, double* z_user
   r.ms = ms;
   if (worst != FJ_OK) r.converged = 0;
   if (rep) *rep = r;
+  if (d2h_issued) {
+    FJ_CK(cudaStreamSynchronize(side.s));
+    if (z_host_done) *z_host_done = true;
+  }
   if (worst != FJ_OK) return fail(worst, "PCG did not reach rtol on the true residual");
   return FJ_OK;
+}
+
+extern "C" {
+
+fj_status fj_approxim(const fj_graph* gc, int k, const double* s, double* z_user, const fj_solve_opts* opts,
+                      fj_quantities_t* qout, fj_solve_report* rep, void* stream) {
+  return approxim_impl(gc, k, s, z_user, opts, qout, rep, stream, nullptr, nullptr);
 }
 
 fj_status fj_approxim_host(int64_t n, int64_t m_in, const int32_t* u_h, const int32_t* v_h, const void* w_h,
@@ -414,8 +445,9 @@ fj_status fj_approxim_host(int64_t n, int64_t m_in, const int32_t* u_h, const in
   fj_graph* g = nullptr;
   FJ_TRY(fj_graph_create(n, nnz, drp.p, dcol.p, wbytes ? dwo.p : nullptr, wtype, 0, stream, &g));
   FJ_CK(cudaStreamWaitEvent(st, side.ev_out, 0));
-  fj_status s = fj_approxim(g, k, ds.p, dz.p, opts, q_h, rep, stream);
-  if ((s == FJ_OK || s == FJ_E_NO_CONVERGENCE) && z_h) {
+  bool z_done = false;
+  fj_status s = approxim_impl(g, k, ds.p, dz.p, opts, q_h, rep, stream, z_h, &z_done);
+  if ((s == FJ_OK || s == FJ_E_NO_CONVERGENCE) && z_h && !z_done) {
     cudaError_t e = cudaMemcpyAsync(z_h, dz.p, sizeof(double) * n * k, cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) s = cuda_fail(e, "z readback", __FILE__, __LINE__);

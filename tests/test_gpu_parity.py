@@ -121,6 +121,7 @@ def test_apply_matches_oracle(fj, wkind, op):
     g, (rp, col, wo) = assert_csr_equal(fj, n, u, v, w)
     G = fj.Graph(n, rp, col, wo)
     assert G.info()["n_long_rows"] >= 3
+    assert np.array_equal(host(G.degrees()), O.degrees(g))   # bit-exact, incl. the warp-summed long u8 rows
     X = rng.normal(size=(n, 3))
     Y = host(G.apply(dev(X), op=op))
     for c in range(3):
