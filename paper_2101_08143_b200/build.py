@@ -49,7 +49,8 @@ def build(force: bool = False, verbose: bool = False, so: str = SO, defines=()) 
         return SO
     objs = []
     tag = "" if not defines else "_" + "_".join(d.replace("=", "") for d in defines)
-    bdir = os.path.join(HERE, "build" + tag)
+    # variant objects live outside the repo (they are not shipped to the GPU box)
+    bdir = os.path.join(HERE, "build") if not defines else os.path.join("/tmp", "fj_build" + tag)
     os.makedirs(bdir, exist_ok=True)
     procs = []
     for src in sources():

@@ -201,14 +201,17 @@ struct ResidOpV {
   }
 };
 
-// Fused quantities pass (rows a5-a7) for all columns at once; the 10 per-row contributions of
-// QuantOp (ops.cuh) per column, part[j * KP + c].
+// Quantities pass (rows a5-a7) for all columns at once, split in two: the four sums that need the
+// neighbours (this row operator: part[j * KP + c], j = 0 Dd = sum_j w (z_i - z_j)^2, 1 (s - (I+L)z)^2,
+// 2 (Lz)^2, 3 rounding allowance^2) and the six row-local sums of QuantOp (k_quant_local).  40
+// per-thread partials in one kernel cost 255 registers and 2 blocks / SM (2.2 ms on C3); split,
+// the row operator runs at the product's occupancy.
 template <int WT, int KP>
 struct QuantOpV {
   using V = DVec<KP>;
   static constexpr int ITEMS = VEC_ITEMS;
-  static constexpr int MIN_BLOCKS = FJ_QUANTV_MIN_BLOCKS;   // 40 per-thread partial sums
-  static constexpr int NA = 3 * KP, NP = 10 * KP;
+  static constexpr int MIN_BLOCKS = FJ_QUANTV_MIN_BLOCKS;
+  static constexpr int NA = 3 * KP, NP = 4 * KP;
   static constexpr bool NEEDS_XI = true;
   static __device__ __forceinline__ V vzero() { return vzero_kp<KP>(); }
   const double* __restrict__ z;   // padded [n][KP]
@@ -216,7 +219,7 @@ struct QuantOpV {
   const double* __restrict__ deg;
   int k;
   double m[KP];                   // mean of s per column
-  double* out;                    // [10][KP]
+  double* out;                    // [4][KP]
   __device__ __forceinline__ bool skip() const { return false; }
   __device__ __forceinline__ bool wants_xi() const { return true; }
   __device__ __forceinline__ V gather(int32_t j) const { return ld_vec<KP>(z + (int64_t)j * KP); }
@@ -242,18 +245,11 @@ struct QuantOpV {
       const double t = fma(1.0 + d, zi, -a[c]);
       const double lz = fma(d, zi, -a[c]);
       const double r = si - t;
-      const double e1 = zi - si, e2 = zi - m[c], e3 = si - m[c];
       const double ab = fabs(si) + fma(1.0 + d, fabs(zi), a[2 * KP + c]);
-      part[0 * KP + c] = fma(e1, e1, part[0 * KP + c]);
-      part[1 * KP + c] += a[KP + c];
-      part[2 * KP + c] = fma(e2, e2, part[2 * KP + c]);
-      part[3 * KP + c] = fma(zi, zi, part[3 * KP + c]);
-      part[4 * KP + c] = fma(si, zi, part[4 * KP + c]);
-      part[5 * KP + c] = fma(e3, e2, part[5 * KP + c]);
-      part[6 * KP + c] = fma(r, r, part[6 * KP + c]);
-      part[7 * KP + c] = fma(lz, lz, part[7 * KP + c]);
-      part[8 * KP + c] = fma(ab, ab, part[8 * KP + c]);
-      part[9 * KP + c] = fma(si, si, part[9 * KP + c]);
+      part[0 * KP + c] += a[KP + c];
+      part[1 * KP + c] = fma(r, r, part[1 * KP + c]);
+      part[2 * KP + c] = fma(lz, lz, part[2 * KP + c]);
+      part[3 * KP + c] = fma(ab, ab, part[3 * KP + c]);
     }
   }
   __device__ __forceinline__ void finalize(const double (&tot)[NP]) const {
@@ -265,6 +261,8 @@ struct QuantOpV {
 // ---------------------------------------------------------------- elementwise kernels
 // One thread per row (KP values, one aligned vector load per array); fixed grid, per-column
 // partials reduced block -> last block in block order (deterministic).
+template <int NPART>
+__device__ __forceinline__ bool vec_reduce(double (&v)[NPART], double* part, unsigned int* ticket, double* s_red);
 template <int NPART>
 __device__ __forceinline__ bool vec_reduce(double (&v)[NPART], double* part, unsigned int* ticket, double* s_red) {
   block_sum<NPART, VETB>(v, s_red);
@@ -284,6 +282,42 @@ __device__ __forceinline__ bool vec_reduce(double (&v)[NPART], double* part, uns
 #pragma unroll
   for (int j = 0; j < NPART; ++j) v[j] = t[j];
   return true;
+}
+
+// Row-local quantity sums (QuantOp order 0 (z-s)^2, 2 (z-m)^2, 3 z^2, 4 s z, 5 (s-m)(z-m), 9 s^2):
+// out[j * KP + c], j = 0..5 in that order.
+template <int KP>
+__global__ void __launch_bounds__(VETB) k_quant_local(int64_t n, int k, const double* __restrict__ s,
+                                                      const double* __restrict__ z, const double* __restrict__ mean,
+                                                      double* part, unsigned int* ticket, double* out) {
+  __shared__ double s_red[6 * KP * VETB / 32];
+  double v[6 * KP];
+#pragma unroll
+  for (int j = 0; j < 6 * KP; ++j) v[j] = 0.0;
+  double m[KP];
+#pragma unroll
+  for (int c = 0; c < KP; ++c) m[c] = c < k ? mean[c] : 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)VETB + threadIdx.x; i < n; i += (int64_t)gridDim.x * VETB) {
+    const DVec<KP> zv = ld_vec<KP>(z + i * KP);
+#pragma unroll
+    for (int c = 0; c < KP; ++c) {
+      if (c < k) {
+        const double zi = zv.v[c], si = s[i * k + c];
+        const double e1 = zi - si, e2 = zi - m[c], e3 = si - m[c];
+        v[0 * KP + c] = fma(e1, e1, v[0 * KP + c]);
+        v[1 * KP + c] = fma(e2, e2, v[1 * KP + c]);
+        v[2 * KP + c] = fma(zi, zi, v[2 * KP + c]);
+        v[3 * KP + c] = fma(si, zi, v[3 * KP + c]);
+        v[4 * KP + c] = fma(e3, e2, v[4 * KP + c]);
+        v[5 * KP + c] = fma(si, si, v[5 * KP + c]);
+      }
+    }
+  }
+  if (vec_reduce<6 * KP>(v, part, ticket, s_red) && threadIdx.x == 0) {
+#pragma unroll
+    for (int j = 0; j < 6 * KP; ++j) out[j] = v[j];
+    *ticket = 0u;
+  }
 }
 
 // fresh start (x = 0, r = s) or restart (r = s - q, q = (I+L) x precomputed); p = dinv o r.
@@ -442,7 +476,7 @@ struct VecWs {
   double *r = nullptr, *p = nullptr, *q = nullptr, *x = nullptr;
   bool x_is_solution = false;        // x holds the padded z of the last solve_vec (for quant_vec)
   VecScalars* sc = nullptr;
-  double* elem_part = nullptr;       // [grid_elem][3 * KVMAX]
+  double* elem_part = nullptr;       // [grid_elem][6 * KVMAX]
   unsigned int* elem_ticket = nullptr;
   TileScratch ts{};
   double* qout = nullptr;            // [VNP_MAX]
@@ -501,7 +535,7 @@ static fj_status get_vec_ws(fj_graph* g, int k, cudaStream_t st, VecWs** out) {
   const int64_t need = (g->n + VETB - 1) / VETB;
   if (ge > need) ge = need > 0 ? need : 1;
   w->grid_elem = (int)ge;
-  FJ_TRY(valloc(&w->elem_part, ge * 3 * KVMAX, st));
+  FJ_TRY(valloc(&w->elem_part, ge * 6 * KVMAX, st));
   FJ_TRY(valloc(&w->elem_ticket, 1, st, true));
   w->grid_max = g->num_sms * (2048 / WTPB);
   FJ_TRY(valloc(&w->ts.block_part, (int64_t)w->grid_max * VNP_MAX, st));
@@ -510,7 +544,7 @@ static fj_status get_vec_ws(fj_graph* g, int k, cudaStream_t st, VecWs** out) {
   FJ_TRY(valloc(&w->ts.chunk_acc, g->sv.n_long_chunks * VNA_MAX, st));
   FJ_TRY(valloc(&w->ts.long_ticket, g->sv.n_long, st, true));
   FJ_TRY(valloc(&w->ts.grid_ticket, 1, st, true));
-  FJ_TRY(valloc(&w->qout, VNP_MAX, st));
+  FJ_TRY(valloc(&w->qout, VNP_MAX + 6 * KVMAX + KVMAX, st));   // [4][KP] engine sums, [6][KP] local, means
   FJ_CK(cudaEventCreate(&w->ev2));
   FJ_CK(cudaEventCreate(&w->ev3));
   FJ_CK(cudaEventCreate(&w->ev4));
@@ -773,8 +807,15 @@ fj_status quant_vec(fj_graph* g, int k, const double* s, const double* z, const 
     FJ_CK_LAUNCH();
     zp = w->q;
   }
+  double* loc = w->qout + 4 * KVMAX;         // [6][KP]
+  double* dmean = loc + 6 * KVMAX;            // [KP]
+  FJ_CK(cudaMemcpyAsync(dmean, mean_host, sizeof(double) * k, cudaMemcpyHostToDevice, st));
   auto launch = [&](auto kpc) -> fj_status {
     constexpr int KP = decltype(kpc)::value;
+    phase_tick("quant: enter", st);
+    k_quant_local<KP><<<w->grid_elem, VETB, 0, st>>>(g->n, k, s, zp, dmean, w->elem_part, w->elem_ticket, loc);
+    FJ_CK_LAUNCH();
+    phase_tick("quant: local sums", st);
     return by_wtype<KP>(g, [&](auto wt) {
       constexpr int WT = decltype(wt)::value;
       QuantOpV<WT, KP> op;
@@ -786,11 +827,15 @@ fj_status quant_vec(fj_graph* g, int k, const double* s, const double* z, const 
   if (kp == 2) FJ_TRY(launch(std::integral_constant<int, 2>()));
   else if (kp == 3) FJ_TRY(launch(std::integral_constant<int, 3>()));
   else FJ_TRY(launch(std::integral_constant<int, 4>()));
-  std::vector<double> h(10 * kp);
-  FJ_CK(cudaMemcpyAsync(h.data(), w->qout, sizeof(double) * 10 * kp, cudaMemcpyDeviceToHost, st));
+  phase_tick("quant: neighbour sums", st);
+  std::vector<double> h(4 * kp + 6 * kp);
+  FJ_CK(cudaMemcpyAsync(h.data(), w->qout, sizeof(double) * 4 * kp, cudaMemcpyDeviceToHost, st));
+  FJ_CK(cudaMemcpyAsync(h.data() + 4 * kp, loc, sizeof(double) * 6 * kp, cudaMemcpyDeviceToHost, st));
   FJ_CK(cudaStreamSynchronize(st));
+  // QuantOp order: 0 (z-s)^2, 1 Dd, 2 (z-m)^2, 3 z^2, 4 sz, 5 (s-m)(z-m), 6 res^2, 7 (Lz)^2, 8 allow^2, 9 s^2
+  static const int src[10] = {4 + 0, 0, 4 + 1, 4 + 2, 4 + 3, 4 + 4, 1, 2, 3, 4 + 5};
   for (int c = 0; c < k; ++c)
-    for (int j = 0; j < 10; ++j) host_out[c * 10 + j] = h[j * kp + c];
+    for (int j = 0; j < 10; ++j) host_out[c * 10 + j] = h[src[j] * kp + c];
   return FJ_OK;
 }
 
