@@ -183,7 +183,7 @@ struct SolveWs {
   int grid_max = 0, grid_elem = 0;
   double *r = nullptr, *p = nullptr, *q = nullptr, *x = nullptr, *col_s = nullptr;
   PcgScalars* sc = nullptr;
-  double* elem_part = nullptr;       // [grid_elem][4]
+  double* elem_part = nullptr;       // [grid_elem][16]
   unsigned int* elem_ticket = nullptr;
   TileScratch ts{};
   double* qout = nullptr;            // [16] quantities totals

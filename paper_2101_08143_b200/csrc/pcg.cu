@@ -68,7 +68,7 @@ fj_status get_ws(fj_graph* g, cudaStream_t st, SolveWs** out) {
   FJ_TRY(dalloc(&w->q, n, st));
   FJ_TRY(dalloc(&w->x, n, st));
   FJ_TRY(dalloc(&w->sc, 1, st, true));
-  FJ_TRY(dalloc(&w->elem_part, (int64_t)w->grid_elem * 4, st));
+  FJ_TRY(dalloc(&w->elem_part, (int64_t)w->grid_elem * 16, st));   // k_stats_k: 4 x 4 per block
   FJ_TRY(dalloc(&w->elem_ticket, 1, st, true));
   constexpr int NPMAX = 16, NAMAX = 4;
   FJ_TRY(dalloc(&w->ts.block_part, (int64_t)w->grid_max * NPMAX, st));

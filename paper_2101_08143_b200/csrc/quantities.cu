@@ -68,14 +68,86 @@ __global__ void __launch_bounds__(STPB) k_stats(int64_t n, const double* __restr
   }
 }
 
+// All k <= 4 columns of row-major [n][k] in one pass (one thread per row); same outputs as k_stats
+// per column: out[4c + {0,1,2,3}] = (sum, sum of squares, min, max), NaN sum on non-finite input.
+template <int K>
+__global__ void __launch_bounds__(STPB) k_stats_k(int64_t n, int k, const double* __restrict__ s,
+                                                  double* part /*[grid][4K]*/, unsigned int* ticket, double* out,
+                                                  int* nonfinite) {
+  __shared__ double s_red[2 * K * STPB / 32];
+  __shared__ double s_mm[2 * K][STPB / 32];
+  __shared__ bool s_last;
+  double v[2 * K], mn[K], mx[K];
+#pragma unroll
+  for (int c = 0; c < K; ++c) { v[2 * c] = 0.0; v[2 * c + 1] = 0.0; mn[c] = INFINITY; mx[c] = -INFINITY; }
+  int bad = 0;
+  for (int64_t i = blockIdx.x * (int64_t)STPB + threadIdx.x; i < n; i += (int64_t)gridDim.x * STPB) {
+#pragma unroll
+    for (int c = 0; c < K; ++c) {
+      if (c < k) {
+        const double x = s[i * k + c];
+        if (!isfinite(x)) { bad = 1; continue; }
+        v[2 * c] += x;
+        v[2 * c + 1] = fma(x, x, v[2 * c + 1]);
+        mn[c] = fmin(mn[c], x);
+        mx[c] = fmax(mx[c], x);
+      }
+    }
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(nonfinite, 1);
+  block_sum<2 * K, STPB>(v, s_red);
+#pragma unroll
+  for (int c = 0; c < K; ++c) {
+    for (int o = 16; o > 0; o >>= 1) {
+      mn[c] = fmin(mn[c], __shfl_xor_sync(0xffffffffu, mn[c], o));
+      mx[c] = fmax(mx[c], __shfl_xor_sync(0xffffffffu, mx[c], o));
+    }
+    if ((threadIdx.x & 31) == 0) { s_mm[2 * c][threadIdx.x >> 5] = mn[c]; s_mm[2 * c + 1][threadIdx.x >> 5] = mx[c]; }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int c = 0; c < K; ++c) {
+      for (int w = 1; w < STPB / 32; ++w) { mn[c] = fmin(mn[c], s_mm[2 * c][w]); mx[c] = fmax(mx[c], s_mm[2 * c + 1][w]); }
+      part[blockIdx.x * 4 * K + 4 * c + 0] = v[2 * c];
+      part[blockIdx.x * 4 * K + 4 * c + 1] = v[2 * c + 1];
+      part[blockIdx.x * 4 * K + 4 * c + 2] = mn[c];
+      part[blockIdx.x * 4 * K + 4 * c + 3] = mx[c];
+    }
+    __threadfence();
+    s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) {
+    __threadfence();
+    for (int c = 0; c < k; ++c) {
+      double a = 0.0, b = 0.0, lo = INFINITY, hi = -INFINITY;
+      for (unsigned q = 0; q < gridDim.x; ++q) {   // fixed order
+        a += __ldcg(part + q * 4 * K + 4 * c + 0);
+        b += __ldcg(part + q * 4 * K + 4 * c + 1);
+        lo = fmin(lo, __ldcg(part + q * 4 * K + 4 * c + 2));
+        hi = fmax(hi, __ldcg(part + q * 4 * K + 4 * c + 3));
+      }
+      out[4 * c + 0] = *(volatile int*)nonfinite ? NAN : a;
+      out[4 * c + 1] = b; out[4 * c + 2] = lo; out[4 * c + 3] = hi;
+    }
+    *ticket = 0u;
+  }
+}
+
 static fj_status stats_cols(fj_graph* g, SolveWs* w, int k, const double* s, std::vector<double>& st4,
                             cudaStream_t st) {
   int* d_bad = nullptr;
   FJ_CK(dmalloc(&d_bad, sizeof(int), st));
   FJ_CK(cudaMemsetAsync(d_bad, 0, sizeof(int), st));
-  for (int c = 0; c < k; ++c) {
-    k_stats<<<w->grid_elem, STPB, 0, st>>>(g->n, s, k, c, w->elem_part, w->elem_ticket, w->stat + 4 * c, d_bad);
+  if (k > 1 && k <= 4) {   // one pass over all columns (SolveWs::elem_part holds grid x 16 doubles)
+    k_stats_k<4><<<w->grid_elem, STPB, 0, st>>>(g->n, k, s, w->elem_part, w->elem_ticket, w->stat, d_bad);
     FJ_CK_LAUNCH();
+  } else {
+    for (int c = 0; c < k; ++c) {
+      k_stats<<<w->grid_elem, STPB, 0, st>>>(g->n, s, k, c, w->elem_part, w->elem_ticket, w->stat + 4 * c, d_bad);
+      FJ_CK_LAUNCH();
+    }
   }
   if (is_dist(g)) FJ_TRY(dist_stats_combine(g, k, w->stat, st));   // global over the ranks' slices
   st4.assign(4 * k, 0.0);

@@ -81,6 +81,26 @@ template <int KP> __device__ __forceinline__ DVec<KP> vzero_kp() {
   return r;
 }
 
+// Rows of the solver's other vectors (x, r, q) are stored KQ wide (KQ = k: 3 for k = 3, no padding);
+// only the gathered direction p is padded to KP.  ld_q/st_q move a KQ-wide row as a KP vector.
+template <int KP, int KQ>
+__device__ __forceinline__ DVec<KP> ld_q(const double* base, int64_t i) {
+  if (KP == KQ) return ld_vec<KP>(base + i * KP);
+  const DVec<KQ> t = ld_vec<KQ>(base + i * KQ);
+  DVec<KP> r;
+#pragma unroll
+  for (int c = 0; c < KP; ++c) r.v[c] = c < KQ ? t.v[c] : 0.0;
+  return r;
+}
+template <int KP, int KQ>
+__device__ __forceinline__ void st_q(double* base, int64_t i, const DVec<KP>& v) {
+  if (KP == KQ) { st_vec<KP>(base + i * KP, *reinterpret_cast<const DVec<KP>*>(&v)); return; }
+  DVec<KQ> t;
+#pragma unroll
+  for (int c = 0; c < KQ; ++c) t.v[c] = v.v[c];
+  st_vec<KQ>(base + i * KQ, t);
+}
+
 // Device scalars of one small-k batched solve (per column), written only by last-block finalisers.
 struct VecScalars {
   double rho[KVMAX], alpha[KVMAX], beta[KVMAX], pq[KVMAX], rr[KVMAX], ss[KVMAX], tol2[KVMAX], res2[KVMAX];
@@ -90,7 +110,7 @@ struct VecScalars {
 
 // ---------------------------------------------------------------- row operators (tiles.cuh Op)
 // q = (I+L) p or L p for all KP columns of a padded [n][KP] block (P:L88 L = D - A).
-template <int WT, int KP, int SEG = SEG_WHOLE>   // SEG: role in a segmented product (segments.cu)
+template <int WT, int KP, int KQ = KP, int SEG = SEG_WHOLE>   // y stored KQ wide; SEG: segments.cu role
 struct ApplyOpV {
   using V = DVec<KP>;
   static constexpr int ITEMS = VEC_ITEMS;
@@ -107,8 +127,8 @@ struct ApplyOpV {
   __device__ __forceinline__ bool skip() const { return sc && *(volatile int32_t*)&sc->done; }
   __device__ __forceinline__ bool wants_xi() const { return SEG != SEG_MID; }
   template <int S>
-  ApplyOpV<WT, KP, S> as_seg() const {
-    ApplyOpV<WT, KP, S> o;
+  ApplyOpV<WT, KP, KQ, S> as_seg() const {
+    ApplyOpV<WT, KP, KQ, S> o;
     static_assert(sizeof o == sizeof *this, "same layout");
     memcpy(static_cast<void*>(&o), this, sizeof o);
     return o;
@@ -129,7 +149,7 @@ struct ApplyOpV {
 #pragma unroll
       for (int c = 0; c < KP; ++c) yv.v[c] = fma(dd, xi.v[c], -a[c]);
     } else {
-      yv = ld_vec<KP>(y + i * KP);
+      yv = ld_q<KP, KQ>(y, i);
 #pragma unroll
       for (int c = 0; c < KP; ++c) yv.v[c] -= a[c];
     }
@@ -137,7 +157,7 @@ struct ApplyOpV {
 #pragma unroll
       for (int c = 0; c < KP; ++c) part[c] = fma(xi.v[c], yv.v[c], part[c]);
     }
-    st_vec<KP>(y + i * KP, yv);
+    st_q<KP, KQ>(y, i, yv);
   }
   __device__ __forceinline__ void finalize(const double (&tot)[NP]) const {
     if (!sc || SEG == SEG_FIRST || SEG == SEG_MID) return;
@@ -321,7 +341,7 @@ __global__ void __launch_bounds__(VETB) k_quant_local(int64_t n, int k, const do
 }
 
 // fresh start (x = 0, r = s) or restart (r = s - q, q = (I+L) x precomputed); p = dinv o r.
-template <int KP>
+template <int KP, int KQ>
 __global__ void __launch_bounds__(VETB) k_v_init(int64_t n, int k, const double* __restrict__ s,
                                                  const double* __restrict__ dinv, const double* __restrict__ q,
                                                  int restart, double* __restrict__ x, double* __restrict__ r,
@@ -336,12 +356,12 @@ __global__ void __launch_bounds__(VETB) k_v_init(int64_t n, int k, const double*
 #pragma unroll
     for (int c = 0; c < KP; ++c) sv.v[c] = c < k ? s[i * k + c] : 0.0;
     if (restart) {
-      const DVec<KP> qv = ld_vec<KP>(q + i * KP);
+      const DVec<KP> qv = ld_q<KP, KQ>(q, i);
 #pragma unroll
       for (int c = 0; c < KP; ++c) rv.v[c] = c < k ? sv.v[c] - qv.v[c] : 0.0;
     } else {
       rv = sv;
-      st_vec<KP>(x + i * KP, vzero_kp<KP>());
+      st_q<KP, KQ>(x, i, vzero_kp<KP>());
     }
     const double di = dinv[i];
 #pragma unroll
@@ -351,7 +371,7 @@ __global__ void __launch_bounds__(VETB) k_v_init(int64_t n, int k, const double*
       v[KP + c] = fma(rv.v[c], rv.v[c], v[KP + c]);
       v[2 * KP + c] = fma(sv.v[c], sv.v[c], v[2 * KP + c]);
     }
-    st_vec<KP>(r + i * KP, rv);
+    st_q<KP, KQ>(r, i, rv);
     st_vec<KP>(p + i * KP, pv);
   }
   if (vec_reduce<3 * KP>(v, part, ticket, s_red) && threadIdx.x == 0) {
@@ -376,7 +396,7 @@ __global__ void __launch_bounds__(VETB) k_v_init(int64_t n, int k, const double*
   }
 }
 
-template <int KP>
+template <int KP, int KQ>
 __global__ void __launch_bounds__(VETB) k_v_update(int64_t n, int k, const double* __restrict__ dinv,
                                                    const double* __restrict__ p, const double* __restrict__ q,
                                                    double* __restrict__ x, double* __restrict__ r, VecScalars* sc,
@@ -394,8 +414,8 @@ __global__ void __launch_bounds__(VETB) k_v_update(int64_t n, int k, const doubl
 #pragma unroll
   for (int j = 0; j < 2 * KP; ++j) v[j] = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)VETB + threadIdx.x; i < n; i += (int64_t)gridDim.x * VETB) {
-    const DVec<KP> pv = ld_vec<KP>(p + i * KP), qv = ld_vec<KP>(q + i * KP);
-    DVec<KP> xv = ld_vec<KP>(x + i * KP), rv = ld_vec<KP>(r + i * KP);
+    const DVec<KP> pv = ld_vec<KP>(p + i * KP), qv = ld_q<KP, KQ>(q, i);
+    DVec<KP> xv = ld_q<KP, KQ>(x, i), rv = ld_q<KP, KQ>(r, i);
     const double di = dinv[i];
 #pragma unroll
     for (int c = 0; c < KP; ++c) {
@@ -404,8 +424,8 @@ __global__ void __launch_bounds__(VETB) k_v_update(int64_t n, int k, const doubl
       v[c] = fma(rv.v[c], di * rv.v[c], v[c]);
       v[KP + c] = fma(rv.v[c], rv.v[c], v[KP + c]);
     }
-    st_vec<KP>(x + i * KP, xv);
-    st_vec<KP>(r + i * KP, rv);
+    st_q<KP, KQ>(x, i, xv);
+    st_q<KP, KQ>(r, i, rv);
   }
   if (vec_reduce<2 * KP>(v, part, ticket, s_red) && threadIdx.x == 0) {
     int any = 0;
@@ -429,7 +449,7 @@ __global__ void __launch_bounds__(VETB) k_v_update(int64_t n, int k, const doubl
   }
 }
 
-template <int KP>
+template <int KP, int KQ>
 __global__ void __launch_bounds__(VETB) k_v_dir(int64_t n, int k, const double* __restrict__ dinv,
                                                 const double* __restrict__ r, double* __restrict__ p,
                                                 const VecScalars* sc) {
@@ -438,7 +458,7 @@ __global__ void __launch_bounds__(VETB) k_v_dir(int64_t n, int k, const double* 
 #pragma unroll
   for (int c = 0; c < KP; ++c) be[c] = (c < k && sc->active[c]) ? sc->beta[c] : 0.0;
   for (int64_t i = blockIdx.x * (int64_t)VETB + threadIdx.x; i < n; i += (int64_t)gridDim.x * VETB) {
-    const DVec<KP> rv = ld_vec<KP>(r + i * KP);
+    const DVec<KP> rv = ld_q<KP, KQ>(r, i);
     DVec<KP> pv = ld_vec<KP>(p + i * KP);
     const double di = dinv[i];
 #pragma unroll
@@ -457,6 +477,11 @@ __global__ void k_v_pack(int64_t n, int k, const double* __restrict__ src, doubl
     st_vec<KP>(dst + i * KP, v);
   }
 }
+template <int KP, int KQ>
+__global__ void k_v_pack_from(int64_t n, const double* __restrict__ src, double* __restrict__ dst) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    st_vec<KP>(dst + i * KP, ld_q<KP, KQ>(src, i));
+}
 template <int KP>
 __global__ void k_v_unpack(int64_t n, int k, const double* __restrict__ src, double* __restrict__ dst) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -471,10 +496,10 @@ __global__ void k_v_unpack(int64_t n, int k, const double* __restrict__ src, dou
 constexpr int VNP_MAX = 10 * KVMAX, VNA_MAX = 3 * KVMAX;
 
 struct VecWs {
-  int k = 0, kp = 0;
+  int k = 0, kp = 0, kq = 0;         // k columns; p rows KP wide (gathered), x / r / q rows KQ wide
   int grid_elem = 0, grid_max = 0;
   double *r = nullptr, *p = nullptr, *q = nullptr, *x = nullptr;
-  bool x_is_solution = false;        // x holds the padded z of the last solve_vec (for quant_vec)
+  bool x_is_solution = false;        // x holds z ([n][KQ]) of the last solve_vec (for quant_vec)
   VecScalars* sc = nullptr;
   double* elem_part = nullptr;       // [grid_elem][6 * KVMAX]
   unsigned int* elem_ticket = nullptr;
@@ -514,11 +539,12 @@ static fj_status valloc(T** p, int64_t count, cudaStream_t st, bool zero = false
 }
 
 static int kp_of(int k) { return k <= 2 ? 2 : k == 3 ? vec_pad3() : 4; }
+static int kq_of(int k) { return k <= 2 ? 2 : k == 3 ? 3 : 4; }   // x, r, q: unpadded
 
 static fj_status get_vec_ws(fj_graph* g, int k, cudaStream_t st, VecWs** out) {
   VecWs* w = vec_cache(g);
-  const int kp = kp_of(k);
-  if (w && w->kp == kp) { w->k = k; *out = w; return FJ_OK; }
+  const int kp = kp_of(k), kq = kq_of(k);
+  if (w && w->kp == kp && w->kq == kq) { w->k = k; *out = w; return FJ_OK; }
   if (w) {
     FJ_CK(cudaStreamSynchronize(st));   // old buffers may still be in use on st
     free_vec_ws(g);
@@ -527,9 +553,10 @@ static fj_status get_vec_ws(fj_graph* g, int k, cudaStream_t st, VecWs** out) {
   g->vec_ws = w;
   w->k = k;
   w->kp = kp;
-  const int64_t nk = g->n * (int64_t)kp;
-  FJ_TRY(valloc(&w->r, nk, st)); FJ_TRY(valloc(&w->p, nk, st));
-  FJ_TRY(valloc(&w->q, nk, st)); FJ_TRY(valloc(&w->x, nk, st));
+  w->kq = kq;
+  const int64_t nkp = g->n * (int64_t)kp, nkq = g->n * (int64_t)kq;
+  FJ_TRY(valloc(&w->r, nkq, st)); FJ_TRY(valloc(&w->p, nkp, st));
+  FJ_TRY(valloc(&w->q, nkq, st)); FJ_TRY(valloc(&w->x, nkq, st));
   FJ_TRY(valloc(&w->sc, 1, st, true));
   int64_t ge = (int64_t)g->num_sms * (2048 / VETB);
   const int64_t need = (g->n + VETB - 1) / VETB;
@@ -579,12 +606,13 @@ static fj_status by_wtype(const fj_graph* g, F&& f) {
   }
 }
 
-template <int KP>
+// y [n][KQ] = (I+L) x (or L x) for x the padded [n][KP] block
+template <int KP, int KQ>
 static fj_status vec_apply_padded(const fj_graph* g, const VecWs* w, const double* x, double* y, int opL,
                                   VecScalars* sc, cudaStream_t st) {
   return by_wtype<KP>(g, [&](auto wt) {
     constexpr int WT = decltype(wt)::value;
-    ApplyOpV<WT, KP> op{x, y, g->deg, opL, sc, w->k};
+    ApplyOpV<WT, KP, KQ> op{x, y, g->deg, opL, sc, w->k};
     int nl = 0;
     FJ_CK(launch_product<WT>(g, seg_for(g, KP), w->ts, w->grid_max, op, st, &nl));   // L2 segments
     if (!g_capturing) count_launch(nl);
@@ -592,18 +620,18 @@ static fj_status vec_apply_padded(const fj_graph* g, const VecWs* w, const doubl
   });
 }
 
-template <int KP>
+template <int KP, int KQ>
 static fj_status vec_iteration(const fj_graph* g, VecWs* w, cudaStream_t st, cudaGraphConditionalHandle h, int use_h) {
-  FJ_TRY(vec_apply_padded<KP>(g, w, w->p, w->q, 0, w->sc, st));
-  k_v_update<KP><<<w->grid_elem, VETB, 0, st>>>(g->n, w->k, g->dinv, w->p, w->q, w->x, w->r, w->sc, w->elem_part,
+  FJ_TRY((vec_apply_padded<KP, KQ>(g, w, w->p, w->q, 0, w->sc, st)));
+  k_v_update<KP, KQ><<<w->grid_elem, VETB, 0, st>>>(g->n, w->k, g->dinv, w->p, w->q, w->x, w->r, w->sc, w->elem_part,
                                                 w->elem_ticket, h, use_h);
   FJ_CK_LAUNCH();
-  k_v_dir<KP><<<w->grid_elem, VETB, 0, st>>>(g->n, w->k, g->dinv, w->r, w->p, w->sc);
+  k_v_dir<KP, KQ><<<w->grid_elem, VETB, 0, st>>>(g->n, w->k, g->dinv, w->r, w->p, w->sc);
   FJ_CK_LAUNCH();
   return FJ_OK;
 }
 
-template <int KP>
+template <int KP, int KQ>
 static fj_status build_vec_graph(fj_graph* g, VecWs* w) {
   if (w->exec) return FJ_OK;
   FJ_CK(cudaStreamCreateWithFlags(&w->cap_stream, cudaStreamNonBlocking));
@@ -622,7 +650,7 @@ static fj_status build_vec_graph(fj_graph* g, VecWs* w) {
   cudaGraph_t body = cp.conditional.phGraph_out[0];
   FJ_CK(cudaStreamBeginCaptureToGraph(w->cap_stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
   g_capturing = true;
-  fj_status s = vec_iteration<KP>(g, w, w->cap_stream, h, 1);
+  fj_status s = vec_iteration<KP, KQ>(g, w, w->cap_stream, h, 1);
   g_capturing = false;
   cudaGraph_t captured = nullptr;
   cudaError_t e = cudaStreamEndCapture(w->cap_stream, &captured);
@@ -632,7 +660,7 @@ static fj_status build_vec_graph(fj_graph* g, VecWs* w) {
   return FJ_OK;
 }
 
-template <int KP>
+template <int KP, int KQ>
 static fj_status solve_vec_t(fj_graph* g, VecWs* w, int k, const double* s, double* z, const fj_solve_opts& o,
                              int warm, fj_solve_report* rep, cudaStream_t st, bool defer) {
   const int64_t n = g->n;
@@ -640,7 +668,7 @@ static fj_status solve_vec_t(fj_graph* g, VecWs* w, int k, const double* s, doub
   w->x_is_solution = false;
   const SegLayout* L = nullptr;
   FJ_TRY(get_segments(g, KP, st, &L));   // before capture: the loop graph launches its passes
-  if (o.use_cuda_graph) FJ_TRY(build_vec_graph<KP>(g, w));
+  if (o.use_cuda_graph) FJ_TRY((build_vec_graph<KP, KQ>(g, w)));
   phase_tick("vec: loop graph capture", st);
   VecScalars h{};
   int restarts = 0, total_iter = 0;
@@ -648,12 +676,15 @@ static fj_status solve_vec_t(fj_graph* g, VecWs* w, int k, const double* s, doub
   for (;;) {
     const bool restart = !first || warm;
     if (restart) {
-      if (first) { k_v_pack<KP><<<cb, 256, 0, st>>>(n, k, z, w->x); FJ_CK_LAUNCH(); }
-      FJ_TRY(vec_apply_padded<KP>(g, w, w->x, w->q, 0, nullptr, st));
+      // restart: q = (I+L) x with x the current iterate (warm: from z), gathered from a padded copy
+      if (first) { k_v_pack<KQ><<<cb, 256, 0, st>>>(n, k, z, w->x); FJ_CK_LAUNCH(); }
+      k_v_pack_from<KP, KQ><<<cb, 256, 0, st>>>(n, w->x, w->p);
+      FJ_CK_LAUNCH();
+      FJ_TRY((vec_apply_padded<KP, KQ>(g, w, w->p, w->q, 0, nullptr, st)));
     }
     const int budget = std::max(0, o.max_iter - total_iter);
     FJ_CK(cudaEventRecord(w->ev2, st));
-    k_v_init<KP><<<w->grid_elem, VETB, 0, st>>>(n, k, s, g->dinv, w->q, restart ? 1 : 0, w->x, w->r, w->p, w->sc,
+    k_v_init<KP, KQ><<<w->grid_elem, VETB, 0, st>>>(n, k, s, g->dinv, w->q, restart ? 1 : 0, w->x, w->r, w->p, w->sc,
                                                 o.rtol, budget, w->elem_part, w->elem_ticket);
     FJ_CK_LAUNCH();
     first = false;
@@ -661,7 +692,7 @@ static fj_status solve_vec_t(fj_graph* g, VecWs* w, int k, const double* s, doub
       FJ_CK(cudaGraphLaunch(w->exec, st));
     } else {
       for (;;) {
-        for (int u = 0; u < 8; ++u) FJ_TRY(vec_iteration<KP>(g, w, st, 0, 0));
+        for (int u = 0; u < 8; ++u) FJ_TRY((vec_iteration<KP, KQ>(g, w, st, 0, 0)));
         int32_t done = 0;
         FJ_CK(cudaMemcpyAsync(&done, &w->sc->done, sizeof done, cudaMemcpyDeviceToHost, st));
         FJ_CK(cudaStreamSynchronize(st));
@@ -681,9 +712,9 @@ static fj_status solve_vec_t(fj_graph* g, VecWs* w, int k, const double* s, doub
       for (int c = 0; c < k; ++c) h.res2[c] = h.rr[c];   // recursive residual stands in
       break;
     }
-    FJ_TRY(by_wtype<KP>(g, [&](auto wt) {   // true residual per column
+    FJ_TRY(by_wtype<KP>(g, [&](auto wt) {   // true residual per column (x gathered KQ wide)
       constexpr int WT = decltype(wt)::value;
-      ResidOpV<WT, KP> op{w->x, s, g->deg, k, w->sc};
+      ResidOpV<WT, KQ> op{w->x, s, g->deg, k, w->sc};
       return launch_vec_items<WT>(g, w, op, st);
     }));
     FJ_CK(cudaMemcpyAsync(&h, w->sc, sizeof h, cudaMemcpyDeviceToHost, st));
@@ -702,7 +733,7 @@ static fj_status solve_vec_t(fj_graph* g, VecWs* w, int k, const double* s, doub
     if (ok || restarts >= o.max_restarts || total_iter >= o.max_iter || brk) break;
     ++restarts;
   }
-  k_v_unpack<KP><<<cb, 256, 0, st>>>(n, k, w->x, z);
+  k_v_unpack<KQ><<<cb, 256, 0, st>>>(n, k, w->x, z);
   FJ_CK_LAUNCH();
   w->x_is_solution = true;
   bool converged = true;
@@ -736,9 +767,10 @@ fj_status solve_vec(fj_graph* g, int k, const double* s, double* z, const fj_sol
   FJ_TRY(get_vec_ws(g, k, st, &w));
   phase_tick("vec: workspace + schedule", st);
   switch (w->kp) {
-    case 2: return solve_vec_t<2>(g, w, k, s, z, o, warm, rep, st, defer);
-    case 3: return solve_vec_t<3>(g, w, k, s, z, o, warm, rep, st, defer);
-    default: return solve_vec_t<4>(g, w, k, s, z, o, warm, rep, st, defer);
+    case 2: return solve_vec_t<2, 2>(g, w, k, s, z, o, warm, rep, st, defer);
+    case 3: return solve_vec_t<3, 3>(g, w, k, s, z, o, warm, rep, st, defer);
+    default: return w->kq == 3 ? solve_vec_t<4, 3>(g, w, k, s, z, o, warm, rep, st, defer)
+                               : solve_vec_t<4, 4>(g, w, k, s, z, o, warm, rep, st, defer);
   }
 }
 
@@ -749,19 +781,22 @@ fj_status apply_vec(fj_graph* g, int k, const double* x, double* y, int opL, cud
   FJ_TRY(get_segments(g, w->kp, st, &L));
   w->x_is_solution = false;
   const unsigned cb = (unsigned)std::min<int64_t>((g->n + 255) / 256, 8192);
-  auto run = [&](auto kpc) -> fj_status {
-    constexpr int KP = decltype(kpc)::value;
+  auto run = [&](auto kpc, auto kqc) -> fj_status {
+    constexpr int KP = decltype(kpc)::value, KQ = decltype(kqc)::value;
     k_v_pack<KP><<<cb, 256, 0, st>>>(g->n, k, x, w->p);
     FJ_CK_LAUNCH();
-    FJ_TRY(vec_apply_padded<KP>(g, w, w->p, w->q, opL, nullptr, st));
-    k_v_unpack<KP><<<cb, 256, 0, st>>>(g->n, k, w->q, y);
+    FJ_TRY((vec_apply_padded<KP, KQ>(g, w, w->p, w->q, opL, nullptr, st)));
+    k_v_unpack<KQ><<<cb, 256, 0, st>>>(g->n, k, w->q, y);
     FJ_CK_LAUNCH();
     return FJ_OK;
   };
+  using I2 = std::integral_constant<int, 2>;
+  using I3 = std::integral_constant<int, 3>;
+  using I4 = std::integral_constant<int, 4>;
   switch (w->kp) {
-    case 2: return run(std::integral_constant<int, 2>());
-    case 3: return run(std::integral_constant<int, 3>());
-    default: return run(std::integral_constant<int, 4>());
+    case 2: return run(I2(), I2());
+    case 3: return run(I3(), I3());
+    default: return w->kq == 3 ? run(I4(), I3()) : run(I4(), I4());
   }
 }
 
@@ -775,9 +810,10 @@ fj_status time_vec_spmv(fj_graph* g, int k, int reps, float* ms_out, cudaStream_
   w->x_is_solution = false;
   auto run = [&]() -> fj_status {
     switch (w->kp) {
-      case 2: return vec_apply_padded<2>(g, w, w->p, w->q, 0, nullptr, st);
-      case 3: return vec_apply_padded<3>(g, w, w->p, w->q, 0, nullptr, st);
-      default: return vec_apply_padded<4>(g, w, w->p, w->q, 0, nullptr, st);
+      case 2: return vec_apply_padded<2, 2>(g, w, w->p, w->q, 0, nullptr, st);
+      case 3: return vec_apply_padded<3, 3>(g, w, w->p, w->q, 0, nullptr, st);
+      default: return w->kq == 3 ? vec_apply_padded<4, 3>(g, w, w->p, w->q, 0, nullptr, st)
+                                 : vec_apply_padded<4, 4>(g, w, w->p, w->q, 0, nullptr, st);
     }
   };
   FJ_TRY(run());
@@ -799,14 +835,15 @@ fj_status quant_vec(fj_graph* g, int k, const double* s, const double* z, const 
   FJ_TRY(get_vec_ws(g, k, st, &w));
   const int kp = w->kp;
   const unsigned cb = (unsigned)std::min<int64_t>((g->n + 255) / 256, 8192);
-  const double* zp = w->x;
-  if (!(z_from_solve && w->x_is_solution && w->k == k)) {
-    if (kp == 2) k_v_pack<2><<<cb, 256, 0, st>>>(g->n, k, z, w->q);
-    else if (kp == 3) k_v_pack<3><<<cb, 256, 0, st>>>(g->n, k, z, w->q);
-    else k_v_pack<4><<<cb, 256, 0, st>>>(g->n, k, z, w->q);
-    FJ_CK_LAUNCH();
-    zp = w->q;
-  }
+  // z gathered from a padded [n][KP] copy in the (free) search-direction buffer p; the source is the
+  // solver's own x when it holds this z, else the caller's [n][k] z
+  const double* zsrc = (z_from_solve && w->x_is_solution && w->k == k) ? w->x : z;
+  if (kp == 2) k_v_pack<2><<<cb, 256, 0, st>>>(g->n, k, zsrc, w->p);
+  else if (kp == 3) k_v_pack<3><<<cb, 256, 0, st>>>(g->n, k, zsrc, w->p);
+  else k_v_pack<4><<<cb, 256, 0, st>>>(g->n, k, zsrc, w->p);
+  FJ_CK_LAUNCH();
+  w->x_is_solution = false;   // p is overwritten by the next solve / apply anyway
+  const double* zp = w->p;
   double* loc = w->qout + 4 * KVMAX;         // [6][KP]
   double* dmean = loc + 6 * KVMAX;            // [KP]
   FJ_CK(cudaMemcpyAsync(dmean, mean_host, sizeof(double) * k, cudaMemcpyHostToDevice, st));
