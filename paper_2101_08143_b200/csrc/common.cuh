@@ -64,7 +64,7 @@ constexpr int MAXK = 64;
 // vector values (spmv_vec.cu), k > 4 on the warp-per-row engine (spmm.cu); fewer columns run the
 // k = 1 path once per column.  FJ_BATCH_MIN_K overrides (tests).
 int batch_min_k();
-// L2 policy bits of the row engine's stream loads (FJ_L2_HINT, default 1; tiles.cuh ld_col/ld_rp)
+// row-engine knobs (FJ_L2_HINT; bit 1 disables the TMA tile prefetch, tiles.cuh)
 int l2_hint();
 // padded row width of the small-k engine for k = 3 (default 4; FJ_VEC_PAD=0: unpadded 3; spmv_vec.cu)
 int vec_pad3();

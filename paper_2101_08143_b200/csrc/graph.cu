@@ -30,7 +30,7 @@ int batch_min_k() {
 int l2_hint() {
   static const int v = [] {
     const char* e = getenv("FJ_L2_HINT");
-    return e ? atoi(e) : 1;
+    return e ? atoi(e) : 0;
   }();
   return v;
 }

@@ -115,6 +115,7 @@ struct ApplyOpV {
   using V = DVec<KP>;
   static constexpr int ITEMS = VEC_ITEMS;
   static constexpr int MIN_BLOCKS = engine_min_blocks<V>();
+  static constexpr bool TMA = true;
   static constexpr int NA = KP, NP = KP;
   static constexpr bool NEEDS_XI = false;
   static __device__ __forceinline__ V vzero() { return vzero_kp<KP>(); }
@@ -186,6 +187,7 @@ struct ResidOpV {
   using V = DVec<KP>;
   static constexpr int ITEMS = VEC_ITEMS;
   static constexpr int MIN_BLOCKS = engine_min_blocks<V>();
+  static constexpr bool TMA = true;
   static constexpr int NA = KP, NP = KP;
   static constexpr bool NEEDS_XI = false;
   static __device__ __forceinline__ V vzero() { return vzero_kp<KP>(); }
@@ -231,6 +233,7 @@ struct QuantOpV {
   using V = DVec<KP>;
   static constexpr int ITEMS = VEC_ITEMS;
   static constexpr int MIN_BLOCKS = FJ_QUANTV_MIN_BLOCKS;
+  static constexpr bool TMA = true;
   static constexpr int NA = 3 * KP, NP = 4 * KP;
   static constexpr bool NEEDS_XI = true;
   static __device__ __forceinline__ V vzero() { return vzero_kp<KP>(); }

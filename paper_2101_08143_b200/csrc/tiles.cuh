@@ -81,28 +81,13 @@ struct TileSched {
   const int32_t* __restrict__ long_item0;     // [n_long] item index of chunk 0
   int64_t n_long, n_chunks;
   int chunk;                                  // nonzeros per long-row chunk
-  int hint;                                   // bit 0: stream col / row_ptr with ld.global.cs (L2 evict-first);
-                                              // bit 1: disable the TMA tile prefetch
+  int hint;                                   // bit 1: disable the TMA tile prefetch (FJ_L2_HINT=2)
 };
 
-// Loads of the CSR streams (read once per product): with hint bit 0 they are marked evict-first so
-// they do not push the gathered vector out of L2.
-__device__ __forceinline__ int32_t ld_col(const TileSched& sc, int64_t p) {
-  if (sc.hint & 1) {
-    int32_t r;
-    asm volatile("ld.global.cs.s32 %0, [%1];" : "=r"(r) : "l"(sc.col + p));
-    return r;
-  }
-  return __ldg(sc.col + p);
-}
-__device__ __forceinline__ int64_t ld_rp(const TileSched& sc, int64_t i) {
-  if (sc.hint & 1) {
-    int64_t r;
-    asm volatile("ld.global.cs.s64 %0, [%1];" : "=l"(r) : "l"(sc.row_ptr + i));
-    return r;
-  }
-  return __ldg(sc.row_ptr + i);
-}
+// Loads of the CSR streams outside the TMA prefetch.  (An evict-first .cs variant was measured
+// 25 % slower on C2 and is not used.)
+__device__ __forceinline__ int32_t ld_col(const TileSched& sc, int64_t p) { return __ldg(sc.col + p); }
+__device__ __forceinline__ int64_t ld_rp(const TileSched& sc, int64_t i) { return __ldg(sc.row_ptr + i); }
 
 inline TileSched make_sched(const fj_graph* g, const Sched& S) {
   TileSched s;
@@ -160,6 +145,7 @@ void free_segments(fj_graph* g);
 //   using V;                                       // gathered value: double (k = 1) or DVec<KP> (k <= 4)
 //   static constexpr int ITEMS;                    // merge items per lane (the schedule's t_cap / 32)
 //   static constexpr int MIN_BLOCKS;               // __launch_bounds__ min blocks / SM (register cap)
+//   static constexpr bool TMA;                     // stage tiles by the TMA bulk-copy prefetch
 //   static constexpr int NA, NP; static constexpr bool NEEDS_XI;
 //   static __device__ V vzero();
 //   __device__ bool skip() const;                  // uniform early exit (solver finished)
@@ -195,7 +181,7 @@ struct TilePre {
   const V* xi;            // x[r0 .. r0+R)
 };
 
-template <int WT, class Op>
+template <int WT, class Op, bool PRE>
 __device__ __forceinline__ void t_tile(const TileSched& sc, const Op& op, const ItemMeta& cur, int lane,
                                        int32_t* s_e, int32_t* s_col_own, typename Op::V* s_xi_own,
                                        double (&part)[Op::NP], const TilePre<typename Op::V>& pre) {
@@ -206,13 +192,13 @@ __device__ __forceinline__ void t_tile(const TileSched& sc, const Op& op, const 
   const int R = cur.info & 63;
   const int N = (cur.info >> 6) & 0xFFFFF;
   const int64_t r0 = cur.r0, k0 = cur.k0;
-  const int32_t* s_col = pre.col ? pre.col : s_col_own;
-  const V* s_xi = pre.xi ? pre.xi : s_xi_own;
+  const int32_t* s_col = (PRE && pre.col) ? pre.col : s_col_own;
+  const V* s_xi = (PRE && pre.xi) ? pre.xi : s_xi_own;
   if (lane < R) {
-    s_e[lane] = (int32_t)((pre.rp ? pre.rp[lane] : ld_rp(sc, r0 + lane + 1)) - k0);
-    if (!pre.xi && op.wants_xi()) s_xi_own[lane] = op.row_value(r0 + lane);
+    s_e[lane] = (int32_t)(((PRE && pre.rp) ? pre.rp[lane] : ld_rp(sc, r0 + lane + 1)) - k0);
+    if (!(PRE && pre.xi) && op.wants_xi()) s_xi_own[lane] = op.row_value(r0 + lane);
   }
-  if (!pre.col) {
+  if (!(PRE && pre.col)) {
 #pragma unroll
     for (int u = 0; u < ITEMS; ++u) {
       const int k = lane + 32 * u;
@@ -299,6 +285,9 @@ __device__ __forceinline__ void t_tile(const TileSched& sc, const Op& op, const 
   __syncwarp();
 }
 
+#ifndef FJ_TMA_PREFETCH
+#define FJ_TMA_PREFETCH 1
+#endif
 // ---------------------------------------------------------------- TMA bulk-copy tile prefetch
 // While a warp works on one T tile, the TMA engine copies the NEXT tile's three contiguous input
 // ranges (col indices, row_ptr entries, row values) global -> shared (cp.async.bulk, completion on
@@ -394,6 +383,72 @@ __device__ __forceinline__ TilePre<typename Op::V> pf_view(const ItemMeta& m, co
   return p;
 }
 
+// W row or C chunk item (lanes stride over the row's nonzeros; chunk partials merged in chunk
+// order by the warp that completes the row).
+template <int WT, class Op>
+__device__ __forceinline__ void wc_item(const TileSched& sc, const Op& op, const TileScratch& ws, const ItemMeta& cur,
+                                        int64_t it, int lane, double (&part)[Op::NP]) {
+  using V = typename Op::V;
+  constexpr int NA = Op::NA, NP = Op::NP;
+  constexpr bool WEIGHTED = (WT != FJ_W_UNIT);
+  const uint32_t type = cur.info >> 30;
+  // ------------------------------------------------ W row or C chunk: lanes stride
+  const int64_t r = cur.r0;
+  const int64_t rb = ld_rp(sc, r), re = ld_rp(sc, r + 1);
+  const int64_t kb = cur.k0;
+  const int64_t ke = (type == IT_W) ? re : min(kb + (int64_t)sc.chunk, re);
+  const V xi = op.wants_xi() ? op.row_value(r) : Op::vzero();
+  double a[NA];
+#pragma unroll
+  for (int f = 0; f < NA; ++f) a[f] = 0.0;
+  for (int64_t k = kb + lane; k < ke; k += 32 * 8) {
+    int32_t c8[8];
+    double w8[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t kk = k + 32 * u;
+      c8[u] = kk < ke ? ld_col(sc, kk) : -1;
+      w8[u] = (WEIGHTED && kk < ke) ? WeightT<WT>::get(sc.w, kk) : 1.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (c8[u] >= 0) op.add(a, w8[u], op.gather(c8[u]), xi);
+  }
+#pragma unroll
+  for (int f = 0; f < NA; ++f) a[f] = warp_sum(a[f]);
+  if (type == IT_W) {
+    if (lane == 0) op.finish_row(r, re - rb, xi, a, part);
+  } else {
+    const uint32_t l = cur.info & 0x3FFFFFFFu;
+    const int64_t first = sc.long_item0[l];
+    const int32_t nch = sc.long_nchunks[l];
+    bool last = false;
+    if (lane == 0) {
+#pragma unroll
+      for (int f = 0; f < NA; ++f) ws.chunk_acc[it * NA + f] = a[f];
+      __threadfence();
+      last = atomicAdd(ws.long_ticket + l, 1u) == (unsigned)nch - 1u;
+      if (last) {
+        __threadfence();
+        double acc[NA];
+#pragma unroll
+        for (int f = 0; f < NA; ++f) acc[f] = 0.0;
+        for (int32_t c = 0; c < nch; ++c) {
+#pragma unroll
+          for (int f = 0; f < NA; ++f) acc[f] += ld_cg(ws.chunk_acc + (first + c) * NA + f);
+        }
+        double lp[NP];
+#pragma unroll
+        for (int j = 0; j < NP; ++j) lp[j] = 0.0;
+        op.finish_row(r, re - rb, xi, acc, lp);
+#pragma unroll
+        for (int j = 0; j < NP; ++j) ws.long_part[(int64_t)l * NP + j] = lp[j];
+        ws.long_ticket[l] = 0u;
+      }
+    }
+  }
+}
+
 template <int WT, class Op>
 __global__ void __launch_bounds__(WTPB, Op::MIN_BLOCKS) warp_kernel(const TileSched sc, const Op op, const TileScratch ws) {
   using V = typename Op::V;
@@ -404,7 +459,8 @@ __global__ void __launch_bounds__(WTPB, Op::MIN_BLOCKS) warp_kernel(const TileSc
   __shared__ V s_xi[WPB][32];
   __shared__ double s_red[(NP > NA ? NP : NA) * WPB];
   __shared__ bool s_last;
-  __shared__ __align__(128) unsigned char s_pf[WPB][2][PfSlot<Op>::BYTES];
+  constexpr bool TMA = Op::TMA && FJ_TMA_PREFETCH != 0;
+  __shared__ __align__(128) unsigned char s_pf[WPB][TMA ? 2 : 1][TMA ? PfSlot<Op>::BYTES : 16];
   __shared__ uint64_t s_bar[WPB][2];
 
   if (op.skip()) return;
@@ -413,109 +469,73 @@ __global__ void __launch_bounds__(WTPB, Op::MIN_BLOCKS) warp_kernel(const TileSc
 #pragma unroll
   for (int j = 0; j < NP; ++j) part[j] = 0.0;
 
-  PfLimits L;
-  L.col = (sc.hint & 2) || (reinterpret_cast<uintptr_t>(sc.col) & 15) ? -1 : ((4 * sc.nnz) & ~(int64_t)15);
-  L.rp = (reinterpret_cast<uintptr_t>(sc.row_ptr) & 15) ? -1 : ((8 * (sc.n + 1)) & ~(int64_t)15);
-  const V* xb = op.xi_base();
-  L.xi = (!xb || !op.wants_xi() || (reinterpret_cast<uintptr_t>(xb) & 15)) ? -1
-                                                                         : (((int64_t)sizeof(V) * sc.n) & ~(int64_t)15);
-  if (lane == 0) {
-    mbar_init(&s_bar[wib][0]);
-    mbar_init(&s_bar[wib][1]);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncwarp();
-
-  const int64_t nwarps = (int64_t)gridDim.x * WPB;
-  int64_t it = (int64_t)blockIdx.x * WPB + wib;
-  ItemMeta m{}, m1{};   // current and next item
-  if (it < sc.n_items) m = sc.items[it];
-  if (it + nwarps < sc.n_items) m1 = sc.items[it + nwarps];
-  uint32_t pend = 0, par = 0;   // per slot: copy in flight / barrier phase parity
-  int slot = 0;
-  if (it < sc.n_items && pf_ok(sc, op, m, L)) {
-    if (lane == 0) pf_issue(sc, op, m, L, s_pf[wib][0], &s_bar[wib][0]);
-    pend = 1;
-  }
-  for (; it < sc.n_items; it += nwarps) {
-    const ItemMeta cur = m;
-    ItemMeta m2{};
-    if (it + 2 * nwarps < sc.n_items) m2 = sc.items[it + 2 * nwarps];   // meta two items ahead
-    if (it + nwarps < sc.n_items && pf_ok(sc, op, m1, L)) {              // stage the next tile
-      __syncwarp();
-      if (lane == 0) pf_issue(sc, op, m1, L, s_pf[wib][slot ^ 1], &s_bar[wib][slot ^ 1]);
-      pend |= 1u << (slot ^ 1);
-    }
-    const uint32_t type = cur.info >> 30;
-    if (type == IT_T) {
-      TilePre<V> pre{nullptr, nullptr, nullptr};
-      if (pend & (1u << slot)) {
-        mbar_wait(&s_bar[wib][slot], (par >> slot) & 1u);
-        par ^= 1u << slot;
-        pend &= ~(1u << slot);
-        pre = pf_view<Op>(cur, L, s_pf[wib][slot]);
-      }
-      t_tile<WT, Op>(sc, op, cur, lane, s_e[wib], s_col[wib], s_xi[wib], part, pre);
-    } else {
-      // ------------------------------------------------ W row or C chunk: lanes stride
-      const int64_t r = cur.r0;
-      const int64_t rb = ld_rp(sc, r), re = ld_rp(sc, r + 1);
-      const int64_t kb = cur.k0;
-      const int64_t ke = (type == IT_W) ? re : min(kb + (int64_t)sc.chunk, re);
-      const V xi = op.wants_xi() ? op.row_value(r) : Op::vzero();
-      double a[NA];
-#pragma unroll
-      for (int f = 0; f < NA; ++f) a[f] = 0.0;
-      for (int64_t k = kb + lane; k < ke; k += 32 * 8) {
-        int32_t c8[8];
-        double w8[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int64_t kk = k + 32 * u;
-          c8[u] = kk < ke ? ld_col(sc, kk) : -1;
-          w8[u] = (WEIGHTED && kk < ke) ? WeightT<WT>::get(sc.w, kk) : 1.0;
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (c8[u] >= 0) op.add(a, w8[u], op.gather(c8[u]), xi);
-      }
-#pragma unroll
-      for (int f = 0; f < NA; ++f) a[f] = warp_sum(a[f]);
-      if (type == IT_W) {
-        if (lane == 0) op.finish_row(r, re - rb, xi, a, part);
+  if constexpr (!TMA) {   // scalar operators: plain loads, next item's meta one ahead
+    const int64_t nwarps = (int64_t)gridDim.x * WPB;
+    int64_t it = (int64_t)blockIdx.x * WPB + wib;
+    ItemMeta m{};
+    if (it < sc.n_items) m = sc.items[it];
+    for (; it < sc.n_items; it += nwarps) {
+      const ItemMeta cur = m;
+      if (it + nwarps < sc.n_items) m = sc.items[it + nwarps];
+      if ((cur.info >> 30) == IT_T) {
+        const TilePre<V> pre{nullptr, nullptr, nullptr};
+        t_tile<WT, Op, false>(sc, op, cur, lane, s_e[wib], s_col[wib], s_xi[wib], part, pre);
       } else {
-        const uint32_t l = cur.info & 0x3FFFFFFFu;
-        const int64_t first = sc.long_item0[l];
-        const int32_t nch = sc.long_nchunks[l];
-        bool last = false;
-        if (lane == 0) {
-#pragma unroll
-          for (int f = 0; f < NA; ++f) ws.chunk_acc[it * NA + f] = a[f];
-          __threadfence();
-          last = atomicAdd(ws.long_ticket + l, 1u) == (unsigned)nch - 1u;
-          if (last) {
-            __threadfence();
-            double acc[NA];
-#pragma unroll
-            for (int f = 0; f < NA; ++f) acc[f] = 0.0;
-            for (int32_t c = 0; c < nch; ++c) {
-#pragma unroll
-              for (int f = 0; f < NA; ++f) acc[f] += ld_cg(ws.chunk_acc + (first + c) * NA + f);
-            }
-            double lp[NP];
-#pragma unroll
-            for (int j = 0; j < NP; ++j) lp[j] = 0.0;
-            op.finish_row(r, re - rb, xi, acc, lp);
-#pragma unroll
-            for (int j = 0; j < NP; ++j) ws.long_part[(int64_t)l * NP + j] = lp[j];
-            ws.long_ticket[l] = 0u;
-          }
-        }
+        wc_item<WT, Op>(sc, op, ws, cur, it, lane, part);
       }
     }
-    m = m1;
-    m1 = m2;
-    slot ^= 1;
+  } else {
+    PfLimits L;
+    L.col = !TMA || (sc.hint & 2) || (reinterpret_cast<uintptr_t>(sc.col) & 15) ? -1 : ((4 * sc.nnz) & ~(int64_t)15);
+    L.rp = (reinterpret_cast<uintptr_t>(sc.row_ptr) & 15) ? -1 : ((8 * (sc.n + 1)) & ~(int64_t)15);
+    const V* xb = op.xi_base();
+    L.xi = (!xb || !op.wants_xi() || (reinterpret_cast<uintptr_t>(xb) & 15)) ? -1
+                                                                           : (((int64_t)sizeof(V) * sc.n) & ~(int64_t)15);
+    if (TMA && lane == 0) {
+      mbar_init(&s_bar[wib][0]);
+      mbar_init(&s_bar[wib][1]);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+
+    const int64_t nwarps = (int64_t)gridDim.x * WPB;
+    int64_t it = (int64_t)blockIdx.x * WPB + wib;
+    ItemMeta m{}, m1{};   // current and next item
+    if (it < sc.n_items) m = sc.items[it];
+    if (it + nwarps < sc.n_items) m1 = sc.items[it + nwarps];
+    uint32_t pend = 0, par = 0;   // per slot: copy in flight / barrier phase parity
+    int slot = 0;
+    if (TMA && it < sc.n_items && pf_ok(sc, op, m, L)) {
+      if (lane == 0) pf_issue(sc, op, m, L, s_pf[wib][0], &s_bar[wib][0]);
+      pend = 1;
+    }
+    for (; it < sc.n_items; it += nwarps) {
+      const ItemMeta cur = m;
+      ItemMeta m2{};
+      if (it + 2 * nwarps < sc.n_items) m2 = sc.items[it + 2 * nwarps];   // meta two items ahead
+      if (TMA && it + nwarps < sc.n_items && pf_ok(sc, op, m1, L)) {       // stage the next tile
+        __syncwarp();
+        if (lane == 0) pf_issue(sc, op, m1, L, s_pf[wib][slot ^ 1], &s_bar[wib][slot ^ 1]);
+        pend |= 1u << (slot ^ 1);
+      }
+      const uint32_t type = cur.info >> 30;
+      if (type == IT_T) {
+        TilePre<V> pre{nullptr, nullptr, nullptr};
+        if (TMA && (pend & (1u << slot))) {
+          mbar_wait(&s_bar[wib][slot], (par >> slot) & 1u);
+          par ^= 1u << slot;
+          pend &= ~(1u << slot);
+          pre = pf_view<Op>(cur, L, s_pf[wib][slot]);
+        }
+        if (pre.col) t_tile<WT, Op, true>(sc, op, cur, lane, s_e[wib], s_col[wib], s_xi[wib], part, pre);
+        else t_tile<WT, Op, false>(sc, op, cur, lane, s_e[wib], s_col[wib], s_xi[wib], part, pre);
+      } else {
+        wc_item<WT, Op>(sc, op, ws, cur, it, lane, part);
+      }
+      m = m1;
+      m1 = m2;
+      slot ^= 1;
+    }
   }
 
   // ---------------------------------------------------- grid-level deterministic reduction
