@@ -125,7 +125,7 @@ struct DistInfo {
   int64_t n_send = 0;
   int32_t* col_local = nullptr;                      // renumbered columns (owned)
   int32_t* send_idx = nullptr;                       // [n_send] local row indices (owned)
-  double* send_buf = nullptr;                        // [n_send]
+  double* send_buf = nullptr;                        // [n_send][kHaloMaxW]
   double d_max_global = 0.0;
   // solver workspace (vectors extended by the ghost segment)
   double *x = nullptr, *r = nullptr, *p = nullptr, *q = nullptr, *red = nullptr;   // red: allreduce payloads
@@ -170,19 +170,25 @@ static fj_status allreduce(DistInfo* d, double* buf, int count, RedOp op, cudaSt
   return FJ_OK;
 }
 
-__global__ void k_pack(int64_t ns, const int32_t* __restrict__ idx, const double* __restrict__ x,
+// send rows of W doubles: buf[i][0..W) = x[idx[i]][0..W)
+__global__ void k_pack(int64_t ns, int W, const int32_t* __restrict__ idx, const double* __restrict__ x,
                        double* __restrict__ buf) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ns; i += (int64_t)gridDim.x * blockDim.x)
-    buf[i] = x[idx[i]];
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < ns * W; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = q / W;
+    buf[q] = x[(int64_t)idx[i] * W + (q - i * W)];
+  }
 }
 
-// x[n_loc .. n_loc + n_ghost) <- owners' x entries (x has the extended layout)
-static fj_status halo_exchange(DistInfo* d, double* x, cudaStream_t st) {
+constexpr int kHaloMaxW = 4;   // widest row the halo carries (the small-k vector engine's KP)
+
+// rows [n_loc .. n_loc + n_ghost) of the W-wide row-major x <- the owners' rows
+static fj_status halo_exchange(DistInfo* d, double* x, cudaStream_t st, int W = 1) {
   fj_comm* c = d->comm;
   if (c->nranks == 1) return FJ_OK;
+  if (W < 1 || W > kHaloMaxW) return fail(FJ_E_INTERNAL, "halo row width");
   if (d->n_send > 0) {
-    const unsigned gb = (unsigned)std::min<int64_t>((d->n_send + 255) / 256, 4096);
-    k_pack<<<gb, 256, 0, st>>>(d->n_send, d->send_idx, x, d->send_buf);
+    const unsigned gb = (unsigned)std::min<int64_t>((d->n_send * W + 255) / 256, 4096);
+    k_pack<<<gb, 256, 0, st>>>(d->n_send, W, d->send_idx, x, d->send_buf);
     FJ_CK_LAUNCH();
   }
   if (c->kind == 0) {
@@ -191,8 +197,10 @@ static fj_status halo_exchange(DistInfo* d, double* x, cudaStream_t st) {
     FJ_NCCL(api->GroupStart());
     for (int q = 0; q < c->nranks; ++q) {
       if (q == d->rank) continue;
-      if (d->send_cnt[q] > 0) FJ_NCCL(api->Send(d->send_buf + d->send_off[q], (size_t)d->send_cnt[q], ncclDouble, q, c->nccl, st));
-      if (d->recv_cnt[q] > 0) FJ_NCCL(api->Recv(x + d->n_loc + d->recv_off[q], (size_t)d->recv_cnt[q], ncclDouble, q, c->nccl, st));
+      if (d->send_cnt[q] > 0)
+        FJ_NCCL(api->Send(d->send_buf + d->send_off[q] * W, (size_t)(d->send_cnt[q] * W), ncclDouble, q, c->nccl, st));
+      if (d->recv_cnt[q] > 0)
+        FJ_NCCL(api->Recv(x + (d->n_loc + d->recv_off[q]) * W, (size_t)(d->recv_cnt[q] * W), ncclDouble, q, c->nccl, st));
     }
     FJ_NCCL(api->GroupEnd());
     return FJ_OK;
@@ -202,8 +210,8 @@ static fj_status halo_exchange(DistInfo* d, double* x, cudaStream_t st) {
   w->barrier();   // all send buffers packed
   for (int o = 0; o < c->nranks; ++o) {
     if (o == d->rank || d->recv_cnt[o] == 0) continue;
-    FJ_CK(cudaMemcpyAsync(x + d->n_loc + d->recv_off[o], w->send_buf[o] + w->send_off[o][d->rank],
-                          sizeof(double) * d->recv_cnt[o], cudaMemcpyDeviceToDevice, st));
+    FJ_CK(cudaMemcpyAsync(x + (d->n_loc + d->recv_off[o]) * W, w->send_buf[o] + w->send_off[o][d->rank] * W,
+                          sizeof(double) * d->recv_cnt[o] * W, cudaMemcpyDeviceToDevice, st));
   }
   FJ_CK(cudaStreamSynchronize(st));
   w->barrier();   // all pulls done before anyone repacks
@@ -607,6 +615,29 @@ fj_status dist_stats_combine(const fj_graph* g, int k, double* dev4k /* [k][4] d
 }
 
 bool is_dist(const fj_graph* g) { return g->dist != nullptr; }
+int64_t dist_n_ghost(const fj_graph* g) { return g->dist ? D(g)->n_ghost : 0; }
+fj_status dist_halo_rows(const fj_graph* g, double* x_ext, int width, cudaStream_t st) {
+  return halo_exchange(D(g), x_ext, st, width);
+}
+fj_status dist_allreduce_sum(const fj_graph* g, double* buf, int count, cudaStream_t st) {
+  return allreduce(D(g), buf, count, RED_SUM, st);
+}
+// ||s_c - (I+L) z_c||^2 over all ranks for column c of the local slices (host result)
+fj_status dist_true_res2(fj_graph* g, const double* s, const double* z, int64_t ld, int64_t c, double* res2_host,
+                         cudaStream_t st) {
+  DistInfo* d = D(g);
+  FJ_TRY(ensure_dist_ws(g, st));
+  const int64_t nl = d->n_loc;
+  const unsigned gb = (unsigned)std::min<int64_t>((nl + 255) / 256, 4096);
+  k_dcopy<<<gb, 256, 0, st>>>(nl, z, ld, c, d->x, 1, 0);
+  FJ_CK_LAUNCH();
+  FJ_TRY(halo_exchange(d, d->x, st));
+  FJ_TRY(d_resid(g, d->x, s, ld, c, d->red + 6, st));
+  FJ_TRY(allreduce(d, d->red + 6, 1, RED_SUM, st));
+  FJ_CK(cudaMemcpyAsync(res2_host, d->red + 6, sizeof(double), cudaMemcpyDeviceToHost, st));
+  FJ_CK(cudaStreamSynchronize(st));
+  return FJ_OK;
+}
 int64_t global_n(const fj_graph* g) { return g->dist ? D(g)->n_global : g->n; }
 double global_dmax(const fj_graph* g) { return g->dist ? D(g)->d_max_global : g->info.d_max; }
 
@@ -812,7 +843,7 @@ fj_status fj_graph_create_dist(fj_comm* comm, int rank, int64_t n_global, const 
   if (acc > 0) {
     if (!send_idx) return bail(fail(FJ_E_INVALID_ARG, "send_idx is NULL"));
     if (dmalloc(&d->send_idx, sizeof(int32_t) * acc, st) != cudaSuccess ||
-        dmalloc(&d->send_buf, sizeof(double) * acc, st) != cudaSuccess)
+        dmalloc(&d->send_buf, sizeof(double) * acc * kHaloMaxW, st) != cudaSuccess)
       return bail(FJ_E_OOM);
     cudaMemcpyAsync(d->send_idx, send_idx, sizeof(int32_t) * acc, cudaMemcpyDeviceToDevice, st);
   }

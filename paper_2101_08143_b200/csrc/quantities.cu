@@ -414,6 +414,47 @@ static fj_status approxim_impl(const fj_graph* gc, int k, const double* s, doubl
       d2h_issued = false;
     }
     r.iterations = spent;
+  } else if (is_dist(g) && vec_supported(k)) {
+    // rows a8 + a9: the k columns of this rank's slice solved together (halo of padded p rows,
+    // allreduce of k-vectors), then the per-column distributed quantities passes
+    fj_solve_opts oc = o;
+    int warm = 0, spent = 0;
+    for (;;) {
+      fj_solve_opts ob = oc;
+      ob.max_iter = std::max(0, o.max_iter - spent);
+      fj_solve_report rb{};
+      rb.converged = 1;
+      rb.rel_res_true = NAN;
+      fj_status sc = dist_solve_vec(g, k, s, z, ob, warm, &rb, st);   // Alg. 1 line 3
+      if (sc != FJ_OK && sc != FJ_E_NO_CONVERGENCE) return sc;
+      spent += rb.iterations;
+      r.ms_loop += rb.ms_loop;
+      r.iterations_total += rb.iterations_total;
+      r.restarts += rb.restarts;
+      r.rel_res_true = rb.rel_res_true;
+      r.rel_res_recursive = rb.rel_res_recursive;
+      r.batch_k = k;
+      double emax = 0.0;
+      for (int c = 0; c < k; ++c) {
+        const double m = v[4 * c] / (double)global_n(g);
+        if (v[4 * c + 2] == v[4 * c + 3]) {   // s = c 1: z = s exactly (P:L129 Omega 1 = 1)
+          k_copy_cols<<<cb, 256, 0, st>>>(g->n, k, c, s, z);
+          FJ_CK_LAUNCH();
+          consensus_quantities(g, v[4 * c + 2], qout[c]);
+          continue;
+        }
+        double t[10];
+        FJ_TRY(quant_pass(g, w, s, z, k, c, m, t, st));   // Alg. 1 lines 5-9
+        memset(&qout[c], 0, sizeof(fj_quantities_t));
+        fill_quantities(g, t, m, qout[c]);
+        for (int j = 0; j < 6; ++j) emax = std::max(emax, qout[c].eps[j]);
+      }
+      if (sc != FJ_OK) { worst = sc; break; }
+      if (o.eps_target <= 0.0 || emax <= o.eps_target || oc.rtol <= 1e-15 || spent >= o.max_iter) break;
+      oc.rtol = std::max(oc.rtol * 1e-2, 1e-15);   // tighten and continue from z (warm start)
+      warm = 1;
+    }
+    r.iterations = spent;
   } else {
   for (int c = 0; c < k; ++c) {
     const double m = v[4 * c] / (double)global_n(g);
