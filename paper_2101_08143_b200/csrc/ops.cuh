@@ -27,7 +27,7 @@ struct ApplyOp {
   using V = double;
   static constexpr int ITEMS = fj::ITEMS;
   static constexpr int MIN_BLOCKS = engine_min_blocks<double>();
-  static constexpr bool TMA = false;   // measured: the plain loop is faster for 8-byte values
+  static constexpr bool TMA = FJ_K1_TMA != 0;   // measured: the plain loop is faster for 8-byte values
   static __device__ __forceinline__ V vzero() { return 0.0; }
   const double* __restrict__ x;
   double* __restrict__ y;
@@ -94,7 +94,7 @@ struct ResidOp {
   using V = double;
   static constexpr int ITEMS = fj::ITEMS;
   static constexpr int MIN_BLOCKS = engine_min_blocks<double>();
-  static constexpr bool TMA = false;   // measured: the plain loop is faster for 8-byte values
+  static constexpr bool TMA = FJ_K1_TMA != 0;   // measured: the plain loop is faster for 8-byte values
   static __device__ __forceinline__ V vzero() { return 0.0; }
   const double* __restrict__ z;     // contiguous [n]
   const double* __restrict__ s;     // column c of row-major [n][ld]
@@ -131,7 +131,7 @@ struct QuantOp {
   using V = double;
   static constexpr int ITEMS = fj::ITEMS;
   static constexpr int MIN_BLOCKS = engine_min_blocks<double>();
-  static constexpr bool TMA = false;   // measured: the plain loop is faster for 8-byte values
+  static constexpr bool TMA = FJ_K1_TMA != 0;   // measured: the plain loop is faster for 8-byte values
   static __device__ __forceinline__ V vzero() { return 0.0; }
   const double* __restrict__ z;
   const double* __restrict__ s;

@@ -27,17 +27,20 @@ constexpr int WPB = WTPB / 32;
 #define FJ_ITEMS 12
 #endif
 #ifndef FJ_K1_MIN_BLOCKS
-#define FJ_K1_MIN_BLOCKS 6
+#define FJ_K1_MIN_BLOCKS 0
 #endif
-// Register caps of the engine (__launch_bounds__ min blocks / SM) per gathered value width.
-// Measured on B200 (C3, C4): KP = 4 at 4 blocks (128 regs, no spill) is 1.2-1.5x faster than the
-// unconstrained 160 regs / 3 blocks; KP = 2 best at 5 blocks; k = 1 at 6 blocks (<= 80 regs; at 8
-// blocks it spills and is 1.5x slower).
+// Register caps of the engine (__launch_bounds__ min blocks / SM) per gathered value width; 0 = no
+// hint.  (A hint of 1 is NOT neutral: ptxas then spends registers on ILP -- 106 instead of 72 for
+// k = 1, 25 % slower.)  Measured on B200 (C2, C3, C4): k = 1 best with no hint (72 regs, 7 blocks);
+// KP = 4 at 4 blocks (128 regs, no spill) 1.2-1.5x faster than 160 regs / 3 blocks; KP = 2 at 5.
+#ifndef FJ_K1_TMA
+#define FJ_K1_TMA 0
+#endif
 #ifndef FJ_VEC_MIN_BLOCKS
 #define FJ_VEC_MIN_BLOCKS 4
 #endif
 #ifndef FJ_QUANTV_MIN_BLOCKS
-#define FJ_QUANTV_MIN_BLOCKS 1
+#define FJ_QUANTV_MIN_BLOCKS 0
 #endif
 #ifndef FJ_VEC2_MIN_BLOCKS
 #define FJ_VEC2_MIN_BLOCKS 5
