@@ -566,3 +566,30 @@ def test_exact_dense_vs_oracle_and_table2_protocol(fj):
         for k in QKEYS:
             sigma = abs(qe[c][k] - qa[c][k]) / qe[c][k]
             assert sigma <= 1e-8 and sigma <= qa[c]["eps"][k] * (1 + 1e-9) + 1e-15, (c, k, sigma)
+
+
+# ---------------------------------------------------------------- degenerate graphs on every engine
+@pytest.mark.parametrize("k", [1, 3, 64])
+@pytest.mark.parametrize("case", ["single", "edgeless", "one_edge"])
+def test_degenerate_graphs_all_engines(fj, k, case):
+    """L = 0 (single node, no edges: z = s exactly, D = C_I = 0) and the 2-node path (S:L218 closed
+    form) through the k = 1 engine, the vector engine (k = 3) and the warp-per-row engine (k = 64)."""
+    n = {"single": 1, "edgeless": 7, "one_edge": 2}[case]
+    u = np.array([0] if case == "one_edge" else [], np.int32)
+    v = np.array([1] if case == "one_edge" else [], np.int32)
+    rp, col, wo, _ = gpu_csr(fj, n, u, v)
+    G = fj.Graph(n, rp, col, wo)
+    S = np.random.default_rng(k).uniform(0.1, 1.0, (n, k))
+    z, q, rep = G.approxim(dev(S if k > 1 else S[:, 0].copy()))
+    Z = host(z).reshape(n, k)
+    assert rep["converged"] == 1
+    if case == "one_edge":
+        inv = np.array([[2.0, 1.0], [1.0, 2.0]]) / 3.0          # (I+L)^{-1} of the unit 2-node path
+        for c in range(k):
+            assert np.allclose(Z[:, c], inv @ S[:, c], rtol=1e-10, atol=0)
+            assert q[c]["D"] == pytest.approx((Z[0, c] - Z[1, c]) ** 2, rel=1e-9)
+    else:
+        assert np.allclose(Z, S, rtol=1e-13, atol=0)
+        for c in range(k):
+            assert q[c]["D"] == 0 and q[c]["CI"] <= 1e-26
+            assert q[c]["C"] == pytest.approx(float((S[:, c] ** 2).sum()), rel=1e-12)
