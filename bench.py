@@ -139,7 +139,9 @@ def run_reference(args, ws, rank):
     t = time.perf_counter()
     O.pcg_fixed_iters(g, s, 1)
     t1 = time.perf_counter() - t
-    iters = int(max(1, min(50, args.ref_seconds / max(t1, 1e-3))))
+    # each step a bounded sample: the whole --steps K --warmup W run stays around a minute or two
+    per_step = min(args.ref_seconds, 90.0 / max(1, args.steps + args.warmup))
+    iters = int(max(1, min(50, per_step / max(t1, 1e-3))))
     for _ in range(args.warmup):
         O.pcg_fixed_iters(g, s, iters)
     times = []
