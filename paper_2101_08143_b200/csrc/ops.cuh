@@ -26,6 +26,7 @@ struct ApplyOp {
   static constexpr bool NEEDS_XI = false;
   using V = double;
   static constexpr int ITEMS = fj::ITEMS;
+  static constexpr int TILE_ROWS = fj::TILE_ROWS;
   static constexpr int MIN_BLOCKS = engine_min_blocks<double>();
   static constexpr bool TMA = FJ_K1_TMA != 0;   // measured: the plain loop is faster for 8-byte values
   static __device__ __forceinline__ V vzero() { return 0.0; }
@@ -93,6 +94,7 @@ struct ResidOp {
   static constexpr bool NEEDS_XI = false;
   using V = double;
   static constexpr int ITEMS = fj::ITEMS;
+  static constexpr int TILE_ROWS = fj::TILE_ROWS;
   static constexpr int MIN_BLOCKS = engine_min_blocks<double>();
   static constexpr bool TMA = FJ_K1_TMA != 0;   // measured: the plain loop is faster for 8-byte values
   static __device__ __forceinline__ V vzero() { return 0.0; }
@@ -130,6 +132,7 @@ struct QuantOp {
   static constexpr bool NEEDS_XI = true;
   using V = double;
   static constexpr int ITEMS = fj::ITEMS;
+  static constexpr int TILE_ROWS = fj::TILE_ROWS;
   static constexpr int MIN_BLOCKS = engine_min_blocks<double>();
   static constexpr bool TMA = FJ_K1_TMA != 0;   // measured: the plain loop is faster for 8-byte values
   static __device__ __forceinline__ V vzero() { return 0.0; }

@@ -66,7 +66,7 @@ __global__ void k_items(int64_t nseg, const int32_t* __restrict__ B, const int64
     const int64_t nk = rp[r1] - k0;
     ItemMeta m;
     m.r0 = (int32_t)r;
-    m.info = ((uint32_t)IT_T << 30) | (uint32_t)(r1 - r) | ((uint32_t)nk << 6);
+    m.info = ((uint32_t)IT_T << 30) | (uint32_t)(r1 - r) | ((uint32_t)nk << 7);   // tiles.cuh tile_rows / tile_nnz
     m.k0 = k0;
     items[n_chunks + n_w + pt[j]] = m;
   } else if (cls == IT_W) {

@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(BTPB) spmm_kernel(const TileSched sc, const Ba
     const ItemMeta cur = sc.items[it];
     const uint32_t type = cur.info >> 30;
     if (type == IT_T) {
-      const int R = cur.info & 63;
+      const int R = tile_rows(cur.info);
       const int64_t r0 = cur.r0;
       int64_t rb = cur.k0;
       for (int t = 0; t < R; ++t) {
@@ -787,7 +787,7 @@ __global__ void __launch_bounds__(BTPB) quant_batch_kernel(const TileSched sc, c
     const ItemMeta cur = sc.items[it];
     const uint32_t type = cur.info >> 30;
     if (type == IT_T) {
-      const int R = cur.info & 63;
+      const int R = tile_rows(cur.info);
       const int64_t r0 = cur.r0;
       int64_t rb = cur.k0;
       for (int t = 0; t < R; ++t) {

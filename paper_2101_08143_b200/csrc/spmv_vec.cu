@@ -114,6 +114,7 @@ template <int WT, int KP, int KQ = KP, int SEG = SEG_WHOLE>   // y stored KQ wid
 struct ApplyOpV {
   using V = DVec<KP>;
   static constexpr int ITEMS = VEC_ITEMS;
+  static constexpr int TILE_ROWS = VEC_TILE_ROWS;
   static constexpr int MIN_BLOCKS = engine_min_blocks<V>();
   static constexpr bool TMA = true;
   static constexpr int NA = KP, NP = KP;
@@ -193,6 +194,7 @@ template <int WT, int KP>
 struct ResidOpV {
   using V = DVec<KP>;
   static constexpr int ITEMS = VEC_ITEMS;
+  static constexpr int TILE_ROWS = VEC_TILE_ROWS;
   static constexpr int MIN_BLOCKS = engine_min_blocks<V>();
   static constexpr bool TMA = true;
   static constexpr int NA = KP, NP = KP;
@@ -239,6 +241,7 @@ template <int WT, int KP>
 struct QuantOpV {
   using V = DVec<KP>;
   static constexpr int ITEMS = VEC_ITEMS;
+  static constexpr int TILE_ROWS = VEC_TILE_ROWS;
   static constexpr int MIN_BLOCKS = FJ_QUANTV_MIN_BLOCKS;
   static constexpr bool TMA = true;
   static constexpr int NA = 3 * KP, NP = 4 * KP;

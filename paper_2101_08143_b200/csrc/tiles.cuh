@@ -61,17 +61,31 @@ constexpr int T_ROW_MAX = 64;             // rows longer than this are W rows or
 template <int IT> constexpr int t_cap() { return 32 * IT; }
 // a tile holds <= t_cap merge items: cut the merge coordinate every t_units = t_cap - (T_ROW_MAX + 1)
 template <int IT> constexpr int t_units() { return t_cap<IT>() - (T_ROW_MAX + 1); }
-// schedule units per row are max(1 + len, t_min_cost): <= 32 rows per tile (one per lane)
-template <int IT> constexpr int t_min_cost() { return (t_units<IT>() + 30) / 31 > 12 ? (t_units<IT>() + 30) / 31 : 12; }
+// schedule units per row are max(1 + len, t_min_cost): <= TILE_ROWS rows per tile
+// rows per T tile: up to ROWS (each lane stages ROWS / 32 row ends).  The scalar engine takes 64,
+// which packs the short rows of power-law graphs (measured: C5 product 16.8 -> 15.8 ms, C2 61.6 ->
+// 59.0 us); the vector engine keeps 32 (64 cost it 28 % on C3: larger shared staging per block).
+#ifndef FJ_TILE_ROWS
+#define FJ_TILE_ROWS 64
+#endif
+constexpr int TILE_ROWS = FJ_TILE_ROWS;   // scalar engine
+constexpr int VEC_TILE_ROWS = 32;
+template <int ROWS> constexpr int t_min_cost_floor() { return ROWS == 32 ? 12 : 6; }
+template <int IT, int ROWS> constexpr int t_min_cost() {
+  return (t_units<IT>() + ROWS - 2) / (ROWS - 1) > t_min_cost_floor<ROWS>()
+             ? (t_units<IT>() + ROWS - 2) / (ROWS - 1) : t_min_cost_floor<ROWS>();
+}
 constexpr int T_CAP = t_cap<ITEMS>();
 constexpr int CHUNK = 2048;               // nonzeros per W row (max) / per long-row chunk
 constexpr int IT_T = 0, IT_W = 1, IT_C = 2;
 
 struct ItemMeta {   // 16 bytes
   int32_t r0;
-  uint32_t info;    // type << 30 | (T: nrows | nk << 6) | (W: nk) | (C: long-row index)
+  uint32_t info;    // type << 30 | (T: nrows | nk << 7) | (W: nk) | (C: long-row index)
   int64_t k0;
 };
+__host__ __device__ __forceinline__ int tile_rows(uint32_t info) { return (int)(info & 127u); }
+__host__ __device__ __forceinline__ int tile_nnz(uint32_t info) { return (int)((info >> 7) & 0x7FFFFu); }
 
 struct TileSched {
   int64_t n, nnz;
@@ -105,9 +119,11 @@ inline TileSched make_sched(const fj_graph* g, const Sched& S) {
 }
 
 // the k = 1 engine's schedule (ITEMS x 32 lanes = T_CAP merge items per tile)
-template <int IT> constexpr SchedParams sched_params() { return SchedParams{T_ROW_MAX, t_units<IT>(), t_min_cost<IT>(), CHUNK}; }
-constexpr SchedParams kSchedK1 = sched_params<ITEMS>();
-constexpr SchedParams kSchedVec = sched_params<VEC_ITEMS>();
+template <int IT, int ROWS> constexpr SchedParams sched_params() {
+  return SchedParams{T_ROW_MAX, t_units<IT>(), t_min_cost<IT, ROWS>(), CHUNK};
+}
+constexpr SchedParams kSchedK1 = sched_params<ITEMS, TILE_ROWS>();
+constexpr SchedParams kSchedVec = sched_params<VEC_ITEMS, VEC_TILE_ROWS>();
 fj_status build_schedule(fj_graph* g, const SchedParams& P, Sched& out, cudaStream_t st);
 void free_sched(Sched& s);
 
@@ -147,6 +163,7 @@ void free_segments(fj_graph* g);
 // Op interface:
 //   using V;                                       // gathered value: double (k = 1) or DVec<KP> (k <= 4)
 //   static constexpr int ITEMS;                    // merge items per lane (the schedule's t_cap / 32)
+//   static constexpr int TILE_ROWS;                // rows per T tile (32 or 64; the schedule's)
 //   static constexpr int MIN_BLOCKS;               // __launch_bounds__ min blocks / SM (register cap)
 //   static constexpr bool TMA;                     // stage tiles by the TMA bulk-copy prefetch
 //   static constexpr int NA, NP; static constexpr bool NEEDS_XI;
@@ -192,14 +209,17 @@ __device__ __forceinline__ void t_tile(const TileSched& sc, const Op& op, const 
   constexpr int NA = Op::NA;
   constexpr int ITEMS = Op::ITEMS;
   constexpr bool WEIGHTED = (WT != FJ_W_UNIT);
-  const int R = cur.info & 63;
-  const int N = (cur.info >> 6) & 0xFFFFF;
+  const int R = tile_rows(cur.info);
+  const int N = tile_nnz(cur.info);
   const int64_t r0 = cur.r0, k0 = cur.k0;
   const int32_t* s_col = (PRE && pre.col) ? pre.col : s_col_own;
   const V* s_xi = (PRE && pre.xi) ? pre.xi : s_xi_own;
-  if (lane < R) {
-    s_e[lane] = (int32_t)(((PRE && pre.rp) ? pre.rp[lane] : ld_rp(sc, r0 + lane + 1)) - k0);
-    if (!(PRE && pre.xi) && op.wants_xi()) s_xi_own[lane] = op.row_value(r0 + lane);
+#pragma unroll
+  for (int rr = lane; rr < Op::TILE_ROWS; rr += 32) {
+    if (rr < R) {
+      s_e[rr] = (int32_t)(((PRE && pre.rp) ? pre.rp[rr] : ld_rp(sc, r0 + rr + 1)) - k0);
+      if (!(PRE && pre.xi) && op.wants_xi()) s_xi_own[rr] = op.row_value(r0 + rr);
+    }
   }
   if (!(PRE && pre.col)) {
 #pragma unroll
@@ -298,12 +318,12 @@ __device__ __forceinline__ void t_tile(const TileSched& sc, const Op& op, const 
 // instead of stalling the warp at the start of every tile.  Copies are 16-byte granular: each range
 // is widened to 16-byte boundaries (never past the array's last full 16-byte unit; such a tile,
 // and any tile whose base pointers are not 16-byte aligned, takes the plain-load path).
-constexpr int PF_RP_BYTES = 32 * 8 + 32;
 template <class Op>
 struct PfSlot {   // [cols | row_ptr | row values] of one tile
   static constexpr int COL_BYTES = t_cap<Op::ITEMS>() * 4 + 32;
-  static constexpr int XI_BYTES = 32 * (int)sizeof(typename Op::V) + 32;
-  static constexpr int BYTES = ((COL_BYTES + PF_RP_BYTES + XI_BYTES) + 15) & ~15;
+  static constexpr int RP_BYTES = Op::TILE_ROWS * 8 + 32;
+  static constexpr int XI_BYTES = Op::TILE_ROWS * (int)sizeof(typename Op::V) + 32;
+  static constexpr int BYTES = ((COL_BYTES + RP_BYTES + XI_BYTES) + 15) & ~15;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -338,7 +358,7 @@ template <class Op>
 __device__ __forceinline__ bool pf_ok(const TileSched& sc, const Op& op, const ItemMeta& m, const PfLimits& L) {
   using V = typename Op::V;
   if ((m.info >> 30) != IT_T || L.col < 0 || L.rp < 0) return false;
-  const int R = m.info & 63, N = (m.info >> 6) & 0xFFFFF;
+  const int R = tile_rows(m.info), N = tile_nnz(m.info);
   const PfRange c = pf_range(4 * m.k0, 4 * (m.k0 + N));
   const PfRange r = pf_range(8 * ((int64_t)m.r0 + 1), 8 * ((int64_t)m.r0 + R + 1));
   if (c.b1 > L.col || r.b1 > L.rp) return false;
@@ -354,7 +374,7 @@ template <class Op>
 __device__ __forceinline__ void pf_issue(const TileSched& sc, const Op& op, const ItemMeta& m, const PfLimits& L,
                                          unsigned char* slot, uint64_t* bar) {
   using V = typename Op::V;
-  const int R = m.info & 63, N = (m.info >> 6) & 0xFFFFF;
+  const int R = tile_rows(m.info), N = tile_nnz(m.info);
   const PfRange c = pf_range(4 * m.k0, 4 * (m.k0 + N));
   const PfRange r = pf_range(8 * ((int64_t)m.r0 + 1), 8 * ((int64_t)m.r0 + R + 1));
   PfRange x{0, 0};
@@ -367,7 +387,7 @@ __device__ __forceinline__ void pf_issue(const TileSched& sc, const Op& op, cons
   bulk_g2s(slot + PF_COL_BYTES, reinterpret_cast<const unsigned char*>(sc.row_ptr) + r.b0, (uint32_t)(r.b1 - r.b0),
            bar);
   if (x.b1 > x.b0)
-    bulk_g2s(slot + PF_COL_BYTES + PF_RP_BYTES, reinterpret_cast<const unsigned char*>(op.xi_base()) + x.b0,
+    bulk_g2s(slot + PF_COL_BYTES + PfSlot<Op>::RP_BYTES, reinterpret_cast<const unsigned char*>(op.xi_base()) + x.b0,
              (uint32_t)(x.b1 - x.b0), bar);
 }
 
@@ -380,7 +400,7 @@ __device__ __forceinline__ TilePre<typename Op::V> pf_view(const ItemMeta& m, co
   TilePre<V> p;
   p.col = reinterpret_cast<const int32_t*>(slot + ((4 * m.k0) & 15));
   p.rp = reinterpret_cast<const int64_t*>(slot + PF_COL_BYTES + ((8 * ((int64_t)m.r0 + 1)) & 15));
-  p.xi = L.xi >= 0 ? reinterpret_cast<const V*>(slot + PF_COL_BYTES + PF_RP_BYTES +
+  p.xi = L.xi >= 0 ? reinterpret_cast<const V*>(slot + PF_COL_BYTES + PfSlot<Op>::RP_BYTES +
                                                  (((int64_t)sizeof(V) * m.r0) & 15))
                    : nullptr;
   return p;
@@ -458,8 +478,8 @@ __global__ void __launch_bounds__(WTPB, Op::MIN_BLOCKS) warp_kernel(const TileSc
   constexpr int NA = Op::NA, NP = Op::NP;
   constexpr bool WEIGHTED = (WT != FJ_W_UNIT);
   __shared__ int32_t s_col[WPB][t_cap<Op::ITEMS>()];
-  __shared__ int32_t s_e[WPB][32];
-  __shared__ V s_xi[WPB][32];
+  __shared__ int32_t s_e[WPB][Op::TILE_ROWS];
+  __shared__ V s_xi[WPB][Op::TILE_ROWS];
   __shared__ double s_red[(NP > NA ? NP : NA) * WPB];
   __shared__ bool s_last;
   constexpr bool TMA = Op::TMA && FJ_TMA_PREFETCH != 0;
