@@ -135,6 +135,68 @@ __global__ void __launch_bounds__(STPB) k_stats_k(int64_t n, int k, const double
   }
 }
 
+// All k <= 64 columns of row-major [n][k] in one pass: warp per row, lane l owns columns l and l + 32
+// (coalesced row reads), per-column partials reduced warps -> blocks in a fixed order; same outputs
+// as k_stats per column.
+__global__ void __launch_bounds__(STPB) k_stats_wide(int64_t n, int k, const double* __restrict__ s,
+                                                     double* part /*[grid][4][64]*/, unsigned int* ticket,
+                                                     double* out, int* nonfinite) {
+  constexpr int NW = STPB / 32;
+  __shared__ double s_v[NW][4][64];
+  __shared__ bool s_last;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  double sm[2] = {0.0, 0.0}, sq[2] = {0.0, 0.0}, mn[2] = {INFINITY, INFINITY}, mx[2] = {-INFINITY, -INFINITY};
+  int bad = 0;
+  for (int64_t i = blockIdx.x * (int64_t)NW + wib; i < n; i += (int64_t)gridDim.x * NW) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int c = lane + 32 * h;
+      if (c < k) {
+        const double x = s[i * k + c];
+        if (!isfinite(x)) { bad = 1; continue; }
+        sm[h] += x;
+        sq[h] = fma(x, x, sq[h]);
+        mn[h] = fmin(mn[h], x);
+        mx[h] = fmax(mx[h], x);
+      }
+    }
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(nonfinite, 1);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int c = lane + 32 * h;
+    s_v[wib][0][c] = sm[h]; s_v[wib][1][c] = sq[h]; s_v[wib][2][c] = mn[h]; s_v[wib][3][c] = mx[h];
+  }
+  __syncthreads();
+  if (threadIdx.x < 64) {
+    const int c = threadIdx.x;
+    double a = 0.0, b = 0.0, lo = INFINITY, hi = -INFINITY;
+    for (int w = 0; w < NW; ++w) {   // warps in order
+      a += s_v[w][0][c]; b += s_v[w][1][c]; lo = fmin(lo, s_v[w][2][c]); hi = fmax(hi, s_v[w][3][c]);
+    }
+    double* pb = part + (int64_t)blockIdx.x * 256;
+    pb[c] = a; pb[64 + c] = b; pb[128 + c] = lo; pb[192 + c] = hi;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (threadIdx.x < 64 && threadIdx.x < k) {
+    const int c = threadIdx.x;
+    double a = 0.0, b = 0.0, lo = INFINITY, hi = -INFINITY;
+    for (unsigned q = 0; q < gridDim.x; ++q) {   // blocks in order
+      const double* pb = part + (int64_t)q * 256;
+      a += __ldcg(pb + c); b += __ldcg(pb + 64 + c);
+      lo = fmin(lo, __ldcg(pb + 128 + c)); hi = fmax(hi, __ldcg(pb + 192 + c));
+    }
+    out[4 * c + 0] = *(volatile int*)nonfinite ? NAN : a;
+    out[4 * c + 1] = b; out[4 * c + 2] = lo; out[4 * c + 3] = hi;
+  }
+  if (threadIdx.x == 0) *ticket = 0u;
+}
+
 static fj_status stats_cols(fj_graph* g, SolveWs* w, int k, const double* s, std::vector<double>& st4,
                             cudaStream_t st) {
   int* d_bad = nullptr;
@@ -143,6 +205,12 @@ static fj_status stats_cols(fj_graph* g, SolveWs* w, int k, const double* s, std
   if (k > 1 && k <= 4) {   // one pass over all columns (SolveWs::elem_part holds grid x 16 doubles)
     k_stats_k<4><<<w->grid_elem, STPB, 0, st>>>(g->n, k, s, w->elem_part, w->elem_ticket, w->stat, d_bad);
     FJ_CK_LAUNCH();
+  } else if (k > 4) {   // one pass, warp per row (part: grid x 256 doubles in a transient buffer)
+    double* part = nullptr;
+    FJ_CK(dmalloc(&part, sizeof(double) * 256 * (size_t)w->grid_elem, st));
+    k_stats_wide<<<w->grid_elem, STPB, 0, st>>>(g->n, k, s, part, w->elem_ticket, w->stat, d_bad);
+    FJ_CK_LAUNCH();
+    FJ_CK(cudaFreeAsync(part, st));
   } else {
     for (int c = 0; c < k; ++c) {
       k_stats<<<w->grid_elem, STPB, 0, st>>>(g->n, s, k, c, w->elem_part, w->elem_ticket, w->stat + 4 * c, d_bad);

@@ -336,7 +336,7 @@ __global__ void __launch_bounds__(ETB) k_b_init(int64_t n, int k, const double* 
   }
 }
 
-__global__ void __launch_bounds__(ETB) k_b_update(int64_t n, int k, const double* __restrict__ dinv,
+__global__ void __launch_bounds__(ETB, 8) k_b_update(int64_t n, int k, const double* __restrict__ dinv,
                                                   const double* __restrict__ p, const double* __restrict__ q,
                                                   double* __restrict__ x, double* __restrict__ r, BatchScalars* bs,
                                                   double* part, unsigned int* ticket, cudaGraphConditionalHandle h,

@@ -26,8 +26,9 @@ S = torch.from_numpy(wl.S[:, :a.k].copy()).cuda()
 u, v = torch.from_numpy(wl.u).cuda(), torch.from_numpy(wl.v).cuda()
 w = None if wl.w is None else torch.from_numpy(wl.w).cuda()
 G = fj.Graph.from_edges(wl.n, u, v, w)
-z, q, rep = G.approxim(S if a.k > 1 else S[:, 0].contiguous())
-z, q, rep = G.approxim(S if a.k > 1 else S[:, 0].contiguous())
+opts = fj.SolveOpts.make(use_cuda_graph=not os.environ.get("FJV_NO_GRAPH"))
+z, q, rep = G.approxim(S if a.k > 1 else S[:, 0].contiguous(), opts=opts)
+z, q, rep = G.approxim(S if a.k > 1 else S[:, 0].contiguous(), opts=opts)
 ms = G.time_spmv(k=a.k, reps=a.reps)
 Sq = S if a.k > 1 else S[:, 0].contiguous()
 G.quantities(Sq, z)
