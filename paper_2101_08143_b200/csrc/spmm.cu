@@ -17,6 +17,9 @@ namespace fj {
 #define FJ_SPMM_NB 8                   // neighbour rows in flight per warp (measured: 8 at 8 blocks/SM
                                        // 7.6 ms per C4 product, 16 unconstrained 8.5 ms)
 #endif
+#ifndef FJ_QB_MIN_BLOCKS
+#define FJ_QB_MIN_BLOCKS 0             // batched quantities pass
+#endif
 #ifndef FJ_SPMM_MIN_BLOCKS
 #define FJ_SPMM_MIN_BLOCKS 8
 #endif
@@ -776,7 +779,7 @@ __device__ __forceinline__ void q_row(const QuantArgs& a, int64_t i, int64_t len
 }
 
 template <int WT, bool PAIR>
-__global__ void __launch_bounds__(BTPB) quant_batch_kernel(const TileSched sc, const QuantArgs a) {
+__global__ void __launch_bounds__(BTPB, FJ_QB_MIN_BLOCKS) quant_batch_kernel(const TileSched sc, const QuantArgs a) {
   __shared__ double s_red[BWPB][MAXK];
   __shared__ bool s_last;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
