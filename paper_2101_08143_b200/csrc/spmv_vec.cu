@@ -10,9 +10,10 @@
 //
 // Per PCG iteration (same algebra as pcg.cu, per column):
 //   K_A warp_kernel<ApplyOpV>  q = (I+L) p (all columns), pq_c = p_c^T q_c -> alpha_c   (last block)
-//   K_B k_v_update             x += alpha p, r -= alpha q, rho'_c, ||r_c||^2 -> beta_c,
+//   K_B k_v_update             r -= alpha q, rho'_c, ||r_c||^2 -> beta_c,
 //                              per-column convergence mask, loop condition             (last block)
-//   K_C k_v_dir                p = dinv o r + beta p
+//   K_C k_v_dir                x += alpha p (old p), then p = dinv o r + beta p; after the final
+//                              iteration only the x update (the multi-GPU path keeps x in K_B)
 // in one CUDA graph with a device-driven conditional WHILE node.  Columns that converged keep
 // alpha_c = 0 (x_c, r_c frozen).  All partial sums are formed and combined in a fixed order:
 // results are bitwise reproducible.
@@ -104,8 +105,10 @@ __device__ __forceinline__ void st_q(double* base, int64_t i, const DVec<KP>& v)
 // Device scalars of one small-k batched solve (per column), written only by last-block finalisers.
 struct VecScalars {
   double rho[KVMAX], alpha[KVMAX], beta[KVMAX], pq[KVMAX], rr[KVMAX], ss[KVMAX], tol2[KVMAX], res2[KVMAX];
+  double alx[KVMAX];   // alpha applied to x by k_v_dir<XD> (0 for columns inactive in that iteration)
   int32_t active[KVMAX], conv[KVMAX], breakdown[KVMAX];
   int32_t iter, max_iter, done, k;
+  int32_t xpend;       // k_v_dir<XD> owes x += alx p for the iteration k_v_update just finished
 };
 
 // ---------------------------------------------------------------- row operators (tiles.cuh Op)
@@ -237,21 +240,19 @@ struct ResidOpV {
 // 2 (Lz)^2, 3 rounding allowance^2) and the six row-local sums of QuantOp (k_quant_local).  40
 // per-thread partials in one kernel cost 255 registers and 2 blocks / SM (2.2 ms on C3); split,
 // the row operator runs at the product's occupancy.
-template <int WT, int KP>
-struct QuantOpV {
+template <int WT, int KP, int KQ>
+struct QuantOpV {   // gathers the padded [n][KP] z; accumulates only the KQ = k real columns
   using V = DVec<KP>;
   static constexpr int ITEMS = VEC_ITEMS;
   static constexpr int TILE_ROWS = VEC_TILE_ROWS;
   static constexpr int MIN_BLOCKS = FJ_QUANTV_MIN_BLOCKS;
   static constexpr bool TMA = true;
-  static constexpr int NA = 3 * KP, NP = 4 * KP;
+  static constexpr int NA = 3 * KQ, NP = 4 * KQ;
   static constexpr bool NEEDS_XI = true;
   static __device__ __forceinline__ V vzero() { return vzero_kp<KP>(); }
   const double* __restrict__ z;   // padded [n][KP]
   const double* __restrict__ s;   // [n][k]
   const double* __restrict__ deg;
-  int k;
-  double m[KP];                   // mean of s per column
   double* out;                    // [4][KP]
   __device__ __forceinline__ bool skip() const { return false; }
   __device__ __forceinline__ bool wants_xi() const { return true; }
@@ -260,34 +261,35 @@ struct QuantOpV {
   __device__ __forceinline__ const V* xi_base() const { return reinterpret_cast<const V*>(z); }
   __device__ __forceinline__ void add(double (&a)[NA], double w, const V& zj, const V& zi) const {
 #pragma unroll
-    for (int c = 0; c < KP; ++c) {
+    for (int c = 0; c < KQ; ++c) {
       const double df = zi.v[c] - zj.v[c];
       a[c] = fma(w, zj.v[c], a[c]);
-      a[KP + c] = fma(w * df, df, a[KP + c]);
-      a[2 * KP + c] = fma(w, fabs(zj.v[c]), a[2 * KP + c]);
+      a[KQ + c] = fma(w * df, df, a[KQ + c]);
+      a[2 * KQ + c] = fma(w, fabs(zj.v[c]), a[2 * KQ + c]);
     }
   }
   __device__ __forceinline__ void finish_row(int64_t i, int64_t len, const V& zv, const double (&a)[NA],
                                              double (&part)[NP]) const {
     const double d = (WT == FJ_W_UNIT) ? (double)len : deg[i];
 #pragma unroll
-    for (int c = 0; c < KP; ++c) {
-      if (c >= k) break;
+    for (int c = 0; c < KQ; ++c) {
       const double zi = zv.v[c];
-      const double si = s[i * k + c];
+      const double si = s[i * KQ + c];
       const double t = fma(1.0 + d, zi, -a[c]);
       const double lz = fma(d, zi, -a[c]);
       const double r = si - t;
-      const double ab = fabs(si) + fma(1.0 + d, fabs(zi), a[2 * KP + c]);
-      part[0 * KP + c] += a[KP + c];
-      part[1 * KP + c] = fma(r, r, part[1 * KP + c]);
-      part[2 * KP + c] = fma(lz, lz, part[2 * KP + c]);
-      part[3 * KP + c] = fma(ab, ab, part[3 * KP + c]);
+      const double ab = fabs(si) + fma(1.0 + d, fabs(zi), a[2 * KQ + c]);
+      part[0 * KQ + c] += a[KQ + c];
+      part[1 * KQ + c] = fma(r, r, part[1 * KQ + c]);
+      part[2 * KQ + c] = fma(lz, lz, part[2 * KQ + c]);
+      part[3 * KQ + c] = fma(ab, ab, part[3 * KQ + c]);
     }
   }
   __device__ __forceinline__ void finalize(const double (&tot)[NP]) const {
 #pragma unroll
-    for (int j = 0; j < NP; ++j) out[j] = tot[j];
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int c = 0; c < KQ; ++c) out[j * KP + c] = tot[j * KQ + c];
   }
 };
 
@@ -402,6 +404,7 @@ __global__ void __launch_bounds__(VETB) k_v_init(int64_t n, int k, const double*
       any |= sc->active[c];
     }
     sc->iter = 0;
+    sc->xpend = 0;
     sc->max_iter = max_iter;
     sc->k = k;
     sc->done = (!any || max_iter <= 0) ? 1 : 0;
@@ -409,7 +412,10 @@ __global__ void __launch_bounds__(VETB) k_v_init(int64_t n, int k, const double*
   }
 }
 
-template <int KP, int KQ>
+// XD: the x update x += alpha p moves to k_v_dir (which reads p anyway), so this pass streams
+// only q and r (one vector stream fewer per iteration); the last block hands the alphas it applied
+// to k_v_dir through sc->alx / sc->xpend.
+template <int KP, int KQ, bool XD>
 __global__ void __launch_bounds__(VETB) k_v_update(int64_t n, int k, const double* __restrict__ dinv,
                                                    const double* __restrict__ p, const double* __restrict__ q,
                                                    double* __restrict__ x, double* __restrict__ r, VecScalars* sc,
@@ -417,7 +423,10 @@ __global__ void __launch_bounds__(VETB) k_v_update(int64_t n, int k, const doubl
                                                    int use_h) {
   __shared__ double s_red[2 * KP * VETB / 32];
   if (*(volatile int32_t*)&sc->done) {
-    if (use_h && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(h, 0);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      if (XD) sc->xpend = 0;    // the loop ended earlier: nothing owed to x any more
+      if (use_h) cudaGraphSetConditional(h, 0);
+    }
     return;
   }
   double al[KP];
@@ -427,20 +436,30 @@ __global__ void __launch_bounds__(VETB) k_v_update(int64_t n, int k, const doubl
 #pragma unroll
   for (int j = 0; j < 2 * KP; ++j) v[j] = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)VETB + threadIdx.x; i < n; i += (int64_t)gridDim.x * VETB) {
-    const DVec<KP> pv = ld_vec<KP>(p + i * KP), qv = ld_q<KP, KQ>(q, i);
-    DVec<KP> xv = ld_q<KP, KQ>(x, i), rv = ld_q<KP, KQ>(r, i);
+    const DVec<KP> qv = ld_q<KP, KQ>(q, i);
+    DVec<KP> rv = ld_q<KP, KQ>(r, i);
     const double di = dinv[i];
+    if (!XD) {
+      const DVec<KP> pv = ld_vec<KP>(p + i * KP);
+      DVec<KP> xv = ld_q<KP, KQ>(x, i);
+#pragma unroll
+      for (int c = 0; c < KP; ++c) xv.v[c] = fma(al[c], pv.v[c], xv.v[c]);
+      st_q<KP, KQ>(x, i, xv);
+    }
 #pragma unroll
     for (int c = 0; c < KP; ++c) {
-      xv.v[c] = fma(al[c], pv.v[c], xv.v[c]);
       rv.v[c] = fma(-al[c], qv.v[c], rv.v[c]);
       v[c] = fma(rv.v[c], di * rv.v[c], v[c]);
       v[KP + c] = fma(rv.v[c], rv.v[c], v[KP + c]);
     }
-    st_q<KP, KQ>(x, i, xv);
     st_q<KP, KQ>(r, i, rv);
   }
   if (vec_reduce<2 * KP>(v, part, ticket, s_red) && threadIdx.x == 0) {
+    if (XD) {
+#pragma unroll
+      for (int c = 0; c < KP; ++c) sc->alx[c] = al[c];
+      sc->xpend = 1;
+    }
     int any = 0;
     for (int c = 0; c < k; ++c) {
       if (sc->active[c]) {
@@ -461,18 +480,29 @@ __global__ void __launch_bounds__(VETB) k_v_update(int64_t n, int k, const doubl
     *ticket = 0u;
   }
 }
-
-template <int KP, int KQ>
+// p = dinv o r + beta p (and, XD, first x += alx p with the old p; after the final iteration only that)
+template <int KP, int KQ, bool XD>
 __global__ void __launch_bounds__(VETB) k_v_dir(int64_t n, int k, const double* __restrict__ dinv,
                                                 const double* __restrict__ r, double* __restrict__ p,
-                                                const VecScalars* sc) {
-  if (*(volatile const int32_t*)&sc->done) return;
-  double be[KP];
+                                                double* __restrict__ x, const VecScalars* sc) {
+  const bool done = *(volatile const int32_t*)&sc->done;
+  if (XD ? !*(volatile const int32_t*)&sc->xpend : done) return;
+  double be[KP], al[KP];
 #pragma unroll
-  for (int c = 0; c < KP; ++c) be[c] = (c < k && sc->active[c]) ? sc->beta[c] : 0.0;
+  for (int c = 0; c < KP; ++c) {
+    be[c] = (c < k && sc->active[c]) ? sc->beta[c] : 0.0;
+    al[c] = XD ? sc->alx[c] : 0.0;
+  }
   for (int64_t i = blockIdx.x * (int64_t)VETB + threadIdx.x; i < n; i += (int64_t)gridDim.x * VETB) {
-    const DVec<KP> rv = ld_q<KP, KQ>(r, i);
     DVec<KP> pv = ld_vec<KP>(p + i * KP);
+    if (XD) {
+      DVec<KP> xv = ld_q<KP, KQ>(x, i);
+#pragma unroll
+      for (int c = 0; c < KP; ++c) xv.v[c] = fma(al[c], pv.v[c], xv.v[c]);
+      st_q<KP, KQ>(x, i, xv);
+      if (done) continue;
+    }
+    const DVec<KP> rv = ld_q<KP, KQ>(r, i);
     const double di = dinv[i];
 #pragma unroll
     for (int c = 0; c < KP; ++c) pv.v[c] = fma(be[c], pv.v[c], di * rv.v[c]);
@@ -639,10 +669,10 @@ static fj_status vec_apply_padded(const fj_graph* g, const VecWs* w, const doubl
 template <int KP, int KQ>
 static fj_status vec_iteration(const fj_graph* g, VecWs* w, cudaStream_t st, cudaGraphConditionalHandle h, int use_h) {
   FJ_TRY((vec_apply_padded<KP, KQ>(g, w, w->p, w->q, 0, w->sc, st)));
-  k_v_update<KP, KQ><<<w->grid_elem, VETB, 0, st>>>(g->n, w->k, g->dinv, w->p, w->q, w->x, w->r, w->sc, w->elem_part,
-                                                w->elem_ticket, h, use_h);
+  k_v_update<KP, KQ, true><<<w->grid_elem, VETB, 0, st>>>(g->n, w->k, g->dinv, w->p, w->q, w->x, w->r, w->sc,
+                                                      w->elem_part, w->elem_ticket, h, use_h);
   FJ_CK_LAUNCH();
-  k_v_dir<KP, KQ><<<w->grid_elem, VETB, 0, st>>>(g->n, w->k, g->dinv, w->r, w->p, w->sc);
+  k_v_dir<KP, KQ, true><<<w->grid_elem, VETB, 0, st>>>(g->n, w->k, g->dinv, w->r, w->p, w->x, w->sc);
   FJ_CK_LAUNCH();
   return FJ_OK;
 }
@@ -961,7 +991,7 @@ static fj_status dist_solve_vec_t(fj_graph* g, VecWs* w, int k, const double* s,
         FJ_TRY(dist_allreduce_sum(g, red + KP, 2 * KP, st));
         k_dv_post<<<1, 1, 0, st>>>(k, KP, red, red + KP, w->sc);
         FJ_CK_LAUNCH();
-        k_v_dir<KP, KQ><<<w->grid_elem, VETB, 0, st>>>(n, k, g->dinv, w->r, w->p, w->sc);
+        k_v_dir<KP, KQ, false><<<w->grid_elem, VETB, 0, st>>>(n, k, g->dinv, w->r, w->p, w->x, w->sc);
         FJ_CK_LAUNCH();
       }
       FJ_CK(cudaMemcpyAsync(&h, w->sc, sizeof h, cudaMemcpyDeviceToHost, st));
@@ -1114,10 +1144,14 @@ fj_status quant_vec(fj_graph* g, int k, const double* s, const double* z, const 
     phase_tick("quant: local sums", st);
     return by_wtype<KP>(g, [&](auto wt) {
       constexpr int WT = decltype(wt)::value;
-      QuantOpV<WT, KP> op;
-      op.z = zp; op.s = s; op.deg = g->deg; op.k = k; op.out = w->qout;
-      for (int c = 0; c < KP; ++c) op.m[c] = c < k ? mean_host[c] : 0.0;
-      return launch_vec_items<WT>(g, w, op, st);
+      auto go = [&](auto kqc) -> fj_status {
+        constexpr int KQ = decltype(kqc)::value;
+        QuantOpV<WT, KP, KQ> op;
+        op.z = zp; op.s = s; op.deg = g->deg; op.out = w->qout;
+        return launch_vec_items<WT>(g, w, op, st);
+      };
+      if (KP == 4 && k == 3) return go(std::integral_constant<int, 3>());
+      return go(std::integral_constant<int, KP>());
     });
   };
   if (kp == 2) FJ_TRY(launch(std::integral_constant<int, 2>()));
