@@ -59,8 +59,9 @@ struct ApplyOp {
   __device__ __forceinline__ void add(double (&a)[NA], double w, double xj, double) const {
     if (WT == FJ_W_UNIT) a[0] += xj; else a[0] = fma(w, xj, a[0]);
   }
+  template <class P>
   __device__ __forceinline__ void finish_row(int64_t i, int64_t len, double xi, const double (&a)[NA],
-                                             double (&part)[NP]) const {
+                                             P& part) const {
     double yi;
     if (SEG <= SEG_FIRST) {
       const double d = (WT == FJ_W_UNIT && SEG == SEG_WHOLE) ? (double)len : deg[i];
@@ -111,8 +112,9 @@ struct ResidOp {
   __device__ __forceinline__ void add(double (&a)[NA], double w, double xj, double) const {
     if (WT == FJ_W_UNIT) a[0] += xj; else a[0] = fma(w, xj, a[0]);
   }
+  template <class P>
   __device__ __forceinline__ void finish_row(int64_t i, int64_t len, double zi, const double (&a)[NA],
-                                             double (&part)[NP]) const {
+                                             P& part) const {
     const double d = (WT == FJ_W_UNIT) ? (double)len : deg[i];
     const double r = s[i * ld + c] - fma(1.0 + d, zi, -a[0]);
     part[0] = fma(r, r, part[0]);
@@ -157,8 +159,9 @@ struct QuantOp {
     a[1] = fma(w * df, df, a[1]);
     a[2] = fma(w, fabs(zj), a[2]);
   }
+  template <class P>
   __device__ __forceinline__ void finish_row(int64_t i, int64_t len, double zi, const double (&a)[NA],
-                                             double (&part)[NP]) const {
+                                             P& part) const {
     const double d = (WT == FJ_W_UNIT) ? (double)len : deg[i];
     const double si = s[i * ld + c];
     const double t = fma(1.0 + d, zi, -a[0]);

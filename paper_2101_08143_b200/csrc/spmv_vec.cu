@@ -147,8 +147,9 @@ struct ApplyOpV {
 #pragma unroll
     for (int c = 0; c < KP; ++c) a[c] = (WT == FJ_W_UNIT) ? a[c] + xj.v[c] : fma(w, xj.v[c], a[c]);
   }
+  template <class P>
   __device__ __forceinline__ void finish_row(int64_t i, int64_t len, const V& xi, const double (&a)[NA],
-                                             double (&part)[NP]) const {
+                                             P& part) const {
     V yv;
     if (SEG <= SEG_FIRST) {
       const double d = (WT == FJ_W_UNIT && SEG == SEG_WHOLE) ? (double)len : deg[i];
@@ -217,8 +218,9 @@ struct ResidOpV {
 #pragma unroll
     for (int c = 0; c < KP; ++c) a[c] = (WT == FJ_W_UNIT) ? a[c] + xj.v[c] : fma(w, xj.v[c], a[c]);
   }
+  template <class P>
   __device__ __forceinline__ void finish_row(int64_t i, int64_t len, const V& zi, const double (&a)[NA],
-                                             double (&part)[NP]) const {
+                                             P& part) const {
     const double d = (WT == FJ_W_UNIT) ? (double)len : deg[i];
 #pragma unroll
     for (int c = 0; c < KP; ++c) {
@@ -240,15 +242,19 @@ struct ResidOpV {
 // 2 (Lz)^2, 3 rounding allowance^2) and the six row-local sums of QuantOp (k_quant_local).  40
 // per-thread partials in one kernel cost 255 registers and 2 blocks / SM (2.2 ms on C3); split,
 // the row operator runs at the product's occupancy.
+#ifndef FJ_QUANTV_PART_SMEM
+#define FJ_QUANTV_PART_SMEM 1
+#endif
 template <int WT, int KP, int KQ>
 struct QuantOpV {   // gathers the padded [n][KP] z; accumulates only the KQ = k real columns
   using V = DVec<KP>;
   static constexpr int ITEMS = VEC_ITEMS;
   static constexpr int TILE_ROWS = VEC_TILE_ROWS;
-  static constexpr int MIN_BLOCKS = FJ_QUANTV_MIN_BLOCKS;
+  static constexpr int MIN_BLOCKS = FJ_QUANTV_MIN_BLOCKS >= 0 ? FJ_QUANTV_MIN_BLOCKS : (KQ <= 3 && WT == FJ_W_UNIT ? 4 : 3);
   static constexpr bool TMA = true;
   static constexpr int NA = 3 * KQ, NP = 4 * KQ;
   static constexpr bool NEEDS_XI = true;
+  static constexpr bool PART_SMEM = FJ_QUANTV_PART_SMEM != 0;   // 4 KQ partials off the registers
   static __device__ __forceinline__ V vzero() { return vzero_kp<KP>(); }
   const double* __restrict__ z;   // padded [n][KP]
   const double* __restrict__ s;   // [n][k]
@@ -268,8 +274,9 @@ struct QuantOpV {   // gathers the padded [n][KP] z; accumulates only the KQ = k
       a[2 * KQ + c] = fma(w, fabs(zj.v[c]), a[2 * KQ + c]);
     }
   }
+  template <class P>
   __device__ __forceinline__ void finish_row(int64_t i, int64_t len, const V& zv, const double (&a)[NA],
-                                             double (&part)[NP]) const {
+                                             P& part) const {
     const double d = (WT == FJ_W_UNIT) ? (double)len : deg[i];
 #pragma unroll
     for (int c = 0; c < KQ; ++c) {

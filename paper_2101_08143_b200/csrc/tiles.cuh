@@ -39,8 +39,8 @@ constexpr int WPB = WTPB / 32;
 #ifndef FJ_VEC_MIN_BLOCKS
 #define FJ_VEC_MIN_BLOCKS 4
 #endif
-#ifndef FJ_QUANTV_MIN_BLOCKS
-#define FJ_QUANTV_MIN_BLOCKS 0
+#ifndef FJ_QUANTV_MIN_BLOCKS   // -1: 4 blocks/SM for unit weights and k <= 3, else 3 (no spills with
+#define FJ_QUANTV_MIN_BLOCKS -1  // the partials in shared memory); 0: no hint
 #endif
 #ifndef FJ_VEC2_MIN_BLOCKS
 #define FJ_VEC2_MIN_BLOCKS 5
@@ -174,7 +174,9 @@ void free_segments(fj_graph* g);
 //   __device__ const V* xi_base() const;           // x_i = xi_base()[i] (contiguous), or nullptr
 //   __device__ bool wants_xi() const;              // false: x_i unused by finish_row (not loaded)
 //   __device__ void add(double (&a)[NA], double w, V xj, V xi) const;
-//   __device__ void finish_row(int64_t i, int64_t len, V xi, const double (&a)[NA], double (&part)[NP]) const;
+//   template <class P>                             // P: double[NP] or PartStore (part[j] += ...)
+//   __device__ void finish_row(int64_t i, int64_t len, V xi, const double (&a)[NA], P& part) const;
+//   static constexpr bool PART_SMEM;               // optional: per-thread partials in shared memory
 //   __device__ void finalize(const double (&tot)[NP]) const;   // single thread of the last block
 
 // Merge-path split (Merrill & Garland): on the merge of the row-end offsets A[0..R) with the nonzero
@@ -194,6 +196,23 @@ __device__ __forceinline__ int merge_rows_before(int d, const int32_t* A, int R,
 // (warp segmented scan).  No shared-memory reduction, no idle lanes on ragged rows.
 // Tile inputs staged by the TMA bulk-copy prefetch (warp_kernel): the tile's col indices, row_ptr
 // entries and row values already sit in shared memory (null members: load them here).
+// Per-thread partial sums of finish_row: registers, or (Op::PART_SMEM, for operators with many
+// partials) a [NP][WTPB] shared-memory column per thread, freeing 2 NP registers in the main loop.
+template <class Op, class = void>
+struct PartSmemT : std::false_type {};
+template <class Op>
+struct PartSmemT<Op, std::void_t<decltype(Op::PART_SMEM)>> : std::integral_constant<bool, Op::PART_SMEM> {};
+template <int NP, bool SMEM>
+struct PartStore {
+  double v[NP];
+  __device__ __forceinline__ double& operator[](int j) { return v[j]; }
+};
+template <int NP>
+struct PartStore<NP, true> {
+  double* b;   // s_part + threadIdx.x, stride WTPB
+  __device__ __forceinline__ double& operator[](int j) { return b[j * WTPB]; }
+};
+
 template <class V>
 struct TilePre {
   const int32_t* col;     // col[k0 .. k0+N)
@@ -201,10 +220,10 @@ struct TilePre {
   const V* xi;            // x[r0 .. r0+R)
 };
 
-template <int WT, class Op, bool PRE>
+template <int WT, class Op, bool PRE, class P>
 __device__ __forceinline__ void t_tile(const TileSched& sc, const Op& op, const ItemMeta& cur, int lane,
                                        int32_t* s_e, int32_t* s_col_own, typename Op::V* s_xi_own,
-                                       double (&part)[Op::NP], const TilePre<typename Op::V>& pre) {
+                                       P& part, const TilePre<typename Op::V>& pre) {
   using V = typename Op::V;
   constexpr int NA = Op::NA;
   constexpr int ITEMS = Op::ITEMS;
@@ -408,9 +427,9 @@ __device__ __forceinline__ TilePre<typename Op::V> pf_view(const ItemMeta& m, co
 
 // W row or C chunk item (lanes stride over the row's nonzeros; chunk partials merged in chunk
 // order by the warp that completes the row).
-template <int WT, class Op>
+template <int WT, class Op, class P>
 __device__ __forceinline__ void wc_item(const TileSched& sc, const Op& op, const TileScratch& ws, const ItemMeta& cur,
-                                        int64_t it, int lane, double (&part)[Op::NP]) {
+                                        int64_t it, int lane, P& part) {
   using V = typename Op::V;
   constexpr int NA = Op::NA, NP = Op::NP;
   constexpr bool WEIGHTED = (WT != FJ_W_UNIT);
@@ -488,7 +507,10 @@ __global__ void __launch_bounds__(WTPB, Op::MIN_BLOCKS) warp_kernel(const TileSc
 
   if (op.skip()) return;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  double part[NP];
+  constexpr bool PS = PartSmemT<Op>::value;
+  __shared__ double s_part[PS ? NP * WTPB : 1];
+  PartStore<NP, PS> part;
+  if constexpr (PS) part.b = s_part + threadIdx.x;
 #pragma unroll
   for (int j = 0; j < NP; ++j) part[j] = 0.0;
 
@@ -562,10 +584,13 @@ __global__ void __launch_bounds__(WTPB, Op::MIN_BLOCKS) warp_kernel(const TileSc
   }
 
   // ---------------------------------------------------- grid-level deterministic reduction
-  block_sum<NP, WTPB>(part, s_red);
+  double pr[NP];
+#pragma unroll
+  for (int j = 0; j < NP; ++j) pr[j] = part[j];
+  block_sum<NP, WTPB>(pr, s_red);
   if (threadIdx.x == 0) {
 #pragma unroll
-    for (int j = 0; j < NP; ++j) ws.block_part[(int64_t)blockIdx.x * NP + j] = part[j];
+    for (int j = 0; j < NP; ++j) ws.block_part[(int64_t)blockIdx.x * NP + j] = pr[j];
     __threadfence();
     s_last = atomicAdd(ws.grid_ticket, 1u) == gridDim.x - 1u;
   }
