@@ -172,6 +172,10 @@ def main():
     ap.add_argument("--impl", default="fj", choices=["fj", "reference"])
     ap.add_argument("--config", default="c3")
     ap.add_argument("--rtol", type=float, default=1e-10)
+    ap.add_argument("--vertex-order", default="auto", choices=["auto", "degree", "natural"],
+                    help="a1 locality relabelling by descending degree, inside the timed step (DESIGN.md "
+                         "§6.7); auto = FJ_ORDER_AUTO's rule (k <= 2 and the gathered vector exceeds L2); "
+                         "the row-partitioned N>1 path always builds in the input labels")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--spmv-reps", type=int, default=20)
@@ -202,7 +206,10 @@ def main():
     w = None if wl.w is None else torch.from_numpy(wl.w).cuda()
     S = torch.from_numpy(wl.S).cuda()
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device="cuda")
-    opts = fj.SolveOpts.make(rtol=args.rtol, use_cuda_graph=not args.no_cuda_graph)
+    order = "natural" if ws > 1 else args.vertex_order
+    if order == "auto":
+        order = "degree" if binding.relabel_pays(n, k) else "natural"
+    opts = fj.SolveOpts.make(rtol=args.rtol, use_cuda_graph=not args.no_cuda_graph, vertex_order=order)
     stream = torch.cuda.current_stream()
 
     dist_mode = ws > 1
@@ -221,12 +228,11 @@ def main():
             info = {"nnz": G.plan["nnz_local"], "bounds": b}
             G.close()
             return q, rep, info, G.plan
-        rp, col, wo, st = fj.csr_from_edges(n, u, v, w)
-        G = fj.Graph(n, rp, col, wo, validate=False)
-        z, q, rep = G.approxim(S, opts=opts)
+        G = fj.Graph.from_edges(n, u, v, w, order=order)   # a1 (+ relabelling) + a2
+        z, q, rep = G.approxim(S, opts=opts)                 # s mapped in, z mapped back out
         info = G.info()
         G.close()
-        return q, rep, info, st
+        return q, rep, info, G.build_stats
 
     for _ in range(args.warmup):
         q, rep, info, bst = step()
@@ -272,8 +278,7 @@ def main():
     # solver buffers), timed live inside the library with CUDA events on the launching stream
     spmv_ms = None
     if not dist_mode:
-        rp, col, wo, _ = fj.csr_from_edges(n, u, v, w)
-        G = fj.Graph(n, rp, col, wo, validate=False)
+        G = fj.Graph.from_edges(n, u, v, w, order=order)
         G.approxim(S, opts=opts)          # fills the solver buffers with a real search direction
         flush.fill_(1)
         spmv_ms = G.time_spmv(k=kb, reps=args.spmv_reps)
@@ -320,7 +325,7 @@ def main():
         "warmup": args.warmup, "ms_per_step": max_step_ms / args.steps, "higher_is_better": True,
         "scaling": "strong" if dist_mode else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{wl.name}: {wl.desc}", "n": n, "nnz": nnz, "k": k, "rtol": args.rtol,
-                   "opinions": wl.kinds,
+                   "opinions": wl.kinds, "vertex_order": order,
                    "parallelism": f"row-partition x{ws} (NCCL halo + allreduce)" if dist_mode else "1 GPU",
                    "l2": "flushed between steps (512 MiB write, outside the timed events)",
                    "pcg_iterations_per_step": iters / args.steps,

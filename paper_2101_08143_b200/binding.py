@@ -23,11 +23,14 @@ class GraphInfo(ctypes.Structure):
 
 class SolveOpts(ctypes.Structure):
     _fields_ = [("rtol", _dbl), ("eps_target", _dbl), ("max_iter", _i32), ("max_restarts", _i32),
-                ("use_cuda_graph", _i32), ("reserved", _i32)]
+                ("use_cuda_graph", _i32), ("vertex_order", _i32)]
 
     @classmethod
-    def make(cls, rtol=1e-10, eps_target=0.0, max_iter=10000, max_restarts=3, use_cuda_graph=True):
-        return cls(rtol, eps_target, max_iter, max_restarts, 1 if use_cuda_graph else 0, 0)
+    def make(cls, rtol=1e-10, eps_target=0.0, max_iter=10000, max_restarts=3, use_cuda_graph=True,
+             vertex_order="natural"):
+        """vertex_order ("natural" | "degree" | "auto"): fj_approxim_host's a1 relabelling (fj.h FJ_ORDER_*)."""
+        vo = {"natural": 0, "degree": 1, "auto": 2}[vertex_order] if isinstance(vertex_order, str) else int(vertex_order)
+        return cls(rtol, eps_target, max_iter, max_restarts, 1 if use_cuda_graph else 0, vo)
 
 
 class SolveReport(ctypes.Structure):
@@ -89,6 +92,12 @@ def load_library(path: str = SO):
     L.fj_default_solve_opts.restype = None
     L.fj_csr_from_edges.argtypes = [_i64, _i64, _vp, _vp, _vp, ctypes.c_int, _vp, _vp, _vp, P(_i64), P(_i64),
                                     P(_i64), _vp]
+    L.fj_csr_from_edges_mapped.argtypes = [_i64, _i64, _vp, _vp, _vp, _vp, ctypes.c_int, _vp, _vp, _vp, P(_i64),
+                                           P(_i64), P(_i64), _vp]
+    L.fj_degree_order.argtypes = [_i64, _i64, _vp, _vp, _vp, _vp, _vp]
+    L.fj_permute_rows.argtypes = [_i64, ctypes.c_int, _vp, _vp, _vp, _vp]
+    L.fj_csr_degree_order.argtypes = [_i64, _vp, _vp, _vp, _vp]
+    L.fj_csr_permute.argtypes = [_i64, _i64, _vp, _vp, _vp, ctypes.c_int, _vp, _vp, _vp, _vp, _vp, _vp]
     L.fj_graph_create.argtypes = [_i64, _i64, _vp, _vp, _vp, ctypes.c_int, ctypes.c_int, _vp, P(_vp)]
     L.fj_graph_info.argtypes = [_vp, P(GraphInfo)]
     L.fj_graph_degrees.argtypes = [_vp, _vp, _vp]
@@ -229,20 +238,82 @@ def _need_cuda(*ts):
             raise ValueError("contiguous tensors required")
 
 
-def csr_from_edges(n: int, u, v, w=None, stream=None):
+def degree_order(n: int, u, v, stream=None):
+    """fj_degree_order: (new2old, old2new) int32 device permutations, vertices by descending raw
+    endpoint count (ties by id) -- the locality relabelling of DESIGN.md §6.7."""
+    import torch
+    _need_cuda(u, v)
+    new2old = torch.empty(n, dtype=torch.int32, device=u.device)
+    old2new = torch.empty(n, dtype=torch.int32, device=u.device)
+    _check(lib().fj_degree_order(n, int(u.numel()), _ptr(u), _ptr(v), _ptr(new2old), _ptr(old2new),
+                                 _stream(stream)))
+    return new2old, old2new
+
+
+def relabel_pays(n: int, k: int) -> bool:
+    """FJ_ORDER_AUTO's rule: relabel only for rows narrower than a 32-byte L2 sector
+    (k <= 2) whose gathered [n][k] vector exceeds the L2."""
+    import torch
+    l2 = getattr(torch.cuda.get_device_properties(torch.cuda.current_device()), "L2_cache_size", 126 << 20)
+    return k <= 2 and n * 8 * k > l2
+
+
+def csr_degree_order(n: int, row_ptr, stream=None):
+    """fj_csr_degree_order: (new2old, old2new) by descending row length of a built CSR."""
+    import torch
+    _need_cuda(row_ptr)
+    new2old = torch.empty(n, dtype=torch.int32, device=row_ptr.device)
+    old2new = torch.empty(n, dtype=torch.int32, device=row_ptr.device)
+    _check(lib().fj_csr_degree_order(n, _ptr(row_ptr), _ptr(new2old), _ptr(old2new), _stream(stream)))
+    return new2old, old2new
+
+
+def csr_permute(n: int, row_ptr, col, w, new2old, old2new, stream=None):
+    """fj_csr_permute: (row_ptr, col, w) of P A P^T (columns in their source order)."""
+    import torch
+    _need_cuda(row_ptr, col, w, new2old, old2new)
+    rp2 = torch.empty_like(row_ptr)
+    col2 = torch.empty_like(col)
+    w2 = None if w is None else torch.empty_like(w)
+    _check(lib().fj_csr_permute(n, int(col.numel()), _ptr(row_ptr), _ptr(col), _ptr(w), _wtype(w), _ptr(new2old),
+                                _ptr(old2new), _ptr(rp2), _ptr(col2), _ptr(w2), _stream(stream)))
+    return rp2, col2, w2
+
+
+def permute_rows(x, idx, stream=None):
+    """fj_permute_rows: out[i] = x[idx[i]] for a [n] or [n][k] fp64 device tensor."""
+    import torch
+    _need_cuda(x, idx)
+    n = int(idx.numel())
+    k = _cols(x, n)
+    out = torch.empty_like(x)
+    _check(lib().fj_permute_rows(n, k, _ptr(idx), _ptr(x), _ptr(out), _stream(stream)))
+    return out
+
+
+def csr_from_edges(n: int, u, v, w=None, stream=None, old2new=None):
     """Row a1: canonical CSR (device) from a raw device edge list.  Returns
-    (row_ptr int64 [n+1], col int32 [nnz], w_out or None, stats dict)."""
+    (row_ptr int64 [n+1], col int32 [nnz], w_out or None, stats dict).  old2new (int32 [n] device
+    permutation): the CSR of the relabelled edge list (fj_csr_from_edges_mapped)."""
     import torch
     L = lib()
-    _need_cuda(u, v, w)
+    _need_cuda(u, v, w, old2new)
     m = int(u.numel())
     dev = u.device
     row_ptr = torch.empty(n + 1, dtype=torch.int64, device=dev)
     col = torch.empty(max(2 * m, 1), dtype=torch.int32, device=dev)
     w_out = None if w is None else torch.empty(max(2 * m, 1), dtype=w.dtype, device=dev)
     nnz, loops, dups = _i64(), _i64(), _i64()
-    _check(L.fj_csr_from_edges(n, m, _ptr(u), _ptr(v), _ptr(w), _wtype(w), _ptr(row_ptr), _ptr(col), _ptr(w_out),
-                               ctypes.byref(nnz), ctypes.byref(loops), ctypes.byref(dups), _stream(stream)))
+    if old2new is None:
+        _check(L.fj_csr_from_edges(n, m, _ptr(u), _ptr(v), _ptr(w), _wtype(w), _ptr(row_ptr), _ptr(col),
+                                   _ptr(w_out), ctypes.byref(nnz), ctypes.byref(loops), ctypes.byref(dups),
+                                   _stream(stream)))
+    else:
+        if old2new.numel() != n or old2new.dtype != torch.int32:
+            raise ValueError("old2new must be an int32 [n] tensor")
+        _check(L.fj_csr_from_edges_mapped(n, m, _ptr(u), _ptr(v), _ptr(old2new), _ptr(w), _wtype(w), _ptr(row_ptr),
+                                          _ptr(col), _ptr(w_out), ctypes.byref(nnz), ctypes.byref(loops),
+                                          ctypes.byref(dups), _stream(stream)))
     k = nnz.value
     col = col[:k]
     if w_out is not None:
@@ -261,12 +332,19 @@ def _cols(t, n):
 
 
 class Graph:
-    """Handle over a borrowed device CSR (rows a2..a7).  Keeps references to the CSR tensors."""
+    """Handle over a borrowed device CSR (rows a2..a7).  Keeps references to the CSR tensors.
+    A graph built with from_edges(..., order="degree") holds the relabelled CSR
+    and maps every vertex-indexed argument in (fj_permute_rows with new2old) and every
+    vertex-indexed result back (old2new): callers always see the input labels."""
+
+    new2old = None   # class defaults: subclasses (DistGraph) build their handles without __init__
+    old2new = None
 
     def __init__(self, n: int, row_ptr, col, w=None, validate: bool = True, stream=None):
         L = lib()
         _need_cuda(row_ptr, col, w)
         self.n = int(n)
+        self.new2old = self.old2new = None
         self._keep = (row_ptr, col, w)
         h = _vp()
         _check(L.fj_graph_create(self.n, int(col.numel()), _ptr(row_ptr), _ptr(col), _ptr(w), _wtype(w),
@@ -274,11 +352,33 @@ class Graph:
         self._h = h
 
     @classmethod
-    def from_edges(cls, n, u, v, w=None, validate=False, stream=None):
+    def from_edges(cls, n, u, v, w=None, validate=False, stream=None, order: str = "natural"):
+        """a1 + a2 from a raw device edge list; order="degree" relabels the built CSR by descending
+        degree (fj_csr_degree_order + fj_csr_permute)."""
+        if order not in ("natural", "degree"):
+            raise ValueError("order must be 'natural' or 'degree'")
+        n2o = o2n = None
         rp, col, wo, stats = csr_from_edges(n, u, v, w, stream)
+        if order == "degree":
+            n2o, o2n = csr_degree_order(n, rp, stream)
+            rp, col, wo = csr_permute(n, rp, col, wo, n2o, o2n, stream)
+            validate = False   # columns are in source order, not ascending in the new labels
         g = cls(n, rp, col, wo, validate=validate, stream=stream)
+        g.new2old, g.old2new = n2o, o2n
         g.build_stats = stats
         return g
+
+    def _in(self, x, stream=None):      # input labels -> the handle's labels
+        return x if self.new2old is None else permute_rows(x, self.new2old, stream)
+
+    def _out(self, x, stream=None, out=None):   # the handle's labels -> input labels
+        if self.old2new is None:
+            return x
+        y = permute_rows(x, self.old2new, stream)
+        if out is not None:
+            out.copy_(y)
+            return out
+        return y
 
     @property
     def handle(self):
@@ -295,15 +395,16 @@ class Graph:
         import torch
         d = torch.empty(self.n, dtype=torch.float64, device=self._keep[0].device)
         _check(lib().fj_graph_degrees(self.handle, _ptr(d), _stream(stream)))
-        return d
+        return self._out(d, stream)
 
     def apply(self, x, op: int = FJ_OP_IPL, stream=None):
         import torch
         _need_cuda(x)
         k = _cols(x, self.n)
+        xi = self._in(x, stream)
         y = torch.empty_like(x)
-        _check(lib().fj_apply(self.handle, op, k, _ptr(x), _ptr(y), _stream(stream)))
-        return y
+        _check(lib().fj_apply(self.handle, op, k, _ptr(xi), _ptr(y), _stream(stream)))
+        return self._out(y, stream)
 
     def time_spmv(self, k: int = 1, reps: int = 20, stream=None) -> float:
         """ms per launch of the k-column PCG product q = (I+L)p (fj_time_spmv; CUDA events)."""
@@ -323,18 +424,24 @@ class Graph:
         import torch
         _need_cuda(s)
         k = _cols(s, self.n)
-        z = torch.empty_like(s) if z is None else z
+        z_user = z
+        si = self._in(s, stream)
+        if self.new2old is not None:   # z (input labels, warm start) in, solution out
+            z = torch.empty_like(s) if z_user is None else self._in(z_user, stream)
+        else:
+            z = torch.empty_like(s) if z is None else z
         rep = SolveReport()
         o = opts or SolveOpts.make()
-        _check(lib().fj_solve(self.handle, k, _ptr(s), _ptr(z), ctypes.byref(o), ctypes.byref(rep), _stream(stream)),
+        _check(lib().fj_solve(self.handle, k, _ptr(si), _ptr(z), ctypes.byref(o), ctypes.byref(rep), _stream(stream)),
                allow=(FJ_E_NO_CONVERGENCE,) if allow_no_convergence else ())
-        return z, rep.to_dict()
+        return self._out(z, stream, out=z_user), rep.to_dict()
 
     def quantities(self, s, z, stream=None):
         _need_cuda(s, z)
         k = _cols(s, self.n)
         q = (Quantities * k)()
-        _check(lib().fj_quantities(self.handle, k, _ptr(s), _ptr(z), q, _stream(stream)))
+        si, zi = self._in(s, stream), self._in(z, stream)
+        _check(lib().fj_quantities(self.handle, k, _ptr(si), _ptr(zi), q, _stream(stream)))
         return [x.to_dict() for x in q]
 
     def approxim(self, s, opts: SolveOpts | None = None, z=None, stream=None):
@@ -342,13 +449,15 @@ class Graph:
         import torch
         _need_cuda(s)
         k = _cols(s, self.n)
-        z = torch.empty_like(s) if z is None else z
+        z_user = z
+        z = torch.empty_like(s) if (z is None or self.new2old is not None) else z
         q = (Quantities * k)()
         rep = SolveReport()
         o = opts or SolveOpts.make()
-        _check(lib().fj_approxim(self.handle, k, _ptr(s), _ptr(z), ctypes.byref(o), q, ctypes.byref(rep),
+        si = self._in(s, stream)
+        _check(lib().fj_approxim(self.handle, k, _ptr(si), _ptr(z), ctypes.byref(o), q, ctypes.byref(rep),
                                  _stream(stream)))
-        return z, [x.to_dict() for x in q], rep.to_dict()
+        return self._out(z, stream, out=z_user), [x.to_dict() for x in q], rep.to_dict()
 
     def approxim_alg1(self, s, eps: float = 1e-6, opts: SolveOpts | None = None, stream=None):
         """Algorithm 1 verbatim (row f2): both solves, lines 5-9 norms.  Returns (dict, report)."""
@@ -358,6 +467,7 @@ class Graph:
         r = Alg1Result()
         rep = SolveReport()
         o = opts or SolveOpts.make()
+        s = self._in(s, stream)
         _check(lib().fj_approxim_alg1(self.handle, _ptr(s), float(eps), ctypes.byref(o), ctypes.byref(r),
                                       ctypes.byref(rep), _stream(stream)))
         return r.to_dict(), rep.to_dict()
@@ -369,20 +479,25 @@ class Graph:
         k = _cols(s, self.n)
         z = torch.empty_like(s)
         q = (Quantities * k)()
-        _check(lib().fj_exact_dense(self.handle, k, _ptr(s), _ptr(z), q, _stream(stream)))
-        return z, [x.to_dict() for x in q]
+        si = self._in(s, stream)
+        _check(lib().fj_exact_dense(self.handle, k, _ptr(si), _ptr(z), q, _stream(stream)))
+        return self._out(z, stream), [x.to_dict() for x in q]
 
     def forest_columns(self, cols, opts: SolveOpts | None = None, stream=None):
         """Columns `cols` of Omega = (I+L)^{-1} (row f4): a [n][len(cols)] fp64 CUDA tensor + report."""
         import numpy as np
         import torch
         c = np.ascontiguousarray(cols, dtype=np.int32)
+        if self.old2new is not None:   # Omega' = P Omega P^T: column c of Omega is column old2new[c] of Omega'
+            if len(c) and (c.min() < 0 or c.max() >= self.n):
+                raise ValueError("column index out of range")
+            c = np.ascontiguousarray(self.old2new.cpu().numpy()[c], dtype=np.int32)
         out = torch.empty((self.n, len(c)), dtype=torch.float64, device=self._keep[0].device)
         rep = SolveReport()
         o = opts or SolveOpts.make()
         _check(lib().fj_forest_columns(self.handle, len(c), ctypes.c_void_p(c.ctypes.data), _ptr(out),
                                        ctypes.byref(o), ctypes.byref(rep), _stream(stream)))
-        return out, rep.to_dict()
+        return self._out(out, stream), rep.to_dict()
 
     def close(self):
         if getattr(self, "_h", None) is not None and _lib is not None:

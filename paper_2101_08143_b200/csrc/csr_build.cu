@@ -23,18 +23,21 @@ struct BuildFlags {
 
 // Both orientations of every raw edge e: keys 2e = (u << b) | v and 2e+1 = (v << b) | u, payload e.
 // Self-loops (and out-of-range ids) get the sentinel key, which sorts last.
+// map (optional, fj_csr_from_edges_mapped): endpoints are relabelled old -> map[old] after the
+// range check, so the CSR is that of the relabelled graph.
 __global__ void k_mirror_keys(int64_t m, int64_t n, const int32_t* __restrict__ u, const int32_t* __restrict__ v,
-                              int b, uint64_t sent, uint64_t* __restrict__ keys, int32_t* __restrict__ vals,
-                              BuildFlags* fl) {
+                              const int32_t* __restrict__ map, int b, uint64_t sent, uint64_t* __restrict__ keys,
+                              int32_t* __restrict__ vals, BuildFlags* fl) {
   unsigned long long loops = 0;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t a = u[e], c = v[e];
+    int64_t a = u[e], c = v[e];
     uint64_t k0 = sent, k1 = sent;
     if (a < 0 || c < 0 || a >= n || c >= n) {
       atomicOr(&fl->bad_range, 1u);
     } else if (a == c) {
       ++loops;
     } else {
+      if (map) { a = map[a]; c = map[c]; }
       k0 = ((uint64_t)a << b) | (uint64_t)c;
       k1 = ((uint64_t)c << b) | (uint64_t)a;
     }
@@ -101,9 +104,9 @@ static inline unsigned grid_for(int64_t n, int num_sms) {
 
 using namespace fj;
 
-extern "C" fj_status fj_csr_from_edges(int64_t n, int64_t m_in, const int32_t* u, const int32_t* v, const void* w,
-                                       int wtype, int64_t* row_ptr, int32_t* col, void* w_out, int64_t* nnz_out,
-                                       int64_t* selfloops_out, int64_t* dups_out, void* stream) {
+static fj_status csr_from_edges(int64_t n, int64_t m_in, const int32_t* u, const int32_t* v, const int32_t* map,
+                                const void* w, int wtype, int64_t* row_ptr, int32_t* col, void* w_out,
+                                int64_t* nnz_out, int64_t* selfloops_out, int64_t* dups_out, void* stream) {
   if (n < 1 || n >= INT32_MAX) return fail(FJ_E_INVALID_ARG, "n must be in [1, 2^31-2]");
   if (m_in < 0 || m_in >= INT32_MAX) return fail(FJ_E_INVALID_ARG, "m_in must be in [0, 2^31-2]");
   if (!row_ptr || !nnz_out || (m_in > 0 && (!u || !v || !col))) return fail(FJ_E_INVALID_ARG, "null argument");
@@ -136,7 +139,7 @@ extern "C" fj_status fj_csr_from_edges(int64_t n, int64_t m_in, const int32_t* u
   FJ_TRY(fl.alloc(1, st));
   FJ_CK(cudaMemsetAsync(fl.p, 0, sizeof(BuildFlags), st));
   phase_tick("csr: alloc", st);
-  k_mirror_keys<<<grid_for(m, sms), 256, 0, st>>>(m, n, u, v, b, sent, ka.p, wbytes ? va.p : nullptr, fl.p);
+  k_mirror_keys<<<grid_for(m, sms), 256, 0, st>>>(m, n, u, v, map, b, sent, ka.p, wbytes ? va.p : nullptr, fl.p);
   FJ_CK_LAUNCH();
   phase_tick("csr: mirror keys", st);
   cub::DoubleBuffer<uint64_t> dk(ka.p, kb.p);
@@ -187,6 +190,22 @@ extern "C" fj_status fj_csr_from_edges(int64_t n, int64_t m_in, const int32_t* u
   if (selfloops_out) *selfloops_out = (int64_t)hf.selfloops;
   if (dups_out) *dups_out = m - (int64_t)hf.selfloops - nnz / 2;
   return FJ_OK;
+}
+
+extern "C" fj_status fj_csr_from_edges(int64_t n, int64_t m_in, const int32_t* u, const int32_t* v, const void* w,
+                                       int wtype, int64_t* row_ptr, int32_t* col, void* w_out, int64_t* nnz_out,
+                                       int64_t* selfloops_out, int64_t* dups_out, void* stream) {
+  return csr_from_edges(n, m_in, u, v, nullptr, w, wtype, row_ptr, col, w_out, nnz_out, selfloops_out, dups_out,
+                        stream);
+}
+
+extern "C" fj_status fj_csr_from_edges_mapped(int64_t n, int64_t m_in, const int32_t* u, const int32_t* v,
+                                              const int32_t* old2new, const void* w, int wtype, int64_t* row_ptr,
+                                              int32_t* col, void* w_out, int64_t* nnz_out, int64_t* selfloops_out,
+                                              int64_t* dups_out, void* stream) {
+  if (!old2new) return fail(FJ_E_INVALID_ARG, "old2new is NULL");
+  return csr_from_edges(n, m_in, u, v, old2new, w, wtype, row_ptr, col, w_out, nnz_out, selfloops_out, dups_out,
+                        stream);
 }
 
 // ---------------------------------------------------------------- a1 for a row block (row a8)

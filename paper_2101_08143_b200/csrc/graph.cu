@@ -299,7 +299,7 @@ void fj_default_solve_opts(fj_solve_opts* o) {
   o->max_iter = 10000;
   o->max_restarts = 3;
   o->use_cuda_graph = 1;
-  o->reserved = 0;
+  o->vertex_order = FJ_ORDER_NATURAL;
 }
 
 fj_status fj_graph_create(int64_t n, int64_t nnz, const int64_t* row_ptr, const int32_t* col, const void* w,

@@ -372,9 +372,11 @@ fj_status fj_quantities(const fj_graph* gc, int k, const double* s, const double
 
 // Algorithm 1 (fj_approxim).  z_host (host-buffer entry point only): after the batched solve the
 // D2H of z runs on a side stream while the fused quantities pass runs on `stream`.
+// z_host_perm (relabelled graph): z_host receives z[z_host_perm[i]] (staged in z_perm_buf).
 static fj_status approxim_impl(const fj_graph* gc, int k, const double* s, double* z_user, const fj_solve_opts* opts,
                                fj_quantities_t* qout, fj_solve_report* rep, void* stream, double* z_host,
-                               bool* z_host_done) {
+                               bool* z_host_done, const int32_t* z_host_perm = nullptr,
+                               double* z_perm_buf = nullptr) {
   if (z_host_done) *z_host_done = false;
   if (!gc || !s || !qout) return fail(FJ_E_INVALID_ARG, "null argument");
   if (k < 1 || k > MAXK) return fail(FJ_E_INVALID_ARG, "k must be in [1, 64]");
@@ -442,7 +444,12 @@ static fj_status approxim_impl(const fj_graph* gc, int k, const double* s, doubl
         if (!side.s) FJ_TRY(side.init());
         FJ_CK(cudaEventRecord(side.ev_in, st));
         FJ_CK(cudaStreamWaitEvent(side.s, side.ev_in, 0));
-        FJ_CK(cudaMemcpyAsync(z_host, z, sizeof(double) * g->n * k, cudaMemcpyDeviceToHost, side.s));
+        const double* zsrc = z;
+        if (z_host_perm) {   // back to the input labels first (fj_permute_rows, on the side stream)
+          FJ_TRY(fj_permute_rows(g->n, k, z_host_perm, z, z_perm_buf, side.s));
+          zsrc = z_perm_buf;
+        }
+        FJ_CK(cudaMemcpyAsync(z_host, zsrc, sizeof(double) * g->n * k, cudaMemcpyDeviceToHost, side.s));
         FJ_CK(cudaEventRecord(side.ev_out, side.s));
         d2h_issued = true;
       }
@@ -589,6 +596,17 @@ fj_status fj_approxim(const fj_graph* gc, int k, const double* s, double* z_user
   return approxim_impl(gc, k, s, z_user, opts, qout, rep, stream, nullptr, nullptr);
 }
 
+// FJ_ORDER_AUTO: relabelling packs several hot x_j into one 32-byte L2 sector, so
+// it pays only for rows narrower than a sector (k = 1: 8 bytes, k = 2: 16) whose gathered vector
+// does not fit the L2 anyway.
+static bool relabel_pays(int64_t n, int k) {
+  if (k > 2) return false;
+  int dev = 0, l2 = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+  return (double)n * 8.0 * k > (double)(l2 > 0 ? l2 : (126 << 20));
+}
+
 fj_status fj_approxim_host(int64_t n, int64_t m_in, const int32_t* u_h, const int32_t* v_h, const void* w_h,
                            int wtype, int k, const double* s_h, double* z_h, const fj_solve_opts* opts,
                            fj_quantities_t* q_h, fj_solve_report* rep, void* stream) {
@@ -601,8 +619,14 @@ fj_status fj_approxim_host(int64_t n, int64_t m_in, const int32_t* u_h, const in
   DevBuf<int32_t> du, dv, dcol;
   DevBuf<uint8_t> dw, dwo;
   DevBuf<int64_t> drp;
-  DevBuf<double> ds, dz;
+  DevBuf<double> ds, dz, ds2;
+  DevBuf<int32_t> n2o, o2n;
+  if (opts && (opts->vertex_order < FJ_ORDER_NATURAL || opts->vertex_order > FJ_ORDER_AUTO))
+    return fail(FJ_E_INVALID_ARG, "bad vertex_order");
+  bool relabel = opts && opts->vertex_order == FJ_ORDER_DEGREE;
+  if (opts && opts->vertex_order == FJ_ORDER_AUTO) relabel = relabel_pays(n, k);
   FJ_TRY(du.alloc(m_in, st)); FJ_TRY(dv.alloc(m_in, st));
+  if (relabel) { FJ_TRY(n2o.alloc(n, st)); FJ_TRY(o2n.alloc(n, st)); FJ_TRY(ds2.alloc(n * (int64_t)k, st)); }
   FJ_TRY(ds.alloc(n * (int64_t)k, st)); FJ_TRY(dz.alloc(n * (int64_t)k, st));
   FJ_TRY(drp.alloc(n + 1, st)); FJ_TRY(dcol.alloc(2 * m_in, st));
   if (wbytes) { FJ_TRY(dw.alloc(m_in * wbytes, st)); FJ_TRY(dwo.alloc(2 * m_in * wbytes, st)); }
@@ -623,13 +647,40 @@ fj_status fj_approxim_host(int64_t n, int64_t m_in, const int32_t* u_h, const in
   FJ_TRY(fj_csr_from_edges(n, m_in, du.p, dv.p, wbytes ? dw.p : nullptr, wtype, drp.p, dcol.p,
                            wbytes ? dwo.p : nullptr, &nnz, nullptr, nullptr, stream));
   du.release(); dv.release(); dw.release();
+  DevBuf<int64_t> drp2;
+  DevBuf<int32_t> dcol2;
+  DevBuf<uint8_t> dwo2;
+  const int64_t* rp_g = drp.p;
+  const int32_t* col_g = dcol.p;
+  const void* w_g = wbytes ? dwo.p : nullptr;
+  if (relabel) {   // relabel the built CSR by descending degree (P A P^T)
+    FJ_TRY(drp2.alloc(n + 1, st)); FJ_TRY(dcol2.alloc(nnz, st));
+    if (wbytes) FJ_TRY(dwo2.alloc(nnz * wbytes, st));
+    FJ_TRY(fj_csr_degree_order(n, drp.p, n2o.p, o2n.p, stream));
+    FJ_TRY(fj_csr_permute(n, nnz, drp.p, dcol.p, w_g, wtype, n2o.p, o2n.p, drp2.p, dcol2.p,
+                          wbytes ? dwo2.p : nullptr, stream));
+    drp.release(); dcol.release(); dwo.release();
+    rp_g = drp2.p; col_g = dcol2.p; w_g = wbytes ? dwo2.p : nullptr;
+  }
   fj_graph* g = nullptr;
-  FJ_TRY(fj_graph_create(n, nnz, drp.p, dcol.p, wbytes ? dwo.p : nullptr, wtype, 0, stream, &g));
+  FJ_TRY(fj_graph_create(n, nnz, rp_g, col_g, w_g, wtype, 0, stream, &g));
   FJ_CK(cudaStreamWaitEvent(st, side.ev_out, 0));
+  const double* s_in = ds.p;
+  if (relabel) {   // s into the new labels; ds then serves as the old-label staging buffer of z
+    FJ_TRY(fj_permute_rows(n, k, n2o.p, ds.p, ds2.p, stream));
+    s_in = ds2.p;
+  }
   bool z_done = false;
-  fj_status s = approxim_impl(g, k, ds.p, dz.p, opts, q_h, rep, stream, z_h, &z_done);
+  fj_status s = approxim_impl(g, k, s_in, dz.p, opts, q_h, rep, stream, z_h, &z_done, relabel ? o2n.p : nullptr,
+                              relabel ? ds.p : nullptr);
   if ((s == FJ_OK || s == FJ_E_NO_CONVERGENCE) && z_h && !z_done) {
-    cudaError_t e = cudaMemcpyAsync(z_h, dz.p, sizeof(double) * n * k, cudaMemcpyDeviceToHost, st);
+    const double* zsrc = dz.p;
+    if (relabel) {
+      fj_status sp = fj_permute_rows(n, k, o2n.p, dz.p, ds.p, stream);
+      if (sp != FJ_OK) { fj_graph_destroy(g); return sp; }
+      zsrc = ds.p;
+    }
+    cudaError_t e = cudaMemcpyAsync(z_h, zsrc, sizeof(double) * n * k, cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) s = cuda_fail(e, "z readback", __FILE__, __LINE__);
   }
