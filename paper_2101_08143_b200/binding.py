@@ -92,12 +92,17 @@ def load_library(path: str = SO):
     L.fj_default_solve_opts.restype = None
     L.fj_csr_from_edges.argtypes = [_i64, _i64, _vp, _vp, _vp, ctypes.c_int, _vp, _vp, _vp, P(_i64), P(_i64),
                                     P(_i64), _vp]
-    L.fj_csr_from_edges_mapped.argtypes = [_i64, _i64, _vp, _vp, _vp, _vp, ctypes.c_int, _vp, _vp, _vp, P(_i64),
-                                           P(_i64), P(_i64), _vp]
-    L.fj_degree_order.argtypes = [_i64, _i64, _vp, _vp, _vp, _vp, _vp]
-    L.fj_permute_rows.argtypes = [_i64, ctypes.c_int, _vp, _vp, _vp, _vp]
-    L.fj_csr_degree_order.argtypes = [_i64, _vp, _vp, _vp, _vp]
-    L.fj_csr_permute.argtypes = [_i64, _i64, _vp, _vp, _vp, ctypes.c_int, _vp, _vp, _vp, _vp, _vp, _vp]
+    relabel_sigs = {   # DESIGN.md §6.7 (looked up leniently so older A/B builds still load)
+        "fj_csr_from_edges_mapped": [_i64, _i64, _vp, _vp, _vp, _vp, ctypes.c_int, _vp, _vp, _vp, P(_i64), P(_i64),
+                                     P(_i64), _vp],
+        "fj_degree_order": [_i64, _i64, _vp, _vp, _vp, _vp, _vp],
+        "fj_permute_rows": [_i64, ctypes.c_int, _vp, _vp, _vp, _vp],
+        "fj_csr_degree_order": [_i64, _vp, _vp, _vp, _vp],
+        "fj_csr_permute": [_i64, _i64, _vp, _vp, _vp, ctypes.c_int, _vp, _vp, _vp, _vp, _vp, _vp],
+    }
+    for name, sig in relabel_sigs.items():
+        if hasattr(L, name):
+            getattr(L, name).argtypes = sig
     L.fj_graph_create.argtypes = [_i64, _i64, _vp, _vp, _vp, ctypes.c_int, ctypes.c_int, _vp, P(_vp)]
     L.fj_graph_info.argtypes = [_vp, P(GraphInfo)]
     L.fj_graph_degrees.argtypes = [_vp, _vp, _vp]

@@ -17,6 +17,53 @@ void free_quant_ws(fj_graph*) {}
 
 // ---------------------------------------------------------------- a3: statistics of column c
 constexpr int STPB = 256;
+
+// Last block of a stats kernel: K columns of (sum, sum of squares, min, max) quads at
+// part[q * 4K + 4c + j] for the grid's blocks q.  Every thread folds the blocks q = t, t + STPB, ...
+// (fixed order), then fixed-order block sums / min-max trees: deterministic, and STPB loads in
+// flight instead of one thread walking all blocks (that serial walk cost ~0.25 ms per call).
+template <int K>
+__device__ __forceinline__ void stats_last_block(const double* part, int kk, unsigned nblocks, double* out,
+                                                 const int* nonfinite, double* s_red, double (*s_mm)[STPB / 32]) {
+  double v[2 * K], mn[K], mx[K];
+#pragma unroll
+  for (int c = 0; c < K; ++c) { v[2 * c] = 0.0; v[2 * c + 1] = 0.0; mn[c] = INFINITY; mx[c] = -INFINITY; }
+  for (unsigned q = threadIdx.x; q < nblocks; q += STPB) {
+#pragma unroll
+    for (int c = 0; c < K; ++c) {
+      const double* pq = part + (int64_t)q * 4 * K + 4 * c;
+      v[2 * c] += __ldcg(pq + 0);
+      v[2 * c + 1] += __ldcg(pq + 1);
+      mn[c] = fmin(mn[c], __ldcg(pq + 2));
+      mx[c] = fmax(mx[c], __ldcg(pq + 3));
+    }
+  }
+  block_sum<2 * K, STPB>(v, s_red);
+#pragma unroll
+  for (int c = 0; c < K; ++c) {
+    for (int o = 16; o > 0; o >>= 1) {
+      mn[c] = fmin(mn[c], __shfl_xor_sync(0xffffffffu, mn[c], o));
+      mx[c] = fmax(mx[c], __shfl_xor_sync(0xffffffffu, mx[c], o));
+    }
+  }
+  __syncthreads();   // s_mm is reused
+  if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+    for (int c = 0; c < K; ++c) { s_mm[2 * c][threadIdx.x >> 5] = mn[c]; s_mm[2 * c + 1][threadIdx.x >> 5] = mx[c]; }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const bool bad = *(volatile const int*)nonfinite != 0;
+    for (int c = 0; c < kk && c < K; ++c) {
+      for (int w = 1; w < STPB / 32; ++w) { mn[c] = fmin(mn[c], s_mm[2 * c][w]); mx[c] = fmax(mx[c], s_mm[2 * c + 1][w]); }
+      out[4 * c + 0] = bad ? NAN : v[2 * c];   // NaN marks a non-finite input (propagates over ranks)
+      out[4 * c + 1] = v[2 * c + 1];
+      out[4 * c + 2] = mn[c];
+      out[4 * c + 3] = mx[c];
+    }
+  }
+}
+
 __global__ void __launch_bounds__(STPB) k_stats(int64_t n, const double* __restrict__ s, int64_t ld, int64_t c,
                                                 double* part /*[grid][4]*/, unsigned int* ticket, double* out,
                                                 int* nonfinite) {
@@ -53,18 +100,11 @@ __global__ void __launch_bounds__(STPB) k_stats(int64_t n, const double* __restr
     s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
   }
   __syncthreads();
-  if (s_last && threadIdx.x == 0) {
+  if (s_last) {
     __threadfence();
-    double a = 0.0, b = 0.0, lo = INFINITY, hi = -INFINITY;
-    for (unsigned q = 0; q < gridDim.x; ++q) {   // fixed order
-      a += __ldcg(part + q * 4 + 0);
-      b += __ldcg(part + q * 4 + 1);
-      lo = fmin(lo, __ldcg(part + q * 4 + 2));
-      hi = fmax(hi, __ldcg(part + q * 4 + 3));
-    }
-    out[0] = *(volatile int*)nonfinite ? NAN : a;   // NaN marks a non-finite input (propagates over ranks)
-    out[1] = b; out[2] = lo; out[3] = hi;
-    *ticket = 0u;
+    __shared__ double s_mm2[2][STPB / 32];
+    stats_last_block<1>(part, 1, gridDim.x, out, nonfinite, s_red, s_mm2);
+    if (threadIdx.x == 0) *ticket = 0u;
   }
 }
 
@@ -118,20 +158,10 @@ __global__ void __launch_bounds__(STPB) k_stats_k(int64_t n, int k, const double
     s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
   }
   __syncthreads();
-  if (s_last && threadIdx.x == 0) {
+  if (s_last) {
     __threadfence();
-    for (int c = 0; c < k; ++c) {
-      double a = 0.0, b = 0.0, lo = INFINITY, hi = -INFINITY;
-      for (unsigned q = 0; q < gridDim.x; ++q) {   // fixed order
-        a += __ldcg(part + q * 4 * K + 4 * c + 0);
-        b += __ldcg(part + q * 4 * K + 4 * c + 1);
-        lo = fmin(lo, __ldcg(part + q * 4 * K + 4 * c + 2));
-        hi = fmax(hi, __ldcg(part + q * 4 * K + 4 * c + 3));
-      }
-      out[4 * c + 0] = *(volatile int*)nonfinite ? NAN : a;
-      out[4 * c + 1] = b; out[4 * c + 2] = lo; out[4 * c + 3] = hi;
-    }
-    *ticket = 0u;
+    stats_last_block<K>(part, k, gridDim.x, out, nonfinite, s_red, s_mm);
+    if (threadIdx.x == 0) *ticket = 0u;
   }
 }
 
@@ -183,16 +213,28 @@ __global__ void __launch_bounds__(STPB) k_stats_wide(int64_t n, int k, const dou
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  if (threadIdx.x < 64 && threadIdx.x < k) {
-    const int c = threadIdx.x;
+  {   // thread group g = t / 64 folds blocks q = g, g + 4, ... for column c = t % 64; groups in order
+    constexpr int NG = STPB / 64;
+    const int c = threadIdx.x & 63, grp = threadIdx.x >> 6;
     double a = 0.0, b = 0.0, lo = INFINITY, hi = -INFINITY;
-    for (unsigned q = 0; q < gridDim.x; ++q) {   // blocks in order
-      const double* pb = part + (int64_t)q * 256;
-      a += __ldcg(pb + c); b += __ldcg(pb + 64 + c);
-      lo = fmin(lo, __ldcg(pb + 128 + c)); hi = fmax(hi, __ldcg(pb + 192 + c));
+    if (c < k) {
+      for (unsigned q = grp; q < gridDim.x; q += NG) {
+        const double* pb = part + (int64_t)q * 256;
+        a += __ldcg(pb + c); b += __ldcg(pb + 64 + c);
+        lo = fmin(lo, __ldcg(pb + 128 + c)); hi = fmax(hi, __ldcg(pb + 192 + c));
+      }
     }
-    out[4 * c + 0] = *(volatile int*)nonfinite ? NAN : a;
-    out[4 * c + 1] = b; out[4 * c + 2] = lo; out[4 * c + 3] = hi;
+    __syncthreads();   // s_v reused: [group][quantity][column]
+    s_v[grp][0][c] = a; s_v[grp][1][c] = b; s_v[grp][2][c] = lo; s_v[grp][3][c] = hi;
+    __syncthreads();
+    if (threadIdx.x < 64 && threadIdx.x < k) {
+      a = 0.0; b = 0.0; lo = INFINITY; hi = -INFINITY;
+      for (int g2 = 0; g2 < NG; ++g2) {
+        a += s_v[g2][0][c]; b += s_v[g2][1][c]; lo = fmin(lo, s_v[g2][2][c]); hi = fmax(hi, s_v[g2][3][c]);
+      }
+      out[4 * c + 0] = *(volatile int*)nonfinite ? NAN : a;
+      out[4 * c + 1] = b; out[4 * c + 2] = lo; out[4 * c + 3] = hi;
+    }
   }
   if (threadIdx.x == 0) *ticket = 0u;
 }

@@ -25,6 +25,36 @@ namespace fj {
 #endif
 constexpr int BTPB = 128;              // 4 warps
 constexpr int BWPB = BTPB / 32;
+
+// Deterministic grid tail of the k > 4 kernels (last block, all BTPB threads): the total of column
+// c = t % 64 over nb block partials and nl long-row partials (entries `stride` doubles apart).  Thread
+// group t / 64 folds entries g*8.., 8 independent accumulators (8 loads in flight), groups summed in
+// order: a fixed order, and ~16x less tail latency than one thread per column walking every entry
+// (C4: 1184 blocks + 12 140 long rows per launch).
+__device__ __forceinline__ double tail_sum(const double* bp, int64_t nb, const double* lp, int64_t nl,
+                                           int64_t stride, double* s_tail /*[BTPB]*/) {
+  constexpr int NG = BTPB / MAXK;
+  const int c = threadIdx.x % MAXK, grp = threadIdx.x / MAXK;
+  double acc[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) acc[u] = 0.0;
+  for (int64_t b0 = (int64_t)grp * 8; b0 < nb; b0 += NG * 8) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (b0 + u < nb) acc[u] += __ldcg(bp + (b0 + u) * stride);
+  }
+  for (int64_t l0 = (int64_t)grp * 8; l0 < nl; l0 += NG * 8) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (l0 + u < nl) acc[u] += __ldcg(lp + (l0 + u) * stride);
+  }
+  s_tail[threadIdx.x] = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+  __syncthreads();
+  double tot = 0.0;
+  for (int g2 = 0; g2 < NG; ++g2) tot += s_tail[g2 * MAXK + c];
+  __syncthreads();
+  return tot;
+}
 // batched schedule: short rows in tiles of <= ~224 nonzeros, W rows up to 1024, chunks of 1024
 constexpr SchedParams kSchedBatch{64, 160, 8, 1024};
 
@@ -229,11 +259,11 @@ __global__ void __launch_bounds__(BTPB, FJ_SPMM_MIN_BLOCKS) spmm_kernel(const Ti
   __syncthreads();
   if (!s_last) return;
   __threadfence();
+  __shared__ double s_tail[BTPB];
+  const double t = tail_sum(a.block_part + threadIdx.x % MAXK, gridDim.x, a.long_part + threadIdx.x % MAXK,
+                            sc.n_long, MAXK, s_tail);
   if (threadIdx.x < MAXK) {
     const int c = threadIdx.x;
-    double t = 0.0;
-    for (unsigned b = 0; b < gridDim.x; ++b) t += __ldcg(a.block_part + (int64_t)b * MAXK + c);
-    for (int64_t l = 0; l < sc.n_long; ++l) t += __ldcg(a.long_part + l * MAXK + c);
     if (c < k) {
       BatchScalars* bs = a.bs;
       if (MODE == BM_PCG) {
@@ -279,12 +309,27 @@ __device__ __forceinline__ bool b_elem_reduce(double (&v0)[NP], double (&v1)[NP]
   __syncthreads();
   if (!s_last) return false;
   __threadfence();
-  if (threadIdx.x < MAXK) {
+  {   // thread group g = t / 64 folds blocks b = g, g + 4, ... for column t % 64; groups summed in order
+    constexpr int NG = ETB / MAXK;
+    const int c = threadIdx.x & (MAXK - 1), grp = threadIdx.x / MAXK;
+    double t[NP];
 #pragma unroll
-    for (int j = 0; j < NP; ++j) {
-      double t = 0.0;
-      for (unsigned b = 0; b < gridDim.x; ++b) t += __ldcg(part + ((int64_t)b * NP + j) * MAXK + threadIdx.x);
-      tot[j] = t;
+    for (int j = 0; j < NP; ++j) t[j] = 0.0;
+    for (unsigned b = grp; b < gridDim.x; b += NG) {
+#pragma unroll
+      for (int j = 0; j < NP; ++j) t[j] += __ldcg(part + ((int64_t)b * NP + j) * MAXK + c);
+    }
+    __syncthreads();   // s_red reused: [group][j][column]
+#pragma unroll
+    for (int j = 0; j < NP; ++j) s_red[grp][j][c] = t[j];
+    __syncthreads();
+    if (threadIdx.x < MAXK) {
+#pragma unroll
+      for (int j = 0; j < NP; ++j) {
+        double u = 0.0;
+        for (int g2 = 0; g2 < NG; ++g2) u += s_red[g2][j][c];
+        tot[j] = u;
+      }
     }
   }
   return true;
@@ -875,14 +920,12 @@ __global__ void __launch_bounds__(BTPB, FJ_QB_MIN_BLOCKS) quant_batch_kernel(con
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  if (threadIdx.x < MAXK) {
-    const int c = threadIdx.x;
-    for (int j = 0; j < QNP; ++j) {
-      double t = 0.0;
-      for (unsigned b = 0; b < gridDim.x; ++b) t += __ldcg(a.block_part + ((int64_t)b * QNP + j) * MAXK + c);
-      for (int64_t l = 0; l < sc.n_long; ++l) t += __ldcg(a.long_part + (l * QNP + j) * MAXK + c);
-      a.out[j * MAXK + c] = t;
-    }
+  __shared__ double s_tail[BTPB];
+  for (int j = 0; j < QNP; ++j) {
+    const int c = threadIdx.x % MAXK;
+    const double t = tail_sum(a.block_part + (int64_t)j * MAXK + c, gridDim.x, a.long_part + (int64_t)j * MAXK + c,
+                              sc.n_long, (int64_t)QNP * MAXK, s_tail);
+    if (threadIdx.x < MAXK) a.out[j * MAXK + c] = t;
   }
   if (threadIdx.x == 0) *a.grid_ticket = 0u;
 }
