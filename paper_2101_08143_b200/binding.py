@@ -376,14 +376,17 @@ class Graph:
     def _in(self, x, stream=None):      # input labels -> the handle's labels
         return x if self.new2old is None else permute_rows(x, self.new2old, stream)
 
-    def _out(self, x, stream=None, out=None):   # the handle's labels -> input labels
+    def _out(self, x, stream=None, out=None):   # the handle's labels -> input labels (into `out` if given)
         if self.old2new is None:
             return x
-        y = permute_rows(x, self.old2new, stream)
-        if out is not None:
-            out.copy_(y)
-            return out
-        return y
+        if out is None:
+            return permute_rows(x, self.old2new, stream)
+        _need_cuda(out)
+        if out.shape != x.shape or out.dtype != x.dtype:
+            raise ValueError("z must match s in shape and dtype")
+        _check(lib().fj_permute_rows(self.n, _cols(x, self.n), _ptr(self.old2new), _ptr(x), _ptr(out),
+                                     _stream(stream)))
+        return out
 
     @property
     def handle(self):
@@ -431,8 +434,8 @@ class Graph:
         k = _cols(s, self.n)
         z_user = z
         si = self._in(s, stream)
-        if self.new2old is not None:   # z (input labels, warm start) in, solution out
-            z = torch.empty_like(s) if z_user is None else self._in(z_user, stream)
+        if self.new2old is not None:   # solve in the handle's labels; z_user receives the input labels
+            z = torch.empty_like(s)
         else:
             z = torch.empty_like(s) if z is None else z
         rep = SolveReport()

@@ -203,3 +203,21 @@ def test_approxim_host_vertex_order(fj, name, k):
         o = fj.SolveOpts.make()
         o.vertex_order = 5
         fj.approxim_host(wl.n, wl.u, wl.v, wl.w, S, opts=o)
+
+
+def test_relabelled_user_buffers(fj):
+    """Caller-owned z buffers: approxim and solve write z (input labels) into them."""
+    import torch
+    wl = synth.make_config("c1", kinds=["uniform", "exponential", "powerlaw"])
+    G = fj.Graph.from_edges(wl.n, dev(wl.u), dev(wl.v), order="degree")
+    S = dev(wl.S)
+    zbuf = torch.full_like(S, 7.0)
+    z, q, _ = G.approxim(S, z=zbuf)
+    assert z.data_ptr() == zbuf.data_ptr()
+    g = O.canonical_csr(wl.n, wl.u, wl.v)
+    for c in range(3):
+        assert np.max(np.abs(host(zbuf)[:, c] - O.solve(g, wl.S[:, c]))) < 1e-8
+    zw = torch.zeros_like(S)
+    z2, rep = G.solve(S, z=zw)
+    assert z2.data_ptr() == zw.data_ptr()
+    assert np.max(np.abs(host(zw) - host(zbuf))) < 1e-9
