@@ -149,23 +149,8 @@ fj_status fj_csr_from_edges(int64_t n, int64_t m_in, const int32_t* u_dev, const
  * x_j most gathered by the PCG product into few L2 sectors.  The relabelled graph is isomorphic:
  * its Laplacian is P L P^T, its solution of (I + L) z = s is P z for the input P s, and the
  * quantities of P:L163-228 (sums over vertices and edges) are unchanged up to rounding order.
- *
- * fj_degree_order: new2old_dev[n] (device int32, written) lists the vertices by descending number
- * of raw endpoint occurrences (non-self-loop edges of the raw list, duplicates counted; ties by
- * ascending id); old2new_dev[n] is its inverse.  Deterministic.  FJ_E_INVALID_ARG for n < 1,
- * m_in < 0, NULL pointers or an endpoint outside [0, n).  Synchronises `stream`. */
-fj_status fj_degree_order(int64_t n, int64_t m_in, const int32_t* u_dev, const int32_t* v_dev,
-                          int32_t* new2old_dev, int32_t* old2new_dev, void* stream);
-/* fj_csr_from_edges of the relabelled edge list (old2new_dev[u_e], old2new_dev[v_e]): the same a1
- * rules (self-loops dropped, keep-first duplicates in input order, columns ascending) applied in
- * the new labels; old2new_dev must be a permutation of [0, n) (not checked). */
-fj_status fj_csr_from_edges_mapped(int64_t n, int64_t m_in, const int32_t* u_dev, const int32_t* v_dev,
-                                   const int32_t* old2new_dev, const void* w_dev, int wtype,
-                                   int64_t* row_ptr_dev, int32_t* col_dev, void* w_out_dev, int64_t* nnz_out,
-                                   int64_t* selfloops_out, int64_t* dups_out, void* stream);
-/* The same relabelling applied to a built canonical CSR (the path the library's own callers take:
- * it keeps a1's fast sort in the input labels).  fj_csr_degree_order: new2old by descending row
- * length = degree (ties by ascending id), old2new its inverse; asynchronous.  fj_csr_permute: the
+ * The relabelling is applied to a built canonical CSR (it keeps a1's sort in the input labels).
+ * fj_csr_degree_order: new2old by descending row length = degree (ties by ascending id), old2new its inverse; asynchronous.  fj_csr_permute: the
  * CSR of P A P^T -- row i' is old row new2old[i'] with every column c replaced by old2new[c], in
  * the old row's order (ascending OLD labels, so weighted degree sums keep a1's order and stay
  * bit-exact), weights moved with their entries.  row_ptr_out [n+1], col_out / w_out [nnz]
@@ -247,11 +232,13 @@ fj_status fj_approxim(const fj_graph* g, int k, const double* s_dev, double* z_d
                       void* stream);
 
 /* End-to-end convenience from HOST buffers: copies the raw edge list (u_host, v_host, w_host)
- * and s_host [n][k] to the device, builds the CSR (a1; relabelled by fj_degree_order when
- * opts->vertex_order == FJ_ORDER_DEGREE, s and z mapped with fj_permute_rows), the handle (a2),
- * runs fj_approxim, and copies z (input labels) back to z_host (may be NULL) and the quantities
- * to q_host.  Pinned host buffers make the copies asynchronous.  Device memory is released
- * before return. */
+ * and s_host [n][k] to the device, builds the CSR (a1), then -- when opts->vertex_order is
+ * FJ_ORDER_DEGREE, or FJ_ORDER_AUTO and the rule of fj_solve_opts.vertex_order holds -- relabels
+ * it with fj_csr_degree_order + fj_csr_permute (the permuted CSR's columns are NOT ascending; the
+ * handle is created without validation) and maps s in / z out with fj_permute_rows; creates the
+ * handle (a2), runs fj_approxim, and copies z (input labels) back to z_host (may be NULL) and the
+ * quantities to q_host.  Pinned host buffers make the copies asynchronous.  Device memory is
+ * released before return, also on every error path. */
 fj_status fj_approxim_host(int64_t n, int64_t m_in, const int32_t* u_host, const int32_t* v_host,
                            const void* w_host, int wtype, int k, const double* s_host,
                            double* z_host, const fj_solve_opts* opts, fj_quantities_t* q_host,

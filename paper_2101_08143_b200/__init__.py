@@ -7,7 +7,7 @@ is no CPU fallback: if libfj.so or a CUDA device is missing, calls raise.
 from .binding import (  # noqa: F401
     FJError, Graph, SolveOpts, approxim_host, csr_from_edges, lib, load_library, FJ_W_UNIT, FJ_W_U8,
     FJ_W_F32, FJ_W_F64, FJ_OP_L, FJ_OP_IPL, Comm, DistGraph, partition_rows, csr_rows_from_edges, dist_ghosts,
-    probe_gather, alg1_delta, opinions_generate, connected_components, lcc, degree_order, permute_rows,
+    probe_gather, alg1_delta, opinions_generate, connected_components, lcc, permute_rows,
     csr_degree_order, csr_permute,
 )
 

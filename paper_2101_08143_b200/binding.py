@@ -93,9 +93,6 @@ def load_library(path: str = SO):
     L.fj_csr_from_edges.argtypes = [_i64, _i64, _vp, _vp, _vp, ctypes.c_int, _vp, _vp, _vp, P(_i64), P(_i64),
                                     P(_i64), _vp]
     relabel_sigs = {   # DESIGN.md §6.7 (looked up leniently so older A/B builds still load)
-        "fj_csr_from_edges_mapped": [_i64, _i64, _vp, _vp, _vp, _vp, ctypes.c_int, _vp, _vp, _vp, P(_i64), P(_i64),
-                                     P(_i64), _vp],
-        "fj_degree_order": [_i64, _i64, _vp, _vp, _vp, _vp, _vp],
         "fj_permute_rows": [_i64, ctypes.c_int, _vp, _vp, _vp, _vp],
         "fj_csr_degree_order": [_i64, _vp, _vp, _vp, _vp],
         "fj_csr_permute": [_i64, _i64, _vp, _vp, _vp, ctypes.c_int, _vp, _vp, _vp, _vp, _vp, _vp],
@@ -228,6 +225,22 @@ def _ptr(t):
     return None if t is None else ctypes.c_void_p(t.data_ptr())
 
 
+def _on(stream=None):
+    """Allocate temporaries on the stream the library works on: torch's caching allocator then
+    reuses their memory only after that stream's pending work (a temporary allocated on
+    the current stream and freed on return could be handed out while `stream` still reads it)."""
+    import contextlib
+    import torch
+    return contextlib.nullcontext() if stream is None else torch.cuda.stream(stream)
+
+
+def _check_out(z, like, what="z"):
+    """A caller-supplied output must be a contiguous CUDA tensor shaped and typed like `like`."""
+    _need_cuda(z)
+    if z.shape != like.shape or z.dtype != like.dtype or z.device != like.device:
+        raise ValueError(f"{what} must match s in shape, dtype and device")
+
+
 def _wtype(w):
     if w is None:
         return FJ_W_UNIT
@@ -241,18 +254,6 @@ def _need_cuda(*ts):
             raise ValueError("device tensors required (torch CUDA tensors)")
         if t is not None and not t.is_contiguous():
             raise ValueError("contiguous tensors required")
-
-
-def degree_order(n: int, u, v, stream=None):
-    """fj_degree_order: (new2old, old2new) int32 device permutations, vertices by descending raw
-    endpoint count (ties by id) -- the locality relabelling of DESIGN.md §6.7."""
-    import torch
-    _need_cuda(u, v)
-    new2old = torch.empty(n, dtype=torch.int32, device=u.device)
-    old2new = torch.empty(n, dtype=torch.int32, device=u.device)
-    _check(lib().fj_degree_order(n, int(u.numel()), _ptr(u), _ptr(v), _ptr(new2old), _ptr(old2new),
-                                 _stream(stream)))
-    return new2old, old2new
 
 
 def relabel_pays(n: int, k: int) -> bool:
@@ -296,29 +297,21 @@ def permute_rows(x, idx, stream=None):
     return out
 
 
-def csr_from_edges(n: int, u, v, w=None, stream=None, old2new=None):
+def csr_from_edges(n: int, u, v, w=None, stream=None):
     """Row a1: canonical CSR (device) from a raw device edge list.  Returns
-    (row_ptr int64 [n+1], col int32 [nnz], w_out or None, stats dict).  old2new (int32 [n] device
-    permutation): the CSR of the relabelled edge list (fj_csr_from_edges_mapped)."""
+    (row_ptr int64 [n+1], col int32 [nnz], w_out or None, stats dict)."""
     import torch
     L = lib()
-    _need_cuda(u, v, w, old2new)
+    _need_cuda(u, v, w)
     m = int(u.numel())
     dev = u.device
     row_ptr = torch.empty(n + 1, dtype=torch.int64, device=dev)
     col = torch.empty(max(2 * m, 1), dtype=torch.int32, device=dev)
     w_out = None if w is None else torch.empty(max(2 * m, 1), dtype=w.dtype, device=dev)
     nnz, loops, dups = _i64(), _i64(), _i64()
-    if old2new is None:
-        _check(L.fj_csr_from_edges(n, m, _ptr(u), _ptr(v), _ptr(w), _wtype(w), _ptr(row_ptr), _ptr(col),
-                                   _ptr(w_out), ctypes.byref(nnz), ctypes.byref(loops), ctypes.byref(dups),
-                                   _stream(stream)))
-    else:
-        if old2new.numel() != n or old2new.dtype != torch.int32:
-            raise ValueError("old2new must be an int32 [n] tensor")
-        _check(L.fj_csr_from_edges_mapped(n, m, _ptr(u), _ptr(v), _ptr(old2new), _ptr(w), _wtype(w), _ptr(row_ptr),
-                                          _ptr(col), _ptr(w_out), ctypes.byref(nnz), ctypes.byref(loops),
-                                          ctypes.byref(dups), _stream(stream)))
+    _check(L.fj_csr_from_edges(n, m, _ptr(u), _ptr(v), _ptr(w), _wtype(w), _ptr(row_ptr), _ptr(col),
+                               _ptr(w_out), ctypes.byref(nnz), ctypes.byref(loops), ctypes.byref(dups),
+                               _stream(stream)))
     k = nnz.value
     col = col[:k]
     if w_out is not None:
@@ -401,18 +394,20 @@ class Graph:
 
     def degrees(self, stream=None):
         import torch
-        d = torch.empty(self.n, dtype=torch.float64, device=self._keep[0].device)
-        _check(lib().fj_graph_degrees(self.handle, _ptr(d), _stream(stream)))
-        return self._out(d, stream)
+        with _on(stream):
+            d = torch.empty(self.n, dtype=torch.float64, device=self._keep[0].device)
+            _check(lib().fj_graph_degrees(self.handle, _ptr(d), _stream(stream)))
+            return self._out(d, stream)
 
     def apply(self, x, op: int = FJ_OP_IPL, stream=None):
         import torch
         _need_cuda(x)
         k = _cols(x, self.n)
-        xi = self._in(x, stream)
-        y = torch.empty_like(x)
-        _check(lib().fj_apply(self.handle, op, k, _ptr(xi), _ptr(y), _stream(stream)))
-        return self._out(y, stream)
+        with _on(stream):
+            xi = self._in(x, stream)
+            y = torch.empty_like(x)
+            _check(lib().fj_apply(self.handle, op, k, _ptr(xi), _ptr(y), _stream(stream)))
+            return self._out(y, stream)
 
     def time_spmv(self, k: int = 1, reps: int = 20, stream=None) -> float:
         """ms per launch of the k-column PCG product q = (I+L)p (fj_time_spmv; CUDA events)."""
@@ -429,9 +424,15 @@ class Graph:
         return out.reshape(k, 4)
 
     def solve(self, s, opts: SolveOpts | None = None, z=None, stream=None, allow_no_convergence=False):
+        with _on(stream):
+            return self._solve(s, opts, z, stream, allow_no_convergence)
+
+    def _solve(self, s, opts, z, stream, allow_no_convergence):
         import torch
         _need_cuda(s)
         k = _cols(s, self.n)
+        if z is not None:
+            _check_out(z, s)
         z_user = z
         si = self._in(s, stream)
         if self.new2old is not None:   # solve in the handle's labels; z_user receives the input labels
@@ -446,17 +447,25 @@ class Graph:
 
     def quantities(self, s, z, stream=None):
         _need_cuda(s, z)
+        _check_out(z, s)
         k = _cols(s, self.n)
         q = (Quantities * k)()
-        si, zi = self._in(s, stream), self._in(z, stream)
-        _check(lib().fj_quantities(self.handle, k, _ptr(si), _ptr(zi), q, _stream(stream)))
+        with _on(stream):
+            si, zi = self._in(s, stream), self._in(z, stream)
+            _check(lib().fj_quantities(self.handle, k, _ptr(si), _ptr(zi), q, _stream(stream)))
         return [x.to_dict() for x in q]
 
     def approxim(self, s, opts: SolveOpts | None = None, z=None, stream=None):
         """Algorithm 1 (single-solve form): returns (z, [quantities per column], report)."""
+        with _on(stream):
+            return self._approxim(s, opts, z, stream)
+
+    def _approxim(self, s, opts, z, stream):
         import torch
         _need_cuda(s)
         k = _cols(s, self.n)
+        if z is not None:
+            _check_out(z, s)
         z_user = z
         z = torch.empty_like(s) if (z is None or self.new2old is not None) else z
         q = (Quantities * k)()
@@ -475,9 +484,10 @@ class Graph:
         r = Alg1Result()
         rep = SolveReport()
         o = opts or SolveOpts.make()
-        s = self._in(s, stream)
-        _check(lib().fj_approxim_alg1(self.handle, _ptr(s), float(eps), ctypes.byref(o), ctypes.byref(r),
-                                      ctypes.byref(rep), _stream(stream)))
+        with _on(stream):
+            s = self._in(s, stream)
+            _check(lib().fj_approxim_alg1(self.handle, _ptr(s), float(eps), ctypes.byref(o), ctypes.byref(r),
+                                          ctypes.byref(rep), _stream(stream)))
         return r.to_dict(), rep.to_dict()
 
     def exact_dense(self, s, stream=None):
@@ -485,11 +495,12 @@ class Graph:
         import torch
         _need_cuda(s)
         k = _cols(s, self.n)
-        z = torch.empty_like(s)
         q = (Quantities * k)()
-        si = self._in(s, stream)
-        _check(lib().fj_exact_dense(self.handle, k, _ptr(si), _ptr(z), q, _stream(stream)))
-        return self._out(z, stream), [x.to_dict() for x in q]
+        with _on(stream):
+            z = torch.empty_like(s)
+            si = self._in(s, stream)
+            _check(lib().fj_exact_dense(self.handle, k, _ptr(si), _ptr(z), q, _stream(stream)))
+            return self._out(z, stream), [x.to_dict() for x in q]
 
     def forest_columns(self, cols, opts: SolveOpts | None = None, stream=None):
         """Columns `cols` of Omega = (I+L)^{-1} (row f4): a [n][len(cols)] fp64 CUDA tensor + report."""
@@ -500,12 +511,13 @@ class Graph:
             if len(c) and (c.min() < 0 or c.max() >= self.n):
                 raise ValueError("column index out of range")
             c = np.ascontiguousarray(self.old2new.cpu().numpy()[c], dtype=np.int32)
-        out = torch.empty((self.n, len(c)), dtype=torch.float64, device=self._keep[0].device)
         rep = SolveReport()
         o = opts or SolveOpts.make()
-        _check(lib().fj_forest_columns(self.handle, len(c), ctypes.c_void_p(c.ctypes.data), _ptr(out),
-                                       ctypes.byref(o), ctypes.byref(rep), _stream(stream)))
-        return self._out(out, stream), rep.to_dict()
+        with _on(stream):
+            out = torch.empty((self.n, len(c)), dtype=torch.float64, device=self._keep[0].device)
+            _check(lib().fj_forest_columns(self.handle, len(c), ctypes.c_void_p(c.ctypes.data), _ptr(out),
+                                           ctypes.byref(o), ctypes.byref(rep), _stream(stream)))
+            return self._out(out, stream), rep.to_dict()
 
     def close(self):
         if getattr(self, "_h", None) is not None and _lib is not None:

@@ -113,7 +113,6 @@ struct fj_graph {
   fj::QuantWs* quant_ws = nullptr;
   void* batch_ws = nullptr;       // spmm.cu BatchWs (k > 4)
   void* vec_ws = nullptr;         // spmv_vec.cu VecWs (2 <= k <= 4)
-  void* seg[5] = {};              // segments.cu SegLayout per gathered width kp (L2-sized column segments)
   void* dist = nullptr;           // dist.cu DistInfo when this is one rank's row block
 };
 

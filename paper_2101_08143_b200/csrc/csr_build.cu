@@ -23,10 +23,8 @@ struct BuildFlags {
 
 // Both orientations of every raw edge e: keys 2e = (u << b) | v and 2e+1 = (v << b) | u, payload e.
 // Self-loops (and out-of-range ids) get the sentinel key, which sorts last.
-// map (optional, fj_csr_from_edges_mapped): endpoints are relabelled old -> map[old] after the
-// range check, so the CSR is that of the relabelled graph.
 __global__ void k_mirror_keys(int64_t m, int64_t n, const int32_t* __restrict__ u, const int32_t* __restrict__ v,
-                              const int32_t* __restrict__ map, int b, uint64_t sent, uint64_t* __restrict__ keys,
+                              int b, uint64_t sent, uint64_t* __restrict__ keys,
                               int32_t* __restrict__ vals, BuildFlags* fl) {
   unsigned long long loops = 0;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
@@ -37,7 +35,6 @@ __global__ void k_mirror_keys(int64_t m, int64_t n, const int32_t* __restrict__ 
     } else if (a == c) {
       ++loops;
     } else {
-      if (map) { a = map[a]; c = map[c]; }
       k0 = ((uint64_t)a << b) | (uint64_t)c;
       k1 = ((uint64_t)c << b) | (uint64_t)a;
     }
@@ -104,7 +101,7 @@ static inline unsigned grid_for(int64_t n, int num_sms) {
 
 using namespace fj;
 
-static fj_status csr_from_edges(int64_t n, int64_t m_in, const int32_t* u, const int32_t* v, const int32_t* map,
+static fj_status csr_from_edges(int64_t n, int64_t m_in, const int32_t* u, const int32_t* v,
                                 const void* w, int wtype, int64_t* row_ptr, int32_t* col, void* w_out,
                                 int64_t* nnz_out, int64_t* selfloops_out, int64_t* dups_out, void* stream) {
   if (n < 1 || n >= INT32_MAX) return fail(FJ_E_INVALID_ARG, "n must be in [1, 2^31-2]");
@@ -139,7 +136,7 @@ static fj_status csr_from_edges(int64_t n, int64_t m_in, const int32_t* u, const
   FJ_TRY(fl.alloc(1, st));
   FJ_CK(cudaMemsetAsync(fl.p, 0, sizeof(BuildFlags), st));
   phase_tick("csr: alloc", st);
-  k_mirror_keys<<<grid_for(m, sms), 256, 0, st>>>(m, n, u, v, map, b, sent, ka.p, wbytes ? va.p : nullptr, fl.p);
+  k_mirror_keys<<<grid_for(m, sms), 256, 0, st>>>(m, n, u, v, b, sent, ka.p, wbytes ? va.p : nullptr, fl.p);
   FJ_CK_LAUNCH();
   phase_tick("csr: mirror keys", st);
   cub::DoubleBuffer<uint64_t> dk(ka.p, kb.p);
@@ -195,16 +192,7 @@ static fj_status csr_from_edges(int64_t n, int64_t m_in, const int32_t* u, const
 extern "C" fj_status fj_csr_from_edges(int64_t n, int64_t m_in, const int32_t* u, const int32_t* v, const void* w,
                                        int wtype, int64_t* row_ptr, int32_t* col, void* w_out, int64_t* nnz_out,
                                        int64_t* selfloops_out, int64_t* dups_out, void* stream) {
-  return csr_from_edges(n, m_in, u, v, nullptr, w, wtype, row_ptr, col, w_out, nnz_out, selfloops_out, dups_out,
-                        stream);
-}
-
-extern "C" fj_status fj_csr_from_edges_mapped(int64_t n, int64_t m_in, const int32_t* u, const int32_t* v,
-                                              const int32_t* old2new, const void* w, int wtype, int64_t* row_ptr,
-                                              int32_t* col, void* w_out, int64_t* nnz_out, int64_t* selfloops_out,
-                                              int64_t* dups_out, void* stream) {
-  if (!old2new) return fail(FJ_E_INVALID_ARG, "old2new is NULL");
-  return csr_from_edges(n, m_in, u, v, old2new, w, wtype, row_ptr, col, w_out, nnz_out, selfloops_out, dups_out,
+  return csr_from_edges(n, m_in, u, v, w, wtype, row_ptr, col, w_out, nnz_out, selfloops_out, dups_out,
                         stream);
 }
 

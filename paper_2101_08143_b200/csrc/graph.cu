@@ -387,7 +387,6 @@ fj_status fj_graph_destroy(fj_graph* g) {
   free_quant_ws(g);
   free_batch_ws(g);
   free_vec_ws(g);
-  free_segments(g);
   free_dist(g);
   dfree(g->deg); dfree(g->dinv);
   free_sched(g->s1);

@@ -20,7 +20,7 @@ struct PcgScalars {
 // (I+L)x_i = (1 + d_i) x_i - sum_j w_ij x_j   (P:L88 L = D - A).
 // If sc != nullptr this is the PCG search-direction product: skip when the solve is done and
 // finalise alpha = rho / p^T q on device.
-template <int WT, int SEG = SEG_WHOLE>   // SEG: role in a segmented product (segments.cu)
+template <int WT>
 struct ApplyOp {
   static constexpr int NA = 1, NP = 1;
   static constexpr bool NEEDS_XI = false;
@@ -39,14 +39,7 @@ struct ApplyOp {
   double* dot_out;                  // optional: x^T y
   int alpha_on_device = 1;          // 0 (distributed): leave alpha to the caller after the allreduce
   __device__ __forceinline__ bool skip() const { return sc && *(volatile int32_t*)&sc->done; }
-  __device__ __forceinline__ bool wants_xi() const { return SEG != SEG_MID; }
-  template <int S>
-  ApplyOp<WT, S> as_seg() const {
-    ApplyOp<WT, S> o;
-    static_assert(sizeof o == sizeof *this, "same layout");
-    memcpy(static_cast<void*>(&o), this, sizeof o);
-    return o;
-  }
+  __device__ __forceinline__ bool wants_xi() const { return true; }
   __device__ __forceinline__ double gather(int32_t j) const {
 #ifdef FJ_GATHER_NC
     return __ldg(x + (int64_t)j * ld + c);
@@ -62,18 +55,12 @@ struct ApplyOp {
   template <class P>
   __device__ __forceinline__ void finish_row(int64_t i, int64_t len, double xi, const double (&a)[NA],
                                              P& part) const {
-    double yi;
-    if (SEG <= SEG_FIRST) {
-      const double d = (WT == FJ_W_UNIT && SEG == SEG_WHOLE) ? (double)len : deg[i];
-      yi = opL ? fma(d, xi, -a[0]) : fma(1.0 + d, xi, -a[0]);
-    } else {
-      yi = y[i * ld + c] - a[0];
-    }
+    const double d = (WT == FJ_W_UNIT) ? (double)len : deg[i];
+    const double yi = opL ? fma(d, xi, -a[0]) : fma(1.0 + d, xi, -a[0]);
     y[i * ld + c] = yi;
-    if (SEG == SEG_WHOLE || SEG == SEG_LAST) part[0] = fma(xi, yi, part[0]);
+    part[0] = fma(xi, yi, part[0]);
   }
   __device__ __forceinline__ void finalize(const double (&tot)[NP]) const {
-    if (SEG == SEG_FIRST || SEG == SEG_MID) return;
     if (dot_out) *dot_out = tot[0];
     if (sc && alpha_on_device) {
       sc->pq = tot[0];
@@ -224,7 +211,7 @@ inline cudaError_t launch_warp_items(const fj_graph* g, const SolveWs* ws, const
   return cudaGetLastError();
 }
 
-// The engine on an explicit schedule / CSR view / scratch (segment passes).
+// The engine on an explicit schedule / scratch.
 template <int WT, class Op>
 inline cudaError_t launch_items_on(const fj_graph* g, const Sched& S, const TileSched& ts, const Op& op,
                                    const TileScratch& scr, int grid_max, cudaStream_t st) {
@@ -242,39 +229,20 @@ inline cudaError_t launch_items_on(const fj_graph* g, const Sched& S, const Tile
   return cudaGetLastError();
 }
 
-// The segment layout built for gathered width kp, if the graph uses one (segments.cu); nullptr:
-// one whole-row pass.  Never builds (safe inside stream capture): get_segments() builds it first.
-inline const SegLayout* seg_for(const fj_graph* g, int kp) {
-  return (kp >= 1 && kp <= 4) ? reinterpret_cast<const SegLayout*>(g->seg[kp]) : nullptr;
-}
-
 // The work-item list matching an operator's tile size (Op::ITEMS).
 template <class Op>
 inline const Sched& sched_of(const fj_graph* g) {
   return Op::ITEMS == ITEMS ? g->s1 : g->sv;
 }
 
-// A product of the ApplyOp family (ApplyOp / ApplyOpV): one launch per column segment when the
-// graph has a segment layout for this width, else one whole-row launch with the workspace scratch.
-// Returns the number of kernel launches (for accounting) through *launches.
+// A product of the ApplyOp family (ApplyOp / ApplyOpV): one whole-row launch with the workspace
+// scratch.  Returns the number of kernel launches (for accounting) through *launches.
 template <int WT, class Op>
-inline cudaError_t launch_product(const fj_graph* g, const SegLayout* L, const TileScratch& scr, int grid_max,
-                                  const Op& op, cudaStream_t st, int* launches) {
-  if (!L) {   // op is the SEG_WHOLE instantiation
-    *launches = 1;
-    const Sched& S = sched_of<Op>(g);
-    return launch_items_on<WT>(g, S, make_sched(g, S), op, scr, grid_max, st);
-  }
-  *launches = L->nseg;
-  for (int s = 0; s < L->nseg; ++s) {
-    const TileSched ts = make_sched_seg(g, *L, s);
-    cudaError_t e;
-    if (s == 0) e = launch_items_on<WT>(g, L->sched[s], ts, op.template as_seg<SEG_FIRST>(), L->ts, L->grid_max, st);
-    else if (s == L->nseg - 1) e = launch_items_on<WT>(g, L->sched[s], ts, op.template as_seg<SEG_LAST>(), L->ts, L->grid_max, st);
-    else e = launch_items_on<WT>(g, L->sched[s], ts, op.template as_seg<SEG_MID>(), L->ts, L->grid_max, st);
-    if (e != cudaSuccess) return e;
-  }
-  return cudaSuccess;
+inline cudaError_t launch_product(const fj_graph* g, const TileScratch& scr, int grid_max, const Op& op,
+                                  cudaStream_t st, int* launches) {
+  *launches = 1;
+  const Sched& S = sched_of<Op>(g);
+  return launch_items_on<WT>(g, S, make_sched(g, S), op, scr, grid_max, st);
 }
 
 }  // namespace fj

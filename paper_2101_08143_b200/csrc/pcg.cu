@@ -196,13 +196,13 @@ __global__ void k_copy_col(int64_t n, const double* __restrict__ src, int64_t sl
     dst[i * dld + dc] = src[i * sld + sc_];
 }
 
-// q = (I+L) x for contiguous x, y (segmented when the graph has an L2 segment layout for k = 1)
+// q = (I+L) x for contiguous x, y
 template <int WT>
 static fj_status launch_product1(const fj_graph* g, const SolveWs* w, const double* x, double* y, int opL,
                                  PcgScalars* sc, cudaStream_t st) {
   ApplyOp<WT> op{x, y, g->deg, 1, 0, opL, sc, nullptr};
   int nl = 0;
-  FJ_CK(launch_product<WT>(g, seg_for(g, 1), w->ts, w->grid_max, op, st, &nl));
+  FJ_CK(launch_product<WT>(g, w->ts, w->grid_max, op, st, &nl));
   if (!g_capturing) count_launch(nl);
   return FJ_OK;
 }
@@ -299,8 +299,6 @@ fj_status solve_col(fj_graph* g, const double* s, double* z, int64_t ld, int64_t
   FJ_TRY(get_ws(g, st, &w));
   const int64_t n = g->n;
   const unsigned cb = (unsigned)std::min<int64_t>((n + 255) / 256, 4096);
-  const SegLayout* L = nullptr;
-  FJ_TRY(get_segments(g, 1, st, &L));   // before capture: the loop graph launches its passes
   if (o.use_cuda_graph) FJ_TRY(build_loop_graph(g, w));
   int restarts = 0, total_iter = 0;
   PcgScalars h{};
@@ -338,7 +336,7 @@ fj_status solve_col(fj_graph* g, const double* s, double* z, int64_t ld, int64_t
     FJ_CK(cudaMemcpyAsync(&h, w->sc, sizeof h, cudaMemcpyDeviceToHost, st));
     FJ_CK(cudaStreamSynchronize(st));
     total_iter += h.iter;
-    if (o.use_cuda_graph) count_launch((2 + (L ? L->nseg : 1)) * std::max(h.iter, 1));
+    if (o.use_cuda_graph) count_launch(3 * std::max(h.iter, 1));
     float lms = 0.f;
     cudaEventElapsedTime(&lms, w->ev2, w->ev3);
     if (rep) { rep->ms_loop += lms; rep->iterations_total += h.iter; }
@@ -379,8 +377,6 @@ fj_status fj_apply(const fj_graph* gc, int op, int k, const double* x, double* y
   if (k > 1) return apply_batch(g, k, x, y, op == FJ_OP_L ? 1 : 0, st);
   SolveWs* w = nullptr;
   FJ_TRY(get_ws(g, st, &w));
-  const SegLayout* L = nullptr;
-  FJ_TRY(get_segments(g, 1, st, &L));
   return apply_col(g, w, x, y, 1, 0, op == FJ_OP_L ? 1 : 0, st);
 }
 
@@ -393,8 +389,6 @@ fj_status fj_time_spmv(const fj_graph* gc, int k, int reps, float* ms_host, void
   if (k >= batch_min_k()) return time_batch_spmv(g, k, reps, ms_host, st);
   SolveWs* w = nullptr;
   FJ_TRY(get_ws(g, st, &w));
-  const SegLayout* L = nullptr;
-  FJ_TRY(get_segments(g, 1, st, &L));
   FJ_TRY(apply_col(g, w, w->p, w->q, 1, 0, 0, st));
   FJ_CK(cudaEventRecord(w->ev2, st));
   for (int i = 0; i < reps; ++i) FJ_TRY(apply_col(g, w, w->p, w->q, 1, 0, 0, st));

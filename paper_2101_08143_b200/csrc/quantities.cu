@@ -706,6 +706,10 @@ fj_status fj_approxim_host(int64_t n, int64_t m_in, const int32_t* u_h, const in
   }
   fj_graph* g = nullptr;
   FJ_TRY(fj_graph_create(n, nnz, rp_g, col_g, w_g, wtype, 0, stream, &g));
+  struct GraphGuard {   // the handle (workspace, schedules) is released on every return path
+    fj_graph* g;
+    ~GraphGuard() { if (g) fj_graph_destroy(g); }
+  } guard{g};
   FJ_CK(cudaStreamWaitEvent(st, side.ev_out, 0));
   const double* s_in = ds.p;
   if (relabel) {   // s into the new labels; ds then serves as the old-label staging buffer of z
@@ -718,15 +722,13 @@ fj_status fj_approxim_host(int64_t n, int64_t m_in, const int32_t* u_h, const in
   if ((s == FJ_OK || s == FJ_E_NO_CONVERGENCE) && z_h && !z_done) {
     const double* zsrc = dz.p;
     if (relabel) {
-      fj_status sp = fj_permute_rows(n, k, o2n.p, dz.p, ds.p, stream);
-      if (sp != FJ_OK) { fj_graph_destroy(g); return sp; }
+      FJ_TRY(fj_permute_rows(n, k, o2n.p, dz.p, ds.p, stream));
       zsrc = ds.p;
     }
     cudaError_t e = cudaMemcpyAsync(z_h, zsrc, sizeof(double) * n * k, cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) s = cuda_fail(e, "z readback", __FILE__, __LINE__);
   }
-  fj_graph_destroy(g);
   return s;
 }
 

@@ -11,9 +11,6 @@
 // unchanged up to the rounding order of those sums.  Callers map s in and z out with
 // fj_permute_rows.
 //
-//   fj_degree_order   counts endpoint occurrences (self-loops and duplicates counted as they come:
-//                     a heuristic key, computed from the raw list before a1), then a stable radix
-//                     sort by descending count (ties: ascending id) -> new2old, old2new
 //   fj_permute_rows   out[i][:] = in[idx[i]][:]   (idx = new2old: into the new labels;
 //                     idx = old2new: back to the old ones)
 #include <cub/cub.cuh>
@@ -22,28 +19,6 @@
 #include "workspace.cuh"
 
 namespace fj {
-
-__global__ void k_endpoint_count(int64_t m, int64_t n, const int32_t* __restrict__ u, const int32_t* __restrict__ v,
-                                 uint32_t* __restrict__ cnt, unsigned int* bad) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t a = u[e], c = v[e];
-    if (a < 0 || c < 0 || a >= n || c >= n) {
-      atomicOr(bad, 1u);
-    } else if (a != c) {
-      atomicAdd(cnt + a, 1u);
-      atomicAdd(cnt + c, 1u);
-    }
-  }
-}
-
-// key = ~count (ascending sort = descending count), value = vertex id
-__global__ void k_order_keys(int64_t n, const uint32_t* __restrict__ cnt, uint32_t* __restrict__ key,
-                             int32_t* __restrict__ id) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    key[i] = ~cnt[i];
-    id[i] = (int32_t)i;
-  }
-}
 
 __global__ void k_invert(int64_t n, const int32_t* __restrict__ new2old, int32_t* __restrict__ old2new) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -266,43 +241,6 @@ extern "C" fj_status fj_csr_permute(int64_t n, int64_t nnz, const int64_t* row_p
     default: k_csr_permute<8><<<gb, PTB, 0, st>>>(nnz, row_ptr, col, w, new2old, old2new, row_ptr_out, cf.p, cl.p, col_out, w_out); break;
   }
   FJ_CK_LAUNCH();
-  return FJ_OK;
-}
-
-extern "C" fj_status fj_degree_order(int64_t n, int64_t m_in, const int32_t* u, const int32_t* v, int32_t* new2old,
-                                     int32_t* old2new, void* stream) {
-  if (n < 1 || n >= INT32_MAX) return fail(FJ_E_INVALID_ARG, "n must be in [1, 2^31-2]");
-  if (m_in < 0 || m_in >= INT32_MAX) return fail(FJ_E_INVALID_ARG, "m_in must be in [0, 2^31-2]");
-  if (!new2old || !old2new || (m_in > 0 && (!u || !v))) return fail(FJ_E_INVALID_ARG, "null argument");
-  cudaStream_t st = S(stream);
-  const int sms = num_sms();
-  DevBuf<uint32_t> cnt, key, key2;
-  DevBuf<int32_t> id;
-  DevBuf<unsigned int> bad;
-  FJ_TRY(cnt.alloc(n, st)); FJ_TRY(key.alloc(n, st)); FJ_TRY(key2.alloc(n, st));
-  FJ_TRY(id.alloc(n, st)); FJ_TRY(bad.alloc(1, st));
-  FJ_CK(cudaMemsetAsync(cnt.p, 0, sizeof(uint32_t) * (size_t)n, st));
-  FJ_CK(cudaMemsetAsync(bad.p, 0, sizeof(unsigned int), st));
-  if (m_in > 0) {
-    k_endpoint_count<<<grid_of(m_in, 256, sms), 256, 0, st>>>(m_in, n, u, v, cnt.p, bad.p);
-    FJ_CK_LAUNCH();
-  }
-  k_order_keys<<<grid_of(n, 256, sms), 256, 0, st>>>(n, cnt.p, key.p, id.p);
-  FJ_CK_LAUNCH();
-  size_t bytes = 0;
-  FJ_CK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, key.p, key2.p, id.p, new2old, n, 0, 32, st));
-  {
-    DevBuf<uint8_t> tmp;
-    FJ_TRY(tmp.alloc((int64_t)bytes, st));
-    FJ_CK(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, key.p, key2.p, id.p, new2old, n, 0, 32, st));
-    count_cub();
-  }
-  k_invert<<<grid_of(n, 256, sms), 256, 0, st>>>(n, new2old, old2new);
-  FJ_CK_LAUNCH();
-  unsigned int hbad = 0;
-  FJ_CK(cudaMemcpyAsync(&hbad, bad.p, sizeof hbad, cudaMemcpyDeviceToHost, st));
-  FJ_CK(cudaStreamSynchronize(st));
-  if (hbad) return fail(FJ_E_INVALID_ARG, "edge endpoint out of [0, n)");
   return FJ_OK;
 }
 

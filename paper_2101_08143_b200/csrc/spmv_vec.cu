@@ -113,7 +113,7 @@ struct VecScalars {
 
 // ---------------------------------------------------------------- row operators (tiles.cuh Op)
 // q = (I+L) p or L p for all KP columns of a padded [n][KP] block (P:L88 L = D - A).
-template <int WT, int KP, int KQ = KP, int SEG = SEG_WHOLE>   // y stored KQ wide; SEG: segments.cu role
+template <int WT, int KP, int KQ = KP>   // y stored KQ wide
 struct ApplyOpV {
   using V = DVec<KP>;
   static constexpr int ITEMS = VEC_ITEMS;
@@ -132,14 +132,7 @@ struct ApplyOpV {
   double* dot_out = nullptr;   // optional: p_c^T q_c per column (distributed: local part)
   int alpha_on_device = 1;     // 0 (distributed): alpha after the allreduce of dot_out
   __device__ __forceinline__ bool skip() const { return sc && *(volatile int32_t*)&sc->done; }
-  __device__ __forceinline__ bool wants_xi() const { return SEG != SEG_MID; }
-  template <int S>
-  ApplyOpV<WT, KP, KQ, S> as_seg() const {
-    ApplyOpV<WT, KP, KQ, S> o;
-    static_assert(sizeof o == sizeof *this, "same layout");
-    memcpy(static_cast<void*>(&o), this, sizeof o);
-    return o;
-  }
+  __device__ __forceinline__ bool wants_xi() const { return true; }
   __device__ __forceinline__ V gather(int32_t j) const { return ld_vec<KP>(x + (int64_t)j * KP); }
   __device__ __forceinline__ V row_value(int64_t i) const { return ld_vec<KP>(x + i * KP); }
   __device__ __forceinline__ const V* xi_base() const { return reinterpret_cast<const V*>(x); }
@@ -151,24 +144,15 @@ struct ApplyOpV {
   __device__ __forceinline__ void finish_row(int64_t i, int64_t len, const V& xi, const double (&a)[NA],
                                              P& part) const {
     V yv;
-    if (SEG <= SEG_FIRST) {
-      const double d = (WT == FJ_W_UNIT && SEG == SEG_WHOLE) ? (double)len : deg[i];
-      const double dd = opL ? d : 1.0 + d;
+    const double d = (WT == FJ_W_UNIT) ? (double)len : deg[i];
+    const double dd = opL ? d : 1.0 + d;
 #pragma unroll
-      for (int c = 0; c < KP; ++c) yv.v[c] = fma(dd, xi.v[c], -a[c]);
-    } else {
-      yv = ld_q<KP, KQ>(y, i);
+    for (int c = 0; c < KP; ++c) yv.v[c] = fma(dd, xi.v[c], -a[c]);
 #pragma unroll
-      for (int c = 0; c < KP; ++c) yv.v[c] -= a[c];
-    }
-    if (SEG == SEG_WHOLE || SEG == SEG_LAST) {
-#pragma unroll
-      for (int c = 0; c < KP; ++c) part[c] = fma(xi.v[c], yv.v[c], part[c]);
-    }
+    for (int c = 0; c < KP; ++c) part[c] = fma(xi.v[c], yv.v[c], part[c]);
     st_q<KP, KQ>(y, i, yv);
   }
   __device__ __forceinline__ void finalize(const double (&tot)[NP]) const {
-    if (SEG == SEG_FIRST || SEG == SEG_MID) return;
     if (dot_out) {
 #pragma unroll
       for (int c = 0; c < KP; ++c) dot_out[c] = tot[c];
@@ -667,7 +651,7 @@ static fj_status vec_apply_padded(const fj_graph* g, const VecWs* w, const doubl
     constexpr int WT = decltype(wt)::value;
     ApplyOpV<WT, KP, KQ> op{x, y, g->deg, opL, sc, w->k};
     int nl = 0;
-    FJ_CK(launch_product<WT>(g, seg_for(g, KP), w->ts, w->grid_max, op, st, &nl));   // L2 segments
+    FJ_CK(launch_product<WT>(g, w->ts, w->grid_max, op, st, &nl));
     if (!g_capturing) count_launch(nl);
     return FJ_OK;
   });
@@ -719,8 +703,6 @@ static fj_status solve_vec_t(fj_graph* g, VecWs* w, int k, const double* s, doub
   const int64_t n = g->n;
   const unsigned cb = (unsigned)std::min<int64_t>((n + 255) / 256, 8192);
   w->x_is_solution = false;
-  const SegLayout* L = nullptr;
-  FJ_TRY(get_segments(g, KP, st, &L));   // before capture: the loop graph launches its passes
   if (o.use_cuda_graph) FJ_TRY((build_vec_graph<KP, KQ>(g, w)));
   phase_tick("vec: loop graph capture", st);
   VecScalars h{};
@@ -758,7 +740,7 @@ static fj_status solve_vec_t(fj_graph* g, VecWs* w, int k, const double* s, doub
       FJ_CK(cudaMemcpyAsync(&h, w->sc, sizeof h, cudaMemcpyDeviceToHost, st));
       FJ_CK(cudaStreamSynchronize(st));
       total_iter += h.iter;
-      if (o.use_cuda_graph) count_launch((2 + (L ? L->nseg : 1)) * std::max(h.iter, 1));
+      if (o.use_cuda_graph) count_launch(3 * std::max(h.iter, 1));
       float lms = 0.f;
       cudaEventElapsedTime(&lms, w->ev2, w->ev3);
       if (rep) { rep->ms_loop += lms; rep->iterations_total += (int64_t)h.iter * k; }
@@ -774,7 +756,7 @@ static fj_status solve_vec_t(fj_graph* g, VecWs* w, int k, const double* s, doub
     FJ_CK(cudaStreamSynchronize(st));
     phase_tick("vec: true residual", st);
     total_iter += h.iter;
-    if (o.use_cuda_graph) count_launch((2 + (L ? L->nseg : 1)) * std::max(h.iter, 1));
+    if (o.use_cuda_graph) count_launch(3 * std::max(h.iter, 1));
     float lms = 0.f;
     cudaEventElapsedTime(&lms, w->ev2, w->ev3);
     if (rep) { rep->ms_loop += lms; rep->iterations_total += (int64_t)h.iter * k; }
@@ -952,7 +934,7 @@ static fj_status dist_apply(const fj_graph* g, const VecWs* w, const double* p, 
     op.dot_out = dot;
     op.alpha_on_device = 0;
     int nl = 0;
-    FJ_CK(launch_product<WT>(g, nullptr, w->ts, w->grid_max, op, st, &nl));
+    FJ_CK(launch_product<WT>(g, w->ts, w->grid_max, op, st, &nl));
     count_launch(nl);
     return FJ_OK;
   });
@@ -1073,8 +1055,6 @@ fj_status solve_vec(fj_graph* g, int k, const double* s, double* z, const fj_sol
 fj_status apply_vec(fj_graph* g, int k, const double* x, double* y, int opL, cudaStream_t st) {
   VecWs* w = nullptr;
   FJ_TRY(get_vec_ws(g, k, st, &w));
-  const SegLayout* L = nullptr;
-  FJ_TRY(get_segments(g, w->kp, st, &L));
   w->x_is_solution = false;
   const unsigned cb = (unsigned)std::min<int64_t>((g->n + 255) / 256, 8192);
   auto run = [&](auto kpc, auto kqc) -> fj_status {
@@ -1101,8 +1081,6 @@ fj_status apply_vec(fj_graph* g, int k, const double* x, double* y, int opL, cud
 fj_status time_vec_spmv(fj_graph* g, int k, int reps, float* ms_out, cudaStream_t st) {
   VecWs* w = nullptr;
   FJ_TRY(get_vec_ws(g, k, st, &w));
-  const SegLayout* L = nullptr;
-  FJ_TRY(get_segments(g, w->kp, st, &L));
   w->x_is_solution = false;
   auto run = [&]() -> fj_status {
     switch (w->kp) {

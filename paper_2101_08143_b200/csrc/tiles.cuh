@@ -136,30 +136,6 @@ struct TileScratch {
   unsigned int* grid_ticket;   // [1], zero-initialised, self-resetting
 };
 
-// L2-sized column segments of the CSR (segments.cu): segment s holds, for every row, the nonzeros
-// whose column lies in [bounds[s], bounds[s+1]), ascending, with its own row_ptr and schedule.
-constexpr int MAXSEG = 64;
-struct SegLayout {
-  int nseg = 0, kp = 0, grid_max = 0;
-  int64_t bounds[MAXSEG + 1] = {};
-  int64_t* rp[MAXSEG] = {};
-  int32_t* col[MAXSEG] = {};
-  void* w[MAXSEG] = {};
-  int64_t nnz[MAXSEG] = {};
-  Sched sched[MAXSEG];
-  TileScratch ts{};
-};
-// pass roles of a segmented product (Op::seg): whole row / first / middle / last segment
-enum { SEG_WHOLE = 0, SEG_FIRST = 1, SEG_MID = 2, SEG_LAST = 3 };
-int seg_count(const fj_graph* g, int kp);
-inline TileSched make_sched_seg(const fj_graph* g, const SegLayout& L, int s) {
-  TileSched t = make_sched(g, L.sched[s]);
-  t.nnz = L.nnz[s]; t.row_ptr = L.rp[s]; t.col = L.col[s]; t.w = L.w[s];
-  return t;
-}
-fj_status get_segments(fj_graph* g, int kp, cudaStream_t st, const SegLayout** out);
-void free_segments(fj_graph* g);
-
 // Op interface:
 //   using V;                                       // gathered value: double (k = 1) or DVec<KP> (k <= 4)
 //   static constexpr int ITEMS;                    // merge items per lane (the schedule's t_cap / 32)

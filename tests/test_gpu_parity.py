@@ -397,27 +397,6 @@ def test_small_k_solve_entry_and_ragged(fj):
     assert np.allclose(Z[4000:], S[4000:], rtol=1e-12)
 
 
-# ---------------------------------------------------------------- L2 column segments (segments.cu)
-@pytest.mark.parametrize("wkind", ["unit", "u8"])
-def test_segmented_product_vs_oracle(fj, wkind):
-    """FJ_SEG_MB=0.05: k = 1 (240 KB) and k = 3 (padded, 960 KB) gathered blocks are cut into 5 and
-    19 column segments, so every PCG product is a multi-pass segmented one (first / middle / last
-    roles, a hub row split across segments).  Quantities, z and the operator against the oracle."""
-    import json
-    import os
-    import subprocess
-    import sys
-    env = dict(os.environ, FJ_SEG_MB="0.05")
-    r = subprocess.run([sys.executable, os.path.join(os.path.dirname(__file__), "seg_worker.py"), wkind],
-                       env=env, capture_output=True, text=True, timeout=600)
-    assert r.returncode == 0, r.stderr[-2000:]
-    res = json.loads(r.stdout.strip().splitlines()[-1])
-    for k, d in res.items():
-        assert d["converged"] == 1 and d["rel_res"] <= 1e-10, (k, d)
-        assert d["err"] <= 1e-8 and d["apply_err"] <= 1e-13, (k, d)
-        assert d["bitwise_graph_vs_loop"], (k, d)
-
-
 # ---------------------------------------------------------------- f2: Algorithm 1 verbatim
 @pytest.mark.parametrize("name", ["c1", "c4s"])
 def test_alg1_verbatim_vs_oracle(fj, name):
