@@ -16,7 +16,9 @@
  *  - Layouts: CSR row_ptr int64 [n+1] (row_ptr[0] = 0), col int32 [nnz], weights [nnz] in the
  *    type given by fj_wtype (FJ_W_UNIT: no array, every w_ij = 1).  Opinion / solution matrices
  *    with k columns are ROW-MAJOR fp64 [n][k] (k = 1: a plain vector).
- *  - Internal workspace is allocated with cudaMallocAsync on `stream` and owned by the handle.
+ *  - Internal workspace is owned by the handle.  It comes from the allocator installed with
+ *    fj_set_allocator, else from a library-owned stream-ordered memory pool (cudaMallocFromPoolAsync
+ *    on `stream`).
  *  - There is NO CPU fallback: without a CUDA device every compute call returns FJ_E_CUDA.
  */
 #ifndef FJ_H
@@ -127,6 +129,27 @@ int64_t fj_kernel_launches(int64_t* cub_launches);
 const char* fj_status_str(int status);
 const char* fj_last_error(void);
 void fj_default_solve_opts(fj_solve_opts* opts);
+
+/* ---------------------------------------------------------------- allocator hook
+ * Route every device workspace allocation of the library (graph handles, solver / quantities
+ * workspaces, setup temporaries) through a caller allocator, e.g. the PyTorch caching allocator
+ * (the Python binding's use_torch_allocator()).
+ *   alloc(bytes, stream, ctx) -> device pointer on the current device, or NULL (-> FJ_E_CUDA /
+ *                                out-of-memory from the calling entry point); `stream` is the
+ *                                cudaStream_t (as void*) the block will first be used on.
+ *   free(ptr, bytes, stream, ctx) returns a block; the library calls it only after the work that
+ *                                used the block on `stream` has completed (it synchronises that
+ *                                stream first), so the allocator need not order it.
+ * alloc and free are both non-NULL (install) or both NULL (back to the library pool); anything
+ * else is FJ_E_INVALID_ARG.  Process-wide; blocks are always returned to the allocator that
+ * produced them, even if another one was installed meanwhile.  Not thread-safe with respect to
+ * concurrent calls that allocate (install it before creating handles).  The callbacks must not
+ * call back into this library. */
+typedef void* (*fj_alloc_fn)(size_t bytes, void* stream, void* ctx);
+typedef void (*fj_free_fn)(void* ptr, size_t bytes, void* stream, void* ctx);
+fj_status fj_set_allocator(fj_alloc_fn alloc, fj_free_fn free_fn, void* ctx);
+/* Blocks currently held from an installed allocator (diagnostic; 0 with the library pool). */
+int64_t fj_allocator_live_blocks(void);
 
 /* ---------------------------------------------------------------- a1: canonical CSR
  * Build the CSR of the simple undirected graph given by m_in raw edges (u_dev[e], v_dev[e]),

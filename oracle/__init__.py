@@ -18,6 +18,12 @@ Functions
 canonical_csr     O-1: simple undirected graph from raw edges -> CSR ("simple graph",
                   P:L88 adjacency A=(w_ij) symmetric; SURVEY §8(c) O-1 readings for self-loops
                   and duplicates).
+canonical_csr_big O-1 as plain C loops, row block by row block (C4, C5 scale).  Pinned against
+                  canonical_csr on random multigraphs, many blocks forced.
+csr_permute       P A P^T of a CSR (relabelling check).  Pinned against a numpy transcription and
+                  against the solve invariance under relabelling.
+quantities_c      Defs. 3.1-3.5 as C loops with Neumaier sums (C5 scale).  Pinned against the
+                  paper's P5 example (golden) and against `quantities` on random graphs.
 degrees           O-2: d_i = sum_j w_ij.
 ipl_apply         (I + L) x with L = D - A (P:L88).
 incidence_apply   W^{1/2} B x, one entry per edge, head = lower id.
@@ -55,9 +61,9 @@ WT_UNIT, WT_U8, WT_F64 = 0, 1, 3
 
 
 def build(force: bool = False) -> str:
-    src = os.path.join(_HERE, "oracle_cg.c")
-    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(src):
-        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-o", _SO, src, "-lm"])
+    srcs = [os.path.join(_HERE, "oracle_cg.c"), os.path.join(_HERE, "oracle_big.c")]
+    if force or not os.path.exists(_SO) or any(os.path.getmtime(_SO) < os.path.getmtime(f) for f in srcs):
+        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-o", _SO, *srcs, "-lm"])
     return _SO
 
 
@@ -74,6 +80,12 @@ def _L():
         lib.oracle_pcg_fixed_iters.argtypes = [i64, ptr, ptr, cint, ptr, ptr, i64, ptr]
         lib.oracle_pcg_fixed_iters.restype = cint
         lib.oracle_num_threads.restype = cint
+        lib.oracle_csr_blocked.argtypes = [i64, i64, ptr, ptr, cint, ptr, i64, ptr, ptr, ptr, ptr]
+        lib.oracle_csr_blocked.restype = i64
+        lib.oracle_quantities.argtypes = [i64, ptr, ptr, cint, ptr, ptr, ptr, ptr]
+        lib.oracle_quantities.restype = cint
+        lib.oracle_csr_permute.argtypes = [i64, ptr, ptr, cint, ptr, ptr, ptr, ptr, ptr, ptr]
+        lib.oracle_csr_permute.restype = cint
         _lib = lib
     return _lib
 
@@ -151,6 +163,49 @@ def canonical_csr(n: int, u, v, w=None) -> CSR:
         if np.any(~np.isfinite(wo.astype(np.float64))) or np.any(wo.astype(np.float64) <= 0):
             raise ValueError("weights must be finite and > 0 (P:L86, w: E -> R_+)")
     return CSR(n, row_ptr, cols.astype(np.int32), wo, selfloops, duplicates)
+
+
+def canonical_csr_big(n: int, u, v, w=None, block_entries: int = 1 << 28) -> CSR:
+    """O-1 (same rules and citations as canonical_csr) as plain C loops, row block by row block
+    (oracle_big.c), for the configs where numpy's sort keys would not fit: C4 and C5."""
+    u = np.ascontiguousarray(u, dtype=np.int32)
+    v = np.ascontiguousarray(v, dtype=np.int32)
+    m = len(u)
+    wsize, wo = 0, None
+    if w is not None:
+        w = np.ascontiguousarray(w)
+        wsize = w.dtype.itemsize
+        if w.dtype not in (np.uint8, np.float64):
+            raise ValueError("weights must be uint8 or float64")
+        wo = np.empty(max(2 * m, 1), dtype=w.dtype)
+    row_ptr = np.empty(n + 1, dtype=np.int64)
+    col = np.empty(max(2 * m, 1), dtype=np.int32)
+    stats = np.zeros(2, dtype=np.int64)
+    nnz = _L().oracle_csr_blocked(n, m, _p(u), _p(v), wsize, _p(w), int(block_entries), _p(row_ptr), _p(col),
+                                  _p(wo), _p(stats))
+    if nnz == -1:
+        raise ValueError("vertex id out of range")
+    if nnz < 0:
+        raise MemoryError(f"oracle_csr_blocked failed ({nnz})")
+    col = col[:nnz]
+    if wo is not None:
+        wo = wo[:nnz]
+        if np.any(~np.isfinite(wo.astype(np.float64))) or np.any(wo.astype(np.float64) <= 0):
+            raise ValueError("weights must be finite and > 0 (P:L86, w: E -> R_+)")
+    return CSR(n, row_ptr, col, wo, int(stats[0]), int(stats[1]))
+
+
+def csr_permute(g: CSR, new2old, old2new) -> CSR:
+    """P A P^T: row i' = old row new2old[i'], columns mapped by old2new,
+    entries in the old row's order (oracle_big.c)."""
+    n2o = np.ascontiguousarray(new2old, dtype=np.int32)
+    o2n = np.ascontiguousarray(old2new, dtype=np.int32)
+    rp = np.empty(g.n + 1, dtype=np.int64)
+    col = np.empty(max(g.nnz, 1), dtype=np.int32)
+    wo = None if g.w is None else np.empty(max(g.nnz, 1), dtype=g.w.dtype)
+    _L().oracle_csr_permute(g.n, _p(g.row_ptr), _p(g.col), 0 if g.w is None else g.w.dtype.itemsize, _p(g.w),
+                            _p(n2o), _p(o2n), _p(rp), _p(col), _p(wo))
+    return CSR(g.n, rp, col[:g.nnz], None if wo is None else wo[:g.nnz])
 
 
 def degrees(g: CSR) -> np.ndarray:
@@ -270,6 +325,20 @@ def quantities(g: CSR, s: np.ndarray, z: np.ndarray) -> dict:
         "sz": _fsum(s * z), "sbzb": _fsum((s - ms) * (z - mz)), "ss": _fsum(s * s),
         "mean_s": ms, "mean_z": mz, "Lz2": _fsum(laplacian_apply(g, z) ** 2),
     }
+
+
+def quantities_c(g: CSR, s: np.ndarray, z: np.ndarray) -> dict:
+    """The same definitions as `quantities` (Defs. 3.1-3.5; PDI = P + D, reading R1)
+    as C loops with Neumaier-compensated per-thread sums (oracle_big.c), for graphs whose per-edge
+    terms would not fit a Python list (C5: 1.05e9 edges).  No ||Lz||^2 diagnostic."""
+    s = np.ascontiguousarray(s, dtype=np.float64)
+    z = np.ascontiguousarray(z, dtype=np.float64)
+    out = np.zeros(9)
+    wsize = 0 if g.w is None else g.w.dtype.itemsize
+    _L().oracle_quantities(g.n, _p(g.row_ptr), _p(g.col), wsize, _p(g.w), _p(s), _p(z), _p(out))
+    CI, D, P, C, sz, sbzb, ss, mz, ms = [float(x) for x in out]
+    return {"CI": CI, "D": D, "P": P, "C": C, "Idc": D + C, "PDI": P + D, "sz": sz, "sbzb": sbzb, "ss": ss,
+            "mean_s": ms, "mean_z": mz}
 
 
 # --------------------------------------------------------------------------- tiny-graph pins

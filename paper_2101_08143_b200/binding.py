@@ -100,6 +100,8 @@ def load_library(path: str = SO):
     for name, sig in relabel_sigs.items():
         if hasattr(L, name):
             getattr(L, name).argtypes = sig
+    L.fj_set_allocator.argtypes = [_ALLOC_FN, _FREE_FN, _vp]
+    L.fj_allocator_live_blocks.restype = _i64
     L.fj_graph_create.argtypes = [_i64, _i64, _vp, _vp, _vp, ctypes.c_int, ctypes.c_int, _vp, P(_vp)]
     L.fj_graph_info.argtypes = [_vp, P(GraphInfo)]
     L.fj_graph_degrees.argtypes = [_vp, _vp, _vp]
@@ -246,6 +248,41 @@ def _wtype(w):
         return FJ_W_UNIT
     import torch
     return {torch.uint8: FJ_W_U8, torch.float32: FJ_W_F32, torch.float64: FJ_W_F64}[w.dtype]
+
+
+_ALLOC_FN = ctypes.CFUNCTYPE(_vp, ctypes.c_size_t, _vp, _vp)
+_FREE_FN = ctypes.CFUNCTYPE(None, _vp, ctypes.c_size_t, _vp, _vp)
+_torch_alloc_cbs = None   # keep the ctypes callbacks alive while installed
+
+
+def use_torch_allocator(enable: bool = True):
+    """fj_set_allocator: route the library's device workspace through torch's caching allocator
+    (torch.cuda.caching_allocator_alloc / _delete, on the stream the library names), or back to the
+    library's own pool (enable=False)."""
+    import torch
+    global _torch_alloc_cbs
+    L = lib()
+    if not enable:
+        _check(L.fj_set_allocator(ctypes.cast(None, _ALLOC_FN), ctypes.cast(None, _FREE_FN), None))
+        _torch_alloc_cbs = None
+        return
+
+    def _alloc(nbytes, stream, ctx):
+        try:
+            return torch.cuda.caching_allocator_alloc(int(nbytes), torch.cuda.current_device(), stream=int(stream or 0))
+        except Exception:   # OOM -> NULL -> the library reports FJ_E_CUDA
+            return None
+
+    def _free(ptr, nbytes, stream, ctx):
+        torch.cuda.caching_allocator_delete(int(ptr))
+
+    cbs = (_ALLOC_FN(_alloc), _FREE_FN(_free))
+    _check(L.fj_set_allocator(cbs[0], cbs[1], None))
+    _torch_alloc_cbs = cbs
+
+
+def allocator_live_blocks() -> int:
+    return int(lib().fj_allocator_live_blocks())
 
 
 def _need_cuda(*ts):

@@ -27,21 +27,24 @@ fj_status cuda_fail(cudaError_t e, const char* what, const char* file, int line)
     if (_s != FJ_OK) return _s;                                                \
   } while (0)
 
-// Device memory: a library-owned stream-ordered pool per device whose release threshold is
-// unbounded, so repeated graph builds / solves reuse memory instead of re-mapping it.
+// Device memory.  Default: a library-owned stream-ordered pool per device whose release threshold
+// is unbounded, so repeated graph builds / solves reuse memory instead of re-mapping it.  With an
+// allocator installed by fj_set_allocator (e.g. the torch caching allocator), every workspace
+// allocation goes through it and is returned to it (graph.cu).
 cudaMemPool_t lib_pool(int device);
+cudaError_t dmalloc_raw(void** p, size_t bytes, cudaStream_t st);
+// Free stream-ordered on `st`: pool memory by cudaFreeAsync; user-allocator memory after `st` has
+// drained (the user's free is not stream-ordered).
+void dfree_on(void* p, cudaStream_t st);
 template <class T>
 inline cudaError_t dmalloc(T** p, size_t bytes, cudaStream_t st) {
-  int dev = 0;
-  cudaError_t e = cudaGetDevice(&dev);
-  if (e != cudaSuccess) return e;
-  return cudaMallocFromPoolAsync(reinterpret_cast<void**>(p), bytes, lib_pool(dev), st);
+  return dmalloc_raw(reinterpret_cast<void**>(p), bytes, st);
 }
 
-// Return pool memory stream-ordered on the legacy stream (callers synchronise the device first);
-// plain cudaFree on pool memory would hand it back to the OS and the next graph would re-map it.
+// Free on the legacy stream (callers synchronise the device first); plain cudaFree on pool memory
+// would hand it back to the OS and the next graph would re-map it.
 inline void dfree(void* p) {
-  if (p) cudaFreeAsync(p, 0);
+  if (p) dfree_on(p, 0);
 }
 
 // FJ_TIMING=1: host-side phase timestamps on stderr (diagnostics; synchronises the stream)
@@ -68,6 +71,9 @@ int batch_min_k();
 int l2_hint();
 // padded row width of the small-k engine for k = 3 (default 4; FJ_VEC_PAD=0: unpadded 3; spmv_vec.cu)
 int vec_pad3();
+// hot-row threshold of the small-k product's L2 eviction hints (FJ_HOT_MB: the hot prefix of the
+// gathered [n][kp] block in MB; unset or 0: no hints, -1)
+int64_t gather_hot_rows(int64_t n, int kp);
 
 // ---------------------------------------------------------------- device workspace per solve
 struct SolveWs;   // pcg.cu

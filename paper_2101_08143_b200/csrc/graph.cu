@@ -6,6 +6,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <unordered_map>
 #include <vector>
 
 #include "common.cuh"
@@ -43,6 +44,16 @@ int vec_pad3() {
   return v;
 }
 
+int64_t gather_hot_rows(int64_t n, int kp) {
+  static const double mb = [] {
+    const char* e = getenv("FJ_HOT_MB");
+    return e ? atof(e) : 0.0;
+  }();
+  if (!(mb > 0.0)) return -1;
+  const int64_t rows = (int64_t)(mb * 1048576.0 / (8.0 * kp));
+  return rows < n ? rows : n;
+}
+
 void phase_tick(const char* label, cudaStream_t st) {
   static const bool on = getenv("FJ_TIMING") != nullptr;
   if (!on) return;
@@ -52,6 +63,63 @@ void phase_tick(const char* label, cudaStream_t st) {
   fprintf(stderr, "[fj] %-28s %9.3f ms\n", label,
           std::chrono::duration<double, std::milli>(now - last).count());
   last = now;
+}
+
+// ---------------------------------------------------------------- allocator hook (fj_set_allocator)
+namespace {
+struct UserAlloc {
+  fj_alloc_fn alloc = nullptr;
+  fj_free_fn free = nullptr;
+  void* ctx = nullptr;
+};
+struct AllocRec {
+  UserAlloc a;
+  size_t bytes;
+};
+std::mutex g_alloc_mu;
+UserAlloc g_user;                                  // installed allocator (alloc == nullptr: pool)
+std::unordered_map<void*, AllocRec> g_user_live;   // user-allocated blocks -> the allocator to return them to
+}  // namespace
+
+cudaError_t dmalloc_raw(void** p, size_t bytes, cudaStream_t st) {
+  UserAlloc a;
+  {
+    std::lock_guard<std::mutex> lk(g_alloc_mu);
+    a = g_user;
+  }
+  if (a.alloc) {
+    void* q = a.alloc(bytes, reinterpret_cast<void*>(st), a.ctx);
+    if (!q) return cudaErrorMemoryAllocation;
+    std::lock_guard<std::mutex> lk(g_alloc_mu);
+    g_user_live[q] = AllocRec{a, bytes};
+    *p = q;
+    return cudaSuccess;
+  }
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  return cudaMallocFromPoolAsync(p, bytes, lib_pool(dev), st);
+}
+
+void dfree_on(void* p, cudaStream_t st) {
+  if (!p) return;
+  AllocRec rec{};
+  bool user = false;
+  {
+    std::lock_guard<std::mutex> lk(g_alloc_mu);
+    auto it = g_user_live.find(p);
+    if (it != g_user_live.end()) {
+      rec = it->second;
+      user = true;
+      g_user_live.erase(it);
+    }
+  }
+  if (!user) {
+    cudaFreeAsync(p, st);
+    return;
+  }
+  cudaStreamSynchronize(st);   // the user's free is not stream-ordered: drain the work using p
+  rec.a.free(p, rec.bytes, reinterpret_cast<void*>(st), rec.a.ctx);
 }
 
 cudaMemPool_t lib_pool(int device) {
@@ -378,6 +446,21 @@ fj_status fj_graph_degrees(const fj_graph* g, double* d, void* stream) {
   if (!g || !d) return fail(FJ_E_INVALID_ARG, "null argument");
   FJ_CK(cudaMemcpyAsync(d, g->deg, sizeof(double) * g->n, cudaMemcpyDeviceToDevice, S(stream)));
   return FJ_OK;
+}
+
+fj_status fj_set_allocator(fj_alloc_fn alloc, fj_free_fn free_fn, void* ctx) {
+  if ((alloc == nullptr) != (free_fn == nullptr))
+    return fail(FJ_E_INVALID_ARG, "fj_set_allocator: alloc and free must both be set or both be NULL");
+  std::lock_guard<std::mutex> lk(g_alloc_mu);
+  g_user.alloc = alloc;
+  g_user.free = free_fn;
+  g_user.ctx = ctx;
+  return FJ_OK;
+}
+
+int64_t fj_allocator_live_blocks(void) {
+  std::lock_guard<std::mutex> lk(g_alloc_mu);
+  return (int64_t)g_user_live.size();
 }
 
 fj_status fj_graph_destroy(fj_graph* g) {

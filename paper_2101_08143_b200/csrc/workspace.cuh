@@ -21,7 +21,7 @@ struct DevBuf {
     return FJ_OK;
   }
   void release() {
-    if (p) cudaFreeAsync(p, st);
+    if (p) dfree_on(p, st);
     p = nullptr;
   }
   ~DevBuf() { release(); }

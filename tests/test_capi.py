@@ -19,7 +19,7 @@ def test_header_declares_the_survey_boundary():
     names = set(declared_functions())
     for required in ["fj_csr_from_edges", "fj_graph_create", "fj_graph_info", "fj_graph_degrees", "fj_apply",
                      "fj_solve", "fj_quantities", "fj_approxim", "fj_graph_destroy", "fj_status_str",
-                     "fj_last_error", "fj_opinion_stats", "fj_approxim_host"]:
+                     "fj_last_error", "fj_opinion_stats", "fj_approxim_host", "fj_set_allocator"]:
         assert required in names
 
 
@@ -44,6 +44,19 @@ def test_invalid_arguments_fail_without_gpu():
     assert st == 1 and not h.value
     assert b"n must be" in L.fj_last_error()
     assert L.fj_solve(None, 1, None, None, None, None, None) == 1
+
+
+def test_set_allocator_argument_rules_without_gpu():
+    """fj_set_allocator: alloc and free both set or both NULL (no device call involved)."""
+    import paper_2101_08143_b200 as fj
+    from paper_2101_08143_b200 import binding as b
+    L = fj.lib()
+    a = b._ALLOC_FN(lambda n, s, c: None)
+    null_free = ctypes.cast(None, b._FREE_FN)
+    assert L.fj_set_allocator(a, null_free, None) == 1
+    assert b"both" in L.fj_last_error()
+    assert L.fj_set_allocator(ctypes.cast(None, b._ALLOC_FN), null_free, None) == 0
+    assert fj.allocator_live_blocks() == 0
 
 
 def test_product_path_does_not_import_oracle():

@@ -572,3 +572,40 @@ def test_degenerate_graphs_all_engines(fj, k, case):
         for c in range(k):
             assert q[c]["D"] == 0 and q[c]["CI"] <= 1e-26
             assert q[c]["C"] == pytest.approx(float((S[:, c] ** 2).sum()), rel=1e-12)
+
+
+# ---------------------------------------------------------------- allocator hook
+@pytest.mark.parametrize("k", [1, 3, 8])
+def test_torch_allocator_hook(fj, k):
+    """fj_set_allocator bound to torch's caching allocator: the library's workspace shows up in
+    torch.cuda.memory_allocated() while the handle lives, every block goes back on close, and the
+    results are bitwise those of the library pool."""
+    import torch
+    wl = synth.make_config("c2", n=200_000, k=k)
+    S = dev(wl.S if k > 1 else wl.S[:, 0].copy())
+    u, v = dev(wl.u), dev(wl.v)
+    G0 = fj.Graph.from_edges(wl.n, u, v)
+    z0, q0, _ = G0.approxim(S)
+    G0.close()
+    torch.cuda.synchronize()
+    fj.use_torch_allocator(True)
+    try:
+        base = torch.cuda.memory_allocated()
+        G = fj.Graph.from_edges(wl.n, u, v)
+        z1, q1, rep = G.approxim(S)
+        torch.cuda.synchronize()
+        assert fj.allocator_live_blocks() > 0
+        held = torch.cuda.memory_allocated() - base
+        # at least the degree / Jacobi arrays and the solver vectors (>= 4 n k doubles) are torch's
+        assert held >= 8 * wl.n * (2 + 4 * k) - 8 * wl.n * k * 2, held
+        G.close()
+        del G
+        torch.cuda.synchronize()
+        assert fj.allocator_live_blocks() == 0
+    finally:
+        fj.use_torch_allocator(False)
+    assert torch.equal(z0, z1)
+    for c in range(k):
+        for key in QKEYS:
+            assert q0[c][key] == q1[c][key], (c, key)
+    assert rep["converged"] == 1

@@ -381,3 +381,104 @@ def test_components_vs_scipy_and_lcc_by_hand():
     assert list(u2) == [0, 1, 2, 3] and list(v2) == [1, 2, 3, 3]            # input order, self-loop kept
     vmap, u2, v2, w2, nl = O.lcc(11, u[[0, 1, 2, 6, 7, 8]], v[[0, 1, 2, 6, 7, 8]], np.arange(6))
     assert nl == 3 and list(np.flatnonzero(vmap >= 0)) == [5, 6, 7] and list(w2) == [0, 1, 2]   # tie -> smaller ids
+
+
+# ---------------------------------------------------------------- C-loop oracle for C4 / C5 scale
+@pytest.mark.parametrize("seed", range(8))
+def test_canonical_csr_big_bruteforce(seed):
+    """oracle_csr_blocked (row block by row block) against the brute-force dict construction of the
+    O-1 rules; block sizes down to one row per block force every block boundary."""
+    rng = np.random.default_rng(50 + seed)
+    n = int(rng.integers(1, 60))
+    m = int(rng.integers(0, 400))
+    u = rng.integers(0, n, m)
+    v = (rng.zipf(1.5, m) % n) if seed % 3 == 0 else rng.integers(0, n, m)
+    w = [None, rng.integers(1, 6, m).astype(np.uint8), rng.uniform(0.1, 3.0, m)][seed % 3]
+    rp, cl, wl = _brute_csr(n, u, v, w)
+    for blk in [1, 7, 1 << 20]:
+        g = O.canonical_csr_big(n, u, v, w, block_entries=blk)
+        assert np.array_equal(g.row_ptr, rp) and np.array_equal(g.col, cl), blk
+        if w is not None:
+            assert np.array_equal(g.w, wl)
+        assert g.selfloops == int((u == v).sum())
+        assert g.duplicates == (m - g.selfloops) - g.nnz // 2
+
+
+def test_canonical_csr_big_edge_cases():
+    e = np.zeros(0, dtype=np.int32)
+    g = O.canonical_csr_big(5, e, e)
+    assert np.array_equal(g.row_ptr, np.zeros(6, np.int64)) and g.nnz == 0
+    g = O.canonical_csr_big(3, np.array([0, 1, 2]), np.array([0, 1, 2]))   # only self-loops
+    assert g.nnz == 0 and g.selfloops == 3
+    with pytest.raises(ValueError):
+        O.canonical_csr_big(3, np.array([0]), np.array([3]))
+    import synth   # R-MAT multigraph with hubs, duplicates and self-loops, u8 weights
+    u, v = synth.rmat(12, 16, 0.57, 0.19, 0.19, 1)
+    w = synth.weights_u8(u, v, 1)
+    a, b = O.canonical_csr(1 << 12, u, v, w), O.canonical_csr_big(1 << 12, u, v, w, block_entries=5000)
+    assert np.array_equal(a.row_ptr, b.row_ptr) and np.array_equal(a.col, b.col) and np.array_equal(a.w, b.w)
+    assert (a.selfloops, a.duplicates) == (b.selfloops, b.duplicates)
+
+
+def test_quantities_c_p5_exact_rationals_and_path2():
+    """The C definitions against the paper's P5 example (s = e1, exact rationals, golden) and the
+    2-node path (golden)."""
+    gold = _golden_fracs("p5_e1_quantities.txt")
+    g = O.canonical_csr_big(5, np.arange(4), np.arange(1, 5))
+    s = np.eye(5)[0]
+    q = O.quantities_c(g, s, O.solve_dense(g, s))
+    for k in ["CI", "D", "P", "C", "Idc", "PDI"]:
+        assert q[k] == pytest.approx(float(gold[k]), rel=1e-14, abs=0), k
+    gold = _golden_fracs("path2_quantities.txt")
+    g = O.canonical_csr_big(2, np.array([0]), np.array([1]))
+    q = O.quantities_c(g, np.array([1.0, 0.0]), np.array([2 / 3, 1 / 3]))
+    for k in ["CI", "D", "P", "C", "Idc"]:
+        assert q[k] == pytest.approx(float(gold[k]), rel=1e-15), k
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_quantities_c_matches_definitions(seed):
+    """Against the fsum definitions on random weighted graphs (both read Defs. 3.1-3.5) and the
+    identities C_I + 2D + C = s^T s (R2), I_dc = s^T z, PDI = s_bar^T z_bar."""
+    rng = np.random.default_rng(seed)
+    n = 300
+    g = random_graph(n, 1500, rng, weighted=seed % 2 == 1)
+    s = rng.uniform(0, 1, n)
+    z = O.solve_dense(g, s)
+    a, b = O.quantities(g, s, z), O.quantities_c(g, s, z)
+    for k in ["CI", "D", "P", "C", "Idc", "PDI", "sz", "sbzb", "ss"]:
+        assert b[k] == pytest.approx(a[k], rel=1e-13), k
+    assert b["CI"] + 2 * b["D"] + b["C"] == pytest.approx(b["ss"], rel=1e-11)
+    assert b["Idc"] == pytest.approx(b["sz"], rel=1e-11)
+    assert b["PDI"] == pytest.approx(b["sbzb"], rel=1e-11)
+
+
+def _permute_ref(g, n2o, o2n):
+    lens = np.diff(g.row_ptr)[n2o]
+    rp = np.zeros(g.n + 1, np.int64)
+    rp[1:] = np.cumsum(lens)
+    idx = np.concatenate([np.arange(g.row_ptr[r], g.row_ptr[r + 1]) for r in n2o]) if g.nnz else np.zeros(0, int)
+    return rp, o2n[g.col[idx]].astype(np.int32), (None if g.w is None else g.w[idx])
+
+
+@pytest.mark.parametrize("weighted", [False, True])
+def test_csr_permute_matches_transcription_and_invariance(weighted):
+    """P A P^T against a numpy transcription; the quantities of the permuted graph with P s equal
+    those of the original (P:L88 L -> P L P^T; sums over vertices and edges)."""
+    rng = np.random.default_rng(3)
+    n = 200
+    g = random_graph(n, 900, rng, weighted=weighted)
+    n2o = rng.permutation(n).astype(np.int32)
+    o2n = np.empty(n, np.int32)
+    o2n[n2o] = np.arange(n, dtype=np.int32)
+    h = O.csr_permute(g, n2o, o2n)
+    rp, cl, wl = _permute_ref(g, n2o, o2n)
+    assert np.array_equal(h.row_ptr, rp) and np.array_equal(h.col, cl)
+    if weighted:
+        assert np.array_equal(h.w, wl)
+    s = rng.uniform(0, 1, n)
+    qa = O.quantities_c(g, s, O.solve_dense(g, s))
+    hs = O.canonical_csr(n, h.rows(), h.col, h.w)   # re-sorted columns for the dense oracle
+    qb = O.quantities_c(hs, s[n2o], O.solve_dense(hs, s[n2o]))
+    for k in ["CI", "D", "P", "C", "Idc", "PDI"]:
+        assert qb[k] == pytest.approx(qa[k], rel=1e-12), k
