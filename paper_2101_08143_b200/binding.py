@@ -270,7 +270,9 @@ def use_torch_allocator(enable: bool = True):
     def _alloc(nbytes, stream, ctx):
         try:
             return torch.cuda.caching_allocator_alloc(int(nbytes), torch.cuda.current_device(), stream=int(stream or 0))
-        except Exception:   # OOM -> NULL -> the library reports FJ_E_CUDA
+        except Exception as e:   # OOM -> NULL -> the library reports an allocation failure
+            import sys
+            print(f"fj torch allocator: {e!r}", file=sys.stderr)
             return None
 
     def _free(ptr, nbytes, stream, ctx):

@@ -71,9 +71,6 @@ int batch_min_k();
 int l2_hint();
 // padded row width of the small-k engine for k = 3 (default 4; FJ_VEC_PAD=0: unpadded 3; spmv_vec.cu)
 int vec_pad3();
-// hot-row threshold of the small-k product's L2 eviction hints (FJ_HOT_MB: the hot prefix of the
-// gathered [n][kp] block in MB; unset or 0: no hints, -1)
-int64_t gather_hot_rows(int64_t n, int kp);
 
 // ---------------------------------------------------------------- device workspace per solve
 struct SolveWs;   // pcg.cu

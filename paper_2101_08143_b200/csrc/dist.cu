@@ -610,7 +610,7 @@ fj_status dist_stats_combine(const fj_graph* g, int k, double* dev4k /* [k][4] d
     FJ_CK(cudaMemcpyAsync(dev4k, h.data(), sizeof(double) * 4 * k, cudaMemcpyHostToDevice, st));
     FJ_CK(cudaStreamSynchronize(st));
   }
-  cudaFreeAsync(tmp, st);
+  dfree_on(tmp, st);
   return s3;
 }
 
@@ -867,7 +867,7 @@ fj_status fj_graph_create_dist(fj_comm* comm, int rank, int64_t n_global, const 
     s = allreduce(d, tmp, 1, RED_MAX, st);
     cudaMemcpyAsync(&d->d_max_global, tmp, sizeof(double), cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
-    cudaFreeAsync(tmp, st);
+    dfree_on(tmp, st);
     if (s != FJ_OK) { fj_graph_destroy(g); return s; }
   }
   *out = g;

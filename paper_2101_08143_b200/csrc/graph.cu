@@ -44,16 +44,6 @@ int vec_pad3() {
   return v;
 }
 
-int64_t gather_hot_rows(int64_t n, int kp) {
-  static const double mb = [] {
-    const char* e = getenv("FJ_HOT_MB");
-    return e ? atof(e) : 0.0;
-  }();
-  if (!(mb > 0.0)) return -1;
-  const int64_t rows = (int64_t)(mb * 1048576.0 / (8.0 * kp));
-  return rows < n ? rows : n;
-}
-
 void phase_tick(const char* label, cudaStream_t st) {
   static const bool on = getenv("FJ_TIMING") != nullptr;
   if (!on) return;
@@ -408,7 +398,7 @@ fj_status fj_graph_create(int64_t n, int64_t nnz, const int64_t* row_ptr, const 
     if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
     if (ce != cudaSuccess) s = cuda_fail(ce, "stats readback", __FILE__, __LINE__);
   }
-  cudaFreeAsync(st_d, st);
+  dfree_on(st_d, st);
   if (s != FJ_OK) return cleanup(s);
   if (validate && h.bad_flags) {
     if (h.bad_flags & 1) return cleanup(fail(FJ_E_NOT_SIMPLE, "CSR not simple: column out of range, self-loop, or columns not strictly ascending"));

@@ -252,7 +252,7 @@ static fj_status stats_cols(fj_graph* g, SolveWs* w, int k, const double* s, std
     FJ_CK(dmalloc(&part, sizeof(double) * 256 * (size_t)w->grid_elem, st));
     k_stats_wide<<<w->grid_elem, STPB, 0, st>>>(g->n, k, s, part, w->elem_ticket, w->stat, d_bad);
     FJ_CK_LAUNCH();
-    FJ_CK(cudaFreeAsync(part, st));
+    dfree_on(part, st);
   } else {
     for (int c = 0; c < k; ++c) {
       k_stats<<<w->grid_elem, STPB, 0, st>>>(g->n, s, k, c, w->elem_part, w->elem_ticket, w->stat + 4 * c, d_bad);
@@ -262,7 +262,7 @@ static fj_status stats_cols(fj_graph* g, SolveWs* w, int k, const double* s, std
   if (is_dist(g)) FJ_TRY(dist_stats_combine(g, k, w->stat, st));   // global over the ranks' slices
   st4.assign(4 * k, 0.0);
   FJ_CK(cudaMemcpyAsync(st4.data(), w->stat, sizeof(double) * 4 * k, cudaMemcpyDeviceToHost, st));
-  FJ_CK(cudaFreeAsync(d_bad, st));
+  dfree_on(d_bad, st);
   FJ_CK(cudaStreamSynchronize(st));
   for (int c = 0; c < k; ++c)   // k_stats poisons the sum with NaN when a slice held NaN / Inf
     if (std::isnan(st4[4 * c])) return fail(FJ_E_NONFINITE_INPUT, "opinion vector contains NaN or Inf");

@@ -61,33 +61,6 @@ template <> __device__ __forceinline__ DVec<3> ld_vec<3>(const double* p) {
   r.v[2] = odd ? b : c;
   return r;
 }
-// Gathers with an L2 eviction priority (ApplyOpV with a hot-row threshold): rows below the
-// threshold (the high-degree prefix of a degree-ordered p) are kept (evict_last), the rest are
-// streamed (evict_first), so the cold rows stop displacing the hot ones from the L2.
-__device__ __forceinline__ uint64_t pol_evict_last() {
-  uint64_t p;
-  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ uint64_t pol_evict_first() {
-  uint64_t p;
-  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-template <int KP> __device__ __forceinline__ DVec<KP> ld_vec_pol(const double* p, uint64_t pol);
-template <> __device__ __forceinline__ DVec<4> ld_vec_pol<4>(const double* p, uint64_t pol) {
-  DVec<4> r;
-  asm volatile("ld.global.L2::cache_hint.v4.f64 {%0, %1, %2, %3}, [%4], %5;"
-               : "=d"(r.v[0]), "=d"(r.v[1]), "=d"(r.v[2]), "=d"(r.v[3]) : "l"(p), "l"(pol));
-  return r;
-}
-template <> __device__ __forceinline__ DVec<2> ld_vec_pol<2>(const double* p, uint64_t pol) {
-  DVec<2> r;
-  asm volatile("ld.global.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(r.v[0]), "=d"(r.v[1]) : "l"(p), "l"(pol));
-  return r;
-}
-template <> __device__ __forceinline__ DVec<3> ld_vec_pol<3>(const double* p, uint64_t) { return ld_vec<3>(p); }
-
 template <int KP> __device__ __forceinline__ void st_vec(double* p, const DVec<KP>& v);
 template <> __device__ __forceinline__ void st_vec<3>(double* p, const DVec<3>& v) {
   const bool odd = (reinterpret_cast<uintptr_t>(p) & 8) != 0;
@@ -158,13 +131,9 @@ struct ApplyOpV {
   int k;
   double* dot_out = nullptr;   // optional: p_c^T q_c per column (distributed: local part)
   int alpha_on_device = 1;     // 0 (distributed): alpha after the allreduce of dot_out
-  int64_t hot = -1;            // >= 0: rows j < hot gathered evict_last, the others evict_first
   __device__ __forceinline__ bool skip() const { return sc && *(volatile int32_t*)&sc->done; }
   __device__ __forceinline__ bool wants_xi() const { return true; }
-  __device__ __forceinline__ V gather(int32_t j) const {
-    if (hot < 0) return ld_vec<KP>(x + (int64_t)j * KP);
-    return ld_vec_pol<KP>(x + (int64_t)j * KP, j < hot ? pol_evict_last() : pol_evict_first());
-  }
+  __device__ __forceinline__ V gather(int32_t j) const { return ld_vec<KP>(x + (int64_t)j * KP); }
   __device__ __forceinline__ V row_value(int64_t i) const { return ld_vec<KP>(x + i * KP); }
   __device__ __forceinline__ const V* xi_base() const { return reinterpret_cast<const V*>(x); }
   __device__ __forceinline__ void add(double (&a)[NA], double w, const V& xj, const V&) const {
@@ -681,7 +650,6 @@ static fj_status vec_apply_padded(const fj_graph* g, const VecWs* w, const doubl
   return by_wtype<KP>(g, [&](auto wt) {
     constexpr int WT = decltype(wt)::value;
     ApplyOpV<WT, KP, KQ> op{x, y, g->deg, opL, sc, w->k};
-    op.hot = gather_hot_rows(g->n, KP);
     int nl = 0;
     FJ_CK(launch_product<WT>(g, w->ts, w->grid_max, op, st, &nl));
     if (!g_capturing) count_launch(nl);

@@ -9,6 +9,11 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
+def _strip_c_comments(txt):
+    """Drop /* */ blocks (across lines) and // line comments (to the end of their line only)."""
+    return re.sub(r"//[^\n]*", "", re.sub(r"/\*.*?\*/", "", txt, flags=re.S))
+
+
 def declared_functions():
     src = open(os.path.join(ROOT, "include", "fj.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
@@ -59,13 +64,23 @@ def test_set_allocator_argument_rules_without_gpu():
     assert fj.allocator_live_blocks() == 0
 
 
+def test_device_frees_go_through_the_allocator_hook():
+    """Workspace memory may come from a caller allocator (fj_set_allocator): only graph.cu's
+    dfree_on may call cudaFreeAsync (a raw free of a torch block would release its whole segment)."""
+    csrc = os.path.join(ROOT, "paper_2101_08143_b200", "csrc")
+    for f in os.listdir(csrc):
+        code = _strip_c_comments(open(os.path.join(csrc, f)).read())
+        n = len(re.findall(r"\bcudaFreeAsync\s*\(", code))
+        assert n == (1 if f == "graph.cu" else 0), (f, n)
+
+
 def test_product_path_does_not_import_oracle():
     pkg = os.path.join(ROOT, "paper_2101_08143_b200")
     for dirpath, _, files in os.walk(pkg):
         for f in files:
             if f.endswith((".py", ".cu", ".cuh", ".h")):
                 txt = open(os.path.join(dirpath, f)).read()
-                code = re.sub(r"#.*|//.*|/\*.*?\*/", "", txt, flags=re.S)
+                code = _strip_c_comments(txt) if not f.endswith(".py") else re.sub(r"#.*", "", txt)
                 assert "oracle" not in code.lower(), f
 
 
