@@ -105,60 +105,93 @@ def dist_init():
     return ws, rank, local
 
 
-def cpu_baseline(wl, g, seconds=12.0):
-    """The oracle's Jacobi-PCG (plain C/OpenMP, as it stands) on the full workload graph: a bounded
-    sample of PCG iterations timed on the host cores.  Same unit as the line's metric."""
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def oracle_ttq(g, s, rtol):
+    """The oracle as it stands: Jacobi-PCG to `rtol` on the true residual (restarts included), then
+    the quantities by their definitions.  Returns (seconds, solve seconds, iterations)."""
     import oracle as O
-    s = np.ascontiguousarray(wl.S[:, 0])
     t = time.perf_counter()
-    O.pcg_fixed_iters(g, s, 1)                       # 1 iteration (+ setup/residual passes)
-    t1 = time.perf_counter() - t
-    iters = int(max(2, min(200, seconds / max(t1, 1e-3))))
-    t = time.perf_counter()
-    O.pcg_fixed_iters(g, s, iters)
-    dt = time.perf_counter() - t
+    z, info = O.solve_pcg(g, s, tol=rtol)
+    t_solve = time.perf_counter() - t
+    O.quantities_c(g, s, z)
+    return time.perf_counter() - t, t_solve, info["iterations"]
+
+
+def cpu_baseline(wl, g, rtol, one_core_budget_s=40.0):
+    """SURVEY §8(d) protocol: the oracle's time-to-quantities at the GPU's rtol on all host cores
+    (every opinion column of the workload, up to 3) and on one core (column 0, when its estimate
+    fits the budget), with the CPU model; value = CG-iteration GB/s of the all-core solves."""
+    import oracle as O
     wb = 0 if wl.w is None else wl.w.dtype.itemsize
-    B = canonical_bytes(g.n, g.nnz, wb, 1)
-    return {"value": B * iters / dt / 1e9, "unit": "GB/s", "cores": O.num_threads(), "kind": "oracle",
-            "sample": f"{iters} oracle Jacobi-PCG iterations (column 0, {wl.kinds[0]}) on the full {wl.name} graph "
-                      f"(n={g.n}, nnz={g.nnz}); includes the oracle's per-call setup and true-residual pass; "
-                      f"{dt:.1f} s"}
+    B1 = canonical_bytes(g.n, g.nnz, wb, 1)
+    allc = O.num_threads()
+    cols = []
+    tot_solve, tot_it = 0.0, 0
+    for c in range(min(wl.k, 3)):
+        s = np.ascontiguousarray(wl.S[:, c])
+        ttq, t_solve, it = oracle_ttq(g, s, rtol)
+        cols.append({"opinions": wl.kinds[c], "time_to_quantities_ms": 1e3 * ttq, "iterations": it})
+        tot_solve += t_solve
+        tot_it += it
+    one = None
+    est = tot_solve / max(len(cols), 1) * allc
+    if est <= one_core_budget_s:
+        O.set_num_threads(1)
+        try:
+            ttq1, ts1, it1 = oracle_ttq(g, np.ascontiguousarray(wl.S[:, 0]), rtol)
+        finally:
+            O.set_num_threads(allc)
+        one = {"cores": 1, "time_to_quantities_ms": 1e3 * ttq1, "iterations": it1, "value": B1 * it1 / ts1 / 1e9}
+    return {"value": B1 * tot_it / tot_solve / 1e9, "unit": "GB/s", "cores": allc, "kind": "oracle",
+            "cpu_model": cpu_model(), "rtol": rtol, "per_column": cols, "one_core": one,
+            "sample": f"oracle Jacobi-PCG to rtol {rtol:g} (true residual, restarts included) + the quantities "
+                      f"by definition, per opinion column ({len(cols)} of {wl.k}) of the full {wl.name} graph "
+                      f"(n={g.n}, nnz={g.nnz}), CSR built untimed; value = B(1) x iterations / solve time"}
 
 
 def run_reference(args, ws, rank):
-    """--impl reference: the CPU oracle as it stands, on this arm's config / metric / unit."""
+    """--impl reference: the CPU oracle as it stands, on this arm's config / metric / unit.  Each
+    step = the oracle's time-to-quantities of opinion column 0 at the GPU's rtol (all host cores)."""
     if rank != 0:
         return 0
     import oracle as O
     import synth
     wl = synth.make_config(args.config)
-    g = O.canonical_csr(wl.n, wl.u, wl.v, wl.w)      # setup, untimed
+    big = wl.name in ("c4", "c5")
+    g = O.canonical_csr_big(wl.n, wl.u, wl.v, wl.w) if big else O.canonical_csr(wl.n, wl.u, wl.v, wl.w)
     wb = 0 if wl.w is None else wl.w.dtype.itemsize
     B = canonical_bytes(g.n, g.nnz, wb, 1)
     s = np.ascontiguousarray(wl.S[:, 0])
-    t = time.perf_counter()
-    O.pcg_fixed_iters(g, s, 1)
-    t1 = time.perf_counter() - t
-    # each step a bounded sample: the whole --steps K --warmup W run stays around a minute or two
-    per_step = min(args.ref_seconds, 90.0 / max(1, args.steps + args.warmup))
-    iters = int(max(1, min(50, per_step / max(t1, 1e-3))))
     for _ in range(args.warmup):
-        O.pcg_fixed_iters(g, s, iters)
-    times = []
+        oracle_ttq(g, s, args.rtol)
+    times, solve_s, iters = [], 0.0, 0
     for _ in range(args.steps):
-        t = time.perf_counter()
-        O.pcg_fixed_iters(g, s, iters)
-        times.append(time.perf_counter() - t)
+        ttq, t_solve, it = oracle_ttq(g, s, args.rtol)
+        times.append(ttq)
+        solve_s += t_solve
+        iters += it
     tot = sum(times)
-    value = B * iters * args.steps / tot / 1e9
-    sample = (f"each step: {iters} oracle Jacobi-PCG iterations (column 0) on the full {wl.name} graph "
-              f"(n={g.n}, nnz={g.nnz}), CSR built once untimed")
+    value = B * iters / solve_s / 1e9
+    sample = (f"each step: the oracle's time-to-quantities of opinion column 0 ({wl.kinds[0]}) at rtol {args.rtol:g} "
+              f"(Jacobi-PCG, true-residual restarts, definitions) on the full {wl.name} graph (n={g.n}, "
+              f"nnz={g.nnz}), CSR built once untimed")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{wl.name}: {wl.desc}", "n": g.n, "nnz": g.nnz},
+            "config": {"workload": f"{wl.name}: {wl.desc}", "n": g.n, "nnz": g.nnz, "rtol": args.rtol},
+            "time_to_quantities_ms": 1e3 * statistics.median(times),
             "cpu_baseline": {"value": value, "unit": "GB/s", "cores": O.num_threads(), "kind": "oracle",
-                             "sample": sample},
+                             "cpu_model": cpu_model(), "sample": sample},
             "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -178,9 +211,9 @@ def main():
                          "the row-partitioned N>1 path always builds in the input labels")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the per-distribution k = 1 lines and the gather probe (profiling runs)")
     ap.add_argument("--spmv-reps", type=int, default=20)
-    ap.add_argument("--ref-seconds", type=float, default=10.0)
-    ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cuda-graph", action="store_true",
                     help="host-driven PCG loop (same kernels); ncu cannot see kernels inside conditional graphs")
     args = ap.parse_args()
@@ -306,7 +339,7 @@ def main():
     # the SpMV's real bound: random gathers (one L2 sector request per nonzero), measured live by
     # fj_probe_gather on the same vector size, index count and gather width
     gather_roof = None
-    if not dist_mode:
+    if not dist_mode and not args.no_extras:
         width = 1 if kb == 1 else (2 if kb == 2 else 4)
         probe = binding.probe_gather(n, nnz, width=width, reps=5)
         ach = nnz / (spmv_ms / 1e3)
@@ -315,10 +348,35 @@ def main():
                        "note": "peak = fj_probe_gather: nnz uniform random int32 indices streamed once, one "
                                f"{8 * width}-byte gather each from an n-row vector, no row logic; achieved = "
                                "nnz / SpMV launch time"}
-    traffic = None
+    # ncu DRAM bytes of one launch of this product, only if captured for this exact config, k,
+    # vertex order and CUDA build (profiles/ncu_traffic.json, tools/record_traffic.py)
+    from paper_2101_08143_b200 import build as FB
+    traffic, traffic_key = None, f"{args.config}/k{kb}/{order}/{FB.source_hash()}"
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tp):
-        traffic = json.load(open(tp)).get(args.config, {}).get("spmv_dram_bytes_per_launch")
+    if os.path.exists(tp) and not dist_mode:
+        traffic = json.load(open(tp)).get(traffic_key, {}).get("spmv_dram_bytes_per_launch")
+
+    # C3 also as separate k = 1 solves, one per opinion distribution (outside the
+    # timed region; same graph build, each column's own solve + quantities pass)
+    per_dist = None
+    if not dist_mode and k > 1 and k <= 4 and not args.no_extras:
+        G = fj.Graph.from_edges(n, u, v, w, order=order)
+        per_dist = []
+        for c in range(k):
+            sc = S[:, c].contiguous()
+            G.approxim(sc, opts=opts)
+            reps1 = []
+            for _ in range(3):
+                flush.fill_(1)
+                _, q1, r1 = G.approxim(sc, opts=opts)
+                reps1.append(r1)
+            r1 = min(reps1, key=lambda r: r["ms"])
+            B1 = canonical_bytes(n, nnz, wb, 1)
+            per_dist.append({"opinions": wl.kinds[c], "iterations": r1["iterations"],
+                             "cg_gbs": B1 * r1["iterations_total"] / (r1["ms_loop"] / 1e3) / 1e9,
+                             "time_to_quantities_ms": r1["ms"], "rel_res_true": r1["rel_res_true"],
+                             "D": q1[0]["D"]})
+        G.close()
 
     line = {
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": ws, "steps": args.steps,
@@ -332,11 +390,12 @@ def main():
                    "bytes_per_iteration": B, "fraction_of_measured_hbm": value / peak},
         "time_to_quantities_ms": statistics.median(ttq_ms),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": None if dist_mode else traffic,
+                     "traffic": None if dist_mode else traffic, "traffic_key": traffic_key,
                      "kernel": ("whole distributed PCG iteration per rank (B(k)/N per iteration time)" if dist_mode
                                 else spmv_kernel_name(kb)),
                      "algorithmic_bytes_per_launch": Bs, "launch_ms": spmv_ms, "peak_source": peak_src},
         "gather_roofline": gather_roof,
+        "per_distribution_k1": per_dist, "build": FB.source_hash(),
         "clocks": clocks, "gpu_launches": launches1 - launches0,
         "cub_calls": cub1 - cub0, "wall_s_timed_region": wall,
         "quantities_step0": {kk: results[0][0][0][kk] for kk in ["CI", "D", "P", "C", "Idc", "PDI"]},
@@ -408,8 +467,9 @@ def main():
 
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         import oracle as O
-        g = O.canonical_csr(wl.n, wl.u, wl.v, wl.w)
-        line["cpu_baseline"] = cpu_baseline(wl, g, args.cpu_seconds)
+        big = wl.name in ("c4", "c5")
+        g = O.canonical_csr_big(wl.n, wl.u, wl.v, wl.w) if big else O.canonical_csr(wl.n, wl.u, wl.v, wl.w)
+        line["cpu_baseline"] = cpu_baseline(wl, g, args.rtol)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if ws > 1:

@@ -80,6 +80,8 @@ def _L():
         lib.oracle_pcg_fixed_iters.argtypes = [i64, ptr, ptr, cint, ptr, ptr, i64, ptr]
         lib.oracle_pcg_fixed_iters.restype = cint
         lib.oracle_num_threads.restype = cint
+        lib.oracle_set_num_threads.argtypes = [cint]
+        lib.oracle_set_num_threads.restype = None
         lib.oracle_csr_blocked.argtypes = [i64, i64, ptr, ptr, cint, ptr, i64, ptr, ptr, ptr, ptr]
         lib.oracle_csr_blocked.restype = i64
         lib.oracle_quantities.argtypes = [i64, ptr, ptr, cint, ptr, ptr, ptr, ptr]
@@ -96,6 +98,10 @@ def _p(a):
 
 def num_threads() -> int:
     return int(_L().oracle_num_threads())
+
+
+def set_num_threads(t: int) -> None:
+    _L().oracle_set_num_threads(int(t))
 
 
 # --------------------------------------------------------------------------- graph

@@ -41,6 +41,15 @@ int oracle_num_threads(void) {
 #endif
 }
 
+/* Thread count of the oracle's OpenMP loops (bench.py times the oracle on all cores and on one). */
+void oracle_set_num_threads(int t) {
+#ifdef _OPENMP
+  if (t > 0) omp_set_num_threads(t);
+#else
+  (void)t;
+#endif
+}
+
 int oracle_degrees(int64_t n, const int64_t* row_ptr, int wtype, const void* w, double* d) {
 #pragma omp parallel for schedule(static)
   for (int64_t i = 0; i < n; ++i) {

@@ -34,8 +34,25 @@ def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 
 
+def source_hash() -> str:
+    """Identity of the CUDA sources a libfj.so is built from (csrc/*.cu, *.cuh, include/fj.h): keys
+    the ncu evidence in profiles/ncu_traffic.json so bench.py never attaches a stale capture."""
+    import hashlib
+    h = hashlib.sha256()
+    files = sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cuh")))
+    for f in files + [os.path.join(ROOT, "include", "fj.h")]:
+        h.update(os.path.basename(f).encode())
+        h.update(open(f, "rb").read())
+    return h.hexdigest()[:16]
+
+
 def needs_build() -> bool:
+    """Rebuild when libfj.so is missing or was built from other sources (content hash recorded
+    beside it at build time), or when a source is newer than it."""
     if not os.path.exists(SO):
+        return True
+    hp = SO + ".srchash"
+    if not os.path.exists(hp) or open(hp).read().strip() != source_hash():
         return True
     t = os.path.getmtime(SO)
     deps = sources() + glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(ROOT, "include", "fj.h"), __file__]
@@ -75,6 +92,9 @@ def build(force: bool = False, verbose: bool = False, so: str = SO, defines=()) 
     subprocess.check_call([NVCC, "-shared", "-cudart", "static", "-gencode", "arch=compute_100a,code=sm_100a",
                            *objs, "-o", tmp, "-ldl"])
     os.replace(tmp, so)
+    if so == SO and not defines:
+        with open(SO + ".srchash", "w") as f:
+            f.write(source_hash() + "\n")
     return so
 
 

@@ -19,13 +19,14 @@ ap.add_argument("--k", type=int, default=3)
 ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--scale", type=int, default=None)
 ap.add_argument("--n", type=int, default=None)
+ap.add_argument("--order", default="natural", choices=["natural", "degree"])
 a = ap.parse_args()
 kinds = (["uniform", "exponential", "powerlaw"] * 22)[:a.k]
 wl = synth.make_config(a.config, kinds=kinds, scale=a.scale, n=a.n)
 S = torch.from_numpy(wl.S[:, :a.k].copy()).cuda()
 u, v = torch.from_numpy(wl.u).cuda(), torch.from_numpy(wl.v).cuda()
 w = None if wl.w is None else torch.from_numpy(wl.w).cuda()
-G = fj.Graph.from_edges(wl.n, u, v, w)
+G = fj.Graph.from_edges(wl.n, u, v, w, order=a.order)
 opts = fj.SolveOpts.make(use_cuda_graph=not os.environ.get("FJV_NO_GRAPH"))
 z, q, rep = G.approxim(S if a.k > 1 else S[:, 0].contiguous(), opts=opts)
 z, q, rep = G.approxim(S if a.k > 1 else S[:, 0].contiguous(), opts=opts)
