@@ -50,6 +50,24 @@ inline void dfree(void* p) {
 // FJ_TIMING=1: host-side phase timestamps on stderr (diagnostics; synchronises the stream)
 void phase_tick(const char* label, cudaStream_t st);
 
+// Device-side invariant checks of the debug build (-DFJ_DEBUG_CHECKS; tools/sanitize_cases.py runs
+// every engine with them, since compute-sanitizer is closed on this GPU pool): a failed check
+// prints the condition and traps (the launch fails with an illegal-instruction error).
+#ifdef FJ_DEBUG_CHECKS
+#define FJ_DCHECK(c)                                                                   \
+  do {                                                                                 \
+    if (!(c)) {                                                                        \
+      printf("FJ_DCHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #c, \
+             (int)blockIdx.x, (int)threadIdx.x);                                       \
+      __trap();                                                                        \
+    }                                                                                  \
+  } while (0)
+#else
+#define FJ_DCHECK(c) \
+  do {               \
+  } while (0)
+#endif
+
 // kernel launch accounting (fj_kernel_launches)
 void count_launch(int64_t n = 1);
 void count_cub(int64_t n = 1);

@@ -149,6 +149,7 @@ __device__ __forceinline__ void b_accumulate(const TileSched& sc, const BatchArg
     double wl = 1.0;
     if (lane < nb) {
       cl = __ldg(sc.col + kk + lane);
+      FJ_DCHECK(cl >= 0 && cl < sc.ncol);
       if (WT != FJ_W_UNIT) wl = WeightT<WT>::get(sc.w, kk + lane);
     }
     double v0[NB], v1[NB];
@@ -760,6 +761,7 @@ __device__ __forceinline__ void q_accumulate(const TileSched& sc, const QuantArg
     double wl = 1.0;
     if (lane < nb) {
       cl = __ldg(sc.col + kk + lane);
+      FJ_DCHECK(cl >= 0 && cl < sc.ncol);
       if (WT != FJ_W_UNIT) wl = WeightT<WT>::get(sc.w, kk + lane);
     }
     double v0[NB], v1[NB];

@@ -89,6 +89,7 @@ __host__ __device__ __forceinline__ int tile_nnz(uint32_t info) { return (int)((
 
 struct TileSched {
   int64_t n, nnz;
+  int64_t ncol;                               // gathered rows: n, or n_loc + ghosts on a rank
   const int64_t* __restrict__ row_ptr;
   const int32_t* __restrict__ col;
   const void* __restrict__ w;
@@ -106,9 +107,11 @@ struct TileSched {
 __device__ __forceinline__ int32_t ld_col(const TileSched& sc, int64_t p) { return __ldg(sc.col + p); }
 __device__ __forceinline__ int64_t ld_rp(const TileSched& sc, int64_t i) { return __ldg(sc.row_ptr + i); }
 
+int64_t dist_n_ghost(const fj_graph* g);   // dist.cu
 inline TileSched make_sched(const fj_graph* g, const Sched& S) {
   TileSched s;
-  s.n = g->n; s.nnz = g->nnz; s.row_ptr = g->row_ptr; s.col = g->col; s.w = g->w;
+  s.n = g->n; s.nnz = g->nnz;
+  s.ncol = g->n + dist_n_ghost(g); s.row_ptr = g->row_ptr; s.col = g->col; s.w = g->w;
   s.items = reinterpret_cast<const ItemMeta*>(S.items);
   s.n_items = S.n_items;
   s.long_nchunks = S.long_nchunks; s.long_item0 = S.long_item0;
@@ -207,6 +210,8 @@ __device__ __forceinline__ void t_tile(const TileSched& sc, const Op& op, const 
   const int R = tile_rows(cur.info);
   const int N = tile_nnz(cur.info);
   const int64_t r0 = cur.r0, k0 = cur.k0;
+  FJ_DCHECK(R >= 1 && R <= Op::TILE_ROWS && N >= 0 && R + N <= 32 * Op::ITEMS);
+  FJ_DCHECK(r0 >= 0 && r0 + R <= sc.n && k0 >= 0 && k0 + N <= sc.nnz);
   const int32_t* s_col = (PRE && pre.col) ? pre.col : s_col_own;
   const V* s_xi = (PRE && pre.xi) ? pre.xi : s_xi_own;
 #pragma unroll
@@ -239,6 +244,7 @@ __device__ __forceinline__ void t_tile(const TileSched& sc, const Op& op, const 
     xv[j] = Op::vzero();
     wv[j] = 1.0;
     if (k < nz_e) {
+      FJ_DCHECK(s_col[k] >= 0 && s_col[k] < sc.ncol);
       xv[j] = op.gather(s_col[k]);
       if (WEIGHTED) wv[j] = (WS)WeightT<WT>::get(sc.w, k0 + k);
     }
@@ -374,6 +380,8 @@ __device__ __forceinline__ void pf_issue(const TileSched& sc, const Op& op, cons
   const PfRange r = pf_range(8 * ((int64_t)m.r0 + 1), 8 * ((int64_t)m.r0 + R + 1));
   PfRange x{0, 0};
   if (L.xi >= 0) x = pf_range((int64_t)sizeof(V) * m.r0, (int64_t)sizeof(V) * (m.r0 + R));
+  FJ_DCHECK(c.b1 - c.b0 <= PfSlot<Op>::COL_BYTES && r.b1 - r.b0 <= PfSlot<Op>::RP_BYTES &&
+            x.b1 - x.b0 <= PfSlot<Op>::XI_BYTES);
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic reads of the slot are done
   mbar_expect_tx(bar, (uint32_t)((c.b1 - c.b0) + (r.b1 - r.b0) + (x.b1 - x.b0)));
   if (c.b1 > c.b0)
@@ -429,8 +437,10 @@ __device__ __forceinline__ void wc_item(const TileSched& sc, const Op& op, const
       w8[u] = (WEIGHTED && kk < ke) ? WeightT<WT>::get(sc.w, kk) : 1.0;
     }
 #pragma unroll
-    for (int u = 0; u < 8; ++u)
+    for (int u = 0; u < 8; ++u) {
+      FJ_DCHECK(c8[u] < sc.ncol);
       if (c8[u] >= 0) op.add(a, w8[u], op.gather(c8[u]), xi);
+    }
   }
 #pragma unroll
   for (int f = 0; f < NA; ++f) a[f] = warp_sum(a[f]);
