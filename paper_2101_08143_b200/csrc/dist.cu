@@ -6,9 +6,10 @@
 //  Ghosts     fj_dist_ghosts: sorted unique off-rank columns = the halo, grouped by owner rank.
 //  Graph      fj_graph_create_dist: columns renumbered (own -> [0, n_loc), ghost -> n_loc + idx);
 //             degrees / schedule on the local rows (full rows, so d_i is exact); halo plan.
-//  Iteration  pack p[send_idx] -> grouped ncclSend/ncclRecv into p[n_loc..] -> row engine
-//             q = (I+L)p on local rows -> allreduce(p^T q) -> update (x, r, rho', ||r||^2)
-//             -> allreduce(rho', ||r||^2) -> beta / convergence (identical on all ranks) -> p.
+//  Iteration  Chronopoulos-Gear PCG (dist_solve_cg, below): one elementwise step, the product of
+//             the preconditioned residual with its halo (grouped ncclSend/ncclRecv on a comm
+//             stream) overlapped with the own-column pass, ONE allreduce of 3 KP doubles; the
+//             iteration is captured in a CUDA graph with the NCCL calls.
 //  Transports NCCL (real ranks) or LOOPBACK (virtual ranks = host threads of one process on one
 //             device; collectives become barrier-ordered device copies / host-ordered sums), so
 //             the distributed algorithm is tested on one GPU without kernels waiting on kernels.
@@ -22,6 +23,7 @@
 #include <cub/cub.cuh>
 
 #include "ops.cuh"
+#include "vec.cuh"
 #include "workspace.cuh"
 
 // NCCL types only (the library dlopens libnccl.so.2 at fj_comm_init, the copy torch also loads)
@@ -134,9 +136,11 @@ struct DistInfo {
   unsigned int* elem_ticket = nullptr;
   int grid_elem = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  struct CgWs* cg = nullptr;                         // single-reduction solver (dist_solve_cg)
 };
 
 static DistInfo* D(const fj_graph* g) { return reinterpret_cast<DistInfo*>(g->dist); }
+static void free_cg(DistInfo* d);
 
 // ---------------------------------------------------------------- collectives
 static fj_status allreduce(DistInfo* d, double* buf, int count, RedOp op, cudaStream_t st) {
@@ -311,95 +315,6 @@ __device__ __forceinline__ bool d_reduce(double (&v)[NPART], double* part, unsig
   return true;
 }
 
-// local part of the (re)start: r = s - q (restart) or s, x = 0 (fresh), p = dinv r;
-// red[3..5] = local (r^T y, r^T r, s^T s)
-__global__ void __launch_bounds__(DTPB) k_dinit(int64_t n, const double* __restrict__ s, int64_t ld, int64_t c,
-                                                const double* __restrict__ dinv, const double* __restrict__ q,
-                                                int restart, double* __restrict__ x, double* __restrict__ r,
-                                                double* __restrict__ p, double* red, double* part,
-                                                unsigned int* ticket) {
-  __shared__ double s_red[3 * DTPB / 32];
-  double v[3] = {0.0, 0.0, 0.0};
-  for (int64_t i = blockIdx.x * (int64_t)DTPB + threadIdx.x; i < n; i += (int64_t)gridDim.x * DTPB) {
-    const double si = s[i * ld + c];
-    const double ri = restart ? si - q[i] : si;
-    if (!restart) x[i] = 0.0;
-    const double yi = dinv[i] * ri;
-    r[i] = ri;
-    p[i] = yi;
-    v[0] = fma(ri, yi, v[0]);
-    v[1] = fma(ri, ri, v[1]);
-    v[2] = fma(si, si, v[2]);
-  }
-  if (d_reduce<3>(v, part, ticket, s_red) && threadIdx.x == 0) {
-    red[3] = v[0]; red[4] = v[1]; red[5] = v[2];
-    *ticket = 0u;
-  }
-}
-
-// global scalars after allreduce(red[3..5])
-__global__ void k_dinit_post(const double* red, PcgScalars* sc, double rtol, int max_iter) {
-  sc->rho = red[3];
-  sc->rr = red[4];
-  sc->ss = red[5];
-  sc->tol2 = rtol * rtol * red[5];
-  sc->iter = 0;
-  sc->max_iter = max_iter;
-  sc->converged = red[4] <= sc->tol2 ? 1 : 0;
-  sc->done = (sc->converged || max_iter <= 0) ? 1 : 0;
-  sc->breakdown = 0;
-  sc->alpha = sc->beta = 0.0;
-}
-
-// K_B with alpha = rho / allreduced p^T q (red[0]); red[1..2] = local (rho', ||r||^2)
-__global__ void __launch_bounds__(DTPB) k_dupdate(int64_t n, const double* __restrict__ dinv,
-                                                  const double* __restrict__ p, const double* __restrict__ q,
-                                                  double* __restrict__ x, double* __restrict__ r,
-                                                  const PcgScalars* sc, double* red, double* part,
-                                                  unsigned int* ticket) {
-  __shared__ double s_red[2 * DTPB / 32];
-  if (*(volatile const int32_t*)&sc->done) return;
-  const double pq = red[0];
-  const double alpha = (pq > 0.0 && isfinite(pq)) ? sc->rho / pq : 0.0;
-  double v[2] = {0.0, 0.0};
-  for (int64_t i = blockIdx.x * (int64_t)DTPB + threadIdx.x; i < n; i += (int64_t)gridDim.x * DTPB) {
-    x[i] = fma(alpha, p[i], x[i]);
-    const double ri = fma(-alpha, q[i], r[i]);
-    r[i] = ri;
-    v[0] = fma(ri, dinv[i] * ri, v[0]);
-    v[1] = fma(ri, ri, v[1]);
-  }
-  if (d_reduce<2>(v, part, ticket, s_red) && threadIdx.x == 0) {
-    red[1] = v[0]; red[2] = v[1];
-    *ticket = 0u;
-  }
-}
-
-// beta / convergence from the allreduced red[0..2]; identical on every rank
-__global__ void k_dpost(const double* red, PcgScalars* sc) {
-  if (sc->done) return;
-  const double pq = red[0];
-  if (!(pq > 0.0) || !isfinite(pq)) { sc->breakdown = 1; sc->done = 1; return; }
-  sc->pq = pq;
-  sc->alpha = sc->rho / pq;
-  sc->beta = red[1] / sc->rho;
-  sc->rho = red[1];
-  sc->rr = red[2];
-  const int it = sc->iter + 1;
-  sc->iter = it;
-  sc->converged = red[2] <= sc->tol2 ? 1 : 0;
-  if (sc->converged || it >= sc->max_iter || !isfinite(red[2])) sc->done = 1;
-}
-
-__global__ void __launch_bounds__(DTPB) k_ddir(int64_t n, const double* __restrict__ dinv,
-                                               const double* __restrict__ r, double* __restrict__ p,
-                                               const PcgScalars* sc) {
-  if (*(volatile const int32_t*)&sc->done) return;
-  const double beta = sc->beta;
-  for (int64_t i = blockIdx.x * (int64_t)DTPB + threadIdx.x; i < n; i += (int64_t)gridDim.x * DTPB)
-    p[i] = fma(beta, p[i], dinv[i] * r[i]);
-}
-
 __global__ void k_dcopy(int64_t n, const double* __restrict__ src, int64_t sld, int64_t sc_, double* __restrict__ dst,
                         int64_t dld, int64_t dc) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -414,41 +329,6 @@ static fj_status dist_rows(const fj_graph* g, const Op& op, cudaStream_t st) {
   FJ_CK(launch_warp_items<WT>(g, w, op, st));
   FJ_CK_LAUNCH();
   return FJ_OK;
-}
-
-template <int WT>
-static fj_status d_apply_wt(const fj_graph* g, const double* x, double* y, const PcgScalars* sc, double* dot,
-                            int opL, cudaStream_t st) {
-  ApplyOp<WT> op{x, y, g->deg, 1, 0, opL, const_cast<PcgScalars*>(sc), dot};
-  op.alpha_on_device = 0;
-  return dist_rows<WT>(g, op, st);
-}
-
-static fj_status d_apply(const fj_graph* g, const double* x, double* y, const PcgScalars* sc, double* dot, int opL,
-                         cudaStream_t st) {
-  switch (g->wtype) {
-    case FJ_W_UNIT: return d_apply_wt<FJ_W_UNIT>(g, x, y, sc, dot, opL, st);
-    case FJ_W_U8: return d_apply_wt<FJ_W_U8>(g, x, y, sc, dot, opL, st);
-    case FJ_W_F32: return d_apply_wt<FJ_W_F32>(g, x, y, sc, dot, opL, st);
-    default: return d_apply_wt<FJ_W_F64>(g, x, y, sc, dot, opL, st);
-  }
-}
-
-template <int WT>
-static fj_status d_resid_wt(const fj_graph* g, const double* xext, const double* s, int64_t ld, int64_t c, double* out,
-                            cudaStream_t st) {
-  ResidOp<WT> op{xext, s, g->deg, ld, c, out};
-  return dist_rows<WT>(g, op, st);
-}
-
-static fj_status d_resid(const fj_graph* g, const double* xext, const double* s, int64_t ld, int64_t c, double* out,
-                         cudaStream_t st) {
-  switch (g->wtype) {
-    case FJ_W_UNIT: return d_resid_wt<FJ_W_UNIT>(g, xext, s, ld, c, out, st);
-    case FJ_W_U8: return d_resid_wt<FJ_W_U8>(g, xext, s, ld, c, out, st);
-    case FJ_W_F32: return d_resid_wt<FJ_W_F32>(g, xext, s, ld, c, out, st);
-    default: return d_resid_wt<FJ_W_F64>(g, xext, s, ld, c, out, st);
-  }
 }
 
 template <int WT>
@@ -484,80 +364,6 @@ static fj_status ensure_dist_ws(fj_graph* g, cudaStream_t st) {
   FJ_CK(cudaEventCreate(&d->ev0));
   FJ_CK(cudaEventCreate(&d->ev1));
   return FJ_OK;
-}
-
-// One column: s column c of [n_loc][ld] -> z column c.  Host-driven loop (NCCL calls between
-// kernels); the host reads the device `done` flag every 8 iterations.
-fj_status dist_solve_col(fj_graph* g, const double* s, double* z, int64_t ld, int64_t c, const fj_solve_opts& o,
-                         int warm, fj_solve_report* rep, cudaStream_t st) {
-  DistInfo* d = D(g);
-  FJ_TRY(ensure_dist_ws(g, st));
-  const int64_t nl = d->n_loc;
-  const unsigned gb = (unsigned)std::min<int64_t>((nl + 255) / 256, 4096);
-  int restarts = 0, total = 0;
-  PcgScalars h{};
-  double rel_true = NAN, res2 = 0.0;
-  bool first = true;
-  for (;;) {
-    const bool restart = !first || warm;
-    if (restart) {
-      if (first) { k_dcopy<<<gb, 256, 0, st>>>(nl, z, ld, c, d->x, 1, 0); FJ_CK_LAUNCH(); }
-      FJ_TRY(halo_exchange(d, d->x, st));
-      FJ_TRY(d_apply(g, d->x, d->q, nullptr, nullptr, 0, st));
-    }
-    const int budget = std::max(0, o.max_iter - total);
-    FJ_CK(cudaEventRecord(d->ev0, st));
-    k_dinit<<<d->grid_elem, DTPB, 0, st>>>(nl, s, ld, c, g->dinv, d->q, restart ? 1 : 0, d->x, d->r, d->p, d->red,
-                                           d->elem_part, d->elem_ticket);
-    FJ_CK_LAUNCH();
-    FJ_TRY(allreduce(d, d->red + 3, 3, RED_SUM, st));
-    k_dinit_post<<<1, 1, 0, st>>>(d->red, d->sc, o.rtol, budget);
-    FJ_CK_LAUNCH();
-    first = false;
-    for (;;) {
-      for (int u = 0; u < 8; ++u) {
-        FJ_TRY(halo_exchange(d, d->p, st));
-        FJ_TRY(d_apply(g, d->p, d->q, d->sc, d->red, 0, st));          // red[0] = local p^T q
-        FJ_TRY(allreduce(d, d->red, 1, RED_SUM, st));
-        k_dupdate<<<d->grid_elem, DTPB, 0, st>>>(nl, g->dinv, d->p, d->q, d->x, d->r, d->sc, d->red, d->elem_part,
-                                                 d->elem_ticket);
-        FJ_CK_LAUNCH();
-        FJ_TRY(allreduce(d, d->red + 1, 2, RED_SUM, st));
-        k_dpost<<<1, 1, 0, st>>>(d->red, d->sc);
-        FJ_CK_LAUNCH();
-        k_ddir<<<d->grid_elem, DTPB, 0, st>>>(nl, g->dinv, d->r, d->p, d->sc);
-        FJ_CK_LAUNCH();
-      }
-      FJ_CK(cudaMemcpyAsync(&h, d->sc, sizeof h, cudaMemcpyDeviceToHost, st));
-      FJ_CK(cudaStreamSynchronize(st));
-      if (h.done) break;
-    }
-    FJ_CK(cudaEventRecord(d->ev1, st));
-    // true residual: halo of x, local ||s - (I+L)x||^2, allreduce
-    FJ_TRY(halo_exchange(d, d->x, st));
-    FJ_TRY(d_resid(g, d->x, s, ld, c, d->red + 6, st));
-    FJ_TRY(allreduce(d, d->red + 6, 1, RED_SUM, st));
-    FJ_CK(cudaMemcpyAsync(&res2, d->red + 6, sizeof res2, cudaMemcpyDeviceToHost, st));
-    FJ_CK(cudaStreamSynchronize(st));
-    float lms = 0.f;
-    cudaEventElapsedTime(&lms, d->ev0, d->ev1);
-    total += h.iter;
-    if (rep) { rep->ms_loop += lms; rep->iterations_total += h.iter; }
-    rel_true = h.ss > 0 ? std::sqrt(res2 / h.ss) : 0.0;
-    if (res2 <= h.tol2 || restarts >= o.max_restarts || total >= o.max_iter || h.breakdown) break;
-    ++restarts;
-  }
-  k_dcopy<<<gb, 256, 0, st>>>(nl, d->x, 1, 0, z, ld, c);
-  FJ_CK_LAUNCH();
-  const bool ok = res2 <= h.tol2;
-  if (rep) {
-    rep->iterations = std::max(rep->iterations, total);
-    rep->restarts = std::max(rep->restarts, restarts);
-    rep->rel_res_recursive = std::max(rep->rel_res_recursive, h.ss > 0 ? std::sqrt(h.rr / h.ss) : 0.0);
-    rep->rel_res_true = std::isnan(rep->rel_res_true) ? rel_true : std::max(rep->rel_res_true, rel_true);
-    if (!ok) rep->converged = 0;
-  }
-  return ok ? FJ_OK : fail(FJ_E_NO_CONVERGENCE, "distributed PCG did not reach rtol on the true residual");
 }
 
 // Quantities of one column: halo of z, fused pass on the local rows, allreduce of the 10 sums.
@@ -614,30 +420,770 @@ fj_status dist_stats_combine(const fj_graph* g, int k, double* dev4k /* [k][4] d
   return s3;
 }
 
-bool is_dist(const fj_graph* g) { return g->dist != nullptr; }
-int64_t dist_n_ghost(const fj_graph* g) { return g->dist ? D(g)->n_ghost : 0; }
-fj_status dist_halo_rows(const fj_graph* g, double* x_ext, int width, cudaStream_t st) {
-  return halo_exchange(D(g), x_ext, st, width);
+// ================================================================ single-reduction distributed PCG
+// Rows a8/e, SURVEY §8(a) "fusion floor" / §8(e): Jacobi-PCG in the Chronopoulos-Gear form, so one
+// iteration needs ONE allreduce (3 KP doubles) instead of two, with the halo exchange of the
+// preconditioned residual u overlapped with the on-rank part of the product:
+//   E  k_cg_step      beta = gamma_i / gamma_{i-1}, alpha = gamma_i / (delta_i - beta gamma_i / alpha_{i-1})
+//                     (alpha_0 = gamma_0 / delta_0), p = u + beta p, s = w + beta s, x += alpha p,
+//                     r -= alpha s, u = dinv o r, local gamma' = r^T u, rho' = ||r||^2
+//   H  halo(u)        pack + grouped ncclSend/ncclRecv on the comm stream          } concurrent
+//   Sd w = (I+L) u    over the OWN columns of every row (diag block), delta part   }
+//   So w -= A_gh u_gh over the ghost columns of the boundary rows (after H), delta
+//   R  allreduce [gamma', delta', rho'] (3 KP doubles)  -> the next E on every rank
+// w = (I+L)u, so s = (I+L)p and the recurrences are those of textbook PCG (same iterates in exact
+// arithmetic).  Columns of a k <= 4 batch are independent (per-column alpha, beta, mask) and padded
+// to KP = 1, 2 or 4 (k = 3 -> 4).  Every decision is taken from allreduced scalars, identically on
+// every rank; partial sums are formed and combined in a fixed order.  With NCCL the iteration is
+// captured once into a CUDA graph of CG_UNROLL iterations (kernels exit early once converged) and
+// replayed until the device `done` flag is set; the LOOPBACK transport runs the same kernels from the
+// host (its exchanges are host-synchronous).
+
+constexpr int CG_UNROLL = 4;
+
+template <int KP> struct VT { using type = DVec<KP>; };
+template <> struct VT<1> { using type = double; };
+template <int KP>
+__device__ __forceinline__ typename VT<KP>::type ldv(const double* p) {
+  if constexpr (KP == 1) return *p;
+  else return ld_vec<KP>(p);
 }
-fj_status dist_allreduce_sum(const fj_graph* g, double* buf, int count, cudaStream_t st) {
-  return allreduce(D(g), buf, count, RED_SUM, st);
+template <int KP>
+__device__ __forceinline__ void stv(double* p, const typename VT<KP>::type& v) {
+  if constexpr (KP == 1) *p = v;
+  else st_vec<KP>(p, v);
 }
-// ||s_c - (I+L) z_c||^2 over all ranks for column c of the local slices (host result)
-fj_status dist_true_res2(fj_graph* g, const double* s, const double* z, int64_t ld, int64_t c, double* res2_host,
-                         cudaStream_t st) {
-  DistInfo* d = D(g);
-  FJ_TRY(ensure_dist_ws(g, st));
-  const int64_t nl = d->n_loc;
-  const unsigned gb = (unsigned)std::min<int64_t>((nl + 255) / 256, 4096);
-  k_dcopy<<<gb, 256, 0, st>>>(nl, z, ld, c, d->x, 1, 0);
-  FJ_CK_LAUNCH();
-  FJ_TRY(halo_exchange(d, d->x, st));
-  FJ_TRY(d_resid(g, d->x, s, ld, c, d->red + 6, st));
-  FJ_TRY(allreduce(d, d->red + 6, 1, RED_SUM, st));
-  FJ_CK(cudaMemcpyAsync(res2_host, d->red + 6, sizeof(double), cudaMemcpyDeviceToHost, st));
-  FJ_CK(cudaStreamSynchronize(st));
+template <int KP>
+__device__ __forceinline__ double cmp(const typename VT<KP>::type& v, int c) {
+  if constexpr (KP == 1) return v;
+  else return v.v[c];
+}
+template <int KP>
+__device__ __forceinline__ void setc(typename VT<KP>::type& v, int c, double x) {
+  if constexpr (KP == 1) v = x;
+  else v.v[c] = x;
+}
+
+// The rank's local CSR split by column owner: own columns (< n_loc) of every row, and the ghost
+// columns of the boundary rows (compact row list), each entry keeping its position order.
+struct SplitCsr {
+  int64_t nnz_d = 0, nnz_o = 0, n_bnd = 0;
+  int64_t *rp_d = nullptr, *rp_o = nullptr;
+  int32_t *col_d = nullptr, *col_o = nullptr, *rows_o = nullptr;
+  void *w_d = nullptr, *w_o = nullptr;
+  uint8_t* bnd = nullptr;
+  Sched sd[2], so[2];             // [0] scalar engine (KP = 1), [1] vector engine (KP > 1)
+  TileScratch tsd[2], tso[2];
+};
+
+struct CgState {
+  double gprev[KVMAX], aprev[KVMAX], tol2[KVMAX], rr[KVMAX], ss[KVMAX];
+  double rtol2;
+  int32_t active[KVMAX], conv[KVMAX], brk[KVMAX];
+  int32_t first, iter, max_iter, done, k;
+};
+
+struct CgWs {
+  int kp = 0;
+  SplitCsr sp;
+  bool split_built = false;
+  double *u = nullptr, *w = nullptr, *p = nullptr, *s = nullptr, *x = nullptr, *r = nullptr;
+  double *red = nullptr, *dpart = nullptr;   // red: [gamma | delta | rho | ss] x KVMAX
+  CgState* cs = nullptr;
+  double* part = nullptr;
+  unsigned int* ticket = nullptr;
+  int grid_elem = 0, grid_max = 0;
+  cudaStream_t comm = nullptr, cap = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev0 = nullptr, ev1 = nullptr;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  int graph_k = 0;                           // the k the graph was captured for
+};
+
+static void free_ts(TileScratch& t) {
+  dfree(t.block_part); dfree(t.long_part); dfree(t.chunk_acc); dfree(t.long_ticket); dfree(t.grid_ticket);
+  t = TileScratch{};
+}
+
+static void free_cg(DistInfo* d) {
+  CgWs* c = d->cg;
+  if (!c) return;
+  if (c->exec) cudaGraphExecDestroy(c->exec);
+  if (c->graph) cudaGraphDestroy(c->graph);
+  if (c->comm) cudaStreamDestroy(c->comm);
+  if (c->cap) cudaStreamDestroy(c->cap);
+  for (cudaEvent_t e : {c->ev_fork, c->ev_join, c->ev0, c->ev1})
+    if (e) cudaEventDestroy(e);
+  SplitCsr& sp = c->sp;
+  dfree(sp.rp_d); dfree(sp.rp_o); dfree(sp.col_d); dfree(sp.col_o); dfree(sp.rows_o); dfree(sp.w_d); dfree(sp.w_o);
+  dfree(sp.bnd);
+  for (int f = 0; f < 2; ++f) {
+    free_sched(sp.sd[f]); free_sched(sp.so[f]);
+    free_ts(sp.tsd[f]); free_ts(sp.tso[f]);
+  }
+  dfree(c->u); dfree(c->w); dfree(c->p); dfree(c->s); dfree(c->x); dfree(c->r);
+  dfree(c->red); dfree(c->dpart); dfree(c->cs); dfree(c->part); dfree(c->ticket);
+  delete c;
+  d->cg = nullptr;
+}
+
+// per row: own / ghost column counts (warp per row: hub rows are long)
+__global__ void k_split_count(int64_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ col, int64_t nl,
+                              int64_t* __restrict__ cd, int64_t* __restrict__ co, uint8_t* __restrict__ bnd) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5, nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = wid; i < n; i += nw) {
+    const int64_t rb = rp[i], re = rp[i + 1];
+    int64_t own = 0;
+    for (int64_t p = rb + lane; p < re; p += 32) own += col[p] < nl ? 1 : 0;
+    for (int o = 16; o > 0; o >>= 1) own += __shfl_xor_sync(0xffffffffu, own, o);
+    if (lane == 0) {
+      cd[i] = own;
+      co[i] = (re - rb) - own;
+      bnd[i] = (re - rb) > own ? 1 : 0;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) { cd[n] = 0; co[n] = 0; }
+}
+
+// scatter each row's own / ghost entries (position order kept) into the two CSRs; warp per row,
+// ballot prefix for the order within each 32-entry step
+__global__ void k_split_scatter(int64_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                                const uint8_t* __restrict__ w, int wb, int64_t nl, const int64_t* __restrict__ pd,
+                                const int64_t* __restrict__ po, int32_t* __restrict__ col_d, uint8_t* __restrict__ w_d,
+                                int32_t* __restrict__ col_o, uint8_t* __restrict__ w_o) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5, nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = wid; i < n; i += nw) {
+    const int64_t rb = rp[i], re = rp[i + 1];
+    int64_t od = pd[i], oo = po[i];
+    for (int64_t b = rb; b < re; b += 32) {
+      const int64_t p = b + lane;
+      const bool in = p < re;
+      const int32_t c = in ? col[p] : 0;
+      const bool own = in && c < nl;
+      const unsigned mo = __ballot_sync(0xffffffffu, own), mg = __ballot_sync(0xffffffffu, in && !own);
+      const unsigned below = (1u << lane) - 1u;
+      if (own) {
+        const int64_t q = od + __popc(mo & below);
+        col_d[q] = c;
+        for (int t = 0; t < wb; ++t) w_d[q * wb + t] = w[p * wb + t];
+      } else if (in) {
+        const int64_t q = oo + __popc(mg & below);
+        col_o[q] = c;
+        for (int t = 0; t < wb; ++t) w_o[q * wb + t] = w[p * wb + t];
+      }
+      od += __popc(mo);
+      oo += __popc(mg);
+    }
+  }
+}
+
+__global__ void k_rows_rp(int64_t nb, const int32_t* __restrict__ rows, const int64_t* __restrict__ po, int64_t tot,
+                          int64_t* __restrict__ rp_o) {
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b <= nb; b += (int64_t)gridDim.x * blockDim.x)
+    rp_o[b] = b < nb ? po[rows[b]] : tot;
+}
+
+static int wbytes_of(int wtype) { return wtype == FJ_W_UNIT ? 0 : wtype == FJ_W_U8 ? 1 : wtype == FJ_W_F32 ? 4 : 8; }
+
+static fj_status alloc_ts(TileScratch& t, int grid_max, const Sched& S, int np, cudaStream_t st) {
+  FJ_CK(dmalloc(&t.block_part, sizeof(double) * (size_t)grid_max * np, st));
+  FJ_CK(dmalloc(&t.long_part, sizeof(double) * (size_t)std::max<int64_t>(S.n_long, 1) * np, st));
+  FJ_CK(dmalloc(&t.chunk_acc, sizeof(double) * (size_t)std::max<int64_t>(S.n_long_chunks, 1) * np, st));
+  FJ_CK(dmalloc(&t.long_ticket, sizeof(unsigned int) * (size_t)std::max<int64_t>(S.n_long, 1), st));
+  FJ_CK(dmalloc(&t.grid_ticket, sizeof(unsigned int), st));
+  FJ_CK(cudaMemsetAsync(t.long_ticket, 0, sizeof(unsigned int) * (size_t)std::max<int64_t>(S.n_long, 1), st));
+  FJ_CK(cudaMemsetAsync(t.grid_ticket, 0, sizeof(unsigned int), st));
   return FJ_OK;
 }
+
+// the split CSR and the two schedules of engine flavour f (0 scalar, 1 vector)
+static fj_status ensure_split(fj_graph* g, CgWs* c, int f, cudaStream_t st) {
+  DistInfo* d = D(g);
+  SplitCsr& sp = c->sp;
+  const int64_t n = g->n, nl = d->n_loc;
+  const int wb = wbytes_of(g->wtype);
+  if (!c->split_built) {
+    DevBuf<int64_t> cd, co, pd, po;
+    FJ_TRY(cd.alloc(n + 1, st)); FJ_TRY(co.alloc(n + 1, st)); FJ_TRY(pd.alloc(n + 1, st)); FJ_TRY(po.alloc(n + 1, st));
+    FJ_CK(dmalloc(&sp.bnd, (size_t)std::max<int64_t>(n, 1), st));
+    const unsigned gb = (unsigned)std::min<int64_t>((n * 32 + 255) / 256, 65535);
+    k_split_count<<<gb, 256, 0, st>>>(n, g->row_ptr, g->col, nl, cd.p, co.p, sp.bnd);
+    FJ_CK_LAUNCH();
+    FJ_TRY(cub_exclusive_sum(cd.p, pd.p, n + 1, st));
+    FJ_TRY(cub_exclusive_sum(co.p, po.p, n + 1, st));
+    int64_t tot[2];
+    FJ_CK(cudaMemcpyAsync(&tot[0], pd.p + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    FJ_CK(cudaMemcpyAsync(&tot[1], po.p + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    FJ_CK(cudaStreamSynchronize(st));
+    sp.nnz_d = tot[0];
+    sp.nnz_o = tot[1];
+    FJ_CK(dmalloc(&sp.rp_d, sizeof(int64_t) * (size_t)(n + 1), st));
+    FJ_CK(cudaMemcpyAsync(sp.rp_d, pd.p, sizeof(int64_t) * (size_t)(n + 1), cudaMemcpyDeviceToDevice, st));
+    FJ_CK(dmalloc(&sp.col_d, sizeof(int32_t) * (size_t)std::max<int64_t>(sp.nnz_d, 1), st));
+    FJ_CK(dmalloc(&sp.col_o, sizeof(int32_t) * (size_t)std::max<int64_t>(sp.nnz_o, 1), st));
+    if (wb) {
+      FJ_CK(dmalloc(&sp.w_d, (size_t)wb * (size_t)std::max<int64_t>(sp.nnz_d, 1), st));
+      FJ_CK(dmalloc(&sp.w_o, (size_t)wb * (size_t)std::max<int64_t>(sp.nnz_o, 1), st));
+    }
+    k_split_scatter<<<gb, 256, 0, st>>>(n, g->row_ptr, g->col, reinterpret_cast<const uint8_t*>(g->w), wb, nl, pd.p,
+                                       po.p, sp.col_d, reinterpret_cast<uint8_t*>(sp.w_d), sp.col_o,
+                                       reinterpret_cast<uint8_t*>(sp.w_o));
+    FJ_CK_LAUNCH();
+    // compact boundary rows
+    FJ_CK(dmalloc(&sp.rows_o, sizeof(int32_t) * (size_t)std::max<int64_t>(n, 1), st));
+    DevBuf<int32_t> nsel;
+    FJ_TRY(nsel.alloc(1, st));
+    FJ_TRY(cub_select_index(sp.bnd, sp.rows_o, nsel.p, n, st));
+    int32_t nb = 0;
+    FJ_CK(cudaMemcpyAsync(&nb, nsel.p, sizeof nb, cudaMemcpyDeviceToHost, st));
+    FJ_CK(cudaStreamSynchronize(st));
+    sp.n_bnd = nb;
+    FJ_CK(dmalloc(&sp.rp_o, sizeof(int64_t) * (size_t)(nb + 1), st));
+    k_rows_rp<<<(unsigned)std::min<int64_t>((nb + 256) / 256, 4096), 256, 0, st>>>(nb, sp.rows_o, po.p, sp.nnz_o,
+                                                                                  sp.rp_o);
+    FJ_CK_LAUNCH();
+    FJ_CK(cudaStreamSynchronize(st));
+    c->split_built = true;
+  }
+  if (!sp.sd[f].built) {
+    const SchedParams P = f == 0 ? kSchedK1 : kSchedVec;
+    fj_graph vd;                        // views: schedules depend only on (n, row_ptr)
+    vd.n = n; vd.row_ptr = sp.rp_d;
+    FJ_TRY(build_schedule(&vd, P, sp.sd[f], st));
+    fj_graph vo;
+    vo.n = sp.n_bnd; vo.row_ptr = sp.rp_o;
+    FJ_TRY(build_schedule(&vo, P, sp.so[f], st));
+    FJ_TRY(alloc_ts(sp.tsd[f], c->grid_max, sp.sd[f], KVMAX, st));
+    FJ_TRY(alloc_ts(sp.tso[f], c->grid_max, sp.so[f], KVMAX, st));
+  }
+  return FJ_OK;
+}
+
+// ---------------------------------------------------------------- the two product passes
+template <int WT, int KP>
+struct CgDiagOp {   // w = (I+L) u over the own columns; (u, w) over the rows without ghost columns
+  using V = typename VT<KP>::type;
+  static constexpr int ITEMS = KP == 1 ? fj::ITEMS : VEC_ITEMS;
+  static constexpr int TILE_ROWS = KP == 1 ? fj::TILE_ROWS : VEC_TILE_ROWS;
+  static constexpr int MIN_BLOCKS = engine_min_blocks<V>();
+  static constexpr bool TMA = KP > 1;
+  static constexpr int NA = KP, NP = KP;
+  static constexpr bool NEEDS_XI = true;
+  static __device__ __forceinline__ V vzero() {
+    V r;
+#pragma unroll
+    for (int c = 0; c < KP; ++c) setc<KP>(r, c, 0.0);
+    return r;
+  }
+  const double* __restrict__ u;
+  double* __restrict__ w;
+  const double* __restrict__ deg;
+  const uint8_t* __restrict__ bnd;
+  double* dot_out;
+  const int32_t* done;
+  __device__ __forceinline__ bool skip() const { return done && *(volatile const int32_t*)done; }
+  __device__ __forceinline__ bool wants_xi() const { return true; }
+  __device__ __forceinline__ V gather(int32_t j) const { return ldv<KP>(u + (int64_t)j * KP); }
+  __device__ __forceinline__ V row_value(int64_t i) const { return ldv<KP>(u + i * KP); }
+  __device__ __forceinline__ const V* xi_base() const { return reinterpret_cast<const V*>(u); }
+  __device__ __forceinline__ void add(double (&a)[NA], double wgt, const V& xj, const V&) const {
+#pragma unroll
+    for (int c = 0; c < KP; ++c) a[c] = (WT == FJ_W_UNIT) ? a[c] + cmp<KP>(xj, c) : fma(wgt, cmp<KP>(xj, c), a[c]);
+  }
+  template <class P>
+  __device__ __forceinline__ void finish_row(int64_t i, int64_t, const V& ui, const double (&a)[NA], P& part) const {
+    const double dd = 1.0 + deg[i];
+    V wi;
+#pragma unroll
+    for (int c = 0; c < KP; ++c) setc<KP>(wi, c, fma(dd, cmp<KP>(ui, c), -a[c]));
+    stv<KP>(w + i * KP, wi);
+    if (!bnd[i]) {
+#pragma unroll
+      for (int c = 0; c < KP; ++c) part[c] = fma(cmp<KP>(ui, c), cmp<KP>(wi, c), part[c]);
+    }
+  }
+  __device__ __forceinline__ void finalize(const double (&tot)[NP]) const {
+#pragma unroll
+    for (int c = 0; c < KP; ++c) dot_out[c] = tot[c];
+  }
+};
+
+template <int WT, int KP>
+struct CgOffOp {    // w_i -= sum over the ghost columns of boundary row i; (u, w) over those rows
+  using V = typename VT<KP>::type;
+  static constexpr int ITEMS = KP == 1 ? fj::ITEMS : VEC_ITEMS;
+  static constexpr int TILE_ROWS = KP == 1 ? fj::TILE_ROWS : VEC_TILE_ROWS;
+  static constexpr int MIN_BLOCKS = engine_min_blocks<V>();
+  static constexpr bool TMA = KP > 1;
+  static constexpr int NA = KP, NP = KP;
+  static constexpr bool NEEDS_XI = true;
+  static __device__ __forceinline__ V vzero() { return CgDiagOp<WT, KP>::vzero(); }
+  const double* __restrict__ u;
+  double* __restrict__ w;
+  const int32_t* __restrict__ rows;
+  const double* dpart;   // the diag pass's (u, w) partial
+  double* red;           // red[KP + c] <- local delta_c
+  const int32_t* done;
+  __device__ __forceinline__ bool skip() const { return done && *(volatile const int32_t*)done; }
+  __device__ __forceinline__ bool wants_xi() const { return true; }
+  __device__ __forceinline__ V gather(int32_t j) const { return ldv<KP>(u + (int64_t)j * KP); }
+  __device__ __forceinline__ V row_value(int64_t b) const { return ldv<KP>(u + (int64_t)rows[b] * KP); }
+  __device__ __forceinline__ const V* xi_base() const { return nullptr; }
+  __device__ __forceinline__ void add(double (&a)[NA], double wgt, const V& xj, const V&) const {
+#pragma unroll
+    for (int c = 0; c < KP; ++c) a[c] = (WT == FJ_W_UNIT) ? a[c] + cmp<KP>(xj, c) : fma(wgt, cmp<KP>(xj, c), a[c]);
+  }
+  template <class P>
+  __device__ __forceinline__ void finish_row(int64_t b, int64_t, const V& ui, const double (&a)[NA], P& part) const {
+    const int64_t i = rows[b];
+    V wi = ldv<KP>(w + i * KP);
+#pragma unroll
+    for (int c = 0; c < KP; ++c) setc<KP>(wi, c, cmp<KP>(wi, c) - a[c]);
+    stv<KP>(w + i * KP, wi);
+#pragma unroll
+    for (int c = 0; c < KP; ++c) part[c] = fma(cmp<KP>(ui, c), cmp<KP>(wi, c), part[c]);
+  }
+  __device__ __forceinline__ void finalize(const double (&tot)[NP]) const {
+#pragma unroll
+    for (int c = 0; c < KP; ++c) red[KP + c] = dpart[c] + tot[c];
+  }
+};
+
+template <int WT, class Op>
+static fj_status launch_view(const fj_graph* g, const Sched& S, const int64_t* rp, const int32_t* col, const void* w,
+                             int64_t nrows, int64_t nnz, const TileScratch& ts, int grid_max, const Op& op,
+                             cudaStream_t st) {
+  static int occ = 0;
+  if (occ == 0) {
+    FJ_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, warp_kernel<WT, Op>, WTPB, 0));
+    if (occ < 1) occ = 1;
+  }
+  TileSched t = make_sched(g, S);
+  t.n = nrows; t.nnz = nnz; t.row_ptr = rp; t.col = col; t.w = w;
+  int64_t grid = (int64_t)g->num_sms * occ;
+  const int64_t need = (S.n_items + WPB - 1) / WPB;
+  if (grid > need) grid = need > 0 ? need : 1;
+  if (grid > grid_max) grid = grid_max;
+  warp_kernel<WT, Op><<<(unsigned)grid, WTPB, 0, st>>>(t, op, ts);
+  FJ_CK_LAUNCH();
+  return FJ_OK;
+}
+
+// w = (I+L) u on the rank's rows, red[KP..2KP) = local (u, w); the halo of u travels on the comm
+// stream while the own-column pass runs (NCCL); LOOPBACK exchanges first, host-synchronously.
+template <int KP>
+static fj_status cg_product(fj_graph* g, CgWs* c, const double* u_in, cudaStream_t st, bool in_loop) {
+  DistInfo* d = D(g);
+  SplitCsr& sp = c->sp;
+  constexpr int f = KP == 1 ? 0 : 1;
+  double* u = c->u;
+  if (u_in != u) FJ_CK(cudaMemcpyAsync(u, u_in, sizeof(double) * (size_t)d->n_loc * KP, cudaMemcpyDeviceToDevice, st));
+  const bool overlap = d->comm->kind == 0 && d->comm->nranks > 1;
+  if (overlap) {
+    FJ_CK(cudaEventRecord(c->ev_fork, st));
+    FJ_CK(cudaStreamWaitEvent(c->comm, c->ev_fork, 0));
+    FJ_TRY(halo_exchange(d, u, c->comm, KP));
+    FJ_CK(cudaEventRecord(c->ev_join, c->comm));
+  } else {
+    FJ_TRY(halo_exchange(d, u, st, KP));
+  }
+  const int32_t* done = in_loop ? &c->cs->done : nullptr;   // loop products exit once converged
+  auto run = [&](auto wt) -> fj_status {
+    constexpr int WT = decltype(wt)::value;
+    CgDiagOp<WT, KP> od{u, c->w, g->deg, sp.bnd, c->dpart, done};
+    FJ_TRY((launch_view<WT>(g, sp.sd[f], sp.rp_d, sp.col_d, sp.w_d, g->n, sp.nnz_d, sp.tsd[f], c->grid_max, od, st)));
+    if (overlap) FJ_CK(cudaStreamWaitEvent(st, c->ev_join, 0));
+    CgOffOp<WT, KP> oo{u, c->w, sp.rows_o, c->dpart, c->red, done};
+    return launch_view<WT>(g, sp.so[f], sp.rp_o, sp.col_o, sp.w_o, sp.n_bnd, sp.nnz_o, sp.tso[f], c->grid_max, oo, st);
+  };
+  switch (g->wtype) {
+    case FJ_W_UNIT: return run(std::integral_constant<int, FJ_W_UNIT>());
+    case FJ_W_U8: return run(std::integral_constant<int, FJ_W_U8>());
+    case FJ_W_F32: return run(std::integral_constant<int, FJ_W_F32>());
+    default: return run(std::integral_constant<int, FJ_W_F64>());
+  }
+}
+
+// ---------------------------------------------------------------- elementwise kernels
+template <int NPART>
+__device__ __forceinline__ bool cg_reduce(double (&v)[NPART], double* part, unsigned int* ticket, double* s_red) {
+  block_sum<NPART, VETB>(v, s_red);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int j = 0; j < NPART; ++j) part[(int64_t)blockIdx.x * NPART + j] = v[j];
+  }
+  if (!last_block_ticket(ticket, gridDim.x)) return false;
+  double t[NPART];
+#pragma unroll
+  for (int j = 0; j < NPART; ++j) t[j] = 0.0;
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += VETB) {
+#pragma unroll
+    for (int j = 0; j < NPART; ++j) t[j] += __ldcg(part + (int64_t)b * NPART + j);
+  }
+  block_sum<NPART, VETB>(t, s_red);
+#pragma unroll
+  for (int j = 0; j < NPART; ++j) v[j] = t[j];
+  return true;
+}
+
+// (re)start: r = s - q (restart, q = (I+L) x) or r = s, x = 0; u = dinv o r;
+// red[0..KP) = local r^T u, red[2KP..3KP) = ||r||^2, red[3KP..4KP) = ||s||^2
+template <int KP>
+__global__ void __launch_bounds__(VETB) k_cg_init(int64_t n, int k, const double* __restrict__ sv, int64_t ld, int c0,
+                                                  const double* __restrict__ dinv, const double* __restrict__ q,
+                                                  int restart, double* __restrict__ x, double* __restrict__ r,
+                                                  double* __restrict__ u, double* red, double* part, unsigned int* ticket) {
+  __shared__ double s_red[3 * KP * VETB / 32];
+  double v[3 * KP];
+#pragma unroll
+  for (int j = 0; j < 3 * KP; ++j) v[j] = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)VETB + threadIdx.x; i < n; i += (int64_t)gridDim.x * VETB) {
+    const double di = dinv[i];
+#pragma unroll
+    for (int c = 0; c < KP; ++c) {
+      const double si = c < k ? sv[i * ld + c0 + c] : 0.0;
+      const double ri = restart ? si - q[i * KP + c] : si;
+      if (!restart) x[i * KP + c] = 0.0;
+      const double ui = di * ri;
+      r[i * KP + c] = ri;
+      u[i * KP + c] = ui;
+      v[c] = fma(ri, ui, v[c]);
+      v[KP + c] = fma(ri, ri, v[KP + c]);
+      v[2 * KP + c] = fma(si, si, v[2 * KP + c]);
+    }
+  }
+  if (cg_reduce<3 * KP>(v, part, ticket, s_red) && threadIdx.x == 0) {
+#pragma unroll
+    for (int c = 0; c < KP; ++c) { red[c] = v[c]; red[2 * KP + c] = v[KP + c]; red[3 * KP + c] = v[2 * KP + c]; }
+    *ticket = 0u;
+  }
+}
+
+__global__ void k_cg_state(CgState* cs, int k, double rtol, int max_iter) {
+  for (int c = 0; c < KVMAX; ++c) {
+    cs->active[c] = c < k ? 1 : 0;
+    cs->conv[c] = 0;
+    cs->brk[c] = 0;
+    cs->gprev[c] = cs->aprev[c] = 0.0;
+  }
+  cs->rtol2 = rtol * rtol;
+  cs->first = 1;
+  cs->iter = 0;
+  cs->max_iter = max_iter;
+  cs->done = 0;
+  cs->k = k;
+}
+
+// one Chronopoulos-Gear step from the allreduced [gamma | delta | rho (| ss on the first step)]
+template <int KP>
+__global__ void __launch_bounds__(VETB) k_cg_step(int64_t n, int k, const double* __restrict__ dinv,
+                                                  double* __restrict__ u, const double* __restrict__ w,
+                                                  double* __restrict__ p, double* __restrict__ s,
+                                                  double* __restrict__ x, double* __restrict__ r, CgState* cs,
+                                                  double* red, double* part, unsigned int* ticket) {
+  __shared__ double s_red[2 * KP * VETB / 32];
+  if (*(volatile int32_t*)&cs->done) return;
+  const int first = cs->first;
+  double al[KP], be[KP], g[KP], rr[KP], t2[KP];
+  bool act[KP];
+  bool any = false;
+#pragma unroll
+  for (int c = 0; c < KP; ++c) {
+    act[c] = false;
+    al[c] = be[c] = 0.0;
+    g[c] = red[c];
+    rr[c] = red[2 * KP + c];
+    t2[c] = first ? cs->rtol2 * red[3 * KP + c] : cs->tol2[c];
+    if (c < k && cs->active[c] && rr[c] > t2[c] && isfinite(rr[c])) {
+      const double dl = red[KP + c];
+      const double b = first ? 0.0 : g[c] / cs->gprev[c];
+      const double den = first ? dl : dl - b * g[c] / cs->aprev[c];
+      if (den > 0.0 && isfinite(den) && isfinite(b)) {
+        act[c] = true;
+        al[c] = g[c] / den;
+        be[c] = b;
+      }
+    }
+    any |= act[c];
+  }
+  const int it = cs->iter;
+  if (!any || it >= cs->max_iter) {   // identical in every block; block 0 records the outcome
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      for (int c = 0; c < k && c < KP; ++c) {
+        if (first) { cs->tol2[c] = t2[c]; cs->ss[c] = red[3 * KP + c]; }
+        cs->rr[c] = rr[c];
+        if (cs->active[c]) {
+          cs->conv[c] = rr[c] <= t2[c] ? 1 : 0;
+          cs->brk[c] = (rr[c] > t2[c] && !act[c] && it < cs->max_iter) ? 1 : 0;
+        }
+        cs->active[c] = 0;
+      }
+      cs->done = 1;
+    }
+    return;
+  }
+  double v[2 * KP];
+#pragma unroll
+  for (int j = 0; j < 2 * KP; ++j) v[j] = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)VETB + threadIdx.x; i < n; i += (int64_t)gridDim.x * VETB) {
+    const double di = dinv[i];
+#pragma unroll
+    for (int c = 0; c < KP; ++c) {
+      const int64_t o = i * KP + c;
+      double ri = r[o], ui = u[o];
+      if (act[c]) {
+        const double pc = first ? ui : fma(be[c], p[o], ui);
+        const double sc = first ? w[o] : fma(be[c], s[o], w[o]);
+        p[o] = pc;
+        s[o] = sc;
+        x[o] = fma(al[c], pc, x[o]);
+        ri = fma(-al[c], sc, ri);
+        r[o] = ri;
+        ui = di * ri;
+        u[o] = ui;
+      }
+      v[c] = fma(ri, ui, v[c]);
+      v[KP + c] = fma(ri, ri, v[KP + c]);
+    }
+  }
+  if (cg_reduce<2 * KP>(v, part, ticket, s_red) && threadIdx.x == 0) {
+#pragma unroll
+    for (int c = 0; c < KP; ++c) {
+      if (c < k) {
+        if (first) { cs->tol2[c] = t2[c]; cs->ss[c] = red[3 * KP + c]; }
+        cs->rr[c] = rr[c];
+        if (act[c]) {
+          cs->gprev[c] = g[c];
+          cs->aprev[c] = al[c];
+        } else if (cs->active[c]) {   // left the batch this step
+          cs->conv[c] = rr[c] <= t2[c] ? 1 : 0;
+          cs->brk[c] = rr[c] > t2[c] ? 1 : 0;
+          cs->active[c] = 0;
+        }
+      }
+      red[c] = v[c];
+      red[2 * KP + c] = v[KP + c];
+    }
+    cs->first = 0;
+    cs->iter = it + 1;
+    *ticket = 0u;
+  }
+}
+
+// local ||s_c - w_c||^2 (w = (I+L) x) -> red[0..KP)
+template <int KP>
+__global__ void __launch_bounds__(VETB) k_cg_resid(int64_t n, int k, const double* __restrict__ sv, int64_t ld, int c0,
+                                                   const double* __restrict__ w, double* red, double* part,
+                                                   unsigned int* ticket) {
+  __shared__ double s_red[KP * VETB / 32];
+  double v[KP];
+#pragma unroll
+  for (int c = 0; c < KP; ++c) v[c] = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)VETB + threadIdx.x; i < n; i += (int64_t)gridDim.x * VETB) {
+#pragma unroll
+    for (int c = 0; c < KP; ++c) {
+      if (c < k) {
+        const double e = sv[i * ld + c0 + c] - w[i * KP + c];
+        v[c] = fma(e, e, v[c]);
+      }
+    }
+  }
+  if (cg_reduce<KP>(v, part, ticket, s_red) && threadIdx.x == 0) {
+#pragma unroll
+    for (int c = 0; c < KP; ++c) red[c] = v[c];
+    *ticket = 0u;
+  }
+}
+
+template <int KP>
+__global__ void k_cg_pack(int64_t n, int k, const double* __restrict__ z, int64_t ld, int c0, double* __restrict__ x) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+#pragma unroll
+    for (int c = 0; c < KP; ++c) x[i * KP + c] = c < k ? z[i * ld + c0 + c] : 0.0;
+}
+template <int KP>
+__global__ void k_cg_unpack(int64_t n, int k, const double* __restrict__ x, double* __restrict__ z, int64_t ld, int c0) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+#pragma unroll
+    for (int c = 0; c < KP; ++c)
+      if (c < k) z[i * ld + c0 + c] = x[i * KP + c];
+}
+
+static fj_status get_cg(fj_graph* g, int kp, cudaStream_t st, CgWs** out) {
+  DistInfo* d = D(g);
+  if (d->cg && d->cg->kp != kp) {
+    FJ_CK(cudaStreamSynchronize(st));
+    SplitCsr keep = d->cg->sp;       // the split CSR does not depend on kp: keep it
+    const bool built = d->cg->split_built;
+    d->cg->sp = SplitCsr{};
+    free_cg(d);
+    d->cg = new CgWs();
+    d->cg->sp = keep;
+    d->cg->split_built = built;
+  }
+  if (!d->cg) d->cg = new CgWs();
+  CgWs* c = d->cg;
+  if (c->u) { *out = c; return FJ_OK; }
+  c->kp = kp;
+  const int64_t nl = d->n_loc, ne = nl + d->n_ghost;
+  c->grid_max = g->num_sms * (2048 / WTPB);
+  int64_t ge = (int64_t)g->num_sms * (2048 / VETB);
+  const int64_t need = (nl + VETB - 1) / VETB;
+  if (ge > need) ge = need > 0 ? need : 1;
+  c->grid_elem = (int)ge;
+  FJ_CK(dmalloc(&c->u, sizeof(double) * (size_t)std::max<int64_t>(ne * kp, 1), st));
+  for (double** b : {&c->w, &c->p, &c->s, &c->x, &c->r})
+    FJ_CK(dmalloc(b, sizeof(double) * (size_t)std::max<int64_t>(nl * kp, 1), st));
+  FJ_CK(dmalloc(&c->red, sizeof(double) * 4 * KVMAX, st));
+  FJ_CK(dmalloc(&c->dpart, sizeof(double) * KVMAX, st));
+  FJ_CK(dmalloc(&c->cs, sizeof(CgState), st));
+  FJ_CK(cudaMemsetAsync(c->cs, 0, sizeof(CgState), st));
+  FJ_CK(dmalloc(&c->part, sizeof(double) * (size_t)ge * 3 * KVMAX, st));
+  FJ_CK(dmalloc(&c->ticket, sizeof(unsigned int), st));
+  FJ_CK(cudaMemsetAsync(c->ticket, 0, sizeof(unsigned int), st));
+  if (!c->comm) FJ_CK(cudaStreamCreateWithFlags(&c->comm, cudaStreamNonBlocking));
+  if (!c->cap) FJ_CK(cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking));
+  for (cudaEvent_t* e : {&c->ev_fork, &c->ev_join})
+    if (!*e) FJ_CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  for (cudaEvent_t* e : {&c->ev0, &c->ev1})
+    if (!*e) FJ_CK(cudaEventCreate(e));
+  FJ_TRY(ensure_split(g, c, kp == 1 ? 0 : 1, st));
+  *out = c;
+  return FJ_OK;
+}
+
+// one iteration: E, then the product of the new u (halo overlapped), then the single allreduce
+template <int KP>
+static fj_status cg_iteration(fj_graph* g, CgWs* c, int k, cudaStream_t st) {
+  DistInfo* d = D(g);
+  k_cg_step<KP><<<c->grid_elem, VETB, 0, st>>>(d->n_loc, k, g->dinv, c->u, c->w, c->p, c->s, c->x, c->r, c->cs,
+                                               c->red, c->part, c->ticket);
+  FJ_CK_LAUNCH();
+  FJ_TRY(cg_product<KP>(g, c, c->u, st, true));
+  FJ_TRY(allreduce(d, c->red, 3 * KP, RED_SUM, st));
+  return FJ_OK;
+}
+
+template <int KP>
+static fj_status build_cg_graph(fj_graph* g, CgWs* c, int k) {
+  if (c->exec) return FJ_OK;
+  FJ_CK(cudaStreamBeginCapture(c->cap, cudaStreamCaptureModeThreadLocal));
+  g_capturing = true;
+  fj_status s = FJ_OK;
+  for (int u = 0; u < CG_UNROLL && s == FJ_OK; ++u) s = cg_iteration<KP>(g, c, k, c->cap);
+  g_capturing = false;
+  cudaGraph_t gr = nullptr;
+  cudaError_t e = cudaStreamEndCapture(c->cap, &gr);
+  FJ_TRY(s);
+  FJ_CK(e);
+  c->graph = gr;
+  FJ_CK(cudaGraphInstantiate(&c->exec, gr, 0));
+  return FJ_OK;
+}
+
+template <int KP>
+static fj_status dist_cg_t(fj_graph* g, int k, const double* sv, double* z, int64_t ld, int c0, const fj_solve_opts& o,
+                           int warm, fj_solve_report* rep, cudaStream_t st) {
+  DistInfo* d = D(g);
+  CgWs* c = nullptr;
+  FJ_TRY(get_cg(g, KP, st, &c));
+  const int64_t nl = d->n_loc;
+  const unsigned cb = (unsigned)std::min<int64_t>((nl + 255) / 256, 8192);
+  const bool graph = o.use_cuda_graph && d->comm->kind == 0;
+  if (graph) {
+    if (c->exec && c->graph_k != k) {
+      cudaGraphExecDestroy(c->exec); cudaGraphDestroy(c->graph);
+      c->exec = nullptr; c->graph = nullptr;
+    }
+    FJ_TRY(build_cg_graph<KP>(g, c, k));
+    c->graph_k = k;
+  }
+  CgState h{};
+  std::vector<double> res2(KP, 0.0);
+  int restarts = 0, total = 0;
+  bool first = true;
+  for (;;) {
+    const bool restart = !first || warm;
+    if (restart) {   // w = (I+L) x, x from z on a warm start
+      if (first) { k_cg_pack<KP><<<cb, 256, 0, st>>>(nl, k, z, ld, c0, c->x); FJ_CK_LAUNCH(); }
+      FJ_TRY(cg_product<KP>(g, c, c->x, st, false));
+    }
+    const int budget = std::max(0, o.max_iter - total);
+    FJ_CK(cudaEventRecord(c->ev0, st));
+    k_cg_state<<<1, 1, 0, st>>>(c->cs, k, o.rtol, budget);
+    FJ_CK_LAUNCH();
+    k_cg_init<KP><<<c->grid_elem, VETB, 0, st>>>(nl, k, sv, ld, c0, g->dinv, c->w, restart ? 1 : 0, c->x, c->r, c->u,
+                                                 c->red, c->part, c->ticket);
+    FJ_CK_LAUNCH();
+    FJ_TRY(cg_product<KP>(g, c, c->u, st, false));    // w = (I+L) u, delta
+    FJ_TRY(allreduce(d, c->red, 4 * KP, RED_SUM, st));
+    first = false;
+    for (;;) {
+      if (graph) {
+        FJ_CK(cudaGraphLaunch(c->exec, st));
+      } else {
+        for (int u = 0; u < CG_UNROLL; ++u) FJ_TRY(cg_iteration<KP>(g, c, k, st));
+      }
+      if (graph) count_launch((int64_t)CG_UNROLL * (3 + (d->comm->nranks > 1 && d->n_send > 0 ? 1 : 0)));
+      FJ_CK(cudaMemcpyAsync(&h, c->cs, sizeof h, cudaMemcpyDeviceToHost, st));
+      FJ_CK(cudaStreamSynchronize(st));
+      if (h.done) break;
+    }
+    FJ_CK(cudaEventRecord(c->ev1, st));
+    // true residual: w = (I+L) x (same product), then ||s - w||^2 per column, allreduced
+    FJ_TRY(cg_product<KP>(g, c, c->x, st, false));
+    k_cg_resid<KP><<<c->grid_elem, VETB, 0, st>>>(nl, k, sv, ld, c0, c->w, c->red + 3 * KVMAX, c->part, c->ticket);
+    FJ_CK_LAUNCH();
+    FJ_TRY(allreduce(d, c->red + 3 * KVMAX, KP, RED_SUM, st));
+    FJ_CK(cudaMemcpyAsync(res2.data(), c->red + 3 * KVMAX, sizeof(double) * KP, cudaMemcpyDeviceToHost, st));
+    FJ_CK(cudaStreamSynchronize(st));
+    float lms = 0.f;
+    cudaEventElapsedTime(&lms, c->ev0, c->ev1);
+    total += h.iter;
+    if (rep) { rep->ms_loop += lms; rep->iterations_total += (int64_t)h.iter * k; }
+    bool ok = true, brk = false;
+    for (int j = 0; j < k; ++j) {
+      if (res2[j] > h.tol2[j]) ok = false;
+      if (h.brk[j]) brk = true;
+    }
+    if (ok || restarts >= o.max_restarts || total >= o.max_iter || brk) break;
+    ++restarts;
+  }
+  k_cg_unpack<KP><<<cb, 256, 0, st>>>(nl, k, c->x, z, ld, c0);
+  FJ_CK_LAUNCH();
+  bool converged = true;
+  double worst_true = 0.0, worst_rec = 0.0;
+  for (int j = 0; j < k; ++j) {
+    if (res2[j] > h.tol2[j]) converged = false;
+    if (h.ss[j] > 0) {
+      worst_true = std::max(worst_true, std::sqrt(res2[j] / h.ss[j]));
+      worst_rec = std::max(worst_rec, std::sqrt(h.rr[j] / h.ss[j]));
+    }
+  }
+  if (rep) {
+    rep->iterations = std::max(rep->iterations, total);
+    rep->restarts = std::max(rep->restarts, restarts);
+    if (k > 1) rep->batch_k = k;
+    rep->rel_res_recursive = std::max(rep->rel_res_recursive, worst_rec);
+    rep->rel_res_true = std::isnan(rep->rel_res_true) ? worst_true : std::max(rep->rel_res_true, worst_true);
+    if (!converged) rep->converged = 0;
+  }
+  return converged ? FJ_OK : fail(FJ_E_NO_CONVERGENCE, "distributed PCG did not reach rtol on the true residual");
+}
+
+// columns [c0, c0 + k) of the row-major [n_loc][ld] slices s, z; 1 <= k <= 4
+fj_status dist_solve_cg(fj_graph* g, int k, const double* s, double* z, int64_t ld, int c0, const fj_solve_opts& o,
+                        int warm, fj_solve_report* rep, cudaStream_t st) {
+  if (k < 1 || k > KVMAX) return fail(FJ_E_INTERNAL, "dist_solve_cg: 1 <= k <= 4");
+  if (k == 1) return dist_cg_t<1>(g, k, s, z, ld, c0, o, warm, rep, st);
+  if (k == 2) return dist_cg_t<2>(g, k, s, z, ld, c0, o, warm, rep, st);
+  return dist_cg_t<4>(g, k, s, z, ld, c0, o, warm, rep, st);
+}
+
+bool is_dist(const fj_graph* g) { return g->dist != nullptr; }
+int64_t dist_n_ghost(const fj_graph* g) { return g->dist ? D(g)->n_ghost : 0; }
 int64_t global_n(const fj_graph* g) { return g->dist ? D(g)->n_global : g->n; }
 double global_dmax(const fj_graph* g) { return g->dist ? D(g)->d_max_global : g->info.d_max; }
 
@@ -652,6 +1198,7 @@ void free_dist(fj_graph* g) {
   dfree(d->elem_part); dfree(d->elem_ticket);
   if (d->ev0) cudaEventDestroy(d->ev0);
   if (d->ev1) cudaEventDestroy(d->ev1);
+  free_cg(d);
   delete d;
   g->dist = nullptr;
 }

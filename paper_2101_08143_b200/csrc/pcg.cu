@@ -418,13 +418,9 @@ fj_status fj_solve(const fj_graph* gc, int k, const double* s, double* z, const 
   r.rel_res_true = NAN;
   FJ_CK(cudaEventRecord(w->ev0, st));
   fj_status worst = FJ_OK;
-  if (is_dist(g) && vec_supported(k)) {   // rows a8 + a9: the slice's k columns together
-    fj_status sc = dist_solve_vec(g, k, s, z, o, 0, &r, st);
-    if (sc != FJ_OK && sc != FJ_E_NO_CONVERGENCE) return sc;
-    worst = sc;
-  } else if (is_dist(g)) {   // row a8: one rank's slice; halo exchange + allreduce inside
-    for (int c = 0; c < k; ++c) {
-      fj_status sc = dist_solve_col(g, s, z, k, c, o, 0, &r, st);
+  if (is_dist(g)) {   // rows a8 (+ a9): this rank's slice, columns in groups of <= 4 solved together
+    for (int c = 0; c < k; c += 4) {
+      fj_status sc = dist_solve_cg(g, std::min(4, k - c), s, z, k, c, o, 0, &r, st);
       if (sc != FJ_OK && sc != FJ_E_NO_CONVERGENCE) return sc;
       if (sc != FJ_OK) worst = sc;
     }

@@ -531,9 +531,9 @@ static fj_status approxim_impl(const fj_graph* gc, int k, const double* s, doubl
       d2h_issued = false;
     }
     r.iterations = spent;
-  } else if (is_dist(g) && vec_supported(k)) {
-    // rows a8 + a9: the k columns of this rank's slice solved together (halo of padded p rows,
-    // allreduce of k-vectors), then the per-column distributed quantities passes
+  } else if (is_dist(g) && k <= 4) {
+    // rows a8 + a9: the k <= 4 columns of this rank's slice solved together by the single-reduction
+    // distributed PCG (dist.cu), then the per-column distributed quantities passes
     fj_solve_opts oc = o;
     int warm = 0, spent = 0;
     for (;;) {
@@ -542,7 +542,7 @@ static fj_status approxim_impl(const fj_graph* gc, int k, const double* s, doubl
       fj_solve_report rb{};
       rb.converged = 1;
       rb.rel_res_true = NAN;
-      fj_status sc = dist_solve_vec(g, k, s, z, ob, warm, &rb, st);   // Alg. 1 line 3
+      fj_status sc = dist_solve_cg(g, k, s, z, k, 0, ob, warm, &rb, st);   // Alg. 1 line 3
       if (sc != FJ_OK && sc != FJ_E_NO_CONVERGENCE) return sc;
       spent += rb.iterations;
       r.ms_loop += rb.ms_loop;
@@ -593,7 +593,7 @@ static fj_status approxim_impl(const fj_graph* gc, int k, const double* s, doubl
       if (is_dist(g)) {   // row a8: this rank's slice, halo exchange + allreduce inside
         const int before = r.iterations;
         r.iterations = 0;
-        sc = dist_solve_col(g, s, z, k, c, ob, warm, &r, st);
+        sc = dist_solve_cg(g, 1, s, z, k, c, ob, warm, &r, st);
         iters = r.iterations;
         r.iterations = std::max(before, iters);
       } else {

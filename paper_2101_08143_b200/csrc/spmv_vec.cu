@@ -716,249 +716,6 @@ static fj_status solve_vec_t(fj_graph* g, VecWs* w, int k, const double* s, doub
   return converged ? FJ_OK : fail(FJ_E_NO_CONVERGENCE, "batched PCG did not reach rtol on the true residual");
 }
 
-// ---------------------------------------------------------------- rows a8 + a9: distributed small-k PCG
-// The k columns of one rank's row slice solved together.  Same algebra as solve_vec; every global
-// sum is a fixed-order local partial followed by an allreduce in rank order, so all ranks take
-// identical decisions.  Per iteration:
-//   halo(p, KP rows)  ->  q = (I+L) p on the local rows, local p_c^T q_c  ->  allreduce(KP)
-//   k_dv_update: alpha_c from the global p^T q, x += alpha p, r -= alpha q, local (rho'_c, ||r_c||^2)
-//   -> allreduce(2 KP) -> k_dv_post: beta_c, convergence mask, loop flag -> k_v_dir.
-template <int KP, int KQ>
-__global__ void __launch_bounds__(VETB) k_dv_init(int64_t n, int k, const double* __restrict__ s,
-                                                  const double* __restrict__ dinv, const double* __restrict__ q,
-                                                  int restart, double* __restrict__ x, double* __restrict__ r,
-                                                  double* __restrict__ p, double* part, unsigned int* ticket,
-                                                  double* red /* [3 KP]: rho, ||r||^2, ||s||^2 partials */) {
-  __shared__ double s_red[3 * KP * VETB / 32];
-  double v[3 * KP];
-#pragma unroll
-  for (int j = 0; j < 3 * KP; ++j) v[j] = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)VETB + threadIdx.x; i < n; i += (int64_t)gridDim.x * VETB) {
-    DVec<KP> sv, rv, pv;
-#pragma unroll
-    for (int c = 0; c < KP; ++c) sv.v[c] = c < k ? s[i * k + c] : 0.0;
-    if (restart) {
-      const DVec<KP> qv = ld_q<KP, KQ>(q, i);
-#pragma unroll
-      for (int c = 0; c < KP; ++c) rv.v[c] = c < k ? sv.v[c] - qv.v[c] : 0.0;
-    } else {
-      rv = sv;
-      st_q<KP, KQ>(x, i, vzero_kp<KP>());
-    }
-    const double di = dinv[i];
-#pragma unroll
-    for (int c = 0; c < KP; ++c) {
-      pv.v[c] = di * rv.v[c];
-      v[c] = fma(rv.v[c], pv.v[c], v[c]);
-      v[KP + c] = fma(rv.v[c], rv.v[c], v[KP + c]);
-      v[2 * KP + c] = fma(sv.v[c], sv.v[c], v[2 * KP + c]);
-    }
-    st_q<KP, KQ>(r, i, rv);
-    st_vec<KP>(p + i * KP, pv);
-  }
-  if (vec_reduce<3 * KP>(v, part, ticket, s_red) && threadIdx.x == 0) {
-#pragma unroll
-    for (int j = 0; j < 3 * KP; ++j) red[j] = v[j];
-    *ticket = 0u;
-  }
-}
-
-__global__ void k_dv_init_post(int k, int KP, const double* red, VecScalars* sc, double rtol, int max_iter) {
-  int any = 0;
-  for (int c = 0; c < k; ++c) {
-    sc->rho[c] = red[c];
-    sc->rr[c] = red[KP + c];
-    sc->ss[c] = red[2 * KP + c];
-    sc->tol2[c] = rtol * rtol * red[2 * KP + c];
-    const int conv = red[KP + c] <= sc->tol2[c];
-    sc->conv[c] = conv;
-    sc->active[c] = conv ? 0 : 1;
-    sc->breakdown[c] = 0;
-    sc->alpha[c] = sc->beta[c] = 0.0;
-    any |= sc->active[c];
-  }
-  sc->iter = 0;
-  sc->max_iter = max_iter;
-  sc->k = k;
-  sc->done = (!any || max_iter <= 0) ? 1 : 0;
-}
-
-template <int KP, int KQ>
-__global__ void __launch_bounds__(VETB) k_dv_update(int64_t n, int k, const double* __restrict__ dinv,
-                                                    const double* __restrict__ p, const double* __restrict__ q,
-                                                    double* __restrict__ x, double* __restrict__ r,
-                                                    const VecScalars* sc, const double* pq /* [KP] global */,
-                                                    double* part, unsigned int* ticket, double* red /* [2 KP] */) {
-  __shared__ double s_red[2 * KP * VETB / 32];
-  if (*(volatile const int32_t*)&sc->done) return;
-  double al[KP];
-#pragma unroll
-  for (int c = 0; c < KP; ++c) {
-    const double d = c < k ? pq[c] : 0.0;
-    al[c] = (c < k && sc->active[c] && d > 0.0 && isfinite(d)) ? sc->rho[c] / d : 0.0;
-  }
-  double v[2 * KP];
-#pragma unroll
-  for (int j = 0; j < 2 * KP; ++j) v[j] = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)VETB + threadIdx.x; i < n; i += (int64_t)gridDim.x * VETB) {
-    const DVec<KP> pv = ld_vec<KP>(p + i * KP), qv = ld_q<KP, KQ>(q, i);
-    DVec<KP> xv = ld_q<KP, KQ>(x, i), rv = ld_q<KP, KQ>(r, i);
-    const double di = dinv[i];
-#pragma unroll
-    for (int c = 0; c < KP; ++c) {
-      xv.v[c] = fma(al[c], pv.v[c], xv.v[c]);
-      rv.v[c] = fma(-al[c], qv.v[c], rv.v[c]);
-      v[c] = fma(rv.v[c], di * rv.v[c], v[c]);
-      v[KP + c] = fma(rv.v[c], rv.v[c], v[KP + c]);
-    }
-    st_q<KP, KQ>(x, i, xv);
-    st_q<KP, KQ>(r, i, rv);
-  }
-  if (vec_reduce<2 * KP>(v, part, ticket, s_red) && threadIdx.x == 0) {
-#pragma unroll
-    for (int j = 0; j < 2 * KP; ++j) red[j] = v[j];
-    *ticket = 0u;
-  }
-}
-
-// alpha (for the record), beta, convergence, loop flag from the allreduced sums; identical on all ranks
-__global__ void k_dv_post(int k, int KP, const double* pq, const double* red, VecScalars* sc) {
-  if (sc->done) return;
-  int any = 0;
-  for (int c = 0; c < k; ++c) {
-    if (sc->active[c]) {
-      const double d = pq[c];
-      if (!(d > 0.0) || !isfinite(d)) {
-        sc->alpha[c] = 0.0;
-        sc->active[c] = 0;
-        sc->breakdown[c] = 1;
-      } else {
-        sc->pq[c] = d;
-        sc->alpha[c] = sc->rho[c] / d;
-        sc->beta[c] = red[c] / sc->rho[c];
-        sc->rho[c] = red[c];
-        sc->rr[c] = red[KP + c];
-        const bool conv = red[KP + c] <= sc->tol2[c];
-        if (conv || !isfinite(red[KP + c])) { sc->active[c] = 0; sc->conv[c] = conv ? 1 : 0; }
-      }
-    }
-    any |= sc->active[c];
-  }
-  const int it = sc->iter + 1;
-  sc->iter = it;
-  if (!any || it >= sc->max_iter) sc->done = 1;
-}
-
-template <int KP, int KQ>
-static fj_status dist_apply(const fj_graph* g, const VecWs* w, const double* p, double* q, VecScalars* sc,
-                            double* dot, cudaStream_t st) {
-  return by_wtype<KP>(g, [&](auto wt) {
-    constexpr int WT = decltype(wt)::value;
-    ApplyOpV<WT, KP, KQ> op{p, q, g->deg, 0, sc, w->k};
-    op.dot_out = dot;
-    op.alpha_on_device = 0;
-    int nl = 0;
-    FJ_CK(launch_product<WT>(g, w->ts, w->grid_max, op, st, &nl));
-    count_launch(nl);
-    return FJ_OK;
-  });
-}
-
-template <int KP, int KQ>
-static fj_status dist_solve_vec_t(fj_graph* g, VecWs* w, int k, const double* s, double* z, const fj_solve_opts& o,
-                                  int warm, fj_solve_report* rep, cudaStream_t st) {
-  const int64_t n = g->n;   // local rows
-  const unsigned cb = (unsigned)std::min<int64_t>((n + 255) / 256, 8192);
-  double* red = w->dred;    // [0, KP) p^T q | [KP, 3KP) rho', ||r||^2 | [4KP, 7KP) init sums
-  w->x_is_solution = false;
-  VecScalars h{};
-  int restarts = 0, total_iter = 0;
-  bool first = true;
-  std::vector<double> res2(k, 0.0);
-  for (;;) {
-    const bool restart = !first || warm;
-    if (restart) {   // q = (I+L) x (x from z on a warm start), through the halo of a padded copy
-      if (first) { k_v_pack<KQ><<<cb, 256, 0, st>>>(n, k, z, w->x); FJ_CK_LAUNCH(); }
-      k_v_pack_from<KP, KQ><<<cb, 256, 0, st>>>(n, w->x, w->p);
-      FJ_CK_LAUNCH();
-      FJ_TRY(dist_halo_rows(g, w->p, KP, st));
-      FJ_TRY((dist_apply<KP, KQ>(g, w, w->p, w->q, nullptr, nullptr, st)));
-    }
-    const int budget = std::max(0, o.max_iter - total_iter);
-    FJ_CK(cudaEventRecord(w->ev2, st));
-    k_dv_init<KP, KQ><<<w->grid_elem, VETB, 0, st>>>(n, k, s, g->dinv, w->q, restart ? 1 : 0, w->x, w->r, w->p,
-                                                     w->elem_part, w->elem_ticket, red + 4 * KP);
-    FJ_CK_LAUNCH();
-    FJ_TRY(dist_allreduce_sum(g, red + 4 * KP, 3 * KP, st));
-    k_dv_init_post<<<1, 1, 0, st>>>(k, KP, red + 4 * KP, w->sc, o.rtol, budget);
-    FJ_CK_LAUNCH();
-    first = false;
-    for (;;) {
-      for (int u = 0; u < 8; ++u) {
-        FJ_TRY(dist_halo_rows(g, w->p, KP, st));
-        FJ_TRY((dist_apply<KP, KQ>(g, w, w->p, w->q, w->sc, red, st)));
-        FJ_TRY(dist_allreduce_sum(g, red, KP, st));
-        k_dv_update<KP, KQ><<<w->grid_elem, VETB, 0, st>>>(n, k, g->dinv, w->p, w->q, w->x, w->r, w->sc, red,
-                                                           w->elem_part, w->elem_ticket, red + KP);
-        FJ_CK_LAUNCH();
-        FJ_TRY(dist_allreduce_sum(g, red + KP, 2 * KP, st));
-        k_dv_post<<<1, 1, 0, st>>>(k, KP, red, red + KP, w->sc);
-        FJ_CK_LAUNCH();
-        k_v_dir<KP, KQ, false><<<w->grid_elem, VETB, 0, st>>>(n, k, g->dinv, w->r, w->p, w->x, w->sc);
-        FJ_CK_LAUNCH();
-      }
-      FJ_CK(cudaMemcpyAsync(&h, w->sc, sizeof h, cudaMemcpyDeviceToHost, st));
-      FJ_CK(cudaStreamSynchronize(st));
-      if (h.done) break;
-    }
-    FJ_CK(cudaEventRecord(w->ev3, st));
-    k_v_unpack<KQ><<<cb, 256, 0, st>>>(n, k, w->x, z);
-    FJ_CK_LAUNCH();
-    for (int c = 0; c < k; ++c) FJ_TRY(dist_true_res2(g, s, z, k, c, &res2[c], st));   // global, per column
-    total_iter += h.iter;
-    float lms = 0.f;
-    cudaEventElapsedTime(&lms, w->ev2, w->ev3);
-    if (rep) { rep->ms_loop += lms; rep->iterations_total += (int64_t)h.iter * k; }
-    bool ok = true, brk = false;
-    for (int c = 0; c < k; ++c) {
-      if (res2[c] > h.tol2[c]) ok = false;
-      if (h.breakdown[c]) brk = true;
-    }
-    if (ok || restarts >= o.max_restarts || total_iter >= o.max_iter || brk) break;
-    ++restarts;
-  }
-  bool converged = true;
-  double worst_true = 0.0, worst_rec = 0.0;
-  for (int c = 0; c < k; ++c) {
-    if (res2[c] > h.tol2[c]) converged = false;
-    if (h.ss[c] > 0) {
-      worst_true = std::max(worst_true, std::sqrt(res2[c] / h.ss[c]));
-      worst_rec = std::max(worst_rec, std::sqrt(h.rr[c] / h.ss[c]));
-    }
-  }
-  if (rep) {
-    rep->iterations = std::max(rep->iterations, total_iter);
-    rep->restarts = std::max(rep->restarts, restarts);
-    rep->batch_k = k;
-    rep->rel_res_recursive = std::max(rep->rel_res_recursive, worst_rec);
-    rep->rel_res_true = std::isnan(rep->rel_res_true) ? worst_true : std::max(rep->rel_res_true, worst_true);
-    if (!converged) rep->converged = 0;
-  }
-  return converged ? FJ_OK : fail(FJ_E_NO_CONVERGENCE, "distributed batched PCG did not reach rtol on the true residual");
-}
-
-fj_status dist_solve_vec(fj_graph* g, int k, const double* s, double* z, const fj_solve_opts& o, int warm,
-                         fj_solve_report* rep, cudaStream_t st) {
-  VecWs* w = nullptr;
-  FJ_TRY(get_vec_ws(g, k, st, &w));
-  switch (w->kp) {
-    case 2: return dist_solve_vec_t<2, 2>(g, w, k, s, z, o, warm, rep, st);
-    case 3: return dist_solve_vec_t<3, 3>(g, w, k, s, z, o, warm, rep, st);
-    default: return w->kq == 3 ? dist_solve_vec_t<4, 3>(g, w, k, s, z, o, warm, rep, st)
-                               : dist_solve_vec_t<4, 4>(g, w, k, s, z, o, warm, rep, st);
-  }
-}
-
 // ---------------------------------------------------------------- entry points (workspace.cuh)
 bool vec_supported(int k) { return k >= 2 && k <= KVMAX; }
 

@@ -104,18 +104,12 @@ void free_dist(fj_graph* g);
 bool is_dist(const fj_graph* g);
 int64_t global_n(const fj_graph* g);
 double global_dmax(const fj_graph* g);
-fj_status dist_solve_col(fj_graph* g, const double* s, double* z, int64_t ld, int64_t c, const fj_solve_opts& o,
-                         int warm, fj_solve_report* rep, cudaStream_t st);
+// columns [c0, c0 + k) (1 <= k <= 4) of this rank's [n_loc][ld] slices solved together by the
+// single-reduction (Chronopoulos-Gear) distributed PCG
+fj_status dist_solve_cg(fj_graph* g, int k, const double* s, double* z, int64_t ld, int c0, const fj_solve_opts& o,
+                        int warm, fj_solve_report* rep, cudaStream_t st);
 fj_status dist_quant_pass(const fj_graph* g, const double* s, const double* z, int64_t ld, int64_t c, double m,
                           double* host10, cudaStream_t st);
 fj_status dist_stats_combine(const fj_graph* g, int k, double* dev4k, cudaStream_t st);
 int64_t dist_n_ghost(const fj_graph* g);
-fj_status dist_halo_rows(const fj_graph* g, double* x_ext, int width, cudaStream_t st);
-fj_status dist_allreduce_sum(const fj_graph* g, double* buf, int count, cudaStream_t st);
-fj_status dist_true_res2(fj_graph* g, const double* s, const double* z, int64_t ld, int64_t c, double* res2_host,
-                         cudaStream_t st);
-// spmv_vec.cu: the k = 2..4 columns of one rank's slice solved together (rows a8 + a9)
-fj_status dist_solve_vec(fj_graph* g, int k, const double* s, double* z, const fj_solve_opts& o, int warm,
-                         fj_solve_report* rep, cudaStream_t st);
-
 }  // namespace fj

@@ -151,3 +151,120 @@ def test_bounds_rule_balances_nnz():
         per = np.diff(g.row_ptr[b])
         assert b[0] == 0 and b[-1] == wl.n and np.all(np.diff(b) >= 0)
         assert per.max() <= g.nnz / P + np.diff(g.row_ptr).max()
+
+
+def _gloo_cg_worker(rank, P, port, q):
+    """The distributed single-reduction (Chronopoulos-Gear) Jacobi-PCG schedule of dist.cu, emulated
+    in numpy over gloo: per iteration one elementwise step, the halo of u, the own-column / ghost-
+    column split product, and exactly ONE allreduce of [gamma, delta, rho]."""
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=P)
+    try:
+        import synth
+        wl = synth.make_config("c4", scale=10, k=1)
+        g = O.canonical_csr(wl.n, wl.u, wl.v, wl.w)
+        bounds = _bounds_by_nnz(g.row_ptr, P)
+        rp, cl, ghosts = _local_plan(g, bounds, rank)
+        counts, send_idx = D.exchange_requests(ghosts, bounds, D.TorchGroup(None, "cpu"))
+        own = D.owners(ghosts, bounds)
+        off = np.concatenate([[0], np.cumsum(counts)])
+        r0, r1 = bounds[rank], bounds[rank + 1]
+        nl = r1 - r0
+        wf = g.wf()[g.row_ptr[r0]:g.row_ptr[r1]]
+        rows = np.repeat(np.arange(nl), np.diff(rp))
+        d = np.bincount(rows, weights=wf, minlength=nl)
+        dinv = 1.0 / (1.0 + d)
+        loc = cl < nl
+
+        def halo(ul):
+            hv = np.zeros(len(ghosts))
+            reqs = [dist.isend(torch.from_numpy(ul[send_idx[off[p]:off[p + 1]]].copy()), p)
+                    for p in range(P) if p != rank]
+            for p in range(P):
+                if p != rank:
+                    rb = torch.zeros(int((own == p).sum()), dtype=torch.float64)
+                    dist.recv(rb, p)
+                    hv[own == p] = rb.numpy()
+            for rq in reqs:
+                rq.wait()
+            return hv
+
+        def product(ul):   # own-column pass, then the ghost-column pass of the boundary rows
+            hv = halo(ul)
+            w = (1.0 + d) * ul - np.bincount(rows[loc], weights=wf[loc] * ul[cl[loc]], minlength=nl)
+            gh = ~loc
+            return w - np.bincount(rows[gh], weights=wf[gh] * hv[cl[gh] - nl], minlength=nl)
+
+        n_allreduce = 0
+
+        def allreduce(vals):
+            nonlocal n_allreduce
+            n_allreduce += 1
+            t = torch.tensor(vals, dtype=torch.float64)
+            dist.all_reduce(t)
+            return t.numpy()
+
+        s = wl.S[r0:r1, 0]
+        x = np.zeros(nl)
+        r = s.copy()
+        u = dinv * r
+        w = product(u)
+        gam, dlt, rho, ss = allreduce([r @ u, u @ w, r @ r, s @ s])
+        tol2 = 1e-20 * ss
+        it, first = 0, True
+        p = sv = None
+        gp = ap = 0.0
+        while rho > tol2 and it < 500:
+            if first:
+                beta, alpha = 0.0, gam / dlt
+                p, sv = u.copy(), w.copy()
+            else:
+                beta = gam / gp
+                alpha = gam / (dlt - beta * gam / ap)
+                p = u + beta * p
+                sv = w + beta * sv
+            x += alpha * p
+            r -= alpha * sv
+            u = dinv * r
+            gp, ap, first = gam, alpha, False
+            w = product(u)
+            gam, dlt, rho = allreduce([r @ u, u @ w, r @ r])
+            it += 1
+        mx = max(bounds[k + 1] - bounds[k] for k in range(P))   # gloo all_gather: equal sizes
+        xs = [torch.zeros(mx, dtype=torch.float64) for _ in range(P)]
+        xp = torch.zeros(mx, dtype=torch.float64)
+        xp[:nl] = torch.from_numpy(x)
+        dist.all_gather(xs, xp)
+        z = np.concatenate([xs[k].numpy()[:bounds[k + 1] - bounds[k]] for k in range(P)])
+        q.put((rank, z, it, n_allreduce))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("P", [2])
+def test_gloo_single_reduction_pcg_schedule(P):
+    import synth
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gloo_cg_worker, args=(r, P, port, q)) for r in range(P)]
+    [p.start() for p in procs]
+    [p.join(180) for p in procs]
+    assert all(p.exitcode == 0 for p in procs)
+    res = sorted([q.get(timeout=5) for _ in range(P)], key=lambda t: t[0])
+    wl = synth.make_config("c4", scale=10, k=1)
+    g = O.canonical_csr(wl.n, wl.u, wl.v, wl.w)
+    zo = O.solve_dense(g, wl.S[:, 0])
+    its = {t[2] for t in res}
+    assert len(its) == 1                                   # identical decisions on every rank
+    it = its.pop()
+    for rank, z, _, nar in res:
+        assert np.max(np.abs(z - zo)) < 1e-8
+        assert nar == it + 1                               # one allreduce per iteration (+ the initial one)
+    # same iteration count as textbook Jacobi-PCG (the recurrences are equivalent in exact arithmetic)
+    _, info = O.solve_pcg(g, wl.S[:, 0], tol=1e-10)
+    assert abs(it - info["iterations"]) <= 1

@@ -159,3 +159,44 @@ def test_loopback_batched_k3_weighted_vs_oracle(fj, P):
                             torch.from_numpy(wl.w).cuda())
     z1, q1, r1 = G.approxim(torch.from_numpy(wl.S.copy()).cuda())
     assert np.max(np.abs(Z - z1.cpu().numpy())) < 1e-8
+
+
+@pytest.mark.parametrize("k", [1, 3])
+def test_nccl_single_rank_graph_matches_host_loop(fj, monkeypatch, k):
+    """The single-reduction loop captured in a CUDA graph together with its NCCL allreduce (1-rank
+    communicator) gives bitwise the iterates of the same kernels launched from the host."""
+    import torch
+    from paper_2101_08143_b200 import dist as D
+    monkeypatch.setenv("FJ_NCCL_FORCE", "1")
+    comm = fj.Comm.nccl(1, 0, fj.Comm.unique_id())
+    wl = synth.make_config("c4", scale=12, kinds=["uniform", "exponential", "powerlaw"][:k])
+    u, v, w = (torch.from_numpy(a).cuda() for a in (wl.u, wl.v, wl.w))
+    G, _ = D.build_dist_graph(comm, 0, wl.n, u, v, w, D.ThreadGroup(D.ThreadWorld(1), 0))
+    S = torch.from_numpy(np.ascontiguousarray(wl.S)).cuda()
+    zg, qg, rg = G.approxim(S, opts=fj.SolveOpts.make(use_cuda_graph=True))
+    zh, qh, rh = G.approxim(S, opts=fj.SolveOpts.make(use_cuda_graph=False))
+    assert torch.equal(zg, zh) and rg["iterations"] == rh["iterations"]
+    g = O.canonical_csr(wl.n, wl.u, wl.v, wl.w)
+    for c in range(k):
+        zo, _ = O.solve_pcg(g, wl.S[:, c], tol=1e-13)
+        qo = O.quantities(g, wl.S[:, c], zo)
+        for key in QKEYS:
+            assert qg[c][key] == qh[c][key]
+            assert abs(qg[c][key] - qo[key]) / qo[key] <= 1e-8, (c, key)
+    assert rg["rel_res_true"] <= 1e-10
+    G.close()
+    comm.close()
+
+
+def test_loopback_eps_target_warm_restart(fj):
+    """eps_target tightens rtol and warm-starts the distributed solve from z (the restart path of
+    the single-reduction loop): certified bounds meet the target, results match the oracle."""
+    wl = synth.make_config("c1", k=1)
+    Z, Q, R, bounds, plans = run_ranks(fj, 3, wl, wl.S, opts=fj.SolveOpts.make(rtol=1e-6, eps_target=1e-9))
+    g = O.canonical_csr(wl.n, wl.u, wl.v)
+    zo = O.solve_dense(g, wl.S[:, 0])
+    qo = O.quantities(g, wl.S[:, 0], zo)
+    for key in QKEYS:
+        assert Q[0][0]["eps"][key] <= 1e-9
+        assert abs(Q[0][0][key] - qo[key]) / qo[key] <= max(Q[0][0]["eps"][key], 1e-12), key
+    assert np.max(np.abs(Z[:, 0] - zo)) < 1e-8
