@@ -208,9 +208,12 @@ def main():
     ap.add_argument("--vertex-order", default="auto", choices=["auto", "degree", "natural"],
                     help="a1 locality relabelling by descending degree, inside the timed step (DESIGN.md "
                          "§6.7); auto = FJ_ORDER_AUTO's rule (k <= 2 and the gathered vector exceeds L2); "
-                         "the row-partitioned N>1 path always builds in the input labels")
+                         "on the row-partitioned N>1 path the relabelling precedes the partition")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dist-selftest", action="store_true",
+                    help="run the row-partitioned (multi-GPU) code path on ONE GPU through a 1-rank NCCL "
+                         "communicator (no halo); checks that bench.py --gpus N is ready")
     ap.add_argument("--no-extras", action="store_true",
                     help="skip the per-distribution k = 1 lines and the gather probe (profiling runs)")
     ap.add_argument("--spmv-reps", type=int, default=20)
@@ -228,7 +231,13 @@ def main():
     from paper_2101_08143_b200 import binding
 
     torch.cuda.set_device(local)
-    if ws > 1:
+    dist_mode = ws > 1 or args.dist_selftest
+    if args.dist_selftest and ws == 1:   # the row-partitioned path on a 1-rank NCCL communicator
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29577")
+        os.environ["FJ_NCCL_FORCE"] = "1"
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", local))
+    elif ws > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     fj.load_library()
     wl = synth.make_config(args.config)
@@ -239,13 +248,12 @@ def main():
     w = None if wl.w is None else torch.from_numpy(wl.w).cuda()
     S = torch.from_numpy(wl.S).cuda()
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device="cuda")
-    order = "natural" if ws > 1 else args.vertex_order
-    if order == "auto":
+    order = args.vertex_order
+    if order == "auto":   # same rule on 1 GPU and on the row-partitioned path
         order = "degree" if binding.relabel_pays(n, k) else "natural"
     opts = fj.SolveOpts.make(rtol=args.rtol, use_cuda_graph=not args.no_cuda_graph, vertex_order=order)
     stream = torch.cuda.current_stream()
 
-    dist_mode = ws > 1
     if dist_mode:   # rows a8/e: the graph row-partitioned over the ranks, NCCL halo + allreduce
         from paper_2101_08143_b200 import dist as FD
         uid = [fj.Comm.unique_id() if rank == 0 else None]
@@ -255,8 +263,8 @@ def main():
 
     def step():
         if dist_mode:
-            G, b = FD.build_dist_graph(comm, rank, n, u, v, w, grp)   # partition + a1 + ghosts + plan + a2
-            Sl = S[b[rank]:b[rank + 1]].contiguous()
+            G, b = FD.build_dist_graph(comm, rank, n, u, v, w, grp, order=order)   # partition + a1 + ghosts + a2
+            Sl = FD.slice_in(G, S, b)
             z, q, rep = G.approxim(Sl, opts=opts)
             info = {"nnz": G.plan["nnz_local"], "bounds": b}
             G.close()
@@ -280,7 +288,7 @@ def main():
 
     sampler = ClockSampler(local)
     launches0, cub0 = binding.kernel_launches()
-    if ws > 1:
+    if dist_mode:
         dist.barrier()
     torch.cuda.synchronize()
     t_wall = time.perf_counter()
@@ -301,7 +309,7 @@ def main():
         ttq_ms.append(rep["ms"])
         results.append((q, rep))
     torch.cuda.synchronize()
-    if ws > 1:
+    if dist_mode:
         dist.barrier()
     wall = time.perf_counter() - t_wall
     launches1, cub1 = binding.kernel_launches()
@@ -321,7 +329,7 @@ def main():
     tot_loop_ms = loop_ms
     tot_bytes = B * iters
     max_step_ms = sum(step_ms)
-    if ws > 1:   # B is already the GLOBAL per-iteration traffic (all ranks iterate together)
+    if dist_mode:   # B is already the GLOBAL per-iteration traffic (all ranks iterate together)
         t = torch.tensor([loop_ms, sum(step_ms)], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tot_loop_ms, max_step_ms = float(t[0]), float(t[1])
@@ -409,9 +417,9 @@ def main():
         uh, vh = torch.from_numpy(wl.u).pin_memory(), torch.from_numpy(wl.v).pin_memory()
         wh = None if wl.w is None else torch.from_numpy(wl.w).pin_memory()
         b = info["bounds"]
-        Sh = torch.from_numpy(np.ascontiguousarray(wl.S[b[rank]:b[rank + 1]])).pin_memory()
+        Sh = torch.from_numpy(np.ascontiguousarray(wl.S)).pin_memory()   # every rank slices on the device
         h2d = uh.nbytes + vh.nbytes + (0 if wh is None else wh.nbytes) + Sh.nbytes
-        d2h = Sh.nbytes + k * 200
+        d2h = 8 * k * (b[rank + 1] - b[rank]) + k * 200
         e_ms, e_iters, reps = 0.0, 0, max(1, min(args.steps, 3))
         for _ in range(reps):
             torch.cuda.synchronize()
@@ -420,8 +428,8 @@ def main():
             ud, vd = uh.cuda(non_blocking=True), vh.cuda(non_blocking=True)
             wd = None if wh is None else wh.cuda(non_blocking=True)
             Sd = Sh.cuda(non_blocking=True)
-            G, _ = FD.build_dist_graph(comm, rank, n, ud, vd, wd, grp)
-            zd, qh, reph = G.approxim(Sd, opts=opts)
+            G, _ = FD.build_dist_graph(comm, rank, n, ud, vd, wd, grp, order=order)
+            zd, qh, reph = G.approxim(FD.slice_in(G, Sd, b), opts=opts)
             zh = zd.cpu()
             G.close()
             e_ms += (time.perf_counter() - t) * 1e3
@@ -431,8 +439,9 @@ def main():
         e_ms = float(t[0])
         line["e2e"] = {"value": B * e_iters / (e_ms / 1e3) / 1e9, "unit": "GB/s", "h2d_bytes_per_step": h2d,
                        "d2h_bytes_per_step": d2h, "ms_per_step": e_ms / reps,
-                       "note": "per rank: pinned H2D of the raw edges + opinion slice, partition, row-block CSR, "
-                               "halo plan, distributed Algorithm 1, D2H z; host wall clock, max over ranks"}
+                       "note": "per rank: pinned H2D of the raw edges + opinions, (relabelling,) partition, "
+                               "row-block CSR, halo plan, distributed Algorithm 1, D2H of the rank's z; host wall "
+                               "clock, max over ranks"}
     if not args.no_e2e and not dist_mode:
         uh = torch.from_numpy(wl.u).pin_memory().numpy()
         vh = torch.from_numpy(wl.v).pin_memory().numpy()
@@ -472,7 +481,7 @@ def main():
         line["cpu_baseline"] = cpu_baseline(wl, g, args.rtol)
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if ws > 1:
+    if dist_mode:
         dist.destroy_process_group()
     return 0
 

@@ -334,8 +334,9 @@ fj_status fj_lcc(int64_t n, int64_t m_in, const int32_t* u_dev, const int32_t* v
  * process per GPU).  Rank r owns rows [bounds[r], bounds[r+1]).  Its CSR first carries GLOBAL
  * column ids; fj_graph_create_dist renumbers them (own columns -> [0, n_loc), off-rank "ghost"
  * columns -> n_loc + their index in the sorted ghost list).  Each PCG iteration exchanges the ghost
- * entries of the search direction (halo; grouped NCCL send/recv over NVLink) and allreduces the dot
- * products; every rank takes identical decisions.  s / z passed to fj_solve / fj_approxim /
+ * entries of the preconditioned residual (halo; grouped NCCL send/recv over NVLink, on a comm stream
+ * overlapped with the own-column part of the product) and allreduces ONE vector of 3 k dot products
+ * (single-reduction Chronopoulos-Gear PCG); every rank takes identical decisions.  s / z passed to fj_solve / fj_approxim /
  * fj_quantities on a distributed handle are the rank's LOCAL row slices [n_loc][k]; quantities are
  * global and identical on every rank.  fj_apply is not available on a distributed handle.
  * Every call on a distributed handle is collective: all ranks must make it, in the same order. */
@@ -350,7 +351,8 @@ fj_status fj_comm_init(int nranks, int rank, const unsigned char id[128], fj_com
 fj_status fj_comm_init_loopback(int nranks, fj_comm** out);
 fj_status fj_comm_destroy(fj_comm* comm);
 
-/* bounds_host[0..nranks]: contiguous row blocks with ~equal raw (pre-dedup) nonzero counts,
+/* bounds_host[0..nranks]: contiguous row blocks of ~equal cost, cost of a row = its raw (pre-dedup)
+ * nonzeros + 6 (a row costs about as much as 6 nonzeros per PCG iteration: DESIGN.md §6 measured),
  * computed from the raw edge list on the device (same result on every rank). */
 fj_status fj_partition_rows(int64_t n, int64_t m_in, const int32_t* u_dev, const int32_t* v_dev, int nranks,
                             int64_t* bounds_host, void* stream);
@@ -360,6 +362,22 @@ fj_status fj_csr_rows_from_edges(int64_t n, int64_t m_in, const int32_t* u_dev, 
                                  const void* w_dev, int wtype, int64_t row_begin, int64_t row_end,
                                  int64_t* row_ptr_local_dev, int32_t* col_global_dev, void* w_out_dev,
                                  int64_t* nnz_out, void* stream);
+/* Locality order for the row partition (DESIGN.md §6.7 applied before partitioning): new2old_dev[n]
+ * lists the vertices by descending raw endpoint count (non-self-loop raw edges, duplicates counted;
+ * ties by ascending id), old2new_dev[n] is its inverse (device int32, written).  Every rank computes
+ * the same permutation from the same raw list.  Ids outside [0, n) are skipped here (the row
+ * builders reject them).  Synchronises. */
+fj_status fj_edge_degree_order(int64_t n, int64_t m_in, const int32_t* u_dev, const int32_t* v_dev,
+                               int32_t* new2old_dev, int32_t* old2new_dev, void* stream);
+/* fj_partition_rows / fj_csr_rows_from_edges of the RELABELLED graph (endpoint e -> old2new[e]):
+ * bounds and rows are in the new labels, columns are new global ids.  The caller maps its opinion
+ * slice in (rows new2old[row_begin .. row_end) of s) and z back out (fj_permute_rows). */
+fj_status fj_partition_rows_relabelled(int64_t n, int64_t m_in, const int32_t* u_dev, const int32_t* v_dev,
+                                       const int32_t* old2new_dev, int nranks, int64_t* bounds_host, void* stream);
+fj_status fj_csr_rows_from_edges_relabelled(int64_t n, int64_t m_in, const int32_t* u_dev, const int32_t* v_dev,
+                                            const int32_t* old2new_dev, const void* w_dev, int wtype,
+                                            int64_t row_begin, int64_t row_end, int64_t* row_ptr_local_dev,
+                                            int32_t* col_global_dev, void* w_out_dev, int64_t* nnz_out, void* stream);
 /* Sorted unique columns outside [row_begin, row_end) (the halo), ghosts_out capacity nnz_local. */
 fj_status fj_dist_ghosts(int64_t nnz_local, const int32_t* col_global_dev, int64_t row_begin, int64_t row_end,
                          int32_t* ghosts_out_dev, int64_t* n_ghost_out, void* stream);

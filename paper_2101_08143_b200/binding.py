@@ -131,6 +131,10 @@ def load_library(path: str = SO):
     L.fj_csr_rows_from_edges.argtypes = [_i64, _i64, _vp, _vp, _vp, ctypes.c_int, _i64, _i64, _vp, _vp, _vp,
                                          P(_i64), _vp]
     L.fj_dist_ghosts.argtypes = [_i64, _vp, _i64, _i64, _vp, P(_i64), _vp]
+    L.fj_edge_degree_order.argtypes = [_i64, _i64, _vp, _vp, _vp, _vp, _vp]
+    L.fj_partition_rows_relabelled.argtypes = [_i64, _i64, _vp, _vp, _vp, ctypes.c_int, _vp, _vp]
+    L.fj_csr_rows_from_edges_relabelled.argtypes = [_i64, _i64, _vp, _vp, _vp, _vp, ctypes.c_int, _i64, _i64, _vp,
+                                                    _vp, _vp, P(_i64), _vp]
     L.fj_graph_create_dist.argtypes = [_vp, ctypes.c_int, _i64, _vp, _i64, _vp, _vp, _vp, ctypes.c_int, _i64, _vp,
                                        _vp, _vp, _vp, P(_vp)]
     for name in ["fj_csr_from_edges", "fj_graph_create", "fj_graph_info", "fj_graph_degrees", "fj_graph_destroy",
@@ -138,7 +142,8 @@ def load_library(path: str = SO):
                  "fj_alg1_delta", "fj_approxim_alg1", "fj_forest_columns", "fj_opinions_generate",
                  "fj_connected_components", "fj_lcc", "fj_exact_dense", "fj_opinion_stats", "fj_solve", "fj_quantities", "fj_approxim", "fj_approxim_host",
                  "fj_comm_unique_id", "fj_comm_init", "fj_comm_init_loopback", "fj_comm_destroy",
-                 "fj_partition_rows", "fj_csr_rows_from_edges", "fj_dist_ghosts", "fj_graph_create_dist"]:
+                 "fj_partition_rows", "fj_csr_rows_from_edges", "fj_dist_ghosts", "fj_graph_create_dist",
+                 "fj_edge_degree_order", "fj_partition_rows_relabelled", "fj_csr_rows_from_edges_relabelled"]:
         getattr(L, name).restype = ctypes.c_int
     _lib = L
     return L
@@ -601,27 +606,49 @@ class Comm:
         self._h = None
 
 
-def partition_rows(n: int, u, v, nranks: int, stream=None):
-    import numpy as np
+def edge_degree_order(n: int, u, v, stream=None):
+    """fj_edge_degree_order: (new2old, old2new) int32 device permutations from the raw edge list."""
+    import torch
     _need_cuda(u, v)
+    new2old = torch.empty(n, dtype=torch.int32, device=u.device)
+    old2new = torch.empty(n, dtype=torch.int32, device=u.device)
+    _check(lib().fj_edge_degree_order(n, int(u.numel()), _ptr(u), _ptr(v), _ptr(new2old), _ptr(old2new),
+                                      _stream(stream)))
+    return new2old, old2new
+
+
+def partition_rows(n: int, u, v, nranks: int, stream=None, old2new=None):
+    """Contiguous nnz-balanced row blocks (in the relabelled ids when old2new is given)."""
+    import numpy as np
+    _need_cuda(u, v, old2new)
     b = np.zeros(nranks + 1, dtype=np.int64)
-    _check(lib().fj_partition_rows(n, int(u.numel()), _ptr(u), _ptr(v), nranks, ctypes.c_void_p(b.ctypes.data),
-                                   _stream(stream)))
+    if old2new is None:
+        _check(lib().fj_partition_rows(n, int(u.numel()), _ptr(u), _ptr(v), nranks, ctypes.c_void_p(b.ctypes.data),
+                                       _stream(stream)))
+    else:
+        _check(lib().fj_partition_rows_relabelled(n, int(u.numel()), _ptr(u), _ptr(v), _ptr(old2new), nranks,
+                                                  ctypes.c_void_p(b.ctypes.data), _stream(stream)))
     return [int(x) for x in b]
 
 
-def csr_rows_from_edges(n: int, u, v, w, r0: int, r1: int, stream=None):
-    """Row a1 for rows [r0, r1): (row_ptr_local, col_global, w_out, nnz)."""
+def csr_rows_from_edges(n: int, u, v, w, r0: int, r1: int, stream=None, old2new=None):
+    """Row a1 for rows [r0, r1) (of the relabelled graph when old2new is given):
+    (row_ptr_local, col_global, w_out, nnz)."""
     import torch
-    _need_cuda(u, v, w)
+    _need_cuda(u, v, w, old2new)
     m = int(u.numel())
     dev = u.device
     rp = torch.empty(r1 - r0 + 1, dtype=torch.int64, device=dev)
     col = torch.empty(max(2 * m, 1), dtype=torch.int32, device=dev)
     wo = None if w is None else torch.empty(max(2 * m, 1), dtype=w.dtype, device=dev)
     nnz = _i64()
-    _check(lib().fj_csr_rows_from_edges(n, m, _ptr(u), _ptr(v), _ptr(w), _wtype(w), r0, r1, _ptr(rp), _ptr(col),
-                                        _ptr(wo), ctypes.byref(nnz), _stream(stream)))
+    if old2new is None:
+        _check(lib().fj_csr_rows_from_edges(n, m, _ptr(u), _ptr(v), _ptr(w), _wtype(w), r0, r1, _ptr(rp), _ptr(col),
+                                            _ptr(wo), ctypes.byref(nnz), _stream(stream)))
+    else:
+        _check(lib().fj_csr_rows_from_edges_relabelled(n, m, _ptr(u), _ptr(v), _ptr(old2new), _ptr(w), _wtype(w), r0,
+                                                       r1, _ptr(rp), _ptr(col), _ptr(wo), ctypes.byref(nnz),
+                                                       _stream(stream)))
     k = nnz.value
     return rp, col[:k], (None if wo is None else wo[:k]), k
 

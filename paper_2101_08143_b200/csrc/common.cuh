@@ -7,6 +7,7 @@
 #include <cmath>
 
 #include "../../include/fj.h"
+#include <nvtx3/nvToolsExt.h>
 
 namespace fj {
 
@@ -67,6 +68,14 @@ void phase_tick(const char* label, cudaStream_t st);
   do {               \
   } while (0)
 #endif
+
+// NVTX range over a public entry point (visible in nsys / ncu --nvtx; header-only NVTX3, a no-op
+// without a tool attached)
+struct NvtxRange {
+  explicit NvtxRange(const char* s) { nvtxRangePushA(s); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+#define FJ_RANGE(name) ::fj::NvtxRange _fj_nvtx_range_(name)
 
 // kernel launch accounting (fj_kernel_launches)
 void count_launch(int64_t n = 1);

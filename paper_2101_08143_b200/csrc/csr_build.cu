@@ -192,6 +192,7 @@ static fj_status csr_from_edges(int64_t n, int64_t m_in, const int32_t* u, const
 extern "C" fj_status fj_csr_from_edges(int64_t n, int64_t m_in, const int32_t* u, const int32_t* v, const void* w,
                                        int wtype, int64_t* row_ptr, int32_t* col, void* w_out, int64_t* nnz_out,
                                        int64_t* selfloops_out, int64_t* dups_out, void* stream) {
+  FJ_RANGE("fj_csr_from_edges");
   return csr_from_edges(n, m_in, u, v, w, wtype, row_ptr, col, w_out, nnz_out, selfloops_out, dups_out,
                         stream);
 }
@@ -200,24 +201,32 @@ extern "C" fj_status fj_csr_from_edges(int64_t n, int64_t m_in, const int32_t* u
 namespace fj {
 
 // per raw edge: how many of its two orientations have their row in [r0, r1)
+// map (optional): endpoints relabelled old -> map[old] after the range check (the rows are those
+// of the relabelled graph; fj_csr_rows_from_edges_relabelled)
 __global__ void k_range_count(int64_t m, int64_t n, const int32_t* __restrict__ u, const int32_t* __restrict__ v,
-                              int64_t r0, int64_t r1, int64_t* __restrict__ cnt, BuildFlags* fl) {
+                              const int32_t* __restrict__ map, int64_t r0, int64_t r1, int64_t* __restrict__ cnt,
+                              BuildFlags* fl) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t a = u[e], c = v[e];
+    int64_t a = u[e], c = v[e];
     int64_t k = 0;
-    if (a < 0 || c < 0 || a >= n || c >= n) atomicOr(&fl->bad_range, 1u);
-    else if (a != c) k = (a >= r0 && a < r1) + (c >= r0 && c < r1);
+    if (a < 0 || c < 0 || a >= n || c >= n) {
+      atomicOr(&fl->bad_range, 1u);
+    } else if (a != c) {
+      if (map) { a = map[a]; c = map[c]; }
+      k = (a >= r0 && a < r1) + (c >= r0 && c < r1);
+    }
     cnt[e] = k;
   }
 }
 
 // emit the in-range orientations in (edge, orientation) order: key = ((row - r0) << b) | col
-__global__ void k_range_emit(int64_t m, const int32_t* __restrict__ u, const int32_t* __restrict__ v, int64_t r0,
-                             int64_t r1, int b, const int64_t* __restrict__ pos, uint64_t* __restrict__ keys,
-                             int32_t* __restrict__ vals) {
+__global__ void k_range_emit(int64_t m, const int32_t* __restrict__ u, const int32_t* __restrict__ v,
+                             const int32_t* __restrict__ map, int64_t r0, int64_t r1, int b,
+                             const int64_t* __restrict__ pos, uint64_t* __restrict__ keys, int32_t* __restrict__ vals) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t a = u[e], c = v[e];
+    int64_t a = u[e], c = v[e];
     if (a == c || a < 0 || c < 0) continue;
+    if (map) { a = map[a]; c = map[c]; }
     int64_t p = pos[e];
     if (a >= r0 && a < r1) {
       keys[p] = ((uint64_t)(a - r0) << b) | (uint64_t)c;
@@ -233,9 +242,9 @@ __global__ void k_range_emit(int64_t m, const int32_t* __restrict__ u, const int
 
 }  // namespace fj
 
-extern "C" fj_status fj_csr_rows_from_edges(int64_t n, int64_t m_in, const int32_t* u, const int32_t* v, const void* w,
-                                            int wtype, int64_t r0, int64_t r1, int64_t* row_ptr, int32_t* col,
-                                            void* w_out, int64_t* nnz_out, void* stream) {
+static fj_status csr_rows(int64_t n, int64_t m_in, const int32_t* u, const int32_t* v, const int32_t* map,
+                          const void* w, int wtype, int64_t r0, int64_t r1, int64_t* row_ptr, int32_t* col,
+                          void* w_out, int64_t* nnz_out, void* stream) {
   if (n < 1 || n >= INT32_MAX) return fail(FJ_E_INVALID_ARG, "n must be in [1, 2^31-2]");
   if (m_in < 0 || m_in >= INT32_MAX) return fail(FJ_E_INVALID_ARG, "m_in must be in [0, 2^31-2]");
   if (r0 < 0 || r1 > n || r1 <= r0) return fail(FJ_E_INVALID_ARG, "bad row range");
@@ -263,7 +272,7 @@ extern "C" fj_status fj_csr_rows_from_edges(int64_t n, int64_t m_in, const int32
   DevBuf<BuildFlags> fl;
   FJ_TRY(cnt.alloc(m, st)); FJ_TRY(pos.alloc(m + 1, st)); FJ_TRY(fl.alloc(1, st));
   FJ_CK(cudaMemsetAsync(fl.p, 0, sizeof(BuildFlags), st));
-  k_range_count<<<grid_for(m, sms), 256, 0, st>>>(m, n, u, v, r0, r1, cnt.p, fl.p);
+  k_range_count<<<grid_for(m, sms), 256, 0, st>>>(m, n, u, v, map, r0, r1, cnt.p, fl.p);
   FJ_CK_LAUNCH();
   FJ_TRY(cub_exclusive_sum(cnt.p, pos.p, m, st));
   int64_t last_pos = 0, last_cnt = 0;
@@ -279,7 +288,7 @@ extern "C" fj_status fj_csr_rows_from_edges(int64_t n, int64_t m_in, const int32
   DevBuf<int32_t> va, vb;
   FJ_TRY(ka.alloc(m2, st)); FJ_TRY(kb.alloc(m2, st));
   if (wbytes) { FJ_TRY(va.alloc(m2, st)); FJ_TRY(vb.alloc(m2, st)); }
-  k_range_emit<<<grid_for(m, sms), 256, 0, st>>>(m, u, v, r0, r1, b, pos.p, ka.p, wbytes ? va.p : nullptr);
+  k_range_emit<<<grid_for(m, sms), 256, 0, st>>>(m, u, v, map, r0, r1, b, pos.p, ka.p, wbytes ? va.p : nullptr);
   FJ_CK_LAUNCH();
   cnt.release();
   pos.release();
@@ -321,4 +330,19 @@ extern "C" fj_status fj_csr_rows_from_edges(int64_t n, int64_t m_in, const int32
   FJ_CK(cudaStreamSynchronize(st));
   *nnz_out = lp + lf;
   return FJ_OK;
+}
+
+extern "C" fj_status fj_csr_rows_from_edges(int64_t n, int64_t m_in, const int32_t* u, const int32_t* v, const void* w,
+                                            int wtype, int64_t r0, int64_t r1, int64_t* row_ptr, int32_t* col,
+                                            void* w_out, int64_t* nnz_out, void* stream) {
+  FJ_RANGE("fj_csr_rows_from_edges");
+  return csr_rows(n, m_in, u, v, nullptr, w, wtype, r0, r1, row_ptr, col, w_out, nnz_out, stream);
+}
+
+extern "C" fj_status fj_csr_rows_from_edges_relabelled(int64_t n, int64_t m_in, const int32_t* u, const int32_t* v,
+                                                       const int32_t* old2new, const void* w, int wtype, int64_t r0,
+                                                       int64_t r1, int64_t* row_ptr, int32_t* col, void* w_out,
+                                                       int64_t* nnz_out, void* stream) {
+  if (!old2new) return fail(FJ_E_INVALID_ARG, "old2new is NULL");
+  return csr_rows(n, m_in, u, v, old2new, w, wtype, r0, r1, row_ptr, col, w_out, nnz_out, stream);
 }

@@ -227,14 +227,39 @@ struct RowRangeBuild {
   int64_t r0, r1;
 };
 
-__global__ void k_degree_hist(int64_t m, const int32_t* __restrict__ u, const int32_t* __restrict__ v,
-                              unsigned long long* __restrict__ cnt) {
+// raw (pre-dedup) endpoint counts, optionally in relabelled ids map[.]
+__global__ void k_degree_hist(int64_t m, int64_t n, const int32_t* __restrict__ u, const int32_t* __restrict__ v,
+                              const int32_t* __restrict__ map, unsigned long long* __restrict__ cnt) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t a = u[e], b = v[e];
-    if (a == b) continue;
+    int32_t a = u[e], b = v[e];
+    if (a == b || a < 0 || b < 0 || a >= n || b >= n) continue;   // ranges are checked by the row builders
+    if (map) { a = map[a]; b = map[b]; }
     atomicAdd(cnt + a, 1ULL);
     atomicAdd(cnt + b, 1ULL);
   }
+}
+
+// Partition cost of a row: its raw nonzeros plus PART_ROW_COST.  Measured per rank on C5 (tools/
+// dist_model.py): a row costs about as much as 6 nonzeros (its T-tile slot in the product plus the
+// elementwise PCG step), so blocks of many short / isolated rows were the stragglers when balanced
+// by nonzeros alone.
+constexpr unsigned long long PART_ROW_COST = 6;
+__global__ void k_fill_u64(int64_t n, unsigned long long v, unsigned long long* __restrict__ a) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    a[i] = v;
+}
+
+// key = ~count (ascending radix sort = descending count, stable: ties by ascending id)
+__global__ void k_deg_keys(int64_t n, const unsigned long long* __restrict__ cnt, uint64_t* __restrict__ key,
+                           int32_t* __restrict__ id) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    key[i] = ~(uint64_t)cnt[i];
+    id[i] = (int32_t)i;
+  }
+}
+__global__ void k_inverse_perm(int64_t n, const int32_t* __restrict__ p, int32_t* __restrict__ inv) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    inv[p[i]] = (int32_t)i;
 }
 
 __global__ void k_bounds(int64_t n, const unsigned long long* __restrict__ pre /*[n+1] exclusive*/, int P,
@@ -1261,8 +1286,8 @@ fj_status fj_comm_destroy(fj_comm* c) {
   return FJ_OK;
 }
 
-fj_status fj_partition_rows(int64_t n, int64_t m, const int32_t* u, const int32_t* v, int nranks, int64_t* bounds_host,
-                            void* stream) {
+static fj_status partition_rows(int64_t n, int64_t m, const int32_t* u, const int32_t* v, const int32_t* map,
+                                int nranks, int64_t* bounds_host, void* stream) {
   if (n < 1 || n >= INT32_MAX || m < 0 || nranks < 1 || !bounds_host || (m > 0 && (!u || !v)))
     return fail(FJ_E_INVALID_ARG, "bad partition arguments");
   cudaStream_t st = S(stream);
@@ -1271,9 +1296,11 @@ fj_status fj_partition_rows(int64_t n, int64_t m, const int32_t* u, const int32_
   FJ_TRY(cnt.alloc(n + 1, st));
   FJ_TRY(pre.alloc(n + 1, st));
   FJ_TRY(b.alloc(nranks + 1, st));
-  FJ_CK(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long) * (n + 1), st));
+  k_fill_u64<<<(unsigned)std::min<int64_t>((n + 256) / 256, 8192), 256, 0, st>>>(n, PART_ROW_COST, cnt.p);
+  FJ_CK_LAUNCH();
+  FJ_CK(cudaMemsetAsync(cnt.p + n, 0, sizeof(unsigned long long), st));
   if (m > 0) {
-    k_degree_hist<<<(unsigned)std::min<int64_t>((m + 255) / 256, 8192), 256, 0, st>>>(m, u, v, cnt.p);
+    k_degree_hist<<<(unsigned)std::min<int64_t>((m + 255) / 256, 8192), 256, 0, st>>>(m, n, u, v, map, cnt.p);
     FJ_CK_LAUNCH();
   }
   size_t bytes = 0;
@@ -1287,6 +1314,50 @@ fj_status fj_partition_rows(int64_t n, int64_t m, const int32_t* u, const int32_
   k_bounds<<<(nranks + 1 + 63) / 64, 64, 0, st>>>(n, pre.p, nranks, b.p);
   FJ_CK_LAUNCH();
   FJ_CK(cudaMemcpyAsync(bounds_host, b.p, sizeof(int64_t) * (nranks + 1), cudaMemcpyDeviceToHost, st));
+  FJ_CK(cudaStreamSynchronize(st));
+  return FJ_OK;
+}
+
+fj_status fj_partition_rows(int64_t n, int64_t m, const int32_t* u, const int32_t* v, int nranks, int64_t* bounds_host,
+                            void* stream) {
+  FJ_RANGE("fj_partition_rows");
+  return partition_rows(n, m, u, v, nullptr, nranks, bounds_host, stream);
+}
+
+fj_status fj_partition_rows_relabelled(int64_t n, int64_t m, const int32_t* u, const int32_t* v, const int32_t* old2new,
+                                       int nranks, int64_t* bounds_host, void* stream) {
+  if (!old2new) return fail(FJ_E_INVALID_ARG, "old2new is NULL");
+  return partition_rows(n, m, u, v, old2new, nranks, bounds_host, stream);
+}
+
+fj_status fj_edge_degree_order(int64_t n, int64_t m, const int32_t* u, const int32_t* v, int32_t* new2old,
+                               int32_t* old2new, void* stream) {
+  FJ_RANGE("fj_edge_degree_order");
+  if (n < 1 || n >= INT32_MAX || m < 0 || !new2old || !old2new || (m > 0 && (!u || !v)))
+    return fail(FJ_E_INVALID_ARG, "bad degree-order arguments");
+  cudaStream_t st = S(stream);
+  DevBuf<unsigned long long> cnt;
+  DevBuf<uint64_t> key, key2;
+  DevBuf<int32_t> id;
+  FJ_TRY(cnt.alloc(n, st)); FJ_TRY(key.alloc(n, st)); FJ_TRY(key2.alloc(n, st)); FJ_TRY(id.alloc(n, st));
+  FJ_CK(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long) * n, st));
+  if (m > 0) {
+    k_degree_hist<<<(unsigned)std::min<int64_t>((m + 255) / 256, 8192), 256, 0, st>>>(m, n, u, v, nullptr, cnt.p);
+    FJ_CK_LAUNCH();
+  }
+  const unsigned gb = (unsigned)std::min<int64_t>((n + 255) / 256, 8192);
+  k_deg_keys<<<gb, 256, 0, st>>>(n, cnt.p, key.p, id.p);
+  FJ_CK_LAUNCH();
+  size_t bytes = 0;
+  FJ_CK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, key.p, key2.p, id.p, new2old, n, 0, 64, st));
+  {
+    DevBuf<uint8_t> tmp;
+    FJ_TRY(tmp.alloc((int64_t)bytes, st));
+    FJ_CK(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, key.p, key2.p, id.p, new2old, n, 0, 64, st));
+    count_cub();
+  }
+  k_inverse_perm<<<gb, 256, 0, st>>>(n, new2old, old2new);
+  FJ_CK_LAUNCH();
   FJ_CK(cudaStreamSynchronize(st));
   return FJ_OK;
 }
@@ -1340,6 +1411,7 @@ fj_status fj_graph_create_dist(fj_comm* comm, int rank, int64_t n_global, const 
                                const int64_t* row_ptr_local, const int32_t* col_global, const void* w, int wtype,
                                int64_t n_ghost, const int32_t* ghosts, const int64_t* send_counts,
                                const int32_t* send_idx, void* stream, fj_graph** out) {
+  FJ_RANGE("fj_graph_create_dist");
   if (!comm || !bounds || !out || !send_counts || rank < 0 || rank >= comm->nranks)
     return fail(FJ_E_INVALID_ARG, "bad distributed graph arguments");
   if (comm->kind == 0 && rank != comm->rank) return fail(FJ_E_INVALID_ARG, "rank does not match the NCCL communicator");

@@ -81,6 +81,7 @@ using namespace fj;
 
 extern "C" fj_status fj_exact_dense(const fj_graph* gc, int k, const double* s_dev, double* z_dev,
                                     fj_quantities_t* q_host, void* stream) {
+  FJ_RANGE("fj_exact_dense");
   if (!gc || !s_dev || !z_dev) return fail(FJ_E_INVALID_ARG, "null argument");
   if (k < 1 || k > MAXK) return fail(FJ_E_INVALID_ARG, "k must be in [1, 64]");
   if (s_dev == z_dev) return fail(FJ_E_INVALID_ARG, "s and z must not alias");

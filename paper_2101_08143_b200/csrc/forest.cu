@@ -38,6 +38,7 @@ using namespace fj;
 
 extern "C" fj_status fj_forest_columns(const fj_graph* gc, int64_t m, const int32_t* cols_host, double* omega_dev,
                                        const fj_solve_opts* opts, fj_solve_report* rep, void* stream) {
+  FJ_RANGE("fj_forest_columns");
   if (!gc || !cols_host || !omega_dev || m < 1) return fail(FJ_E_INVALID_ARG, "null argument or m < 1");
   fj_graph* g = const_cast<fj_graph*>(gc);
   if (g->dist) return fail(FJ_E_UNSUPPORTED, "fj_forest_columns on a distributed graph");

@@ -362,6 +362,7 @@ void fj_default_solve_opts(fj_solve_opts* o) {
 
 fj_status fj_graph_create(int64_t n, int64_t nnz, const int64_t* row_ptr, const int32_t* col, const void* w,
                           int wtype, int validate, void* stream, fj_graph** out) {
+  FJ_RANGE("fj_graph_create");
   if (!out) return fail(FJ_E_INVALID_ARG, "out is NULL");
   *out = nullptr;
   if (n < 1 || n >= INT32_MAX) return fail(FJ_E_INVALID_ARG, "n must be in [1, 2^31-2]");

@@ -191,6 +191,7 @@ fj_status fj_opinions_generate(int64_t n, int kind, uint64_t seed, double* s_dev
 
 fj_status fj_connected_components(int64_t n, int64_t m_in, const int32_t* u_dev, const int32_t* v_dev,
                                   int32_t* label_dev, int64_t* n_comp, void* stream) {
+  FJ_RANGE("fj_connected_components");
   if (n < 1 || n > INT32_MAX || m_in < 0 || !label_dev || (m_in > 0 && (!u_dev || !v_dev)))
     return fail(FJ_E_INVALID_ARG, "n in [1, 2^31), m_in >= 0, non-null buffers");
   cudaStream_t st = S(stream);
@@ -222,6 +223,7 @@ fj_status fj_connected_components(int64_t n, int64_t m_in, const int32_t* u_dev,
 fj_status fj_lcc(int64_t n, int64_t m_in, const int32_t* u_dev, const int32_t* v_dev, const void* w_dev, int wtype,
                  int32_t* vmap_dev, int32_t* u_out, int32_t* v_out, void* w_out, int64_t* n_lcc, int64_t* m_lcc,
                  void* stream) {
+  FJ_RANGE("fj_lcc");
   if (n < 1 || n > INT32_MAX || m_in < 0 || !vmap_dev || !n_lcc || !m_lcc || (m_in > 0 && (!u_dev || !v_dev)))
     return fail(FJ_E_INVALID_ARG, "n in [1, 2^31), m_in >= 0, non-null buffers");
   if (wtype < FJ_W_UNIT || wtype > FJ_W_F64) return fail(FJ_E_INVALID_ARG, "bad wtype");

@@ -367,6 +367,7 @@ using namespace fj;
 extern "C" {
 
 fj_status fj_apply(const fj_graph* gc, int op, int k, const double* x, double* y, void* stream) {
+  FJ_RANGE("fj_apply");
   if (!gc || !x || !y) return fail(FJ_E_INVALID_ARG, "null argument");
   if (k < 1 || k > MAXK) return fail(FJ_E_INVALID_ARG, "k must be in [1, 64]");
   if (op != FJ_OP_L && op != FJ_OP_IPL) return fail(FJ_E_INVALID_ARG, "bad op");
@@ -402,6 +403,7 @@ fj_status fj_time_spmv(const fj_graph* gc, int k, int reps, float* ms_host, void
 
 fj_status fj_solve(const fj_graph* gc, int k, const double* s, double* z, const fj_solve_opts* opts,
                    fj_solve_report* rep, void* stream) {
+  FJ_RANGE("fj_solve");
   if (!gc || !s || !z) return fail(FJ_E_INVALID_ARG, "null argument");
   if (k < 1 || k > MAXK) return fail(FJ_E_INVALID_ARG, "k must be in [1, 64]");
   if (s == z) return fail(FJ_E_INVALID_ARG, "s and z must not alias");

@@ -368,6 +368,7 @@ using namespace fj;
 extern "C" {
 
 fj_status fj_opinion_stats(const fj_graph* gc, int k, const double* s, double* stats_host, void* stream) {
+  FJ_RANGE("fj_opinion_stats");
   if (!gc || !s || !stats_host) return fail(FJ_E_INVALID_ARG, "null argument");
   if (k < 1 || k > MAXK) return fail(FJ_E_INVALID_ARG, "k must be in [1, 64]");
   fj_graph* g = const_cast<fj_graph*>(gc);
@@ -382,6 +383,7 @@ fj_status fj_opinion_stats(const fj_graph* gc, int k, const double* s, double* s
 
 fj_status fj_quantities(const fj_graph* gc, int k, const double* s, const double* z, fj_quantities_t* out,
                         void* stream) {
+  FJ_RANGE("fj_quantities");
   if (!gc || !s || !z || !out) return fail(FJ_E_INVALID_ARG, "null argument");
   if (k < 1 || k > MAXK) return fail(FJ_E_INVALID_ARG, "k must be in [1, 64]");
   fj_graph* g = const_cast<fj_graph*>(gc);
@@ -635,6 +637,7 @@ extern "C" {
 
 fj_status fj_approxim(const fj_graph* gc, int k, const double* s, double* z_user, const fj_solve_opts* opts,
                       fj_quantities_t* qout, fj_solve_report* rep, void* stream) {
+  FJ_RANGE("fj_approxim");
   return approxim_impl(gc, k, s, z_user, opts, qout, rep, stream, nullptr, nullptr);
 }
 
@@ -652,6 +655,7 @@ static bool relabel_pays(int64_t n, int k) {
 fj_status fj_approxim_host(int64_t n, int64_t m_in, const int32_t* u_h, const int32_t* v_h, const void* w_h,
                            int wtype, int k, const double* s_h, double* z_h, const fj_solve_opts* opts,
                            fj_quantities_t* q_h, fj_solve_report* rep, void* stream) {
+  FJ_RANGE("fj_approxim_host");
   if (n < 1 || m_in < 0 || !s_h || !q_h || (m_in > 0 && (!u_h || !v_h))) return fail(FJ_E_INVALID_ARG, "null argument");
   if (k < 1 || k > MAXK) return fail(FJ_E_INVALID_ARG, "k must be in [1, 64]");
   if (wtype < FJ_W_UNIT || wtype > FJ_W_F64) return fail(FJ_E_INVALID_ARG, "bad wtype");
@@ -787,6 +791,7 @@ fj_status fj_alg1_delta(int64_t n, double w_min, double w_max, double d_max, dou
 
 fj_status fj_approxim_alg1(const fj_graph* gc, const double* s, double eps, const fj_solve_opts* opts,
                            fj_alg1_t* out, fj_solve_report* rep, void* stream) {
+  FJ_RANGE("fj_approxim_alg1");
   if (!gc || !s || !out) return fail(FJ_E_INVALID_ARG, "null argument");
   fj_graph* g = const_cast<fj_graph*>(gc);
   if (is_dist(g)) return fail(FJ_E_UNSUPPORTED, "fj_approxim_alg1 on a distributed graph");

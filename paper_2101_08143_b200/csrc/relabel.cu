@@ -187,6 +187,7 @@ using namespace fj;
 
 extern "C" fj_status fj_csr_degree_order(int64_t n, const int64_t* row_ptr, int32_t* new2old, int32_t* old2new,
                                          void* stream) {
+  FJ_RANGE("fj_csr_degree_order");
   if (n < 1 || n >= INT32_MAX) return fail(FJ_E_INVALID_ARG, "n must be in [1, 2^31-2]");
   if (!row_ptr || !new2old || !old2new) return fail(FJ_E_INVALID_ARG, "null argument");
   cudaStream_t st = S(stream);
@@ -212,6 +213,7 @@ extern "C" fj_status fj_csr_degree_order(int64_t n, const int64_t* row_ptr, int3
 extern "C" fj_status fj_csr_permute(int64_t n, int64_t nnz, const int64_t* row_ptr, const int32_t* col, const void* w,
                                     int wtype, const int32_t* new2old, const int32_t* old2new, int64_t* row_ptr_out,
                                     int32_t* col_out, void* w_out, void* stream) {
+  FJ_RANGE("fj_csr_permute");
   if (n < 1 || nnz < 0) return fail(FJ_E_INVALID_ARG, "n < 1 or nnz < 0");
   if (!row_ptr || !new2old || !old2new || !row_ptr_out || (nnz > 0 && (!col || !col_out)))
     return fail(FJ_E_INVALID_ARG, "null argument");

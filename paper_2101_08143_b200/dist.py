@@ -87,17 +87,46 @@ def exchange_requests(ghosts: np.ndarray, bounds, group):
     return counts, idx.astype(np.int32)
 
 
-def build_dist_graph(comm, rank, n, u, v, w, group, bounds=None, stream=None):
-    """One rank's DistGraph from the full raw edge list on this rank's device (rows a1 + a2, a8 set-up)."""
+def build_dist_graph(comm, rank, n, u, v, w, group, bounds=None, stream=None, order="natural"):
+    """One rank's DistGraph from the full raw edge list on this rank's device (rows a1 + a2, a8 set-up).
+    order="degree": the graph is relabelled by descending degree BEFORE partitioning
+    (fj_edge_degree_order), so every rank's gathered vector packs its hot rows; the
+    rank's opinion slice is then rows new2old[r0:r1] of s (slice_in below) and row i of the rank's z
+    is row G.rows_global[i] of the global z."""
     import torch
     from . import binding as B
+    n2o = o2n = None
+    if order == "degree":
+        n2o, o2n = B.edge_degree_order(n, u, v, stream)
+    elif order != "natural":
+        raise ValueError("order must be 'natural' or 'degree'")
     if bounds is None:
-        bounds = B.partition_rows(n, u, v, comm.nranks, stream)
+        bounds = B.partition_rows(n, u, v, comm.nranks, stream, old2new=o2n)
     r0, r1 = bounds[rank], bounds[rank + 1]
-    rp, colg, wo, nnz = B.csr_rows_from_edges(n, u, v, w, r0, r1, stream)
+    rp, colg, wo, nnz = B.csr_rows_from_edges(n, u, v, w, r0, r1, stream, old2new=o2n)
     gh = B.dist_ghosts(colg, r0, r1, stream)
     counts, idx = exchange_requests(gh.cpu().numpy(), bounds, group)
     send_idx = torch.from_numpy(idx).to(u.device)
     G = B.DistGraph(comm, rank, n, bounds, rp, colg, wo, gh, counts, send_idx, stream)
-    G.plan = {"n_ghost": int(gh.numel()), "send": counts, "nnz_local": nnz}
+    G.plan = {"n_ghost": int(gh.numel()), "send": counts, "nnz_local": nnz, "order": order}
+    G.rows_global = None if n2o is None else n2o[r0:r1].contiguous()   # input id of each local row
     return G, bounds
+
+
+def slice_in(G, S, bounds, stream=None):
+    """This rank's opinion rows: S[r0:r1] (natural order) or S[new2old[r0:r1]] (degree order),
+    gathered by the library's fj_permute_rows."""
+    r0, r1 = bounds[G.rank], bounds[G.rank + 1]
+    if G.rows_global is None:
+        return S[r0:r1].contiguous()
+    return _gather_rows(S, G.rows_global, stream)
+
+
+def _gather_rows(S, idx, stream=None):
+    """out[i] = S[idx[i]] for a global S (more rows than idx): fj_permute_rows over len(idx) rows."""
+    import torch
+    from . import binding as B
+    k = 1 if S.dim() == 1 else S.shape[1]
+    out = torch.empty((idx.numel(),) + tuple(S.shape[1:]), dtype=S.dtype, device=S.device)
+    B._check(B.lib().fj_permute_rows(int(idx.numel()), k, B._ptr(idx), B._ptr(S), B._ptr(out), B._stream(stream)))
+    return out

@@ -14,13 +14,15 @@ import oracle as O
 from paper_2101_08143_b200 import dist as D
 
 
-def _bounds_by_nnz(row_ptr, P):
-    """Same rule as fj_partition_rows (first row whose prefix reaches r/P of the total)."""
-    tot = int(row_ptr[-1])
+def _bounds_by_nnz(row_ptr, P, row_cost=6):
+    """Same rule as fj_partition_rows (first row whose cost prefix, nonzeros + row_cost per row,
+    reaches r/P of the total)."""
+    pre = row_ptr + row_cost * np.arange(len(row_ptr), dtype=np.int64)
+    tot = int(pre[-1])
     b = [0]
     for r in range(1, P):
         target = (tot // P) * r + (tot % P) * r // P
-        b.append(int(np.searchsorted(row_ptr[:-1], target, side="left")))
+        b.append(int(np.searchsorted(pre[:-1], target, side="left")))
     b.append(len(row_ptr) - 1)
     return b
 
@@ -148,9 +150,10 @@ def test_bounds_rule_balances_nnz():
     g = O.canonical_csr(wl.n, wl.u, wl.v, wl.w)
     for P in [2, 4, 8]:
         b = _bounds_by_nnz(g.row_ptr, P)
-        per = np.diff(g.row_ptr[b])
+        cost = g.row_ptr + 6 * np.arange(wl.n + 1)
+        per = np.diff(cost[b])
         assert b[0] == 0 and b[-1] == wl.n and np.all(np.diff(b) >= 0)
-        assert per.max() <= g.nnz / P + np.diff(g.row_ptr).max()
+        assert per.max() <= cost[-1] / P + np.diff(g.row_ptr).max() + 6
 
 
 def _gloo_cg_worker(rank, P, port, q):

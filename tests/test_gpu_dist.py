@@ -25,7 +25,7 @@ def fj():
     return m
 
 
-def run_ranks(fj, P, wl, S, opts=None):
+def run_ranks(fj, P, wl, S, opts=None, order="natural"):
     import torch
     from paper_2101_08143_b200 import dist as D
     comm = fj.Comm.loopback(P)
@@ -33,18 +33,22 @@ def run_ranks(fj, P, wl, S, opts=None):
     u = torch.from_numpy(wl.u).cuda()
     v = torch.from_numpy(wl.v).cuda()
     w = None if wl.w is None else torch.from_numpy(wl.w).cuda()
-    bounds = fj.partition_rows(wl.n, u, v, P)
+    o2n = fj.binding.edge_degree_order(wl.n, u, v)[1] if order == "degree" else None
+    bounds = fj.partition_rows(wl.n, u, v, P, old2new=o2n)
+    Sd = torch.from_numpy(np.ascontiguousarray(S)).cuda()
     out, errs = [None] * P, []
 
     def rank_main(r):
         try:
             st = torch.cuda.Stream()
             with torch.cuda.stream(st):
-                G, _ = D.build_dist_graph(comm, r, wl.n, u, v, w, D.ThreadGroup(world, r), bounds=bounds, stream=st)
-                Sl = torch.from_numpy(np.ascontiguousarray(S[bounds[r]:bounds[r + 1]])).cuda()
+                G, _ = D.build_dist_graph(comm, r, wl.n, u, v, w, D.ThreadGroup(world, r), bounds=bounds, stream=st,
+                                          order=order)
+                Sl = D.slice_in(G, Sd, bounds, stream=st)
                 z, q, rep = G.approxim(Sl, opts=opts, stream=st)
                 st.synchronize()
-                out[r] = (z.cpu().numpy(), q, rep, G.plan)
+                rows = None if G.rows_global is None else G.rows_global.cpu().numpy()
+                out[r] = (z.cpu().numpy(), q, rep, G.plan, rows)
                 G.close()
         except Exception as e:  # surface in the main thread
             errs.append(e)
@@ -55,7 +59,12 @@ def run_ranks(fj, P, wl, S, opts=None):
     [t.join(300) for t in ts]
     comm.close()
     assert not errs, errs
-    Z = np.concatenate([o[0] for o in out])
+    if order == "natural":
+        Z = np.concatenate([o[0] for o in out])
+    else:   # z rows back to the input labels
+        Z = np.zeros_like(np.asarray(S, dtype=np.float64))
+        for o in out:
+            Z[o[4]] = o[0]
     return Z, [o[1] for o in out], [o[2] for o in out], bounds, [o[3] for o in out]
 
 
@@ -200,3 +209,28 @@ def test_loopback_eps_target_warm_restart(fj):
         assert Q[0][0]["eps"][key] <= 1e-9
         assert abs(Q[0][0][key] - qo[key]) / qo[key] <= max(Q[0][0]["eps"][key], 1e-12), key
     assert np.max(np.abs(Z[:, 0] - zo)) < 1e-8
+
+
+@pytest.mark.parametrize("P,k", [(2, 1), (3, 3)])
+def test_loopback_degree_relabelled_partition_vs_oracle(fj, P, k):
+    """The graph relabelled by descending degree before partitioning (fj_edge_degree_order,
+    fj_partition_rows_relabelled, fj_csr_rows_from_edges_relabelled): z mapped back to the input
+    labels and the quantities against the oracle on the ORIGINAL graph (P:L88 P L P^T invariance)."""
+    import torch
+    wl = synth.make_config("c4", scale=13, kinds=["uniform", "exponential", "powerlaw"][:k])
+    Z, Q, R, bounds, plans = run_ranks(fj, P, wl, wl.S, order="degree")
+    g = O.canonical_csr(wl.n, wl.u, wl.v, wl.w)
+    u, v = torch.from_numpy(wl.u).cuda(), torch.from_numpy(wl.v).cuda()
+    n2o, o2n = fj.binding.edge_degree_order(wl.n, u, v)
+    keep = wl.u != wl.v
+    cnt = np.bincount(np.concatenate([wl.u[keep], wl.v[keep]]), minlength=wl.n)
+    assert np.array_equal(n2o.cpu().numpy(), np.argsort(-cnt, kind="stable"))
+    assert sum(p["nnz_local"] for p in plans) == g.nnz
+    for c in range(k):
+        zo, _ = O.solve_pcg(g, wl.S[:, c], tol=1e-13)
+        qo = O.quantities(g, wl.S[:, c], zo)
+        assert np.max(np.abs(Z[:, c] - zo)) < 1e-8
+        for r in range(P):
+            for key in QKEYS:
+                assert Q[r][c][key] == Q[0][c][key]
+                assert abs(Q[r][c][key] - qo[key]) / qo[key] <= 1e-8, (r, c, key)
