@@ -234,3 +234,66 @@ def test_loopback_degree_relabelled_partition_vs_oracle(fj, P, k):
             for key in QKEYS:
                 assert Q[r][c][key] == Q[0][c][key]
                 assert abs(Q[r][c][key] - qo[key]) / qo[key] <= 1e-8, (r, c, key)
+
+
+class _WL:   # a minimal workload record for hand-built graphs
+    def __init__(self, n, u, v, S, w=None):
+        self.n, self.u, self.v, self.S, self.w = n, u.astype(np.int32), v.astype(np.int32), S, w
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_loopback_star_hub_and_isolated(fj, P):
+    """A star (one hub row holding most of the nonzeros) plus isolated vertices: blocks of very
+    unequal row counts, ranks whose halo is the hub only, isolated rows (z_i = s_i)."""
+    n = 3000
+    leaves = np.arange(1, 2000)
+    wl = _WL(n, np.zeros(len(leaves), np.int64), leaves,
+             np.random.default_rng(3).uniform(0, 1, (n, 2)))
+    Z, Q, R, bounds, plans = run_ranks(fj, P, wl, wl.S)
+    g = O.canonical_csr(n, wl.u, wl.v)
+    for c in range(2):
+        zo = O.solve_dense(g, wl.S[:, c])
+        qo = O.quantities(g, wl.S[:, c], zo)
+        assert np.max(np.abs(Z[:, c] - zo)) < 1e-9
+        assert np.max(np.abs(Z[2000:, c] - wl.S[2000:, c])) < 1e-9   # isolated rows: z_i = s_i
+        for key in QKEYS:
+            assert abs(Q[0][c][key] - qo[key]) / qo[key] <= 1e-8, (c, key)
+
+
+def test_loopback_rank_without_halo(fj):
+    """Two disjoint graphs split exactly at the component boundary: a rank whose local rows have no
+    ghost columns (empty halo, no boundary rows) -- the off-diagonal pass is empty."""
+    import torch
+    from paper_2101_08143_b200 import dist as D
+    a = synth.make_config("c1", n=1500, k=1)
+    u = np.concatenate([a.u, a.u + 1500])
+    v = np.concatenate([a.v, a.v + 1500])
+    S = np.random.default_rng(5).uniform(0, 1, (3000, 1))
+    wl = _WL(3000, u, v, S)
+    comm = fj.Comm.loopback(2)
+    world = D.ThreadWorld(2)
+    ud, vd = torch.from_numpy(wl.u).cuda(), torch.from_numpy(wl.v).cuda()
+    bounds = [0, 1500, 3000]
+    out = [None, None]
+
+    def rank_main(r):
+        st = torch.cuda.Stream()
+        with torch.cuda.stream(st):
+            G, _ = D.build_dist_graph(comm, r, 3000, ud, vd, None, D.ThreadGroup(world, r), bounds=bounds, stream=st)
+            z, q, rep = G.approxim(torch.from_numpy(np.ascontiguousarray(S[bounds[r]:bounds[r + 1]])).cuda(), stream=st)
+            st.synchronize()
+            out[r] = (z.cpu().numpy(), q, rep, G.plan)
+            G.close()
+    import threading
+    ts = [threading.Thread(target=rank_main, args=(r,)) for r in range(2)]
+    [t.start() for t in ts]
+    [t.join(300) for t in ts]
+    comm.close()
+    assert out[0][3]["n_ghost"] == 0 and out[1][3]["n_ghost"] == 0
+    g = O.canonical_csr(3000, wl.u, wl.v)
+    zo = O.solve_dense(g, S[:, 0])
+    qo = O.quantities(g, S[:, 0], zo)
+    Z = np.concatenate([out[0][0], out[1][0]]).reshape(-1)
+    assert np.max(np.abs(Z - zo)) < 1e-9
+    for key in QKEYS:
+        assert abs(out[0][1][0][key] - qo[key]) / qo[key] <= 1e-8, key
