@@ -221,6 +221,7 @@ def main():
                     help="host-driven PCG loop (same kernels); ncu cannot see kernels inside conditional graphs")
     args = ap.parse_args()
     ws, rank, local = dist_init()
+    os.environ.setdefault("NCCL_DEBUG", "WARN")   # keep rank 0's stdout to the one JSON line
     if args.impl == "reference":
         return run_reference(args, ws, rank)
 

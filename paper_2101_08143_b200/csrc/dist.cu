@@ -453,11 +453,13 @@ fj_status dist_stats_combine(const fj_graph* g, int k, double* dev4k /* [k][4] d
 //                     (alpha_0 = gamma_0 / delta_0), p = u + beta p, s = w + beta s, x += alpha p,
 //                     r -= alpha s, u = dinv o r, local gamma' = r^T u, rho' = ||r||^2
 //   H  halo(u)        pack + grouped ncclSend/ncclRecv on the comm stream          } concurrent
-//   Sd w = (I+L) u    over the OWN columns of every row (diag block), delta part   }
-//   So w -= A_gh u_gh over the ghost columns of the boundary rows (after H), delta
-//   R  allreduce [gamma', delta', rho'] (3 KP doubles)  -> the next E on every rank
+//   Sd t = A_own u    adjacency product over the OWN columns of every row          }
+//   So t += A_gh u_gh over the ghost columns of the boundary rows (after H); both add u^T t
+//   R  allreduce [gamma', u^T t, rho']  (3 KP doubles)  -> the next E on every rank, which forms
+//      w = (I+L)u = r - t  and  delta = u^T w = gamma - u^T t   ((1+d) o u = r since u = dinv o r)
 // w = (I+L)u, so s = (I+L)p and the recurrences are those of textbook PCG (same iterates in exact
-// arithmetic).  Columns of a k <= 4 batch are independent (per-column alpha, beta, mask) and padded
+// arithmetic).  The product needs no degree and no per-row boundary flag (no per-row dependent
+// loads).  Columns of a k <= 4 batch are independent (per-column alpha, beta, mask) and padded
 // to KP = 1, 2 or 4 (k = 3 -> 4).  Every decision is taken from allreduced scalars, identically on
 // every rank; partial sums are formed and combined in a fixed order.  With NCCL the iteration is
 // captured once into a CUDA graph of CG_UNROLL iterations (kernels exit early once converged) and
@@ -688,7 +690,7 @@ static fj_status ensure_split(fj_graph* g, CgWs* c, int f, cudaStream_t st) {
 
 // ---------------------------------------------------------------- the two product passes
 template <int WT, int KP>
-struct CgDiagOp {   // w = (I+L) u over the own columns; (u, w) over the rows without ghost columns
+struct CgDiagOp {   // t = A u over the own columns of every row; u^T t
   using V = typename VT<KP>::type;
   static constexpr int ITEMS = KP == 1 ? fj::ITEMS : VEC_ITEMS;
   static constexpr int TILE_ROWS = KP == 1 ? fj::TILE_ROWS : VEC_TILE_ROWS;
@@ -703,9 +705,7 @@ struct CgDiagOp {   // w = (I+L) u over the own columns; (u, w) over the rows wi
     return r;
   }
   const double* __restrict__ u;
-  double* __restrict__ w;
-  const double* __restrict__ deg;
-  const uint8_t* __restrict__ bnd;
+  double* __restrict__ w;   // t
   double* dot_out;
   const int32_t* done;
   __device__ __forceinline__ bool skip() const { return done && *(volatile const int32_t*)done; }
@@ -719,15 +719,12 @@ struct CgDiagOp {   // w = (I+L) u over the own columns; (u, w) over the rows wi
   }
   template <class P>
   __device__ __forceinline__ void finish_row(int64_t i, int64_t, const V& ui, const double (&a)[NA], P& part) const {
-    const double dd = 1.0 + deg[i];
-    V wi;
+    V ti;
 #pragma unroll
-    for (int c = 0; c < KP; ++c) setc<KP>(wi, c, fma(dd, cmp<KP>(ui, c), -a[c]));
-    stv<KP>(w + i * KP, wi);
-    if (!bnd[i]) {
+    for (int c = 0; c < KP; ++c) setc<KP>(ti, c, a[c]);
+    stv<KP>(w + i * KP, ti);
 #pragma unroll
-      for (int c = 0; c < KP; ++c) part[c] = fma(cmp<KP>(ui, c), cmp<KP>(wi, c), part[c]);
-    }
+    for (int c = 0; c < KP; ++c) part[c] = fma(cmp<KP>(ui, c), a[c], part[c]);
   }
   __device__ __forceinline__ void finalize(const double (&tot)[NP]) const {
 #pragma unroll
@@ -736,7 +733,7 @@ struct CgDiagOp {   // w = (I+L) u over the own columns; (u, w) over the rows wi
 };
 
 template <int WT, int KP>
-struct CgOffOp {    // w_i -= sum over the ghost columns of boundary row i; (u, w) over those rows
+struct CgOffOp {    // t_i += sum over the ghost columns of boundary row i; u^T (that part)
   using V = typename VT<KP>::type;
   static constexpr int ITEMS = KP == 1 ? fj::ITEMS : VEC_ITEMS;
   static constexpr int TILE_ROWS = KP == 1 ? fj::TILE_ROWS : VEC_TILE_ROWS;
@@ -749,7 +746,7 @@ struct CgOffOp {    // w_i -= sum over the ghost columns of boundary row i; (u, 
   double* __restrict__ w;
   const int32_t* __restrict__ rows;
   const double* dpart;   // the diag pass's (u, w) partial
-  double* red;           // red[KP + c] <- local delta_c
+  double* red;           // red[KP + c] <- local u^T t
   const int32_t* done;
   __device__ __forceinline__ bool skip() const { return done && *(volatile const int32_t*)done; }
   __device__ __forceinline__ bool wants_xi() const { return true; }
@@ -763,12 +760,12 @@ struct CgOffOp {    // w_i -= sum over the ghost columns of boundary row i; (u, 
   template <class P>
   __device__ __forceinline__ void finish_row(int64_t b, int64_t, const V& ui, const double (&a)[NA], P& part) const {
     const int64_t i = rows[b];
-    V wi = ldv<KP>(w + i * KP);
+    V ti = ldv<KP>(w + i * KP);
 #pragma unroll
-    for (int c = 0; c < KP; ++c) setc<KP>(wi, c, cmp<KP>(wi, c) - a[c]);
-    stv<KP>(w + i * KP, wi);
+    for (int c = 0; c < KP; ++c) setc<KP>(ti, c, cmp<KP>(ti, c) + a[c]);
+    stv<KP>(w + i * KP, ti);
 #pragma unroll
-    for (int c = 0; c < KP; ++c) part[c] = fma(cmp<KP>(ui, c), cmp<KP>(wi, c), part[c]);
+    for (int c = 0; c < KP; ++c) part[c] = fma(cmp<KP>(ui, c), a[c], part[c]);
   }
   __device__ __forceinline__ void finalize(const double (&tot)[NP]) const {
 #pragma unroll
@@ -796,8 +793,8 @@ static fj_status launch_view(const fj_graph* g, const Sched& S, const int64_t* r
   return FJ_OK;
 }
 
-// w = (I+L) u on the rank's rows, red[KP..2KP) = local (u, w); the halo of u travels on the comm
-// stream while the own-column pass runs (NCCL); LOOPBACK exchanges first, host-synchronously.
+// t = A v on the rank's rows (into c->w), red[KP..2KP) = local v^T t; the halo of v travels on the
+// comm stream while the own-column pass runs (NCCL); LOOPBACK exchanges first, host-synchronously.
 template <int KP>
 static fj_status cg_product(fj_graph* g, CgWs* c, const double* u_in, cudaStream_t st, bool in_loop) {
   DistInfo* d = D(g);
@@ -817,7 +814,7 @@ static fj_status cg_product(fj_graph* g, CgWs* c, const double* u_in, cudaStream
   const int32_t* done = in_loop ? &c->cs->done : nullptr;   // loop products exit once converged
   auto run = [&](auto wt) -> fj_status {
     constexpr int WT = decltype(wt)::value;
-    CgDiagOp<WT, KP> od{u, c->w, g->deg, sp.bnd, c->dpart, done};
+    CgDiagOp<WT, KP> od{u, c->w, c->dpart, done};
     FJ_TRY((launch_view<WT>(g, sp.sd[f], sp.rp_d, sp.col_d, sp.w_d, g->n, sp.nnz_d, sp.tsd[f], c->grid_max, od, st)));
     if (overlap) FJ_CK(cudaStreamWaitEvent(st, c->ev_join, 0));
     CgOffOp<WT, KP> oo{u, c->w, sp.rows_o, c->dpart, c->red, done};
@@ -853,31 +850,40 @@ __device__ __forceinline__ bool cg_reduce(double (&v)[NPART], double* part, unsi
   return true;
 }
 
-// (re)start: r = s - q (restart, q = (I+L) x) or r = s, x = 0; u = dinv o r;
-// red[0..KP) = local r^T u, red[2KP..3KP) = ||r||^2, red[3KP..4KP) = ||s||^2
+// (re)start: r = s - (I+L) x = s - ((1+d) o x - t) with t = A x (restart), or r = s, x = 0;
+// u = dinv o r; red[0..KP) = local r^T u, red[2KP..3KP) = ||r||^2, red[3KP..4KP) = ||s||^2.
+// Rows are KP-wide vectors (one aligned load / store per row and array).
 template <int KP>
 __global__ void __launch_bounds__(VETB) k_cg_init(int64_t n, int k, const double* __restrict__ sv, int64_t ld, int c0,
-                                                  const double* __restrict__ dinv, const double* __restrict__ q,
-                                                  int restart, double* __restrict__ x, double* __restrict__ r,
-                                                  double* __restrict__ u, double* red, double* part, unsigned int* ticket) {
+                                                  const double* __restrict__ dinv, const double* __restrict__ deg,
+                                                  const double* __restrict__ t, int restart, double* __restrict__ x,
+                                                  double* __restrict__ r, double* __restrict__ u, double* red,
+                                                  double* part, unsigned int* ticket) {
+  using V = typename VT<KP>::type;
   __shared__ double s_red[3 * KP * VETB / 32];
   double v[3 * KP];
 #pragma unroll
   for (int j = 0; j < 3 * KP; ++j) v[j] = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)VETB + threadIdx.x; i < n; i += (int64_t)gridDim.x * VETB) {
     const double di = dinv[i];
+    V xv, tv, rv, uv;
+    if (restart) { xv = ldv<KP>(x + i * KP); tv = ldv<KP>(t + i * KP); }
+    const double dd = restart ? 1.0 + deg[i] : 0.0;
 #pragma unroll
     for (int c = 0; c < KP; ++c) {
       const double si = c < k ? sv[i * ld + c0 + c] : 0.0;
-      const double ri = restart ? si - q[i * KP + c] : si;
-      if (!restart) x[i * KP + c] = 0.0;
+      const double ri = restart ? si - fma(dd, cmp<KP>(xv, c), -cmp<KP>(tv, c)) : si;
       const double ui = di * ri;
-      r[i * KP + c] = ri;
-      u[i * KP + c] = ui;
+      setc<KP>(rv, c, ri);
+      setc<KP>(uv, c, ui);
+      if (!restart) setc<KP>(xv, c, 0.0);
       v[c] = fma(ri, ui, v[c]);
       v[KP + c] = fma(ri, ri, v[KP + c]);
       v[2 * KP + c] = fma(si, si, v[2 * KP + c]);
     }
+    if (!restart) stv<KP>(x + i * KP, xv);
+    stv<KP>(r + i * KP, rv);
+    stv<KP>(u + i * KP, uv);
   }
   if (cg_reduce<3 * KP>(v, part, ticket, s_red) && threadIdx.x == 0) {
 #pragma unroll
@@ -901,13 +907,15 @@ __global__ void k_cg_state(CgState* cs, int k, double rtol, int max_iter) {
   cs->k = k;
 }
 
-// one Chronopoulos-Gear step from the allreduced [gamma | delta | rho (| ss on the first step)]
+// one Chronopoulos-Gear step from the allreduced [gamma | u^T t | rho (| ss on the first step)]:
+// w = (I+L) u = r - t (t = A u from the product), delta = u^T w = gamma - u^T t
 template <int KP>
 __global__ void __launch_bounds__(VETB) k_cg_step(int64_t n, int k, const double* __restrict__ dinv,
-                                                  double* __restrict__ u, const double* __restrict__ w,
+                                                  double* __restrict__ u, const double* __restrict__ t,
                                                   double* __restrict__ p, double* __restrict__ s,
                                                   double* __restrict__ x, double* __restrict__ r, CgState* cs,
                                                   double* red, double* part, unsigned int* ticket) {
+  using V = typename VT<KP>::type;
   __shared__ double s_red[2 * KP * VETB / 32];
   if (*(volatile int32_t*)&cs->done) return;
   const int first = cs->first;
@@ -922,7 +930,7 @@ __global__ void __launch_bounds__(VETB) k_cg_step(int64_t n, int k, const double
     rr[c] = red[2 * KP + c];
     t2[c] = first ? cs->rtol2 * red[3 * KP + c] : cs->tol2[c];
     if (c < k && cs->active[c] && rr[c] > t2[c] && isfinite(rr[c])) {
-      const double dl = red[KP + c];
+      const double dl = g[c] - red[KP + c];
       const double b = first ? 0.0 : g[c] / cs->gprev[c];
       const double den = first ? dl : dl - b * g[c] / cs->aprev[c];
       if (den > 0.0 && isfinite(den) && isfinite(b)) {
@@ -954,24 +962,36 @@ __global__ void __launch_bounds__(VETB) k_cg_step(int64_t n, int k, const double
   for (int j = 0; j < 2 * KP; ++j) v[j] = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)VETB + threadIdx.x; i < n; i += (int64_t)gridDim.x * VETB) {
     const double di = dinv[i];
+    V rv = ldv<KP>(r + i * KP), uv = ldv<KP>(u + i * KP);
+    const V tv = ldv<KP>(t + i * KP);
+    V pv, sv, xv = ldv<KP>(x + i * KP);
+    if (!first) { pv = ldv<KP>(p + i * KP); sv = ldv<KP>(s + i * KP); }
 #pragma unroll
     for (int c = 0; c < KP; ++c) {
-      const int64_t o = i * KP + c;
-      double ri = r[o], ui = u[o];
+      double ri = cmp<KP>(rv, c), ui = cmp<KP>(uv, c);
+      const double wi = ri - cmp<KP>(tv, c);
+      double pc = first ? ui : fma(be[c], cmp<KP>(pv, c), ui);
+      double sc = first ? wi : fma(be[c], cmp<KP>(sv, c), wi);
       if (act[c]) {
-        const double pc = first ? ui : fma(be[c], p[o], ui);
-        const double sc = first ? w[o] : fma(be[c], s[o], w[o]);
-        p[o] = pc;
-        s[o] = sc;
-        x[o] = fma(al[c], pc, x[o]);
+        setc<KP>(xv, c, fma(al[c], pc, cmp<KP>(xv, c)));
         ri = fma(-al[c], sc, ri);
-        r[o] = ri;
         ui = di * ri;
-        u[o] = ui;
+      } else if (!first) {   // frozen column: keep its p, s
+        pc = cmp<KP>(pv, c);
+        sc = cmp<KP>(sv, c);
       }
+      setc<KP>(pv, c, pc);
+      setc<KP>(sv, c, sc);
+      setc<KP>(rv, c, ri);
+      setc<KP>(uv, c, ui);
       v[c] = fma(ri, ui, v[c]);
       v[KP + c] = fma(ri, ri, v[KP + c]);
     }
+    stv<KP>(p + i * KP, pv);
+    stv<KP>(s + i * KP, sv);
+    stv<KP>(x + i * KP, xv);
+    stv<KP>(r + i * KP, rv);
+    stv<KP>(u + i * KP, uv);
   }
   if (cg_reduce<2 * KP>(v, part, ticket, s_red) && threadIdx.x == 0) {
 #pragma unroll
@@ -997,20 +1017,24 @@ __global__ void __launch_bounds__(VETB) k_cg_step(int64_t n, int k, const double
   }
 }
 
-// local ||s_c - w_c||^2 (w = (I+L) x) -> red[0..KP)
+// local ||s_c - (I+L) x_c||^2 = ||s - ((1+d) o x - t)||^2 (t = A x) -> red[0..KP)
 template <int KP>
 __global__ void __launch_bounds__(VETB) k_cg_resid(int64_t n, int k, const double* __restrict__ sv, int64_t ld, int c0,
-                                                   const double* __restrict__ w, double* red, double* part,
+                                                   const double* __restrict__ deg, const double* __restrict__ x,
+                                                   const double* __restrict__ t, double* red, double* part,
                                                    unsigned int* ticket) {
+  using V = typename VT<KP>::type;
   __shared__ double s_red[KP * VETB / 32];
   double v[KP];
 #pragma unroll
   for (int c = 0; c < KP; ++c) v[c] = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)VETB + threadIdx.x; i < n; i += (int64_t)gridDim.x * VETB) {
+    const V xv = ldv<KP>(x + i * KP), tv = ldv<KP>(t + i * KP);
+    const double dd = 1.0 + deg[i];
 #pragma unroll
     for (int c = 0; c < KP; ++c) {
       if (c < k) {
-        const double e = sv[i * ld + c0 + c] - w[i * KP + c];
+        const double e = sv[i * ld + c0 + c] - fma(dd, cmp<KP>(xv, c), -cmp<KP>(tv, c));
         v[c] = fma(e, e, v[c]);
       }
     }
@@ -1131,7 +1155,7 @@ static fj_status dist_cg_t(fj_graph* g, int k, const double* sv, double* z, int6
   bool first = true;
   for (;;) {
     const bool restart = !first || warm;
-    if (restart) {   // w = (I+L) x, x from z on a warm start
+    if (restart) {   // t = A x (x from z on a warm start); k_cg_init forms (I+L) x = (1+d) o x - t
       if (first) { k_cg_pack<KP><<<cb, 256, 0, st>>>(nl, k, z, ld, c0, c->x); FJ_CK_LAUNCH(); }
       FJ_TRY(cg_product<KP>(g, c, c->x, st, false));
     }
@@ -1139,10 +1163,10 @@ static fj_status dist_cg_t(fj_graph* g, int k, const double* sv, double* z, int6
     FJ_CK(cudaEventRecord(c->ev0, st));
     k_cg_state<<<1, 1, 0, st>>>(c->cs, k, o.rtol, budget);
     FJ_CK_LAUNCH();
-    k_cg_init<KP><<<c->grid_elem, VETB, 0, st>>>(nl, k, sv, ld, c0, g->dinv, c->w, restart ? 1 : 0, c->x, c->r, c->u,
-                                                 c->red, c->part, c->ticket);
+    k_cg_init<KP><<<c->grid_elem, VETB, 0, st>>>(nl, k, sv, ld, c0, g->dinv, g->deg, c->w, restart ? 1 : 0, c->x,
+                                                 c->r, c->u, c->red, c->part, c->ticket);
     FJ_CK_LAUNCH();
-    FJ_TRY(cg_product<KP>(g, c, c->u, st, false));    // w = (I+L) u, delta
+    FJ_TRY(cg_product<KP>(g, c, c->u, st, false));    // t = A u, u^T t
     FJ_TRY(allreduce(d, c->red, 4 * KP, RED_SUM, st));
     first = false;
     for (;;) {
@@ -1157,9 +1181,10 @@ static fj_status dist_cg_t(fj_graph* g, int k, const double* sv, double* z, int6
       if (h.done) break;
     }
     FJ_CK(cudaEventRecord(c->ev1, st));
-    // true residual: w = (I+L) x (same product), then ||s - w||^2 per column, allreduced
+    // true residual: t = A x (same product), then ||s - ((1+d) o x - t)||^2 per column, allreduced
     FJ_TRY(cg_product<KP>(g, c, c->x, st, false));
-    k_cg_resid<KP><<<c->grid_elem, VETB, 0, st>>>(nl, k, sv, ld, c0, c->w, c->red + 3 * KVMAX, c->part, c->ticket);
+    k_cg_resid<KP><<<c->grid_elem, VETB, 0, st>>>(nl, k, sv, ld, c0, g->deg, c->x, c->w, c->red + 3 * KVMAX,
+                                                  c->part, c->ticket);
     FJ_CK_LAUNCH();
     FJ_TRY(allreduce(d, c->red + 3 * KVMAX, KP, RED_SUM, st));
     FJ_CK(cudaMemcpyAsync(res2.data(), c->red + 3 * KVMAX, sizeof(double) * KP, cudaMemcpyDeviceToHost, st));
