@@ -36,7 +36,9 @@ struct VecScalars {
 };
 
 // ---------------------------------------------------------------- row operators (tiles.cuh Op)
-// q = (I+L) p or L p for all KP columns of a padded [n][KP] block (P:L88 L = D - A).
+// q = (I+L) p or L p for the KQ real columns of a padded [n][KP] block (P:L88 L = D - A): the
+// gathered row is the whole KP-wide vector (one aligned load), but only the KQ real columns are
+// accumulated, carried through the warp's segmented scan and stored (k = 3: 3 of 4 lanes of work).
 template <int WT, int KP, int KQ = KP>   // y stored KQ wide
 struct ApplyOpV {
   using V = DVec<KP>;
@@ -44,7 +46,7 @@ struct ApplyOpV {
   static constexpr int TILE_ROWS = VEC_TILE_ROWS;
   static constexpr int MIN_BLOCKS = engine_min_blocks<V>();
   static constexpr bool TMA = true;
-  static constexpr int NA = KP, NP = KP;
+  static constexpr int NA = KQ, NP = KQ;
   static constexpr bool NEEDS_XI = false;
   static __device__ __forceinline__ V vzero() { return vzero_kp<KP>(); }
   const double* __restrict__ x;
@@ -62,7 +64,7 @@ struct ApplyOpV {
   __device__ __forceinline__ const V* xi_base() const { return reinterpret_cast<const V*>(x); }
   __device__ __forceinline__ void add(double (&a)[NA], double w, const V& xj, const V&) const {
 #pragma unroll
-    for (int c = 0; c < KP; ++c) a[c] = (WT == FJ_W_UNIT) ? a[c] + xj.v[c] : fma(w, xj.v[c], a[c]);
+    for (int c = 0; c < KQ; ++c) a[c] = (WT == FJ_W_UNIT) ? a[c] + xj.v[c] : fma(w, xj.v[c], a[c]);
   }
   template <class P>
   __device__ __forceinline__ void finish_row(int64_t i, int64_t len, const V& xi, const double (&a)[NA],
@@ -71,19 +73,19 @@ struct ApplyOpV {
     const double d = (WT == FJ_W_UNIT) ? (double)len : deg[i];
     const double dd = opL ? d : 1.0 + d;
 #pragma unroll
-    for (int c = 0; c < KP; ++c) yv.v[c] = fma(dd, xi.v[c], -a[c]);
+    for (int c = 0; c < KP; ++c) yv.v[c] = c < KQ ? fma(dd, xi.v[c], -a[c < KQ ? c : 0]) : 0.0;
 #pragma unroll
-    for (int c = 0; c < KP; ++c) part[c] = fma(xi.v[c], yv.v[c], part[c]);
+    for (int c = 0; c < KQ; ++c) part[c] = fma(xi.v[c], yv.v[c], part[c]);
     st_q<KP, KQ>(y, i, yv);
   }
   __device__ __forceinline__ void finalize(const double (&tot)[NP]) const {
     if (dot_out) {
 #pragma unroll
-      for (int c = 0; c < KP; ++c) dot_out[c] = tot[c];
+      for (int c = 0; c < KQ; ++c) dot_out[c] = tot[c];
     }
     if (!sc || !alpha_on_device) return;
 #pragma unroll
-    for (int c = 0; c < KP; ++c) {
+    for (int c = 0; c < KQ; ++c) {
       if (c >= k) break;
       sc->pq[c] = tot[c];
       if (sc->active[c]) {
