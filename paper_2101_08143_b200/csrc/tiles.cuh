@@ -50,11 +50,12 @@ constexpr int engine_min_blocks() {
   return sizeof(V) == 8 ? FJ_K1_MIN_BLOCKS : (sizeof(V) == 16 ? FJ_VEC2_MIN_BLOCKS : FJ_VEC_MIN_BLOCKS);
 }
 #ifndef FJ_VEC_ITEMS
-#define FJ_VEC_ITEMS 8
-#endif
+#define FJ_VEC_ITEMS 10   // r02: 10 once the product carries only the KQ real columns (C3 k = 3
+#endif                    // 0.643 -> 0.607 ms, C2 k = 2 80.6 -> 74.3 us; R-MAT k = 4 +3 %)
 // Merge items (row ends + nonzeros) per lane in a T tile, per engine: the k = 1 operators use
 // ITEMS (32 x 12 = 384 per tile); the vector operators (spmv_vec.cu) hold KP doubles per item and
-// use VEC_ITEMS (32 x 8 = 256): fewer registers, 4 instead of 3 blocks / SM (measured 21 % faster).
+// use VEC_ITEMS (32 x 10 = 320): 4 blocks / SM at 128 registers (12 overflows the quantities
+// pass's 48 KB of static shared memory).
 constexpr int ITEMS = FJ_ITEMS;
 constexpr int VEC_ITEMS = FJ_VEC_ITEMS;
 constexpr int T_ROW_MAX = 64;             // rows longer than this are W rows or chunked
