@@ -697,7 +697,7 @@ struct CgDiagOp {   // t = A u over the own columns of every row; u^T t
   static constexpr int MIN_BLOCKS = engine_min_blocks<V>();
   static constexpr bool TMA = KP > 1;
   static constexpr int NA = KP, NP = KP;
-  static constexpr bool NEEDS_XI = true;
+  static constexpr bool NEEDS_XI = false;   // add() does not use x_i
   static __device__ __forceinline__ V vzero() {
     V r;
 #pragma unroll
@@ -740,7 +740,7 @@ struct CgOffOp {    // t_i += sum over the ghost columns of boundary row i; u^T 
   static constexpr int MIN_BLOCKS = engine_min_blocks<V>();
   static constexpr bool TMA = KP > 1;
   static constexpr int NA = KP, NP = KP;
-  static constexpr bool NEEDS_XI = true;
+  static constexpr bool NEEDS_XI = false;   // add() does not use x_i
   static __device__ __forceinline__ V vzero() { return CgDiagOp<WT, KP>::vzero(); }
   const double* __restrict__ u;
   double* __restrict__ w;

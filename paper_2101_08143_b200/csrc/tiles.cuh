@@ -146,7 +146,7 @@ struct TileScratch {
 //   static constexpr int TILE_ROWS;                // rows per T tile (32 or 64; the schedule's)
 //   static constexpr int MIN_BLOCKS;               // __launch_bounds__ min blocks / SM (register cap)
 //   static constexpr bool TMA;                     // stage tiles by the TMA bulk-copy prefetch
-//   static constexpr int NA, NP; static constexpr bool NEEDS_XI;
+//   static constexpr int NA, NP; static constexpr bool NEEDS_XI;   // NEEDS_XI: add() reads x_i
 //   static __device__ V vzero();
 //   __device__ bool skip() const;                  // uniform early exit (solver finished)
 //   __device__ V gather(int32_t j) const;          // x_j for a nonzero (i, j)
@@ -255,8 +255,11 @@ __device__ __forceinline__ void t_tile(const TileSched& sc, const Op& op, const 
   for (int f = 0; f < NA; ++f) { a[f] = 0.0; a_first[f] = 0.0; }
   bool has_first = false;
   int row = row_s;
-  int re = row < R ? s_e[row] : INT_MAX;
-  V xi = row < R ? s_xi[row] : Op::vzero();
+  // the next row end inside this lane's range (rows [row_s, row_e) end here; the row it ends inside
+  // continues in later lanes: INT_MAX), so the per-nonzero test is one compare
+  int re = row < row_e ? s_e[row] : INT_MAX;
+  V xi = Op::vzero();   // x_i for operators whose add() uses it (NEEDS_XI)
+  if constexpr (Op::NEEDS_XI) xi = row < R ? s_xi[row] : Op::vzero();
   auto close_row = [&](int r) {
     if (r == row_s) {           // may have started in earlier lanes: finish after the carry scan
       has_first = true;
@@ -273,11 +276,11 @@ __device__ __forceinline__ void t_tile(const TileSched& sc, const Op& op, const 
   for (int j = 0; j < ITEMS; ++j) {
     const int k = nz_s + j;
     if (k < nz_e) {
-      while (row < row_e && re <= k) {
+      while (re <= k) {
         close_row(row);
         ++row;
-        re = row < R ? s_e[row] : INT_MAX;
-        xi = row < R ? s_xi[row] : Op::vzero();
+        re = row < row_e ? s_e[row] : INT_MAX;
+        if constexpr (Op::NEEDS_XI) xi = row < R ? s_xi[row] : Op::vzero();
       }
       op.add(a, (double)wv[j], xv[j], xi);
     }
