@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <string>
+#include <utility>
 #include <cstdio>
 #include <cmath>
 
@@ -76,6 +77,33 @@ struct NvtxRange {
   ~NvtxRange() { nvtxRangePop(); }
 };
 #define FJ_RANGE(name) ::fj::NvtxRange _fj_nvtx_range_(name)
+
+// Programmatic dependent launch (PDL) between the kernels of a solver iteration: a kernel launched
+// with pdl_launch() may start its blocks while its predecessor's last blocks drain; each such kernel
+// calls pdl_prologue() first -- it allows its own successor to launch early, then waits until the
+// predecessor grid has completed and its writes are visible.  Without the launch attribute both
+// instructions are no-ops.  FJ_PDL=0 disables (A/B).
+#ifndef FJ_PDL
+#define FJ_PDL 1
+#endif
+__device__ __forceinline__ void pdl_prologue() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+template <class... KArgs, class... Args>
+inline cudaError_t pdl_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = FJ_PDL ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 // kernel launch accounting (fj_kernel_launches)
 void count_launch(int64_t n = 1);

@@ -214,7 +214,7 @@ inline cudaError_t launch_warp_items(const fj_graph* g, const SolveWs* ws, const
 // The engine on an explicit schedule / scratch.
 template <int WT, class Op>
 inline cudaError_t launch_items_on(const fj_graph* g, const Sched& S, const TileSched& ts, const Op& op,
-                                   const TileScratch& scr, int grid_max, cudaStream_t st) {
+                                   const TileScratch& scr, int grid_max, cudaStream_t st, bool pdl = false) {
   static int occ = 0;   // per template instantiation
   if (occ == 0) {
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, warp_kernel<WT, Op>, WTPB, 0);
@@ -225,6 +225,7 @@ inline cudaError_t launch_items_on(const fj_graph* g, const Sched& S, const Tile
   const int64_t need = (S.n_items + WPB - 1) / WPB;
   if (grid > need) grid = need > 0 ? need : 1;
   if (grid > grid_max) grid = grid_max;
+  if (pdl) return pdl_launch(warp_kernel<WT, Op>, dim3((unsigned)grid), dim3(WTPB), st, ts, op, scr);
   warp_kernel<WT, Op><<<(unsigned)grid, WTPB, 0, st>>>(ts, op, scr);
   return cudaGetLastError();
 }
@@ -239,10 +240,10 @@ inline const Sched& sched_of(const fj_graph* g) {
 // scratch.  Returns the number of kernel launches (for accounting) through *launches.
 template <int WT, class Op>
 inline cudaError_t launch_product(const fj_graph* g, const TileScratch& scr, int grid_max, const Op& op,
-                                  cudaStream_t st, int* launches) {
+                                  cudaStream_t st, int* launches, bool pdl = false) {
   *launches = 1;
   const Sched& S = sched_of<Op>(g);
-  return launch_items_on<WT>(g, S, make_sched(g, S), op, scr, grid_max, st);
+  return launch_items_on<WT>(g, S, make_sched(g, S), op, scr, grid_max, st, pdl);
 }
 
 }  // namespace fj

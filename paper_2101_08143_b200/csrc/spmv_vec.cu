@@ -339,6 +339,7 @@ __global__ void __launch_bounds__(VETB) k_v_update(int64_t n, int k, const doubl
                                                    double* part, unsigned int* ticket, cudaGraphConditionalHandle h,
                                                    int use_h) {
   __shared__ double s_red[2 * KP * VETB / 32];
+  pdl_prologue();
   if (*(volatile int32_t*)&sc->done) {
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       if (XD) sc->xpend = 0;    // the loop ended earlier: nothing owed to x any more
@@ -402,6 +403,7 @@ template <int KP, int KQ, bool XD>
 __global__ void __launch_bounds__(VETB) k_v_dir(int64_t n, int k, const double* __restrict__ dinv,
                                                 const double* __restrict__ r, double* __restrict__ p,
                                                 double* __restrict__ x, const VecScalars* sc) {
+  pdl_prologue();
   const bool done = *(volatile const int32_t*)&sc->done;
   if (XD ? !*(volatile const int32_t*)&sc->xpend : done) return;
   double be[KP], al[KP];
@@ -572,12 +574,12 @@ static fj_status by_wtype(const fj_graph* g, F&& f) {
 // y [n][KQ] = (I+L) x (or L x) for x the padded [n][KP] block
 template <int KP, int KQ>
 static fj_status vec_apply_padded(const fj_graph* g, const VecWs* w, const double* x, double* y, int opL,
-                                  VecScalars* sc, cudaStream_t st) {
+                                  VecScalars* sc, cudaStream_t st, bool pdl = false) {
   return by_wtype<KP>(g, [&](auto wt) {
     constexpr int WT = decltype(wt)::value;
     ApplyOpV<WT, KP, KQ> op{x, y, g->deg, opL, sc, w->k};
     int nl = 0;
-    FJ_CK(launch_product<WT>(g, w->ts, w->grid_max, op, st, &nl));
+    FJ_CK(launch_product<WT>(g, w->ts, w->grid_max, op, st, &nl, pdl));
     if (!g_capturing) count_launch(nl);
     return FJ_OK;
   });
@@ -585,11 +587,13 @@ static fj_status vec_apply_padded(const fj_graph* g, const VecWs* w, const doubl
 
 template <int KP, int KQ>
 static fj_status vec_iteration(const fj_graph* g, VecWs* w, cudaStream_t st, cudaGraphConditionalHandle h, int use_h) {
-  FJ_TRY((vec_apply_padded<KP, KQ>(g, w, w->p, w->q, 0, w->sc, st)));
-  k_v_update<KP, KQ, true><<<w->grid_elem, VETB, 0, st>>>(g->n, w->k, g->dinv, w->p, w->q, w->x, w->r, w->sc,
-                                                      w->elem_part, w->elem_ticket, h, use_h);
+  // the three kernels of an iteration are chained by programmatic dependent launch (PDL)
+  FJ_TRY((vec_apply_padded<KP, KQ>(g, w, w->p, w->q, 0, w->sc, st, true)));
+  FJ_CK(pdl_launch(k_v_update<KP, KQ, true>, dim3(w->grid_elem), dim3(VETB), st, g->n, w->k, g->dinv,
+                   (const double*)w->p, (const double*)w->q, w->x, w->r, w->sc, w->elem_part, w->elem_ticket, h, use_h));
   FJ_CK_LAUNCH();
-  k_v_dir<KP, KQ, true><<<w->grid_elem, VETB, 0, st>>>(g->n, w->k, g->dinv, w->r, w->p, w->x, w->sc);
+  FJ_CK(pdl_launch(k_v_dir<KP, KQ, true>, dim3(w->grid_elem), dim3(VETB), st, g->n, w->k, g->dinv,
+                   (const double*)w->r, w->p, w->x, (const VecScalars*)w->sc));
   FJ_CK_LAUNCH();
   return FJ_OK;
 }

@@ -495,6 +495,7 @@ __global__ void __launch_bounds__(WTPB, Op::MIN_BLOCKS) warp_kernel(const TileSc
   __shared__ __align__(128) unsigned char s_pf[WPB][TMA ? 2 : 1][TMA ? PfSlot<Op>::BYTES : 16];
   __shared__ uint64_t s_bar[WPB][2];
 
+  pdl_prologue();   // solver iterations chain this kernel with PDL (no-op otherwise)
   if (op.skip()) return;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   constexpr bool PS = PartSmemT<Op>::value;
