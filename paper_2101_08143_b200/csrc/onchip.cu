@@ -33,7 +33,7 @@ inline size_t onchip_bytes(int64_t n, int64_t nnz, int wbytes) {
   add(4 * (size_t)(n + 1));
   add(4 * (size_t)nnz);
   add((size_t)wbytes * nnz);
-  add(8 * (size_t)n * (wbytes ? 7 : 6));
+  for (int v = 0; v < (wbytes ? 7 : 6); ++v) add(8 * (size_t)n);   // carved one by one, as k_onchip does
   return b;
 }
 

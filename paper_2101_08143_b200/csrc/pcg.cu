@@ -294,7 +294,7 @@ fj_status resid_col(const fj_graph* g, const SolveWs* w, const double* z, const 
 // the starting iterate.  Always ends with a recomputed true residual (restarting while it misses
 // rtol); *iters_out receives the iterations spent on this column.
 fj_status solve_col(fj_graph* g, const double* s, double* z, int64_t ld, int64_t c, const fj_solve_opts& o,
-                    int warm, fj_solve_report* rep, cudaStream_t st, int* iters_out) {
+                    int warm, fj_solve_report* rep, cudaStream_t st, int* iters_out, bool defer) {
   SolveWs* w = nullptr;
   FJ_TRY(get_ws(g, st, &w));
   const int64_t n = g->n;
@@ -331,10 +331,12 @@ fj_status solve_col(fj_graph* g, const double* s, double* z, int64_t ld, int64_t
       }
     }
     FJ_CK(cudaEventRecord(w->ev3, st));
-    // true residual ||s - (I+L) x||^2
-    FJ_TRY(resid_col(g, w, w->x, s, ld, c, &w->sc->res2, st));
+    // true residual ||s - (I+L) x||^2 (defer: the caller's fused quantities pass computes it and
+    // decides the restart, one CSR pass less per solve)
+    if (!defer) FJ_TRY(resid_col(g, w, w->x, s, ld, c, &w->sc->res2, st));
     FJ_CK(cudaMemcpyAsync(&h, w->sc, sizeof h, cudaMemcpyDeviceToHost, st));
     FJ_CK(cudaStreamSynchronize(st));
+    if (defer) h.res2 = h.rr;   // recursive residual stands in
     total_iter += h.iter;
     if (o.use_cuda_graph) count_launch(3 * std::max(h.iter, 1));
     float lms = 0.f;
@@ -342,7 +344,7 @@ fj_status solve_col(fj_graph* g, const double* s, double* z, int64_t ld, int64_t
     if (rep) { rep->ms_loop += lms; rep->iterations_total += h.iter; }
     rel_true = h.ss > 0 ? sqrt(h.res2 / h.ss) : 0.0;
     const bool ok = h.res2 <= h.tol2;
-    if (ok || restarts >= o.max_restarts || total_iter >= o.max_iter || h.breakdown) break;
+    if (defer || ok || restarts >= o.max_restarts || total_iter >= o.max_iter || h.breakdown) break;
     ++restarts;
   }
   k_copy_col<<<cb, 256, 0, st>>>(n, w->x, 1, 0, z, ld, c);
@@ -352,10 +354,10 @@ fj_status solve_col(fj_graph* g, const double* s, double* z, int64_t ld, int64_t
     rep->restarts = std::max(rep->restarts, restarts);
     const double rr = h.ss > 0 ? sqrt(h.rr / h.ss) : 0.0;
     rep->rel_res_recursive = std::max(rep->rel_res_recursive, rr);
-    rep->rel_res_true = std::isnan(rep->rel_res_true) ? rel_true : std::max(rep->rel_res_true, rel_true);
+    if (!defer) rep->rel_res_true = std::isnan(rep->rel_res_true) ? rel_true : std::max(rep->rel_res_true, rel_true);
   }
   const bool converged = h.res2 <= h.tol2;
-  if (rep && !converged) rep->converged = 0;
+  if (rep && !converged && !defer) rep->converged = 0;
   if (iters_out) *iters_out = total_iter;
   return converged ? FJ_OK : fail(FJ_E_NO_CONVERGENCE, "PCG did not reach rtol on the true residual");
 }
@@ -432,7 +434,7 @@ fj_status fj_solve(const fj_graph* gc, int k, const double* s, double* z, const 
     worst = sc;
   } else {
     for (int c = 0; c < k; ++c) {
-      fj_status sc = solve_col(g, s, z, k, c, o, 0, &r, st, nullptr);
+      fj_status sc = solve_col(g, s, z, k, c, o, 0, &r, st, nullptr, false);
       if (sc != FJ_OK && sc != FJ_E_NO_CONVERGENCE) return sc;
       if (sc != FJ_OK) worst = sc;
     }

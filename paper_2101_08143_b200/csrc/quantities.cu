@@ -11,7 +11,8 @@
 namespace fj {
 
 fj_status solve_col(fj_graph* g, const double* s, double* z, int64_t ld, int64_t c, const fj_solve_opts& o,
-                    int warm, fj_solve_report* rep, cudaStream_t st, int* iters_out);
+                    int warm, fj_solve_report* rep, cudaStream_t st, int* iters_out,
+                    bool defer = false);
 
 void free_quant_ws(fj_graph*) {}
 
@@ -610,19 +611,21 @@ static fj_status approxim_impl(const fj_graph* gc, int k, const double* s, doubl
         continue;
       }
     }
+    int true_restarts = 0;
     for (int round = 0;; ++round) {
       fj_solve_opts ob = oc;
       ob.max_iter = std::max(0, o.max_iter - spent);
       phase_tick("approxim: before solve", st);
       fj_status sc;
+      const bool deferred = !is_dist(g);
       if (is_dist(g)) {   // row a8: this rank's slice, halo exchange + allreduce inside
         const int before = r.iterations;
         r.iterations = 0;
         sc = dist_solve_cg(g, 1, s, z, k, c, ob, warm, &r, st);
         iters = r.iterations;
         r.iterations = std::max(before, iters);
-      } else {
-        sc = solve_col(g, s, z, k, c, ob, warm, &r, st, &iters);   // Alg. 1 line 3
+      } else {   // Alg. 1 line 3; the true residual comes from the quantities pass below
+        sc = solve_col(g, s, z, k, c, ob, warm, &r, st, &iters, true);
       }
       spent += iters;
       if (sc != FJ_OK && sc != FJ_E_NO_CONVERGENCE) return sc;
@@ -631,6 +634,18 @@ static fj_status approxim_impl(const fj_graph* gc, int k, const double* s, doubl
       phase_tick("approxim: quantities", st);
       memset(&qout[c], 0, sizeof(fj_quantities_t));
       fill_quantities(g, t, m, qout[c]);
+      if (deferred) {   // t[6] = ||s - (I+L) z||^2 of the fused pass decides convergence / restart
+        const double rel = t[9] > 0 ? std::sqrt(t[6] / t[9]) : 0.0;
+        const bool ok = t[6] <= ob.rtol * ob.rtol * t[9];
+        if (!ok && true_restarts < o.max_restarts && spent < o.max_iter) {
+          ++true_restarts;
+          r.restarts = std::max(r.restarts, true_restarts);
+          warm = 1;   // restart from z
+          continue;
+        }
+        r.rel_res_true = std::isnan(r.rel_res_true) ? rel : std::max(r.rel_res_true, rel);
+        if (!ok) sc = FJ_E_NO_CONVERGENCE;
+      }
       if (sc != FJ_OK) { worst = sc; break; }
       double emax = 0.0;
       for (int j = 0; j < 6; ++j) emax = std::max(emax, qout[c].eps[j]);
