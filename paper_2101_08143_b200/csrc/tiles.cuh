@@ -193,6 +193,25 @@ struct PartStore<NP, true> {
   __device__ __forceinline__ double& operator[](int j) { return b[j * WTPB]; }
 };
 
+// Deferred row finish (r02): rows that close inside a lane's merge range park their sums in a
+// per-warp shared-memory slot instead of running finish_row at the close (divergent: 1-2 lanes
+// active, ~10 times per tile); after the carry scan lane r finishes row r of the tile, all lanes
+// together, and the row results are stored coalesced.  Used when the slots fit FJ_DEFER_BYTES per
+// block.  FJ_DEFER: 0 off, 1 every operator, 2 (default) operators without the TMA tile staging
+// (the scalar k = 1 engine).  Measured (profiles/r02_ab_defer_prefetch.log): k = 1 C2 product
+// 58.1 -> 53.6 us; but the k = 3 C3 product 0.611 -> 0.690 ms, whose gathers miss L2: the finish
+// work done at the row closes overlaps the gathers still in flight, deferred it does not.
+#ifndef FJ_DEFER
+#define FJ_DEFER 2
+#endif
+#ifndef FJ_DEFER_BYTES
+#define FJ_DEFER_BYTES 4096
+#endif
+template <class Op>
+constexpr bool defer_finish() {
+  return (FJ_DEFER == 1 || (FJ_DEFER == 2 && !Op::TMA)) && Op::TILE_ROWS * Op::NA * 8 * WPB <= FJ_DEFER_BYTES;
+}
+
 template <class V>
 struct TilePre {
   const int32_t* col;     // col[k0 .. k0+N)
@@ -203,7 +222,7 @@ struct TilePre {
 template <int WT, class Op, bool PRE, class P>
 __device__ __forceinline__ void t_tile(const TileSched& sc, const Op& op, const ItemMeta& cur, int lane,
                                        int32_t* s_e, int32_t* s_col_own, typename Op::V* s_xi_own,
-                                       P& part, const TilePre<typename Op::V>& pre) {
+                                       double* s_acc, P& part, const TilePre<typename Op::V>& pre) {
   using V = typename Op::V;
   constexpr int NA = Op::NA;
   constexpr int ITEMS = Op::ITEMS;
@@ -260,11 +279,15 @@ __device__ __forceinline__ void t_tile(const TileSched& sc, const Op& op, const 
   int re = row < row_e ? s_e[row] : INT_MAX;
   V xi = Op::vzero();   // x_i for operators whose add() uses it (NEEDS_XI)
   if constexpr (Op::NEEDS_XI) xi = row < R ? s_xi[row] : Op::vzero();
+  constexpr bool DEFER = defer_finish<Op>();
   auto close_row = [&](int r) {
     if (r == row_s) {           // may have started in earlier lanes: finish after the carry scan
       has_first = true;
 #pragma unroll
       for (int f = 0; f < NA; ++f) a_first[f] = a[f];
+    } else if constexpr (DEFER) {
+#pragma unroll
+      for (int f = 0; f < NA; ++f) s_acc[r * NA + f] = a[f];
     } else {
       const int rb = r == 0 ? 0 : s_e[r - 1];
       op.finish_row(r0 + r, s_e[r] - rb, s_xi[r], a, part);
@@ -307,8 +330,26 @@ __device__ __forceinline__ void t_tile(const TileSched& sc, const Op& op, const 
     if (lane > 0) a_first[f] += cin;
   }
   if (has_first) {
-    const int rb = row_s == 0 ? 0 : s_e[row_s - 1];
-    op.finish_row(r0 + row_s, s_e[row_s] - rb, s_xi[row_s], a_first, part);
+    if constexpr (DEFER) {
+#pragma unroll
+      for (int f = 0; f < NA; ++f) s_acc[row_s * NA + f] = a_first[f];
+    } else {
+      const int rb = row_s == 0 ? 0 : s_e[row_s - 1];
+      op.finish_row(r0 + row_s, s_e[row_s] - rb, s_xi[row_s], a_first, part);
+    }
+  }
+  if constexpr (DEFER) {   // every row of the tile was parked by exactly one lane
+    __syncwarp();
+#pragma unroll
+    for (int rr = lane; rr < Op::TILE_ROWS; rr += 32) {
+      if (rr < R) {
+        double acc[NA];
+#pragma unroll
+        for (int f = 0; f < NA; ++f) acc[f] = s_acc[rr * NA + f];
+        const int rb = rr == 0 ? 0 : s_e[rr - 1];
+        op.finish_row(r0 + rr, s_e[rr] - rb, s_xi[rr], acc, part);
+      }
+    }
   }
   __syncwarp();
 }
@@ -485,10 +526,10 @@ template <int WT, class Op>
 __global__ void __launch_bounds__(WTPB, Op::MIN_BLOCKS) warp_kernel(const TileSched sc, const Op op, const TileScratch ws) {
   using V = typename Op::V;
   constexpr int NA = Op::NA, NP = Op::NP;
-  constexpr bool WEIGHTED = (WT != FJ_W_UNIT);
   __shared__ int32_t s_col[WPB][t_cap<Op::ITEMS>()];
   __shared__ int32_t s_e[WPB][Op::TILE_ROWS];
   __shared__ V s_xi[WPB][Op::TILE_ROWS];
+  __shared__ double s_acc[WPB][defer_finish<Op>() ? Op::TILE_ROWS * NA : 1];
   __shared__ double s_red[(NP > NA ? NP : NA) * WPB];
   __shared__ bool s_last;
   constexpr bool TMA = Op::TMA && FJ_TMA_PREFETCH != 0;
@@ -515,7 +556,7 @@ __global__ void __launch_bounds__(WTPB, Op::MIN_BLOCKS) warp_kernel(const TileSc
       if (it + nwarps < sc.n_items) m = sc.items[it + nwarps];
       if ((cur.info >> 30) == IT_T) {
         const TilePre<V> pre{nullptr, nullptr, nullptr};
-        t_tile<WT, Op, false>(sc, op, cur, lane, s_e[wib], s_col[wib], s_xi[wib], part, pre);
+        t_tile<WT, Op, false>(sc, op, cur, lane, s_e[wib], s_col[wib], s_xi[wib], s_acc[wib], part, pre);
       } else {
         wc_item<WT, Op>(sc, op, ws, cur, it, lane, part);
       }
@@ -563,8 +604,8 @@ __global__ void __launch_bounds__(WTPB, Op::MIN_BLOCKS) warp_kernel(const TileSc
           pend &= ~(1u << slot);
           pre = pf_view<Op>(cur, L, s_pf[wib][slot]);
         }
-        if (pre.col) t_tile<WT, Op, true>(sc, op, cur, lane, s_e[wib], s_col[wib], s_xi[wib], part, pre);
-        else t_tile<WT, Op, false>(sc, op, cur, lane, s_e[wib], s_col[wib], s_xi[wib], part, pre);
+        if (pre.col) t_tile<WT, Op, true>(sc, op, cur, lane, s_e[wib], s_col[wib], s_xi[wib], s_acc[wib], part, pre);
+        else t_tile<WT, Op, false>(sc, op, cur, lane, s_e[wib], s_col[wib], s_xi[wib], s_acc[wib], part, pre);
       } else {
         wc_item<WT, Op>(sc, op, ws, cur, it, lane, part);
       }
