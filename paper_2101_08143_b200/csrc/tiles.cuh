@@ -357,6 +357,9 @@ __device__ __forceinline__ void t_tile(const TileSched& sc, const Op& op, const 
 #ifndef FJ_TMA_PREFETCH
 #define FJ_TMA_PREFETCH 1
 #endif
+#ifndef FJ_SLOT_STAGE
+#define FJ_SLOT_STAGE 1
+#endif
 // ---------------------------------------------------------------- TMA bulk-copy tile prefetch
 // While a warp works on one T tile, the TMA engine copies the NEXT tile's three contiguous input
 // ranges (col indices, row_ptr entries, row values) global -> shared (cp.async.bulk, completion on
@@ -526,13 +529,19 @@ template <int WT, class Op>
 __global__ void __launch_bounds__(WTPB, Op::MIN_BLOCKS) warp_kernel(const TileSched sc, const Op op, const TileScratch ws) {
   using V = typename Op::V;
   constexpr int NA = Op::NA, NP = Op::NP;
-  __shared__ int32_t s_col[WPB][t_cap<Op::ITEMS>()];
+  constexpr bool TMA = Op::TMA && FJ_TMA_PREFETCH != 0;
+  // with the TMA ring, a tile that was not prefetched stages its cols / row values in its own idle
+  // slot, so the block needs no separate staging arrays (r02: C3 k = 3 engine 32.2 -> 23.0 KB of
+  // shared memory per block).  Shared memory per block is a measured lever here: 6.6 KB MORE (any
+  // use: a pad, a shared-memory carry, the deferred finish) made the C3 product 13 % slower at the
+  // same occupancy and instruction count (more short-scoreboard stalls; profiles/r02_ab_smem.log)
+  constexpr bool SLOT = TMA && FJ_SLOT_STAGE != 0;
+  __shared__ int32_t s_col[WPB][SLOT ? 1 : t_cap<Op::ITEMS>()];
   __shared__ int32_t s_e[WPB][Op::TILE_ROWS];
-  __shared__ V s_xi[WPB][Op::TILE_ROWS];
+  __shared__ V s_xi[WPB][SLOT ? 1 : Op::TILE_ROWS];
   __shared__ double s_acc[WPB][defer_finish<Op>() ? Op::TILE_ROWS * NA : 1];
   __shared__ double s_red[(NP > NA ? NP : NA) * WPB];
   __shared__ bool s_last;
-  constexpr bool TMA = Op::TMA && FJ_TMA_PREFETCH != 0;
   __shared__ __align__(128) unsigned char s_pf[WPB][TMA ? 2 : 1][TMA ? PfSlot<Op>::BYTES : 16];
   __shared__ uint64_t s_bar[WPB][2];
 
@@ -604,8 +613,14 @@ __global__ void __launch_bounds__(WTPB, Op::MIN_BLOCKS) warp_kernel(const TileSc
           pend &= ~(1u << slot);
           pre = pf_view<Op>(cur, L, s_pf[wib][slot]);
         }
-        if (pre.col) t_tile<WT, Op, true>(sc, op, cur, lane, s_e[wib], s_col[wib], s_xi[wib], s_acc[wib], part, pre);
-        else t_tile<WT, Op, false>(sc, op, cur, lane, s_e[wib], s_col[wib], s_xi[wib], s_acc[wib], part, pre);
+        int32_t* own_col = s_col[wib];
+        V* own_xi = s_xi[wib];
+        if constexpr (SLOT) {   // this tile's slot: in use by its own TMA copy, or idle
+          own_col = reinterpret_cast<int32_t*>(s_pf[wib][slot]);
+          own_xi = reinterpret_cast<V*>(s_pf[wib][slot] + PfSlot<Op>::COL_BYTES + PfSlot<Op>::RP_BYTES);
+        }
+        if (pre.col) t_tile<WT, Op, true>(sc, op, cur, lane, s_e[wib], own_col, own_xi, s_acc[wib], part, pre);
+        else t_tile<WT, Op, false>(sc, op, cur, lane, s_e[wib], own_col, own_xi, s_acc[wib], part, pre);
       } else {
         wc_item<WT, Op>(sc, op, ws, cur, it, lane, part);
       }
