@@ -41,11 +41,17 @@ def spmv_bytes(n, nnz, wb, k):
     return (4 + wb) * nnz + 8 * (n + 1) + 16 * n * k
 
 
-def spmv_kernel_name(k):
+def spmv_kernel_name(k, path="engine"):
     if k == 1:
         return "warp_kernel<ApplyOp> ((I+L)p SpMV, warp-item engine, k = 1)"
+    kp = 2 if k <= 2 else 4
+    if k <= 4 and path == "rows_slabs":
+        return (f"k_rows_chunks + k_rows<PASS 0> + k_rows<PASS 1> ((I+L)P, lean row kernel over two column "
+                f"slabs, k = {k} padded to {kp}; one product = these launches, DESIGN.md 6.10)")
+    if k <= 4 and path == "rows":
+        return f"k_rows_chunks + k_rows<PASS 2> ((I+L)P, lean row kernel, one pass, k = {k} padded to {kp})"
     if k <= 4:
-        return f"warp_kernel<ApplyOpV<KP={2 if k <= 2 else 4}>> ((I+L)P SpMM, warp-item engine, k = {k} padded)"
+        return f"warp_kernel<ApplyOpV<KP={kp}>> ((I+L)P SpMM, warp-item engine, k = {k} padded)"
     return f"spmm_kernel<BM_APPLY> ((I+L)P SpMM, warp per row, k = {k})"
 
 
@@ -318,12 +324,13 @@ def main():
 
     # dominant kernel: the PCG's (I+L)p product exactly as the solve loop launches it (k columns,
     # solver buffers), timed live inside the library with CUDA events on the launching stream
-    spmv_ms = None
+    spmv_ms, prod_path = None, "engine"
     if not dist_mode:
         G = fj.Graph.from_edges(n, u, v, w, order=order)
         G.approxim(S, opts=opts)          # fills the solver buffers with a real search direction
         flush.fill_(1)
         spmv_ms = G.time_spmv(k=kb, reps=args.spmv_reps)
+        prod_path = G.product_path(kb)
         G.close()
 
     # aggregate over ranks: time = max over ranks, bytes = sum over ranks
@@ -401,7 +408,7 @@ def main():
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": None if dist_mode else traffic, "traffic_key": traffic_key,
                      "kernel": ("whole distributed PCG iteration per rank (B(k)/N per iteration time)" if dist_mode
-                                else spmv_kernel_name(kb)),
+                                else spmv_kernel_name(kb, prod_path)),
                      "algorithmic_bytes_per_launch": Bs, "launch_ms": spmv_ms, "peak_source": peak_src},
         "gather_roofline": gather_roof,
         "per_distribution_k1": per_dist, "build": FB.source_hash(),

@@ -108,6 +108,7 @@ def load_library(path: str = SO):
     L.fj_graph_destroy.argtypes = [_vp]
     L.fj_apply.argtypes = [_vp, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp]
     L.fj_time_spmv.argtypes = [_vp, ctypes.c_int, ctypes.c_int, P(ctypes.c_float), _vp]
+    L.fj_product_path.argtypes = [_vp, ctypes.c_int, P(ctypes.c_int), _vp]
     L.fj_probe_gather.argtypes = [_i64, _i64, ctypes.c_int, ctypes.c_int, P(ctypes.c_double), _vp]
     L.fj_alg1_delta.argtypes = [_i64, _dbl, _dbl, _dbl, _dbl, _dbl, P(_dbl), P(_dbl), P(_dbl),
                                 P(ctypes.c_int), P(ctypes.c_int)]
@@ -138,7 +139,7 @@ def load_library(path: str = SO):
     L.fj_graph_create_dist.argtypes = [_vp, ctypes.c_int, _i64, _vp, _i64, _vp, _vp, _vp, ctypes.c_int, _i64, _vp,
                                        _vp, _vp, _vp, P(_vp)]
     for name in ["fj_csr_from_edges", "fj_graph_create", "fj_graph_info", "fj_graph_degrees", "fj_graph_destroy",
-                 "fj_apply", "fj_time_spmv", "fj_probe_gather",
+                 "fj_apply", "fj_time_spmv", "fj_product_path", "fj_probe_gather",
                  "fj_alg1_delta", "fj_approxim_alg1", "fj_forest_columns", "fj_opinions_generate",
                  "fj_connected_components", "fj_lcc", "fj_exact_dense", "fj_opinion_stats", "fj_solve", "fj_quantities", "fj_approxim", "fj_approxim_host",
                  "fj_comm_unique_id", "fj_comm_init", "fj_comm_init_loopback", "fj_comm_destroy",
@@ -458,6 +459,12 @@ class Graph:
         ms = ctypes.c_float()
         _check(lib().fj_time_spmv(self.handle, int(k), int(reps), ctypes.byref(ms), _stream(stream)))
         return float(ms.value)
+
+    def product_path(self, k: int = 1, stream=None) -> str:
+        """Kernel path of the k-column PCG product (fj_product_path): engine / rows / rows_slabs / batch."""
+        v = ctypes.c_int()
+        _check(lib().fj_product_path(self.handle, int(k), ctypes.byref(v), _stream(stream)))
+        return ["engine", "rows", "rows_slabs", "batch"][v.value]
 
     def opinion_stats(self, s, stream=None):
         import numpy as np

@@ -403,6 +403,19 @@ fj_status fj_time_spmv(const fj_graph* gc, int k, int reps, float* ms_host, void
   return FJ_OK;
 }
 
+fj_status fj_product_path(const fj_graph* gc, int k, int* path, void* stream) {
+  if (!gc || !path) return fail(FJ_E_INVALID_ARG, "null argument");
+  if (k < 1 || k > MAXK) return fail(FJ_E_INVALID_ARG, "k must be in [1, 64]");
+  fj_graph* g = const_cast<fj_graph*>(gc);
+  if (is_dist(g)) return fail(FJ_E_UNSUPPORTED, "fj_product_path on a distributed graph");
+  if (k < batch_min_k()) { *path = FJ_PATH_ENGINE; return FJ_OK; }
+  if (!vec_supported(k)) { *path = FJ_PATH_BATCH; return FJ_OK; }
+  int mode = 0;
+  FJ_TRY(vec_product_mode(g, k, S(stream), &mode));
+  *path = mode == 0 ? FJ_PATH_ENGINE : (mode == 2 ? FJ_PATH_ROWS_SLABS : FJ_PATH_ROWS);
+  return FJ_OK;
+}
+
 fj_status fj_solve(const fj_graph* gc, int k, const double* s, double* z, const fj_solve_opts* opts,
                    fj_solve_report* rep, void* stream) {
   FJ_RANGE("fj_solve");

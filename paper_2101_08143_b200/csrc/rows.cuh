@@ -1,0 +1,312 @@
+// rows.cuh — the small-k PCG product q = (I+L)p (rows a4/a9, KP = 2 or 4 padded gathered rows) as a
+// lean row kernel over COLUMN SLABS.  DESIGN.md §6.10.
+//
+// Why (measured, profiles/r02_slab2_probe_*.jsonl): on C3 (BA 4e6, k = 3) the gathered block p is
+// [n][4] fp64 = 128 MB, above the ~80 MB the L2 holds for random 32-byte gathers, so the merge-path
+// engine (tiles.cuh) runs at the DRAM-miss bound of that footprint (0.61 ms, 3.06 GB DRAM per
+// launch for 0.48 GB algorithmic).  Splitting each row's entries at the column n/2 into two slabs
+// and running one pass per slab keeps every pass's gathered half of p (64 MB) L2-resident; with a
+// lean row kernel (G lanes per row, U gathers in flight per lane, no shared-memory staging, no
+// merge-path search or carry scan) the two passes cost less than the one engine pass.
+//
+// Layout: the canonical CSR has ascending columns in every row, so a row's slab-A entries are a
+// PREFIX of the row: per row one int32 offset (off[i] = #cols < n/2) is the whole slab split, no
+// second copy of col.  Rows longer than ROWS_LONG nonzeros (hubs) are cut into ROWS_CH-nonzero
+// chunks, each summed by one warp into chunk_acc (one launch before the row passes); the finishing
+// pass adds a long row's chunk sums in chunk order.  Every partial is formed and combined in a fixed
+// order (lane-strided sums, xor-shuffle tree, chunks in order, pass A + pass B, blocks in order):
+// results are bitwise reproducible run to run.
+//
+// Per launch sequence (single GPU, inside the PCG graph):
+//   k_rows_chunks   (if the graph has long rows)   chunk_acc[c] = sum over the chunk of w p_j
+//   k_rows<PASS 0>  slab A of every short row       q_i = sum_{j < n/2} w_ij p_j        (partial)
+//   k_rows<PASS 1>  slab B + finish                 q_i = (1+d_i) p_i - (q_i + sum_{j >= n/2})
+//   (or k_rows<PASS 2>: one pass over whole rows when the block fits the L2 or columns are unsorted)
+// The finishing pass also forms p_c^T q_c (deterministic two-stage reduction) and alpha_c on device,
+// exactly as ApplyOpV::finalize (spmv_vec.cu).
+#pragma once
+#include "vec.cuh"
+
+namespace fj {
+
+constexpr int ROWS_LONG = 256;   // rows with more nonzeros are summed by chunk warps
+constexpr int ROWS_CH = 1024;    // nonzeros per long-row chunk
+constexpr int RTB = 256;         // threads per block of the row kernels
+#ifndef FJ_ROWS_G
+#define FJ_ROWS_G 2              // lanes per row (measured on C3: 2 > 1, 4 > 8 > 16, 32)
+#endif
+#ifndef FJ_ROWS_U
+#define FJ_ROWS_U 4              // independent gathers in flight per lane
+#endif
+#ifndef FJ_ROWS_MINB
+#define FJ_ROWS_MINB 8           // slab-A pass: 8 x 256 threads per SM (32 registers, no spill)
+#endif
+#ifndef FJ_ROWS_MINB_FIN
+#define FJ_ROWS_MINB_FIN 6       // finishing passes (p^T q partials, the epilogue): 40 registers
+#endif
+
+// Gathered row of p through the non-coherent path (p is read-only during a product).  Plain (not
+// volatile) asm so the U loads of a batch are issued back to back.
+template <int KP> __device__ __forceinline__ DVec<KP> ldg_vec(const double* p);
+template <> __device__ __forceinline__ DVec<2> ldg_vec<2>(const double* p) {
+  DVec<2> r;
+  asm("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(r.v[0]), "=d"(r.v[1]) : "l"(p));
+  return r;
+}
+template <> __device__ __forceinline__ DVec<4> ldg_vec<4>(const double* p) {
+  DVec<4> r;
+  asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(r.v[0]), "=d"(r.v[1]), "=d"(r.v[2]), "=d"(r.v[3])
+      : "l"(p));
+  return r;
+}
+
+// L2 eviction hints (FJ_ROWS_HINT bits, A/B): 1 = the streams (col, row_ptr, off) evict-first,
+// 2 = the gathers of p evict-last, 4 = the own-row read of p in the finishing pass evict-first.
+#ifndef FJ_ROWS_HINT
+#define FJ_ROWS_HINT 0
+#endif
+__device__ __forceinline__ uint64_t pol_first() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t pol_last() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ int32_t ldh_i32(const int32_t* a, uint64_t pol) {
+  int32_t r;
+  asm("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(r) : "l"(a), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ int64_t ldh_i64(const int64_t* a, uint64_t pol) {
+  int64_t r;
+  asm("ld.global.nc.L2::cache_hint.b64 %0, [%1], %2;" : "=l"(r) : "l"(a), "l"(pol));
+  return r;
+}
+template <int KP> __device__ __forceinline__ DVec<KP> ldgh_vec(const double* p, uint64_t pol);
+template <> __device__ __forceinline__ DVec<2> ldgh_vec<2>(const double* p, uint64_t pol) {
+  DVec<2> r;
+  asm("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(r.v[0]), "=d"(r.v[1]) : "l"(p), "l"(pol));
+  return r;
+}
+template <> __device__ __forceinline__ DVec<4> ldgh_vec<4>(const double* p, uint64_t pol) {
+  DVec<4> r;
+  asm("ld.global.nc.L2::cache_hint.v4.f64 {%0, %1, %2, %3}, [%4], %5;"
+      : "=d"(r.v[0]), "=d"(r.v[1]), "=d"(r.v[2]), "=d"(r.v[3]) : "l"(p), "l"(pol));
+  return r;
+}
+template <int KP> __device__ __forceinline__ DVec<KP> ld_gather(const double* p, uint64_t pol) {
+  if constexpr ((FJ_ROWS_HINT & 2) != 0) return ldgh_vec<KP>(p, pol); else return ldg_vec<KP>(p);
+}
+__device__ __forceinline__ int32_t ld_colh(const int32_t* a, uint64_t pol) {
+  if constexpr ((FJ_ROWS_HINT & 1) != 0) return ldh_i32(a, pol); else return __ldg(a);
+}
+__device__ __forceinline__ int64_t ld_i64h(const int64_t* a, uint64_t pol) {
+  if constexpr ((FJ_ROWS_HINT & 1) != 0) return ldh_i64(a, pol); else return *a;
+}
+
+struct RowsArgs {
+  int64_t n;
+  const int64_t* __restrict__ rp;
+  const int32_t* __restrict__ col;
+  const void* __restrict__ w;
+  const int32_t* __restrict__ off;      // [n] slab-A entries per row (2-slab mode)
+  const int32_t* __restrict__ c0;       // [n] first chunk of a long row
+  const int64_t* __restrict__ tab;      // [n_chunks][2] (row, first nonzero)
+  int64_t n_chunks;
+  double* chunk_acc;                    // [n_chunks][4]
+  const double* __restrict__ x;         // gathered block, padded [n][KP]
+  double* y;                            // [n][KQ]
+  const double* __restrict__ deg;
+  int opL, k;
+  VecScalars* sc;                       // PCG mode: alpha_c on device (null: plain apply)
+  double* part;                         // [grid][4] block partials of p^T q
+  unsigned int* ticket;                 // [1], self-resetting
+};
+
+template <int WT, int KP, int KQ, int U>
+__device__ __forceinline__ void rows_accumulate(const RowsArgs& a, int64_t k, int64_t ke, int stride,
+                                                double (&acc)[KQ], uint64_t ps = 0, uint64_t pg = 0) {
+  using WS = typename std::conditional<WT == FJ_W_F64, double, float>::type;   // exact for u8 / f32
+  for (; k + (int64_t)(U - 1) * stride < ke; k += (int64_t)U * stride) {   // full batches
+    int32_t j[U];
+    WS wv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      j[u] = ld_colh(a.col + k + u * stride, ps);
+      wv[u] = (WT == FJ_W_UNIT) ? (WS)1 : (WS)WeightT<WT>::get(a.w, k + u * stride);
+    }
+    DVec<KP> v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = ld_gather<KP>(a.x + (int64_t)j[u] * KP, pg);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int c = 0; c < KQ; ++c) acc[c] = (WT == FJ_W_UNIT) ? acc[c] + v[u].v[c] : fma((double)wv[u], v[u].v[c], acc[c]);
+  }
+  for (; k < ke; k += stride) {
+    const DVec<KP> v = ld_gather<KP>(a.x + (int64_t)ld_colh(a.col + k, ps) * KP, pg);
+    const double wk = (WT == FJ_W_UNIT) ? 1.0 : (double)WeightT<WT>::get(a.w, k);
+#pragma unroll
+    for (int c = 0; c < KQ; ++c) acc[c] = (WT == FJ_W_UNIT) ? acc[c] + v.v[c] : fma(wk, v.v[c], acc[c]);
+  }
+}
+
+// Long-row chunks: one warp per chunk (grid-stride), chunk_acc[c] = sum w p_j over the chunk.
+template <int WT, int KP, int KQ>
+__global__ void __launch_bounds__(RTB) k_rows_chunks(const RowsArgs a) {
+  if (a.sc && *(volatile int32_t*)&a.sc->done) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (RTB / 32);
+  const uint64_t ps = (FJ_ROWS_HINT & 1) ? pol_first() : 0, pg = (FJ_ROWS_HINT & 2) ? pol_last() : 0;
+  for (int64_t c = (blockIdx.x * (int64_t)RTB + threadIdx.x) >> 5; c < a.n_chunks; c += nw) {
+    const int64_t r = a.tab[2 * c], k0 = a.tab[2 * c + 1];
+    const int64_t k1 = min(k0 + (int64_t)ROWS_CH, a.rp[r + 1]);
+    FJ_DCHECK(r >= 0 && r < a.n && k0 >= a.rp[r] && k0 < k1);
+    double acc[KQ];
+#pragma unroll
+    for (int f = 0; f < KQ; ++f) acc[f] = 0.0;
+    rows_accumulate<WT, KP, KQ, 4>(a, k0 + lane, k1, 32, acc, ps, pg);
+#pragma unroll
+    for (int f = 0; f < KQ; ++f) acc[f] = warp_sum(acc[f]);
+    if (lane == 0) {
+#pragma unroll
+      for (int f = 0; f < KQ; ++f) a.chunk_acc[c * 4 + f] = acc[f];
+    }
+  }
+}
+
+// PASS 0: slab A partial sums; PASS 1: slab B + finish; PASS 2: whole rows + finish.
+template <int WT, int KP, int KQ, int PASS>
+__global__ void __launch_bounds__(RTB, PASS == 0 ? FJ_ROWS_MINB : FJ_ROWS_MINB_FIN) k_rows(const RowsArgs a) {
+  constexpr int G = FJ_ROWS_G, U = FJ_ROWS_U;
+  constexpr bool FIN = PASS != 0;
+  __shared__ double s_red[4 * RTB / 32];
+  if (a.sc && *(volatile int32_t*)&a.sc->done) return;
+  const int64_t ng = (int64_t)gridDim.x * (RTB / G);
+  const int sub = threadIdx.x % G;
+  const uint64_t ps = (FJ_ROWS_HINT & 5) ? pol_first() : 0, pg = (FJ_ROWS_HINT & 2) ? pol_last() : 0;
+  double part[KQ];
+#pragma unroll
+  for (int f = 0; f < KQ; ++f) part[f] = 0.0;
+  // the loop runs on the warp's first row (warp-uniform trip count: the group shuffles below use
+  // the full mask); groups past the last row take an empty range
+  for (int64_t i0 = (blockIdx.x * (int64_t)RTB + (threadIdx.x & ~31)) / G; i0 < a.n; i0 += ng) {
+    const int64_t i = i0 + (threadIdx.x & 31) / G;
+    const bool valid = i < a.n;
+    const int64_t b = valid ? ld_i64h(a.rp + i, ps) : 0, e = valid ? ld_i64h(a.rp + i + 1, ps) : 0;
+    const bool lng = e - b > ROWS_LONG;
+    int64_t kb = b, ke = e;
+    if (PASS == 0 && valid) ke = b + ld_colh(a.off + i, ps);
+    if (PASS == 1 && valid) kb = b + ld_colh(a.off + i, ps);
+    FJ_DCHECK(kb >= b && ke <= e && kb <= ke);
+    double acc[KQ];
+#pragma unroll
+    for (int f = 0; f < KQ; ++f) acc[f] = 0.0;
+    if (!lng) rows_accumulate<WT, KP, KQ, U>(a, kb + sub, ke, G, acc, ps, pg);
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1)
+#pragma unroll
+      for (int f = 0; f < KQ; ++f) acc[f] += __shfl_xor_sync(0xffffffffu, acc[f], o, G);
+    if (sub != 0 || !valid) continue;
+    DVec<KP> yv;
+#pragma unroll
+    for (int c = 0; c < KP; ++c) yv.v[c] = c < KQ ? acc[c < KQ ? c : 0] : 0.0;
+    if (PASS == 0) { st_q<KP, KQ>(a.y, i, yv); continue; }
+    double tot[KQ];
+    if (lng) {   // chunk sums in chunk order
+#pragma unroll
+      for (int f = 0; f < KQ; ++f) tot[f] = 0.0;
+      const int64_t c0 = a.c0[i], nch = (e - b + ROWS_CH - 1) / ROWS_CH;
+      for (int64_t c = c0; c < c0 + nch; ++c)
+#pragma unroll
+        for (int f = 0; f < KQ; ++f) tot[f] += __ldcg(a.chunk_acc + c * 4 + f);
+    } else if (PASS == 1) {
+      const DVec<KP> ya = ld_q<KP, KQ>(a.y, i);
+#pragma unroll
+      for (int f = 0; f < KQ; ++f) tot[f] = ya.v[f] + acc[f];
+    } else {
+#pragma unroll
+      for (int f = 0; f < KQ; ++f) tot[f] = acc[f];
+    }
+    const double d = (WT == FJ_W_UNIT) ? (double)(e - b) : a.deg[i];
+    const double dd = a.opL ? d : 1.0 + d;
+    // own row of p: in the finishing pass of two slabs, rows of slab A are not being gathered
+    const DVec<KP> xi = ((FJ_ROWS_HINT & 4) && PASS == 1 && i < a.n / 2) ? ldgh_vec<KP>(a.x + i * KP, ps)
+                                                                       : ldg_vec<KP>(a.x + i * KP);
+#pragma unroll
+    for (int c = 0; c < KQ; ++c) {
+      yv.v[c] = fma(dd, xi.v[c], -tot[c]);
+      part[c] = fma(xi.v[c], yv.v[c], part[c]);
+    }
+    st_q<KP, KQ>(a.y, i, yv);
+  }
+  if constexpr (FIN) {
+    block_sum<KQ, RTB>(part, s_red);
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int f = 0; f < KQ; ++f) a.part[(int64_t)blockIdx.x * 4 + f] = part[f];
+    }
+    if (!last_block_ticket(a.ticket, gridDim.x)) return;
+    double t[KQ];
+#pragma unroll
+    for (int f = 0; f < KQ; ++f) t[f] = 0.0;
+    for (int bb = threadIdx.x; bb < (int)gridDim.x; bb += RTB)
+#pragma unroll
+      for (int f = 0; f < KQ; ++f) t[f] += __ldcg(a.part + (int64_t)bb * 4 + f);
+    block_sum<KQ, RTB>(t, s_red);
+    if (threadIdx.x != 0) return;
+    *a.ticket = 0u;
+    VecScalars* sc = a.sc;
+    if (!sc) return;
+#pragma unroll
+    for (int c = 0; c < KQ; ++c) {   // alpha_c = rho_c / p_c^T q_c (as ApplyOpV::finalize)
+      if (c >= a.k) break;
+      sc->pq[c] = t[c];
+      if (sc->active[c]) {
+        if (!(t[c] > 0.0) || !isfinite(t[c])) {
+          sc->alpha[c] = 0.0;
+          sc->active[c] = 0;
+          sc->breakdown[c] = 1;
+        } else {
+          sc->alpha[c] = sc->rho[c] / t[c];
+        }
+      } else {
+        sc->alpha[c] = 0.0;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- plan (built once per graph)
+// nch[i] = chunks of a long row; off[i] = entries with column < split; *bad |= 1 if some row's
+// slab-A entries are not a prefix of the row (columns not ascending: the 2-slab split is off).
+__global__ void k_rows_plan1(int64_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                             int64_t split, int32_t* __restrict__ nch, int32_t* __restrict__ off, int* bad) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = rp[i], e = rp[i + 1];
+    nch[i] = e - b > ROWS_LONG ? (int32_t)((e - b + ROWS_CH - 1) / ROWS_CH) : 0;
+    if (!off) continue;
+    int32_t lo = 0;
+    bool hi_seen = false, viol = false;
+    for (int64_t k = b; k < e; ++k) {
+      if (col[k] < split) { ++lo; viol |= hi_seen; } else { hi_seen = true; }
+    }
+    off[i] = lo;
+    if (viol) atomicOr(bad, 1);
+  }
+}
+__global__ void k_rows_plan2(int64_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ nch,
+                             const int32_t* __restrict__ c0, int64_t* __restrict__ tab) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t m = nch[i];
+    for (int32_t c = 0; c < m; ++c) {
+      tab[2 * ((int64_t)c0[i] + c)] = i;
+      tab[2 * ((int64_t)c0[i] + c) + 1] = rp[i] + (int64_t)c * ROWS_CH;
+    }
+  }
+}
+
+}  // namespace fj

@@ -99,6 +99,7 @@ fj_status apply_vec(fj_graph* g, int k, const double* x, double* y, int opL, cud
 fj_status quant_vec(fj_graph* g, int k, const double* s, const double* z, const double* mean_host,
                     double* host_out, bool z_from_solve, cudaStream_t st);
 fj_status time_vec_spmv(fj_graph* g, int k, int reps, float* ms_out, cudaStream_t st);
+fj_status vec_product_mode(fj_graph* g, int k, cudaStream_t st, int* mode);   // RowsPlan::mode
 // onchip.cu: the whole solve + quantities pass of column c in one thread block when the graph fits
 // in shared memory (*used = false otherwise)
 fj_status onchip_col(fj_graph* g, const double* s, double* z, int64_t ld, int64_t c, double mean,

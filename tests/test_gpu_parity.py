@@ -221,8 +221,10 @@ def test_c1_vs_dense_oracle(fj):
 def test_full_config_vs_pcg_oracle(fj, name):
     wl = synth.make_config(name)
     g = O.canonical_csr(wl.n, wl.u, wl.v)
-    _, Z, Q, rep = solve_quant(fj, wl.n, wl.u, wl.v, None, wl.S)
+    G, Z, Q, rep = solve_quant(fj, wl.n, wl.u, wl.v, None, wl.S)
     assert rep["converged"] == 1 and rep["rel_res_true"] <= 1e-10
+    if wl.k == 3:   # c3: the bench's product path (two column slabs)
+        assert G.product_path(3) == "rows_slabs"
     for c in range(wl.k):
         zo, info = O.solve_pcg(g, wl.S[:, c], tol=1e-13)
         assert info["converged"]
