@@ -12,16 +12,17 @@
 // Layout: the canonical CSR has ascending columns in every row, so a row's slab-A entries are a
 // PREFIX of the row: per row one int32 offset (off[i] = #cols < n/2) is the whole slab split, no
 // second copy of col.  Rows longer than ROWS_LONG nonzeros (hubs) are cut into ROWS_CH-nonzero
-// chunks, each summed by one warp into chunk_acc (one launch before the row passes); the finishing
+// chunks, each summed by one warp into chunk_acc (in the first pass); the finishing
 // pass adds a long row's chunk sums in chunk order.  Every partial is formed and combined in a fixed
 // order (lane-strided sums, xor-shuffle tree, chunks in order, pass A + pass B, blocks in order):
 // results are bitwise reproducible run to run.
 //
 // Per launch sequence (single GPU, inside the PCG graph):
-//   k_rows_chunks   (if the graph has long rows)   chunk_acc[c] = sum over the chunk of w p_j
-//   k_rows<PASS 0>  slab A of every short row       q_i = sum_{j < n/2} w_ij p_j        (partial)
+//   k_rows<PASS 0>  long-row chunk warps: chunk_acc[c] = sum over the chunk of w p_j; then slab A of
+//                   every short row: q_i = sum_{j < n/2} w_ij p_j                  (partial)
 //   k_rows<PASS 1>  slab B + finish                 q_i = (1+d_i) p_i - (q_i + sum_{j >= n/2})
-//   (or k_rows<PASS 2>: one pass over whole rows when the block fits the L2 or columns are unsorted)
+//   (or k_rows_chunks + k_rows<PASS 2>: one pass over whole rows when the block fits the L2 or
+//   some row's columns do not ascend)
 // The finishing pass also forms p_c^T q_c (deterministic two-stage reduction) and alpha_c on device,
 // exactly as ApplyOpV::finalize (spmv_vec.cu).
 #pragma once
@@ -29,8 +30,14 @@
 
 namespace fj {
 
-constexpr int ROWS_LONG = 256;   // rows with more nonzeros are summed by chunk warps
-constexpr int ROWS_CH = 1024;    // nonzeros per long-row chunk
+#ifndef FJ_ROWS_LONG
+#define FJ_ROWS_LONG 128        // measured C3: 128 0.478 ms, 64 0.496, 256 0.487, 512 0.504
+#endif
+#ifndef FJ_ROWS_CH
+#define FJ_ROWS_CH 256          // measured C3: 256 0.481 ms vs 1024 0.487
+#endif
+constexpr int ROWS_LONG = FJ_ROWS_LONG;   // rows with more nonzeros are summed by chunk warps
+constexpr int ROWS_CH = FJ_ROWS_CH;       // nonzeros per long-row chunk
 constexpr int RTB = 256;         // threads per block of the row kernels
 #ifndef FJ_ROWS_G
 #define FJ_ROWS_G 2              // lanes per row (measured on C3: 2 > 1, 4 > 8 > 16, 32)
@@ -154,13 +161,12 @@ __device__ __forceinline__ void rows_accumulate(const RowsArgs& a, int64_t k, in
   }
 }
 
-// Long-row chunks: one warp per chunk (grid-stride), chunk_acc[c] = sum w p_j over the chunk.
+// Long-row chunks: one warp per chunk (grid-stride over the launch's warps), chunk_acc[c] = sum
+// w p_j over the chunk.
 template <int WT, int KP, int KQ>
-__global__ void __launch_bounds__(RTB) k_rows_chunks(const RowsArgs a) {
-  if (a.sc && *(volatile int32_t*)&a.sc->done) return;
+__device__ __forceinline__ void rows_chunk_items(const RowsArgs& a, uint64_t ps, uint64_t pg) {
   const int lane = threadIdx.x & 31;
   const int64_t nw = (int64_t)gridDim.x * (RTB / 32);
-  const uint64_t ps = (FJ_ROWS_HINT & 1) ? pol_first() : 0, pg = (FJ_ROWS_HINT & 2) ? pol_last() : 0;
   for (int64_t c = (blockIdx.x * (int64_t)RTB + threadIdx.x) >> 5; c < a.n_chunks; c += nw) {
     const int64_t r = a.tab[2 * c], k0 = a.tab[2 * c + 1];
     const int64_t k1 = min(k0 + (int64_t)ROWS_CH, a.rp[r + 1]);
@@ -177,8 +183,20 @@ __global__ void __launch_bounds__(RTB) k_rows_chunks(const RowsArgs a) {
     }
   }
 }
+// One-pass mode: the chunks in their own launch before k_rows<PASS 2> (which reads them).
+template <int WT, int KP, int KQ>
+__global__ void __launch_bounds__(RTB) k_rows_chunks(const RowsArgs a) {
+  if (a.sc && *(volatile int32_t*)&a.sc->done) return;
+  const uint64_t ps = (FJ_ROWS_HINT & 1) ? pol_first() : 0, pg = (FJ_ROWS_HINT & 2) ? pol_last() : 0;
+  rows_chunk_items<WT, KP, KQ>(a, ps, pg);
+}
 
-// PASS 0: slab A partial sums; PASS 1: slab B + finish; PASS 2: whole rows + finish.
+// PASS 0: the long-row chunks (fused: the chunk warps run beside the row groups of other warps;
+// FJ_ROWS_FUSE_CHUNKS=0 launches them apart) then slab A partial sums; PASS 1: slab B + finish;
+// PASS 2: whole rows + finish.
+#ifndef FJ_ROWS_FUSE_CHUNKS
+#define FJ_ROWS_FUSE_CHUNKS 1
+#endif
 template <int WT, int KP, int KQ, int PASS>
 __global__ void __launch_bounds__(RTB, PASS == 0 ? FJ_ROWS_MINB : FJ_ROWS_MINB_FIN) k_rows(const RowsArgs a) {
   constexpr int G = FJ_ROWS_G, U = FJ_ROWS_U;
@@ -188,6 +206,7 @@ __global__ void __launch_bounds__(RTB, PASS == 0 ? FJ_ROWS_MINB : FJ_ROWS_MINB_F
   const int64_t ng = (int64_t)gridDim.x * (RTB / G);
   const int sub = threadIdx.x % G;
   const uint64_t ps = (FJ_ROWS_HINT & 5) ? pol_first() : 0, pg = (FJ_ROWS_HINT & 2) ? pol_last() : 0;
+  if constexpr (PASS == 0 && FJ_ROWS_FUSE_CHUNKS) rows_chunk_items<WT, KP, KQ>(a, ps, pg);
   double part[KQ];
 #pragma unroll
   for (int f = 0; f < KQ; ++f) part[f] = 0.0;
@@ -289,6 +308,7 @@ __global__ void k_rows_plan1(int64_t n, const int64_t* __restrict__ rp, const in
     const int64_t b = rp[i], e = rp[i + 1];
     nch[i] = e - b > ROWS_LONG ? (int32_t)((e - b + ROWS_CH - 1) / ROWS_CH) : 0;
     if (!off) continue;
+    if (e - b > ROWS_LONG) { off[i] = 0; continue; }   // long rows are summed whole by chunk warps
     int32_t lo = 0;
     bool hi_seen = false, viol = false;
     for (int64_t k = b; k < e; ++k) {

@@ -496,7 +496,9 @@ static VecWs* vec_cache(fj_graph* g) { return reinterpret_cast<VecWs*>(g->vec_ws
 
 // kernel launches of one PCG iteration (product + k_v_update + k_v_dir), for fj_kernel_launches
 static int vec_iter_launches(const VecWs* w) {
-  const int prod = w->rows.mode == 0 ? 1 : (w->rows.mode == 2 ? 2 : 1) + (w->rows.n_chunks > 0 ? 1 : 0);
+  const RowsPlan& R = w->rows;
+  const int prod = R.mode == 0 ? 1
+                              : (R.mode == 2 ? 2 : 1) + (R.n_chunks > 0 && (R.mode == 1 || !FJ_ROWS_FUSE_CHUNKS) ? 1 : 0);
   return prod + 2;
 }
 
@@ -687,7 +689,7 @@ static fj_status vec_apply_padded(const fj_graph* g, const VecWs* w, const doubl
       if (R.mode != 0) {   // column-slab row product (rows.cuh)
         RowsArgs a{g->n, g->row_ptr, g->col, g->w, R.off, R.c0, R.tab, R.n_chunks, R.chunk_acc,
                    x, y, g->deg, opL, w->k, sc, R.part, R.ticket};
-        if (R.n_chunks > 0) {
+        if (R.n_chunks > 0 && (R.mode == 1 || !FJ_ROWS_FUSE_CHUNKS)) {
           k_rows_chunks<WT, KP, KQ><<<R.grid_chunks, RTB, 0, st>>>(a);
           FJ_CK_LAUNCH();
         }
