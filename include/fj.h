@@ -216,12 +216,13 @@ fj_status fj_apply(const fj_graph* g, int op, int k, const double* x_dev, double
 fj_status fj_time_spmv(const fj_graph* g, int k, int reps, float* ms_host, void* stream);
 
 /* Diagnostic: which kernel path computes the k-column PCG product on this graph (*path, host):
- * FJ_PATH_ENGINE (0) the load-balanced merge-path warp-item engine (k = 1, tiles.cuh);
- * FJ_PATH_ROWS (1) the lean row kernel, one pass (2 <= k <= 4, rows.cuh);
- * FJ_PATH_ROWS_SLABS (2) the lean row kernel over two column slabs (2 <= k <= 4, when the padded
- * gathered block exceeds 64 MB and every row's columns ascend);
- * FJ_PATH_BATCH (3) the warp-per-row batched engine (k > 4, spmm.cu).  FJ_VEC_ROWS=0 in the
- * environment selects the engine for 2 <= k <= 4 (A/B).  May build the k-column workspace. */
+ * FJ_PATH_ENGINE (0) the load-balanced merge-path warp-item engine (tiles.cuh);
+ * FJ_PATH_ROWS (1) the lean row kernel, one pass (k <= 4, rows.cuh);
+ * FJ_PATH_ROWS_SLABS (2) the lean row kernel over two column slabs (k <= 4, when the gathered
+ * block is in (64 MB, 160 MB] and every row's columns ascend);
+ * FJ_PATH_BATCH (3) the warp-per-row batched engine (k > 4, spmm.cu).  FJ_ROWS=0/1/2 in the
+ * environment forces engine / one pass / two slabs for k <= 4 (A/B, tests).  May build the
+ * k-column workspace. */
 enum { FJ_PATH_ENGINE = 0, FJ_PATH_ROWS = 1, FJ_PATH_ROWS_SLABS = 2, FJ_PATH_BATCH = 3 };
 fj_status fj_product_path(const fj_graph* g, int k, int* path, void* stream);
 

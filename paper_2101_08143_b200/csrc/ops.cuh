@@ -173,9 +173,12 @@ struct QuantOp {
   }
 };
 
+struct RowsPlan;   // rows.cuh: the lean row product of the k = 1 PCG (built with this workspace)
+
 // Per-graph workspace shared by the solver and the quantities pass (stream-ordered use only).
 struct SolveWs {
   int64_t n = 0;
+  RowsPlan* rows = nullptr;
   int grid_max = 0, grid_elem = 0;
   double *r = nullptr, *p = nullptr, *q = nullptr, *x = nullptr, *col_s = nullptr;
   PcgScalars* sc = nullptr;

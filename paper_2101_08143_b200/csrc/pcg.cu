@@ -12,6 +12,7 @@
 #include <cstring>
 
 #include "ops.cuh"
+#include "rows.cuh"
 #include "workspace.cuh"
 
 namespace fj {
@@ -40,6 +41,7 @@ void free_solve_ws(fj_graph* g) {
   dfree(w->ts.block_part); dfree(w->ts.long_part); dfree(w->ts.chunk_acc);
   dfree(w->ts.long_ticket); dfree(w->ts.grid_ticket);
   dfree(w->qout); dfree(w->stat);
+  if (w->rows) { rows_plan_free(*w->rows); delete w->rows; }
   delete w;
   g->solve_ws = nullptr;
 }
@@ -82,6 +84,8 @@ fj_status get_ws(fj_graph* g, cudaStream_t st, SolveWs** out) {
   FJ_CK(cudaEventCreate(&w->ev1));
   FJ_CK(cudaEventCreate(&w->ev2));
   FJ_CK(cudaEventCreate(&w->ev3));
+  w->rows = new RowsPlan();
+  FJ_TRY(rows_plan_build(g, 1, *w->rows, st));
   *out = w;
   return FJ_OK;
 }
@@ -200,6 +204,8 @@ __global__ void k_copy_col(int64_t n, const double* __restrict__ src, int64_t sl
 template <int WT>
 static fj_status launch_product1(const fj_graph* g, const SolveWs* w, const double* x, double* y, int opL,
                                  PcgScalars* sc, cudaStream_t st) {
+  if (w->rows && w->rows->mode != 0)   // lean row kernel (rows.cuh)
+    return rows_product<WT, 1, 1>(g, *w->rows, x, y, opL, 1, nullptr, sc, st);
   ApplyOp<WT> op{x, y, g->deg, 1, 0, opL, sc, nullptr};
   int nl = 0;
   FJ_CK(launch_product<WT>(g, w->ts, w->grid_max, op, st, &nl));
@@ -338,7 +344,7 @@ fj_status solve_col(fj_graph* g, const double* s, double* z, int64_t ld, int64_t
     FJ_CK(cudaStreamSynchronize(st));
     if (defer) h.res2 = h.rr;   // recursive residual stands in
     total_iter += h.iter;
-    if (o.use_cuda_graph) count_launch(3 * std::max(h.iter, 1));
+    if (o.use_cuda_graph) count_launch((int64_t)(rows_launches(*w->rows) + 2) * std::max(h.iter, 1));
     float lms = 0.f;
     cudaEventElapsedTime(&lms, w->ev2, w->ev3);
     if (rep) { rep->ms_loop += lms; rep->iterations_total += h.iter; }
@@ -408,7 +414,13 @@ fj_status fj_product_path(const fj_graph* gc, int k, int* path, void* stream) {
   if (k < 1 || k > MAXK) return fail(FJ_E_INVALID_ARG, "k must be in [1, 64]");
   fj_graph* g = const_cast<fj_graph*>(gc);
   if (is_dist(g)) return fail(FJ_E_UNSUPPORTED, "fj_product_path on a distributed graph");
-  if (k < batch_min_k()) { *path = FJ_PATH_ENGINE; return FJ_OK; }
+  if (k < batch_min_k()) {
+    SolveWs* w = nullptr;
+    FJ_TRY(get_ws(g, S(stream), &w));
+    const int m = w->rows ? w->rows->mode : 0;
+    *path = m == 0 ? FJ_PATH_ENGINE : (m == 2 ? FJ_PATH_ROWS_SLABS : FJ_PATH_ROWS);
+    return FJ_OK;
+  }
   if (!vec_supported(k)) { *path = FJ_PATH_BATCH; return FJ_OK; }
   int mode = 0;
   FJ_TRY(vec_product_mode(g, k, S(stream), &mode));

@@ -1,0 +1,136 @@
+// rows.cu — the plan of the lean row product (rows.cuh), built once per graph
+// and gathered row width with the solver workspace.
+#include <algorithm>
+#include <cstdlib>
+
+#include "rows.cuh"
+#include "workspace.cuh"
+
+namespace fj {
+
+// ---------------------------------------------------------------- plan (built once per graph)
+// nch[i] = chunks of a long row; off[i] = entries with column < split; *bad |= 1 if some row's
+// slab-A entries are not a prefix of the row (columns not ascending: the 2-slab split is off).
+__global__ void k_rows_plan1(int64_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                             int64_t split, int64_t long_row, int32_t* __restrict__ nch, int32_t* __restrict__ off,
+                             int* bad) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = rp[i], e = rp[i + 1];
+    nch[i] = e - b > long_row ? (int32_t)((e - b + ROWS_CH - 1) / ROWS_CH) : 0;
+    if (!off) continue;
+    if (e - b > long_row) { off[i] = 0; continue; }   // long rows are summed whole by chunk warps
+    int32_t lo = 0;
+    bool hi_seen = false, viol = false;
+    for (int64_t k = b; k < e; ++k) {
+      if (col[k] < split) { ++lo; viol |= hi_seen; } else { hi_seen = true; }
+    }
+    off[i] = lo;
+    if (viol) atomicOr(bad, 1);
+  }
+}
+__global__ void k_rows_plan2(int64_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ nch,
+                             const int32_t* __restrict__ c0, int64_t* __restrict__ tab) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t m = nch[i];
+    for (int32_t c = 0; c < m; ++c) {
+      tab[2 * ((int64_t)c0[i] + c)] = i;
+      tab[2 * ((int64_t)c0[i] + c) + 1] = rp[i] + (int64_t)c * ROWS_CH;
+    }
+  }
+}
+
+
+// FJ_ROWS (A/B, tests): -1 auto (default), 0 merge-path engine, 1 one row pass, 2 two column
+// slabs.  Auto: two slabs when the gathered block (n x kp doubles) is in (64 MB, 160 MB] -- each half
+// then fits the ~80 MB the L2 holds for random gathers -- and every row's columns
+// ascend; else one row pass.
+static int rows_knob() {
+  static const int v = [] { const char* e = getenv("FJ_ROWS"); return e ? atoi(e) : -1; }();
+  return v;
+}
+constexpr int64_t kRowsSlabMin = 64ll << 20, kRowsSlabMax = 160ll << 20;
+
+void rows_plan_free(RowsPlan& R) {
+  dfree(R.off); dfree(R.c0); dfree(R.tab); dfree(R.chunk_acc); dfree(R.part); dfree(R.ticket);
+  R = RowsPlan{};
+}
+
+template <class T>
+static fj_status ralloc(T** p, int64_t count, cudaStream_t st) {
+  if (count < 1) count = 1;
+  FJ_CK(dmalloc(p, sizeof(T) * (size_t)count, st));
+  return FJ_OK;
+}
+
+fj_status rows_plan_build(fj_graph* g, int kp, RowsPlan& R, cudaStream_t st) {
+  rows_plan_free(R);
+  const int knob = rows_knob();
+  if (knob == 0 || g->dist) return FJ_OK;   // mode 0: the engine
+  const int64_t n = g->n;
+  const int64_t bytes_p = n * (int64_t)kp * 8;
+  bool two = knob == 2 || (knob < 0 && bytes_p > kRowsSlabMin && bytes_p <= kRowsSlabMax);
+  R.long_row = kp == 1 ? FJ_ROWS_LONG1 : FJ_ROWS_LONG;
+  const unsigned cb = (unsigned)std::min<int64_t>((n + 255) / 256, 8192);
+  DevBuf<int32_t> nch;
+  DevBuf<int> bad;
+  FJ_TRY(nch.alloc(n, st));
+  FJ_TRY(bad.alloc(1, st));
+  FJ_CK(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
+  FJ_TRY(ralloc(&R.c0, n, st));
+  if (two) FJ_TRY(ralloc(&R.off, n, st));
+  if (n > 0) {
+    k_rows_plan1<<<cb, 256, 0, st>>>(n, g->row_ptr, g->col, n / 2, R.long_row, nch.p, two ? R.off : nullptr, bad.p);
+    FJ_CK_LAUNCH();
+    size_t tb = 0;
+    FJ_CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, nch.p, R.c0, n, st));
+    DevBuf<uint8_t> tmp;
+    FJ_TRY(tmp.alloc((int64_t)tb, st));
+    FJ_CK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, nch.p, R.c0, n, st));
+    count_cub();
+  }
+  int32_t last[2] = {0, 0};
+  int hbad = 0;
+  if (n > 0) {
+    FJ_CK(cudaMemcpyAsync(&last[0], R.c0 + n - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    FJ_CK(cudaMemcpyAsync(&last[1], nch.p + n - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  }
+  FJ_CK(cudaMemcpyAsync(&hbad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  FJ_CK(cudaStreamSynchronize(st));
+  R.n_chunks = (int64_t)last[0] + last[1];
+  if (two && hbad) {   // columns not ascending in some row: slab A is not a prefix -> one pass
+    if (knob == 2) return fail(FJ_E_INVALID_ARG, "FJ_ROWS=2 needs ascending columns in every row");
+    two = false;
+    dfree(R.off);
+    R.off = nullptr;
+  }
+  FJ_TRY(ralloc(&R.tab, 2 * R.n_chunks, st));
+  FJ_TRY(ralloc(&R.chunk_acc, 4 * R.n_chunks, st));
+  if (R.n_chunks > 0) {
+    k_rows_plan2<<<cb, 256, 0, st>>>(n, g->row_ptr, nch.p, R.c0, R.tab);
+    FJ_CK_LAUNCH();
+  }
+  int occ = 0;
+  FJ_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_rows<FJ_W_UNIT, 4, 3, 2>, RTB, 0));
+  if (occ < 1) occ = 1;
+  // Grid: `waves` x the resident blocks, waves = rows / (8 x resident row groups) clamped to [1, 4]
+  // (measured, profiles/r02_ab_rows_variants.log: C3 (4e6 rows) 4 waves 0.496 ms vs 1 wave 0.514;
+  // C2 (1e6 rows) 1 wave 61.5 us vs 4 waves 71 us).  FJ_ROWS_WAVES > 0 fixes it (A/B).
+#ifndef FJ_ROWS_WAVES
+#define FJ_ROWS_WAVES 0
+#endif
+  const int64_t resident_groups = (int64_t)g->num_sms * occ * (RTB / FJ_ROWS_G);
+  const int64_t waves = FJ_ROWS_WAVES > 0 ? FJ_ROWS_WAVES
+                                          : std::max<int64_t>(1, std::min<int64_t>(4, n / (8 * resident_groups)));
+  int64_t grid = (int64_t)g->num_sms * occ * waves;
+  const int64_t need = (n * FJ_ROWS_G + RTB - 1) / RTB;
+  if (grid > need) grid = need > 0 ? need : 1;
+  R.grid = (int)grid;
+  R.grid_chunks = (int)std::max<int64_t>(1, std::min<int64_t>((R.n_chunks * 32 + RTB - 1) / RTB, (int64_t)g->num_sms * 8));
+  FJ_TRY(ralloc(&R.part, 4 * grid, st));
+  FJ_TRY(ralloc(&R.ticket, 1, st));
+  FJ_CK(cudaMemsetAsync(R.ticket, 0, sizeof(unsigned int), st));
+  R.mode = two ? 2 : 1;
+  return FJ_OK;
+}
+
+}  // namespace fj

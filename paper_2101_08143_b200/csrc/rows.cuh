@@ -26,17 +26,22 @@
 // The finishing pass also forms p_c^T q_c (deterministic two-stage reduction) and alpha_c on device,
 // exactly as ApplyOpV::finalize (spmv_vec.cu).
 #pragma once
+#include "ops.cuh"
 #include "vec.cuh"
 
 namespace fj {
 
+#ifndef FJ_ROWS_LONG1
+#define FJ_ROWS_LONG1 128       // k = 1 (one 8-byte gather per nonzero)
+#endif
 #ifndef FJ_ROWS_LONG
-#define FJ_ROWS_LONG 128        // measured C3: 128 0.478 ms, 64 0.496, 256 0.487, 512 0.504
+#define FJ_ROWS_LONG 128        // KP = 2, 4; measured C3 k = 3: 128 0.478 ms, 64 0.496, 256 0.487, 512 0.504
 #endif
 #ifndef FJ_ROWS_CH
 #define FJ_ROWS_CH 256          // measured C3: 256 0.481 ms vs 1024 0.487
 #endif
-constexpr int ROWS_LONG = FJ_ROWS_LONG;   // rows with more nonzeros are summed by chunk warps
+// rows with more nonzeros than the plan's long_row (FJ_ROWS_LONG, or FJ_ROWS_LONG1 for k = 1) are
+// summed by chunk warps
 constexpr int ROWS_CH = FJ_ROWS_CH;       // nonzeros per long-row chunk
 constexpr int RTB = 256;         // threads per block of the row kernels
 #ifndef FJ_ROWS_G
@@ -55,6 +60,11 @@ constexpr int RTB = 256;         // threads per block of the row kernels
 // Gathered row of p through the non-coherent path (p is read-only during a product).  Plain (not
 // volatile) asm so the U loads of a batch are issued back to back.
 template <int KP> __device__ __forceinline__ DVec<KP> ldg_vec(const double* p);
+template <> __device__ __forceinline__ DVec<1> ldg_vec<1>(const double* p) {
+  DVec<1> r;
+  asm("ld.global.nc.f64 %0, [%1];" : "=d"(r.v[0]) : "l"(p));
+  return r;
+}
 template <> __device__ __forceinline__ DVec<2> ldg_vec<2>(const double* p) {
   DVec<2> r;
   asm("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(r.v[0]), "=d"(r.v[1]) : "l"(p));
@@ -93,6 +103,11 @@ __device__ __forceinline__ int64_t ldh_i64(const int64_t* a, uint64_t pol) {
   return r;
 }
 template <int KP> __device__ __forceinline__ DVec<KP> ldgh_vec(const double* p, uint64_t pol);
+template <> __device__ __forceinline__ DVec<1> ldgh_vec<1>(const double* p, uint64_t pol) {
+  DVec<1> r;
+  asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r.v[0]) : "l"(p), "l"(pol));
+  return r;
+}
 template <> __device__ __forceinline__ DVec<2> ldgh_vec<2>(const double* p, uint64_t pol) {
   DVec<2> r;
   asm("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(r.v[0]), "=d"(r.v[1]) : "l"(p), "l"(pol));
@@ -123,12 +138,14 @@ struct RowsArgs {
   const int32_t* __restrict__ c0;       // [n] first chunk of a long row
   const int64_t* __restrict__ tab;      // [n_chunks][2] (row, first nonzero)
   int64_t n_chunks;
+  int64_t long_row;                     // rows longer than this are summed by chunk warps
   double* chunk_acc;                    // [n_chunks][4]
   const double* __restrict__ x;         // gathered block, padded [n][KP]
   double* y;                            // [n][KQ]
   const double* __restrict__ deg;
   int opL, k;
-  VecScalars* sc;                       // PCG mode: alpha_c on device (null: plain apply)
+  VecScalars* sc;                       // small-k PCG mode: alpha_c on device (null: plain apply)
+  PcgScalars* sc1;                      // k = 1 PCG mode (pcg.cu): alpha on device
   double* part;                         // [grid][4] block partials of p^T q
   unsigned int* ticket;                 // [1], self-resetting
 };
@@ -184,9 +201,12 @@ __device__ __forceinline__ void rows_chunk_items(const RowsArgs& a, uint64_t ps,
   }
 }
 // One-pass mode: the chunks in their own launch before k_rows<PASS 2> (which reads them).
+__device__ __forceinline__ bool rows_skip(const RowsArgs& a) {   // the solver has finished
+  return (a.sc && *(volatile int32_t*)&a.sc->done) || (a.sc1 && *(volatile int32_t*)&a.sc1->done);
+}
 template <int WT, int KP, int KQ>
 __global__ void __launch_bounds__(RTB) k_rows_chunks(const RowsArgs a) {
-  if (a.sc && *(volatile int32_t*)&a.sc->done) return;
+  if (rows_skip(a)) return;
   const uint64_t ps = (FJ_ROWS_HINT & 1) ? pol_first() : 0, pg = (FJ_ROWS_HINT & 2) ? pol_last() : 0;
   rows_chunk_items<WT, KP, KQ>(a, ps, pg);
 }
@@ -202,7 +222,7 @@ __global__ void __launch_bounds__(RTB, PASS == 0 ? FJ_ROWS_MINB : FJ_ROWS_MINB_F
   constexpr int G = FJ_ROWS_G, U = FJ_ROWS_U;
   constexpr bool FIN = PASS != 0;
   __shared__ double s_red[4 * RTB / 32];
-  if (a.sc && *(volatile int32_t*)&a.sc->done) return;
+  if (rows_skip(a)) return;
   const int64_t ng = (int64_t)gridDim.x * (RTB / G);
   const int sub = threadIdx.x % G;
   const uint64_t ps = (FJ_ROWS_HINT & 5) ? pol_first() : 0, pg = (FJ_ROWS_HINT & 2) ? pol_last() : 0;
@@ -216,7 +236,7 @@ __global__ void __launch_bounds__(RTB, PASS == 0 ? FJ_ROWS_MINB : FJ_ROWS_MINB_F
     const int64_t i = i0 + (threadIdx.x & 31) / G;
     const bool valid = i < a.n;
     const int64_t b = valid ? ld_i64h(a.rp + i, ps) : 0, e = valid ? ld_i64h(a.rp + i + 1, ps) : 0;
-    const bool lng = e - b > ROWS_LONG;
+    const bool lng = e - b > a.long_row;
     int64_t kb = b, ke = e;
     if (PASS == 0 && valid) ke = b + ld_colh(a.off + i, ps);
     if (PASS == 1 && valid) kb = b + ld_colh(a.off + i, ps);
@@ -278,6 +298,17 @@ __global__ void __launch_bounds__(RTB, PASS == 0 ? FJ_ROWS_MINB : FJ_ROWS_MINB_F
     block_sum<KQ, RTB>(t, s_red);
     if (threadIdx.x != 0) return;
     *a.ticket = 0u;
+    if (PcgScalars* s1 = a.sc1) {   // k = 1 (as ApplyOp::finalize)
+      s1->pq = t[0];
+      if (!(t[0] > 0.0) || !isfinite(t[0])) {   // (I+L) is SPD: p^T q > 0 unless p = 0
+        s1->alpha = 0.0;
+        s1->breakdown = 1;
+        s1->done = 1;
+      } else {
+        s1->alpha = s1->rho / t[0];
+      }
+      return;
+    }
     VecScalars* sc = a.sc;
     if (!sc) return;
 #pragma unroll
@@ -299,34 +330,48 @@ __global__ void __launch_bounds__(RTB, PASS == 0 ? FJ_ROWS_MINB : FJ_ROWS_MINB_F
   }
 }
 
-// ---------------------------------------------------------------- plan (built once per graph)
-// nch[i] = chunks of a long row; off[i] = entries with column < split; *bad |= 1 if some row's
-// slab-A entries are not a prefix of the row (columns not ascending: the 2-slab split is off).
-__global__ void k_rows_plan1(int64_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
-                             int64_t split, int32_t* __restrict__ nch, int32_t* __restrict__ off, int* bad) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t b = rp[i], e = rp[i + 1];
-    nch[i] = e - b > ROWS_LONG ? (int32_t)((e - b + ROWS_CH - 1) / ROWS_CH) : 0;
-    if (!off) continue;
-    if (e - b > ROWS_LONG) { off[i] = 0; continue; }   // long rows are summed whole by chunk warps
-    int32_t lo = 0;
-    bool hi_seen = false, viol = false;
-    for (int64_t k = b; k < e; ++k) {
-      if (col[k] < split) { ++lo; viol |= hi_seen; } else { hi_seen = true; }
-    }
-    off[i] = lo;
-    if (viol) atomicOr(bad, 1);
-  }
+// ---------------------------------------------------------------- plan + launcher (host)
+// The rows product of one graph for one gathered row width KP: built once with the solver
+// workspace (rows.cu).  mode 0: the merge-path engine (tiles.cuh) computes the product instead.
+struct RowsPlan {
+  int mode = 0;                      // 0: engine; 1: one row pass; 2: two column slabs
+  int grid = 0, grid_chunks = 0;
+  int32_t* off = nullptr;            // [n] slab-A entries per row (mode 2)
+  int32_t* c0 = nullptr;             // [n] first long-row chunk
+  int64_t* tab = nullptr;            // [n_chunks][2]
+  int64_t n_chunks = 0;
+  int64_t long_row = 0;
+  double* chunk_acc = nullptr;       // [n_chunks][4]
+  double* part = nullptr;            // [grid][4]
+  unsigned int* ticket = nullptr;
+};
+// Selection (FJ_ROWS: -1 auto (default), 0 engine, 1 one pass, 2 two slabs): see rows.cu.
+fj_status rows_plan_build(fj_graph* g, int kp, RowsPlan& R, cudaStream_t st);
+void rows_plan_free(RowsPlan& R);
+inline int rows_launches(const RowsPlan& R) {   // kernel launches of one product
+  if (R.mode == 0) return 1;
+  return (R.mode == 2 ? 2 : 1) + (R.n_chunks > 0 && (R.mode == 1 || !FJ_ROWS_FUSE_CHUNKS) ? 1 : 0);
 }
-__global__ void k_rows_plan2(int64_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ nch,
-                             const int32_t* __restrict__ c0, int64_t* __restrict__ tab) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t m = nch[i];
-    for (int32_t c = 0; c < m; ++c) {
-      tab[2 * ((int64_t)c0[i] + c)] = i;
-      tab[2 * ((int64_t)c0[i] + c) + 1] = rp[i] + (int64_t)c * ROWS_CH;
-    }
+
+// y = (I+L) x (or L x) on the rows plan; PCG mode with vsc (small k) or psc (k = 1).
+template <int WT, int KP, int KQ>
+fj_status rows_product(const fj_graph* g, const RowsPlan& R, const double* x, double* y, int opL, int k,
+                       VecScalars* vsc, PcgScalars* psc, cudaStream_t st) {
+  RowsArgs a{g->n, g->row_ptr, g->col, g->w, R.off, R.c0, R.tab, R.n_chunks, R.long_row, R.chunk_acc,
+             x, y, g->deg, opL, k, vsc, psc, R.part, R.ticket};
+  if (R.n_chunks > 0 && (R.mode == 1 || !FJ_ROWS_FUSE_CHUNKS)) {
+    k_rows_chunks<WT, KP, KQ><<<R.grid_chunks, RTB, 0, st>>>(a);
+    FJ_CK_LAUNCH();
   }
+  if (R.mode == 2) {
+    k_rows<WT, KP, KQ, 0><<<R.grid, RTB, 0, st>>>(a);
+    FJ_CK_LAUNCH();
+    k_rows<WT, KP, KQ, 1><<<R.grid, RTB, 0, st>>>(a);
+  } else {
+    k_rows<WT, KP, KQ, 2><<<R.grid, RTB, 0, st>>>(a);
+  }
+  FJ_CK_LAUNCH();
+  return FJ_OK;
 }
 
 }  // namespace fj

@@ -21,23 +21,11 @@
 #include <vector>
 
 #include "ops.cuh"
+#include "rows.cuh"
 #include "vec.cuh"
 #include "workspace.cuh"
 
 namespace fj {
-
-// Device scalars of one small-k batched solve (per column), written only by last-block finalisers.
-struct VecScalars {
-  double rho[KVMAX], alpha[KVMAX], beta[KVMAX], pq[KVMAX], rr[KVMAX], ss[KVMAX], tol2[KVMAX], res2[KVMAX];
-  double alx[KVMAX];   // alpha applied to x by k_v_dir<XD> (0 for columns inactive in that iteration)
-  int32_t active[KVMAX], conv[KVMAX], breakdown[KVMAX];
-  int32_t iter, max_iter, done, k;
-  int32_t xpend;       // k_v_dir<XD> owes x += alx p for the iteration k_v_update just finished
-};
-}  // namespace fj
-#include "rows.cuh"   // needs VecScalars
-namespace fj {
-
 
 // ---------------------------------------------------------------- row operators (tiles.cuh Op)
 // q = (I+L) p or L p for the KQ real columns of a padded [n][KP] block (P:L88 L = D - A): the
@@ -461,19 +449,6 @@ __global__ void k_v_unpack(int64_t n, int k, const double* __restrict__ src, dou
 // ---------------------------------------------------------------- workspace
 constexpr int VNP_MAX = 10 * KVMAX, VNA_MAX = 3 * KVMAX;
 
-// Column-slab row product (rows.cuh) of one graph: built with the workspace.
-struct RowsPlan {
-  int mode = 0;                      // 0: warp-item engine; 1: one row pass; 2: two column slabs
-  int grid = 0, grid_chunks = 0;
-  int32_t* off = nullptr;            // [n] slab-A entries per row (mode 2)
-  int32_t* c0 = nullptr;             // [n] first long-row chunk
-  int64_t* tab = nullptr;            // [n_chunks][2]
-  int64_t n_chunks = 0;
-  double* chunk_acc = nullptr;       // [n_chunks][4]
-  double* part = nullptr;            // [grid][4]
-  unsigned int* ticket = nullptr;
-};
-
 struct VecWs {
   int k = 0, kp = 0, kq = 0;
   RowsPlan rows;         // k columns; p rows KP wide (gathered), x / r / q rows KQ wide
@@ -495,12 +470,7 @@ struct VecWs {
 static VecWs* vec_cache(fj_graph* g) { return reinterpret_cast<VecWs*>(g->vec_ws); }
 
 // kernel launches of one PCG iteration (product + k_v_update + k_v_dir), for fj_kernel_launches
-static int vec_iter_launches(const VecWs* w) {
-  const RowsPlan& R = w->rows;
-  const int prod = R.mode == 0 ? 1
-                              : (R.mode == 2 ? 2 : 1) + (R.n_chunks > 0 && (R.mode == 1 || !FJ_ROWS_FUSE_CHUNKS) ? 1 : 0);
-  return prod + 2;
-}
+static int vec_iter_launches(const VecWs* w) { return rows_launches(w->rows) + 2; }
 
 void free_vec_ws(fj_graph* g) {
   VecWs* w = vec_cache(g);
@@ -515,8 +485,7 @@ void free_vec_ws(fj_graph* g) {
   dfree(w->elem_part); dfree(w->elem_ticket);
   dfree(w->ts.block_part); dfree(w->ts.long_part); dfree(w->ts.chunk_acc);
   dfree(w->ts.long_ticket); dfree(w->ts.grid_ticket); dfree(w->qout); dfree(w->dred);
-  dfree(w->rows.off); dfree(w->rows.c0); dfree(w->rows.tab); dfree(w->rows.chunk_acc);
-  dfree(w->rows.part); dfree(w->rows.ticket);
+  rows_plan_free(w->rows);
   delete w;
   g->vec_ws = nullptr;
 }
@@ -532,83 +501,6 @@ static fj_status valloc(T** p, int64_t count, cudaStream_t st, bool zero = false
 static int kp_of(int k) { return k <= 2 ? 2 : k == 3 ? vec_pad3() : 4; }
 static int kq_of(int k) { return k <= 2 ? 2 : k == 3 ? 3 : 4; }   // x, r, q: unpadded
 
-
-// Product selection for the single-GPU small-k solve (FJ_VEC_ROWS: -1 auto (default), 0 engine,
-// 1 one row pass, 2 two column slabs).  Auto: two slabs when the gathered block exceeds
-// kRowsSlabBytes and every row's columns ascend, else one row pass.
-constexpr int64_t kRowsSlabBytes = 64ll << 20;
-static int rows_knob() {
-  static const int v = [] { const char* e = getenv("FJ_VEC_ROWS"); return e ? atoi(e) : -1; }();
-  return v;
-}
-
-static fj_status build_rows_plan(fj_graph* g, VecWs* w, cudaStream_t st) {
-  RowsPlan& R = w->rows;
-  const int knob = rows_knob();
-  if (knob == 0 || g->dist) { R.mode = 0; return FJ_OK; }
-  const int64_t n = g->n;
-  bool two = knob == 2 || (knob < 0 && n * (int64_t)w->kp * 8 > kRowsSlabBytes);
-  const unsigned cb = (unsigned)std::min<int64_t>((n + 255) / 256, 8192);
-  DevBuf<int32_t> nch;
-  DevBuf<int> bad;
-  FJ_TRY(nch.alloc(n, st));
-  FJ_TRY(bad.alloc(1, st));
-  FJ_CK(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
-  FJ_TRY(valloc(&R.c0, n, st));
-  if (two) FJ_TRY(valloc(&R.off, n, st));
-  if (n > 0) {
-    k_rows_plan1<<<cb, 256, 0, st>>>(n, g->row_ptr, g->col, n / 2, nch.p, two ? R.off : nullptr, bad.p);
-    FJ_CK_LAUNCH();
-    size_t bytes = 0;
-    FJ_CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, nch.p, R.c0, n, st));
-    DevBuf<uint8_t> tmp;
-    FJ_TRY(tmp.alloc((int64_t)bytes, st));
-    FJ_CK(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, nch.p, R.c0, n, st));
-    count_cub();
-  }
-  int32_t last[2] = {0, 0};
-  int hbad = 0;
-  if (n > 0) {
-    FJ_CK(cudaMemcpyAsync(&last[0], R.c0 + n - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    FJ_CK(cudaMemcpyAsync(&last[1], nch.p + n - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-  }
-  FJ_CK(cudaMemcpyAsync(&hbad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, st));
-  FJ_CK(cudaStreamSynchronize(st));
-  R.n_chunks = (int64_t)last[0] + last[1];
-  if (two && hbad) {   // columns not ascending in some row: slab A is not a prefix -> one pass
-    if (knob == 2) return fail(FJ_E_INVALID_ARG, "FJ_VEC_ROWS=2 needs ascending columns in every row");
-    two = false;
-    dfree(R.off);
-    R.off = nullptr;
-  }
-  FJ_TRY(valloc(&R.tab, 2 * R.n_chunks, st));
-  FJ_TRY(valloc(&R.chunk_acc, 4 * R.n_chunks, st));
-  if (R.n_chunks > 0) {
-    k_rows_plan2<<<cb, 256, 0, st>>>(n, g->row_ptr, nch.p, R.c0, R.tab);
-    FJ_CK_LAUNCH();
-  }
-  int occ = 0;
-  FJ_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_rows<FJ_W_UNIT, 4, 3, 2>, RTB, 0));
-  if (occ < 1) occ = 1;
-  // Grid: `waves` x the resident blocks, waves = rows / (8 x resident row groups) clamped to [1, 4]
-  // (measured, profiles/r02_ab_rows_variants.log: C3 (4e6 rows) 4 waves 0.496 ms vs 1 wave 0.514;
-  // C2 (1e6 rows) 1 wave 61.5 us vs 4 waves 71 us).  FJ_ROWS_WAVES > 0 fixes it (A/B).
-#ifndef FJ_ROWS_WAVES
-#define FJ_ROWS_WAVES 0
-#endif
-  const int64_t resident_groups = (int64_t)g->num_sms * occ * (RTB / FJ_ROWS_G);
-  const int64_t waves = FJ_ROWS_WAVES > 0 ? FJ_ROWS_WAVES
-                                          : std::max<int64_t>(1, std::min<int64_t>(4, n / (8 * resident_groups)));
-  int64_t grid = (int64_t)g->num_sms * occ * waves;
-  const int64_t need = (n * FJ_ROWS_G + RTB - 1) / RTB;
-  if (grid > need) grid = need > 0 ? need : 1;
-  R.grid = (int)grid;
-  R.grid_chunks = (int)std::max<int64_t>(1, std::min<int64_t>((R.n_chunks * 32 + RTB - 1) / RTB, (int64_t)g->num_sms * 8));
-  FJ_TRY(valloc(&R.part, 4 * grid, st));
-  FJ_TRY(valloc(&R.ticket, 1, st, true));
-  R.mode = two ? 2 : 1;
-  return FJ_OK;
-}
 
 static fj_status get_vec_ws(fj_graph* g, int k, cudaStream_t st, VecWs** out) {
   VecWs* w = vec_cache(g);
@@ -646,7 +538,7 @@ static fj_status get_vec_ws(fj_graph* g, int k, cudaStream_t st, VecWs** out) {
   FJ_CK(cudaEventCreate(&w->ev2));
   FJ_CK(cudaEventCreate(&w->ev3));
   FJ_CK(cudaEventCreate(&w->ev4));
-  FJ_TRY(build_rows_plan(g, w, st));
+  FJ_TRY(rows_plan_build(g, kp, w->rows, st));
   *out = w;
   return FJ_OK;
 }
@@ -685,24 +577,7 @@ static fj_status vec_apply_padded(const fj_graph* g, const VecWs* w, const doubl
   return by_wtype<KP>(g, [&](auto wt) {
     constexpr int WT = decltype(wt)::value;
     if constexpr (KP == 2 || KP == 4) {
-      const RowsPlan& R = w->rows;
-      if (R.mode != 0) {   // column-slab row product (rows.cuh)
-        RowsArgs a{g->n, g->row_ptr, g->col, g->w, R.off, R.c0, R.tab, R.n_chunks, R.chunk_acc,
-                   x, y, g->deg, opL, w->k, sc, R.part, R.ticket};
-        if (R.n_chunks > 0 && (R.mode == 1 || !FJ_ROWS_FUSE_CHUNKS)) {
-          k_rows_chunks<WT, KP, KQ><<<R.grid_chunks, RTB, 0, st>>>(a);
-          FJ_CK_LAUNCH();
-        }
-        if (R.mode == 2) {
-          k_rows<WT, KP, KQ, 0><<<R.grid, RTB, 0, st>>>(a);
-          FJ_CK_LAUNCH();
-          k_rows<WT, KP, KQ, 1><<<R.grid, RTB, 0, st>>>(a);
-        } else {
-          k_rows<WT, KP, KQ, 2><<<R.grid, RTB, 0, st>>>(a);
-        }
-        FJ_CK_LAUNCH();
-        return FJ_OK;
-      }
+      if (w->rows.mode != 0) return rows_product<WT, KP, KQ>(g, w->rows, x, y, opL, w->k, sc, nullptr, st);
     }
     ApplyOpV<WT, KP, KQ> op{x, y, g->deg, opL, sc, w->k};
     int nl = 0;

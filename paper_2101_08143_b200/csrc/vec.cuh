@@ -13,7 +13,22 @@ struct alignas(KP == 3 ? 8 : KP * 8) DVec {
   double v[KP];
 };
 
+// Device scalars of one small-k batched solve (per column), written only by last-block finalisers
+// (spmv_vec.cu; the rows product's finaliser, rows.cuh).
+struct VecScalars {
+  double rho[KVMAX], alpha[KVMAX], beta[KVMAX], pq[KVMAX], rr[KVMAX], ss[KVMAX], tol2[KVMAX], res2[KVMAX];
+  double alx[KVMAX];   // alpha applied to x by k_v_dir<XD> (0 for columns inactive in that iteration)
+  int32_t active[KVMAX], conv[KVMAX], breakdown[KVMAX];
+  int32_t iter, max_iter, done, k;
+  int32_t xpend;       // k_v_dir<XD> owes x += alx p for the iteration k_v_update just finished
+};
+
 template <int KP> __device__ __forceinline__ DVec<KP> ld_vec(const double* p);
+template <> __device__ __forceinline__ DVec<1> ld_vec<1>(const double* p) {
+  DVec<1> r;
+  r.v[0] = *p;
+  return r;
+}
 template <> __device__ __forceinline__ DVec<2> ld_vec<2>(const double* p) {
   DVec<2> r;
   asm volatile("ld.global.v2.f64 {%0, %1}, [%2];" : "=d"(r.v[0]), "=d"(r.v[1]) : "l"(p));
@@ -48,6 +63,7 @@ template <> __device__ __forceinline__ void st_vec<3>(double* p, const DVec<3>& 
   asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(p + (odd ? 1 : 0)), "d"(a), "d"(b) : "memory");
   asm volatile("st.global.f64 [%0], %1;" ::"l"(p + (odd ? 0 : 2)), "d"(c) : "memory");
 }
+template <> __device__ __forceinline__ void st_vec<1>(double* p, const DVec<1>& v) { *p = v.v[0]; }
 template <> __device__ __forceinline__ void st_vec<2>(double* p, const DVec<2>& v) {
   asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.v[0]), "d"(v.v[1]) : "memory");
 }

@@ -1,7 +1,7 @@
 """Graphs of tests/test_gpu_rows.py (shared by the test and its subprocess worker; inputs only)."""
 import numpy as np
 
-CASES = ["hub_k3_unit", "hub_k2_u8", "hub_k4_f64", "ragged_k3", "tiny_k3"]
+CASES = ["hub_k3_unit", "hub_k2_u8", "hub_k4_f64", "ragged_k3", "tiny_k3", "hub_k1_unit", "hub_k1_u8", "ragged_k1"]
 
 
 def _hubs(rng, n, degs, extra, lo=0):
@@ -31,14 +31,14 @@ def case_inputs(name):
         if k == 4:
             S[:, 3] = 0.375                            # consensus column: z = s exactly
         return n, u, v, w, S
-    if name == "ragged_k3":
+    if name.startswith("ragged_k"):
         n = 5003
         # rows of exactly 256 / 257 / 1024 / 1025 neighbours (long-row and chunk boundaries), 1000
         # isolated vertices (rows 4003..5002), a single-edge component
         u, v = _hubs(rng, 4000, [256, 257, 1024, 1025], 9000, lo=10)
         u = np.concatenate([u, [4001]]).astype(np.int32)
         v = np.concatenate([v, [4002]]).astype(np.int32)
-        return n, u, v, None, rng.uniform(0, 1, (n, 3))
+        return n, u, v, None, rng.uniform(0, 1, (n, int(name[-1])))
     if name == "tiny_k3":
         n = 7                                          # fewer rows than a warp's row groups
         u = np.array([0, 1, 2, 3, 0, 5], dtype=np.int32)

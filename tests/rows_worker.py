@@ -1,7 +1,7 @@
 """Subprocess worker of tests/test_gpu_rows.py (not a test module): runs the small-k solve, the
 quantities and the product on the graphs of that test with the product path selected by the
-environment (FJ_VEC_ROWS is read once per process), and saves the GPU results to an .npz.
-  FJ_VEC_ROWS=<0|1|2> python tests/rows_worker.py <out.npz>"""
+environment (FJ_ROWS is read once per process), and saves the GPU results to an .npz.
+  FJ_ROWS=<0|1|2> python tests/rows_worker.py <out.npz>"""
 import os
 import sys
 
