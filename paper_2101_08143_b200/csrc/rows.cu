@@ -1,6 +1,7 @@
 // rows.cu — the plan of the lean row product (rows.cuh), built once per graph
 // and gathered row width with the solver workspace.
 #include <algorithm>
+#include <climits>
 #include <cstdlib>
 
 #include "rows.cuh"
@@ -12,10 +13,12 @@ namespace fj {
 // nch[i] = chunks of a long row; off[i] = entries with column < split; *bad |= 1 if some row's
 // slab-A entries are not a prefix of the row (columns not ascending: the 2-slab split is off).
 __global__ void k_rows_plan1(int64_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
-                             int64_t split, int64_t long_row, int32_t* __restrict__ nch, int32_t* __restrict__ off,
-                             int* bad) {
+                             int64_t split, int64_t long_row, int32_t* __restrict__ nch, uint16_t* __restrict__ off,
+                             int32_t* __restrict__ rp32, int* bad) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t b = rp[i], e = rp[i + 1];
+    rp32[i + 1] = (int32_t)e;
+    if (i == 0) rp32[0] = (int32_t)b;
     nch[i] = e - b > long_row ? (int32_t)((e - b + ROWS_CH - 1) / ROWS_CH) : 0;
     if (!off) continue;
     if (e - b > long_row) { off[i] = 0; continue; }   // long rows are summed whole by chunk warps
@@ -24,7 +27,7 @@ __global__ void k_rows_plan1(int64_t n, const int64_t* __restrict__ rp, const in
     for (int64_t k = b; k < e; ++k) {
       if (col[k] < split) { ++lo; viol |= hi_seen; } else { hi_seen = true; }
     }
-    off[i] = lo;
+    off[i] = (uint16_t)lo;   // <= long_row < 2^16
     if (viol) atomicOr(bad, 1);
   }
 }
@@ -51,7 +54,7 @@ static int rows_knob() {
 constexpr int64_t kRowsSlabMin = 64ll << 20, kRowsSlabMax = 160ll << 20;
 
 void rows_plan_free(RowsPlan& R) {
-  dfree(R.off); dfree(R.c0); dfree(R.tab); dfree(R.chunk_acc); dfree(R.part); dfree(R.ticket);
+  dfree(R.off); dfree(R.rp32); dfree(R.c0); dfree(R.tab); dfree(R.chunk_acc); dfree(R.part); dfree(R.ticket);
   R = RowsPlan{};
 }
 
@@ -65,7 +68,8 @@ static fj_status ralloc(T** p, int64_t count, cudaStream_t st) {
 fj_status rows_plan_build(fj_graph* g, int kp, RowsPlan& R, cudaStream_t st) {
   rows_plan_free(R);
   const int knob = rows_knob();
-  if (knob == 0 || g->dist) return FJ_OK;   // mode 0: the engine
+  // mode 0, the engine: forced, a distributed slice, or a CSR beyond the plan's int32 row_ptr
+  if (knob == 0 || g->dist || g->nnz >= (int64_t)INT32_MAX) return FJ_OK;
   const int64_t n = g->n;
   const int64_t bytes_p = n * (int64_t)kp * 8;
   bool two = knob == 2 || (knob < 0 && bytes_p > kRowsSlabMin && bytes_p <= kRowsSlabMax);
@@ -77,9 +81,12 @@ fj_status rows_plan_build(fj_graph* g, int kp, RowsPlan& R, cudaStream_t st) {
   FJ_TRY(bad.alloc(1, st));
   FJ_CK(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
   FJ_TRY(ralloc(&R.c0, n, st));
+  FJ_TRY(ralloc(&R.rp32, n + 1, st));
+  if (n == 0) FJ_CK(cudaMemsetAsync(R.rp32, 0, sizeof(int32_t), st));
   if (two) FJ_TRY(ralloc(&R.off, n, st));
   if (n > 0) {
-    k_rows_plan1<<<cb, 256, 0, st>>>(n, g->row_ptr, g->col, n / 2, R.long_row, nch.p, two ? R.off : nullptr, bad.p);
+    k_rows_plan1<<<cb, 256, 0, st>>>(n, g->row_ptr, g->col, n / 2, R.long_row, nch.p, two ? R.off : nullptr, R.rp32,
+                                     bad.p);
     FJ_CK_LAUNCH();
     size_t tb = 0;
     FJ_CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, nch.p, R.c0, n, st));

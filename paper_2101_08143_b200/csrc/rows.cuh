@@ -44,6 +44,7 @@ namespace fj {
 // summed by chunk warps
 constexpr int ROWS_CH = FJ_ROWS_CH;       // nonzeros per long-row chunk
 constexpr int RTB = 256;         // threads per block of the row kernels
+static_assert(FJ_ROWS_LONG < 65536 && FJ_ROWS_LONG1 < 65536, "slab offsets are uint16");
 #ifndef FJ_ROWS_G
 #define FJ_ROWS_G 2              // lanes per row (measured on C3: 2 > 1, 4 > 8 > 16, 32)
 #endif
@@ -97,11 +98,6 @@ __device__ __forceinline__ int32_t ldh_i32(const int32_t* a, uint64_t pol) {
   asm("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(r) : "l"(a), "l"(pol));
   return r;
 }
-__device__ __forceinline__ int64_t ldh_i64(const int64_t* a, uint64_t pol) {
-  int64_t r;
-  asm("ld.global.nc.L2::cache_hint.b64 %0, [%1], %2;" : "=l"(r) : "l"(a), "l"(pol));
-  return r;
-}
 template <int KP> __device__ __forceinline__ DVec<KP> ldgh_vec(const double* p, uint64_t pol);
 template <> __device__ __forceinline__ DVec<1> ldgh_vec<1>(const double* p, uint64_t pol) {
   DVec<1> r;
@@ -125,16 +121,14 @@ template <int KP> __device__ __forceinline__ DVec<KP> ld_gather(const double* p,
 __device__ __forceinline__ int32_t ld_colh(const int32_t* a, uint64_t pol) {
   if constexpr ((FJ_ROWS_HINT & 1) != 0) return ldh_i32(a, pol); else return __ldg(a);
 }
-__device__ __forceinline__ int64_t ld_i64h(const int64_t* a, uint64_t pol) {
-  if constexpr ((FJ_ROWS_HINT & 1) != 0) return ldh_i64(a, pol); else return *a;
-}
 
 struct RowsArgs {
   int64_t n;
   const int64_t* __restrict__ rp;
   const int32_t* __restrict__ col;
   const void* __restrict__ w;
-  const int32_t* __restrict__ off;      // [n] slab-A entries per row (2-slab mode)
+  const int32_t* __restrict__ rp32;     // [n+1] row_ptr as int32 (the plan's copy: nnz < 2^31)
+  const uint16_t* __restrict__ off;     // [n] slab-A entries per short row (2-slab mode)
   const int32_t* __restrict__ c0;       // [n] first chunk of a long row
   const int64_t* __restrict__ tab;      // [n_chunks][2] (row, first nonzero)
   int64_t n_chunks;
@@ -186,8 +180,8 @@ __device__ __forceinline__ void rows_chunk_items(const RowsArgs& a, uint64_t ps,
   const int64_t nw = (int64_t)gridDim.x * (RTB / 32);
   for (int64_t c = (blockIdx.x * (int64_t)RTB + threadIdx.x) >> 5; c < a.n_chunks; c += nw) {
     const int64_t r = a.tab[2 * c], k0 = a.tab[2 * c + 1];
-    const int64_t k1 = min(k0 + (int64_t)ROWS_CH, a.rp[r + 1]);
-    FJ_DCHECK(r >= 0 && r < a.n && k0 >= a.rp[r] && k0 < k1);
+    const int64_t k1 = min(k0 + (int64_t)ROWS_CH, (int64_t)a.rp32[r + 1]);
+    FJ_DCHECK(r >= 0 && r < a.n && k0 >= a.rp32[r] && k0 < k1);
     double acc[KQ];
 #pragma unroll
     for (int f = 0; f < KQ; ++f) acc[f] = 0.0;
@@ -235,11 +229,11 @@ __global__ void __launch_bounds__(RTB, PASS == 0 ? FJ_ROWS_MINB : FJ_ROWS_MINB_F
   for (int64_t i0 = (blockIdx.x * (int64_t)RTB + (threadIdx.x & ~31)) / G; i0 < a.n; i0 += ng) {
     const int64_t i = i0 + (threadIdx.x & 31) / G;
     const bool valid = i < a.n;
-    const int64_t b = valid ? ld_i64h(a.rp + i, ps) : 0, e = valid ? ld_i64h(a.rp + i + 1, ps) : 0;
+    const int64_t b = valid ? ld_colh(a.rp32 + i, ps) : 0, e = valid ? ld_colh(a.rp32 + i + 1, ps) : 0;
     const bool lng = e - b > a.long_row;
     int64_t kb = b, ke = e;
-    if (PASS == 0 && valid) ke = b + ld_colh(a.off + i, ps);
-    if (PASS == 1 && valid) kb = b + ld_colh(a.off + i, ps);
+    if (PASS == 0 && valid) ke = b + __ldg(a.off + i);
+    if (PASS == 1 && valid) kb = b + __ldg(a.off + i);
     FJ_DCHECK(kb >= b && ke <= e && kb <= ke);
     double acc[KQ];
 #pragma unroll
@@ -336,7 +330,8 @@ __global__ void __launch_bounds__(RTB, PASS == 0 ? FJ_ROWS_MINB : FJ_ROWS_MINB_F
 struct RowsPlan {
   int mode = 0;                      // 0: engine; 1: one row pass; 2: two column slabs
   int grid = 0, grid_chunks = 0;
-  int32_t* off = nullptr;            // [n] slab-A entries per row (mode 2)
+  int32_t* rp32 = nullptr;           // [n+1] int32 copy of row_ptr
+  uint16_t* off = nullptr;           // [n] slab-A entries per short row (mode 2)
   int32_t* c0 = nullptr;             // [n] first long-row chunk
   int64_t* tab = nullptr;            // [n_chunks][2]
   int64_t n_chunks = 0;
@@ -357,7 +352,7 @@ inline int rows_launches(const RowsPlan& R) {   // kernel launches of one produc
 template <int WT, int KP, int KQ>
 fj_status rows_product(const fj_graph* g, const RowsPlan& R, const double* x, double* y, int opL, int k,
                        VecScalars* vsc, PcgScalars* psc, cudaStream_t st) {
-  RowsArgs a{g->n, g->row_ptr, g->col, g->w, R.off, R.c0, R.tab, R.n_chunks, R.long_row, R.chunk_acc,
+  RowsArgs a{g->n, g->row_ptr, g->col, g->w, R.rp32, R.off, R.c0, R.tab, R.n_chunks, R.long_row, R.chunk_acc,
              x, y, g->deg, opL, k, vsc, psc, R.part, R.ticket};
   if (R.n_chunks > 0 && (R.mode == 1 || !FJ_ROWS_FUSE_CHUNKS)) {
     k_rows_chunks<WT, KP, KQ><<<R.grid_chunks, RTB, 0, st>>>(a);
