@@ -21,6 +21,7 @@ constexpr int ETPB = 256;
 
 template <int WT, class Op>
 inline fj_status launch_tiles_wt(const fj_graph* g, const SolveWs* ws, const Op& op, cudaStream_t st) {
+  if (ws->rows && ws->rows->mode != 0) return rows_op<WT>(*ws->rows, g->n, g->col, g->w, op, st);   // rows.cuh
   FJ_CK(launch_warp_items<WT>(g, ws, op, st));
   FJ_CK_LAUNCH();
   return FJ_OK;

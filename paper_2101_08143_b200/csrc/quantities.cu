@@ -6,6 +6,7 @@
 #include <vector>
 
 #include "ops.cuh"
+#include "rows.cuh"
 #include "workspace.cuh"
 
 namespace fj {
@@ -275,6 +276,7 @@ template <int WT>
 static fj_status launch_quant_wt(const fj_graph* g, const SolveWs* w, const double* s, const double* z, int64_t ld,
                                  int64_t c, double m, cudaStream_t st) {
   QuantOp<WT> op{z, s, g->deg, ld, c, m, w->qout};
+  if (w->rows && w->rows->mode != 0) return rows_op<WT>(*w->rows, g->n, g->col, g->w, op, st);   // rows.cuh
   FJ_CK(launch_warp_items<WT>(g, w, op, st));
   FJ_CK_LAUNCH();
   return FJ_OK;

@@ -55,6 +55,7 @@ constexpr int64_t kRowsSlabMin = 64ll << 20, kRowsSlabMax = 160ll << 20;
 
 void rows_plan_free(RowsPlan& R) {
   dfree(R.off); dfree(R.rp32); dfree(R.c0); dfree(R.tab); dfree(R.chunk_acc); dfree(R.part); dfree(R.ticket);
+  dfree(R.op_acc); dfree(R.op_part); dfree(R.op_ticket);
   R = RowsPlan{};
 }
 
@@ -65,14 +66,16 @@ static fj_status ralloc(T** p, int64_t count, cudaStream_t st) {
   return FJ_OK;
 }
 
-fj_status rows_plan_build(fj_graph* g, int kp, RowsPlan& R, cudaStream_t st) {
+// mode 2 allowed only for a graph's own CSR (two_ok); the knob and the size rule as described above
+static fj_status plan_core(int64_t n, int64_t nnz, const int64_t* row_ptr, const int32_t* col, int kp, int num_sms,
+                           bool two_ok, RowsPlan& R, cudaStream_t st) {
   rows_plan_free(R);
   const int knob = rows_knob();
-  // mode 0, the engine: forced, a distributed slice, or a CSR beyond the plan's int32 row_ptr
-  if (knob == 0 || g->dist || g->nnz >= (int64_t)INT32_MAX) return FJ_OK;
-  const int64_t n = g->n;
+  // mode 0, the engine: forced, or a CSR beyond the plan's int32 row_ptr
+  if (knob == 0 || nnz >= (int64_t)INT32_MAX) return FJ_OK;
+  R.num_sms = num_sms;
   const int64_t bytes_p = n * (int64_t)kp * 8;
-  bool two = knob == 2 || (knob < 0 && bytes_p > kRowsSlabMin && bytes_p <= kRowsSlabMax);
+  bool two = two_ok && (knob == 2 || (knob < 0 && bytes_p > kRowsSlabMin && bytes_p <= kRowsSlabMax));
   R.long_row = kp == 1 ? FJ_ROWS_LONG1 : FJ_ROWS_LONG;
   const unsigned cb = (unsigned)std::min<int64_t>((n + 255) / 256, 8192);
   DevBuf<int32_t> nch;
@@ -85,7 +88,7 @@ fj_status rows_plan_build(fj_graph* g, int kp, RowsPlan& R, cudaStream_t st) {
   if (n == 0) FJ_CK(cudaMemsetAsync(R.rp32, 0, sizeof(int32_t), st));
   if (two) FJ_TRY(ralloc(&R.off, n, st));
   if (n > 0) {
-    k_rows_plan1<<<cb, 256, 0, st>>>(n, g->row_ptr, g->col, n / 2, R.long_row, nch.p, two ? R.off : nullptr, R.rp32,
+    k_rows_plan1<<<cb, 256, 0, st>>>(n, row_ptr, col, n / 2, R.long_row, nch.p, two ? R.off : nullptr, R.rp32,
                                      bad.p);
     FJ_CK_LAUNCH();
     size_t tb = 0;
@@ -112,8 +115,9 @@ fj_status rows_plan_build(fj_graph* g, int kp, RowsPlan& R, cudaStream_t st) {
   }
   FJ_TRY(ralloc(&R.tab, 2 * R.n_chunks, st));
   FJ_TRY(ralloc(&R.chunk_acc, 4 * R.n_chunks, st));
+  FJ_TRY(ralloc(&R.op_acc, ROWS_NA_MAX * R.n_chunks, st));
   if (R.n_chunks > 0) {
-    k_rows_plan2<<<cb, 256, 0, st>>>(n, g->row_ptr, nch.p, R.c0, R.tab);
+    k_rows_plan2<<<cb, 256, 0, st>>>(n, row_ptr, nch.p, R.c0, R.tab);
     FJ_CK_LAUNCH();
   }
   int occ = 0;
@@ -125,19 +129,33 @@ fj_status rows_plan_build(fj_graph* g, int kp, RowsPlan& R, cudaStream_t st) {
 #ifndef FJ_ROWS_WAVES
 #define FJ_ROWS_WAVES 0
 #endif
-  const int64_t resident_groups = (int64_t)g->num_sms * occ * (RTB / FJ_ROWS_G);
+  const int64_t resident_groups = (int64_t)num_sms * occ * (RTB / FJ_ROWS_G);
   const int64_t waves = FJ_ROWS_WAVES > 0 ? FJ_ROWS_WAVES
                                           : std::max<int64_t>(1, std::min<int64_t>(4, n / (8 * resident_groups)));
-  int64_t grid = (int64_t)g->num_sms * occ * waves;
+  int64_t grid = (int64_t)num_sms * occ * waves;
   const int64_t need = (n * FJ_ROWS_G + RTB - 1) / RTB;
   if (grid > need) grid = need > 0 ? need : 1;
   R.grid = (int)grid;
-  R.grid_chunks = (int)std::max<int64_t>(1, std::min<int64_t>((R.n_chunks * 32 + RTB - 1) / RTB, (int64_t)g->num_sms * 8));
+  R.grid_chunks = (int)std::max<int64_t>(1, std::min<int64_t>((R.n_chunks * 32 + RTB - 1) / RTB, (int64_t)num_sms * 8));
   FJ_TRY(ralloc(&R.part, 4 * grid, st));
   FJ_TRY(ralloc(&R.ticket, 1, st));
   FJ_CK(cudaMemsetAsync(R.ticket, 0, sizeof(unsigned int), st));
+  R.grid_op_max = num_sms * (2048 / RTB);
+  FJ_TRY(ralloc(&R.op_part, (int64_t)ROWS_NP_MAX * R.grid_op_max, st));
+  FJ_TRY(ralloc(&R.op_ticket, 1, st));
+  FJ_CK(cudaMemsetAsync(R.op_ticket, 0, sizeof(unsigned int), st));
   R.mode = two ? 2 : 1;
   return FJ_OK;
+}
+
+fj_status rows_plan_build(fj_graph* g, int kp, RowsPlan& R, cudaStream_t st) {
+  if (g->dist) { rows_plan_free(R); return FJ_OK; }   // the distributed path plans its own views
+  return plan_core(g->n, g->nnz, g->row_ptr, g->col, kp, g->num_sms, true, R, st);
+}
+
+fj_status rows_plan_build_csr(int64_t n, int64_t nnz, const int64_t* row_ptr, const int32_t* col, int kp,
+                              int num_sms, RowsPlan& R, cudaStream_t st) {
+  return plan_core(n, nnz, row_ptr, col, kp, num_sms, false, R, st);
 }
 
 }  // namespace fj

@@ -339,9 +339,20 @@ struct RowsPlan {
   double* chunk_acc = nullptr;       // [n_chunks][4]
   double* part = nullptr;            // [grid][4]
   unsigned int* ticket = nullptr;
+  // generic row operators (k_op_rows): chunk partials [n_chunks][ROWS_NA_MAX], block partials
+  // [grid][ROWS_NP_MAX]
+  double* op_acc = nullptr;
+  double* op_part = nullptr;
+  unsigned int* op_ticket = nullptr;
+  int num_sms = 148;
+  int grid_op_max = 0;               // rows of op_part (>= #SMs x occupancy of any k_op_rows)
 };
 // Selection (FJ_ROWS: -1 auto (default), 0 engine, 1 one pass, 2 two slabs): see rows.cu.
 fj_status rows_plan_build(fj_graph* g, int kp, RowsPlan& R, cudaStream_t st);
+// The plan of any CSR view (rows [0, n), int64 row_ptr, columns < ncol): one row pass, no slabs
+// (the distributed path's diagonal / ghost CSRs).  Mode 0 if forced (FJ_ROWS=0) or nnz >= 2^31.
+fj_status rows_plan_build_csr(int64_t n, int64_t nnz, const int64_t* row_ptr, const int32_t* col, int kp,
+                              int num_sms, RowsPlan& R, cudaStream_t st);
 void rows_plan_free(RowsPlan& R);
 inline int rows_launches(const RowsPlan& R) {   // kernel launches of one product
   if (R.mode == 0) return 1;
@@ -365,6 +376,161 @@ fj_status rows_product(const fj_graph* g, const RowsPlan& R, const double* x, do
   } else {
     k_rows<WT, KP, KQ, 2><<<R.grid, RTB, 0, st>>>(a);
   }
+  FJ_CK_LAUNCH();
+  return FJ_OK;
+}
+
+
+// ---------------------------------------------------------------- any row operator (tiles.cuh Op)
+// The same lean scheme for the engine's other row operators (the fused quantities pass, the true
+// residual; the distributed product's diagonal and ghost passes): G lanes per row gather through
+// op.gather(), accumulate with op.add() (x_i = op.row_value(i) for operators that read it), the
+// group's sums are reduced by an xor-shuffle tree, long rows are summed by chunk warps in a launch
+// before (k_op_chunks, their NA partials in chunk order), then op.finish_row() on the group's first
+// lane and op.finalize() on the fixed-order grid reduction.  One pass over whole rows (no slabs).
+constexpr int ROWS_NA_MAX = 12, ROWS_NP_MAX = 16;
+struct RowsView {   // a CSR (rows [0, nrows)) and its rows plan
+  int64_t nrows;
+  const int32_t* __restrict__ rp32;
+  const int32_t* __restrict__ col;
+  const void* __restrict__ w;
+  int64_t long_row;
+  const int32_t* __restrict__ c0;
+  const int64_t* __restrict__ tab;
+  int64_t n_chunks;
+  double* acc;              // [n_chunks][ROWS_NA_MAX]
+  double* part;             // [grid][ROWS_NP_MAX]
+  unsigned int* ticket;
+};
+
+template <int WT, class Op, int U>
+__device__ __forceinline__ void op_accumulate(const RowsView& v, const Op& op, int64_t k, int64_t ke, int stride,
+                                              const typename Op::V& xi, double (&acc)[Op::NA]) {
+  using V = typename Op::V;
+  for (; k + (int64_t)(U - 1) * stride < ke; k += (int64_t)U * stride) {
+    int32_t j[U];
+    double wv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      j[u] = __ldg(v.col + k + u * stride);
+      wv[u] = (WT == FJ_W_UNIT) ? 1.0 : WeightT<WT>::get(v.w, k + u * stride);
+    }
+    V xv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) xv[u] = op.gather(j[u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u) op.add(acc, wv[u], xv[u], xi);
+  }
+  for (; k < ke; k += stride) {
+    const double wk = (WT == FJ_W_UNIT) ? 1.0 : WeightT<WT>::get(v.w, k);
+    op.add(acc, wk, op.gather(__ldg(v.col + k)), xi);
+  }
+}
+
+template <int WT, class Op>
+__global__ void __launch_bounds__(RTB) k_op_chunks(const RowsView v, const Op op) {
+  constexpr int NA = Op::NA;
+  static_assert(NA <= ROWS_NA_MAX, "row operator accumulators");
+  if (op.skip()) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (RTB / 32);
+  for (int64_t c = (blockIdx.x * (int64_t)RTB + threadIdx.x) >> 5; c < v.n_chunks; c += nw) {
+    const int64_t r = v.tab[2 * c], k0 = v.tab[2 * c + 1];
+    const int64_t k1 = min(k0 + (int64_t)ROWS_CH, (int64_t)v.rp32[r + 1]);
+    FJ_DCHECK(r >= 0 && r < v.nrows && k0 >= v.rp32[r] && k0 < k1);
+    const typename Op::V xi = Op::NEEDS_XI ? op.row_value(r) : Op::vzero();
+    double acc[NA];
+#pragma unroll
+    for (int f = 0; f < NA; ++f) acc[f] = 0.0;
+    op_accumulate<WT, Op, 4>(v, op, k0 + lane, k1, 32, xi, acc);
+#pragma unroll
+    for (int f = 0; f < NA; ++f) acc[f] = warp_sum(acc[f]);
+    if (lane == 0) {
+#pragma unroll
+      for (int f = 0; f < NA; ++f) v.acc[c * ROWS_NA_MAX + f] = acc[f];
+    }
+  }
+}
+
+#ifndef FJ_ROWS_OP_MINB
+#define FJ_ROWS_OP_MINB 3
+#endif
+template <int WT, class Op>
+__global__ void __launch_bounds__(RTB, FJ_ROWS_OP_MINB) k_op_rows(const RowsView v, const Op op) {
+  constexpr int G = FJ_ROWS_G, U = FJ_ROWS_U, NA = Op::NA, NP = Op::NP;
+  static_assert(NP <= ROWS_NP_MAX, "row operator partials");
+  using V = typename Op::V;
+  __shared__ double s_red[ROWS_NP_MAX * RTB / 32];
+  if (op.skip()) return;
+  const int64_t ng = (int64_t)gridDim.x * (RTB / G);
+  const int sub = threadIdx.x % G;
+  double part[NP];
+#pragma unroll
+  for (int f = 0; f < NP; ++f) part[f] = 0.0;
+  for (int64_t i0 = (blockIdx.x * (int64_t)RTB + (threadIdx.x & ~31)) / G; i0 < v.nrows; i0 += ng) {
+    const int64_t i = i0 + (threadIdx.x & 31) / G;
+    const bool valid = i < v.nrows;
+    const int64_t b = valid ? __ldg(v.rp32 + i) : 0, e = valid ? __ldg(v.rp32 + i + 1) : 0;
+    const bool lng = e - b > v.long_row;
+    const V xi = valid ? op.row_value(i) : Op::vzero();
+    double acc[NA];
+#pragma unroll
+    for (int f = 0; f < NA; ++f) acc[f] = 0.0;
+    if (!lng) op_accumulate<WT, Op, U>(v, op, b + sub, e, G, xi, acc);
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1)
+#pragma unroll
+      for (int f = 0; f < NA; ++f) acc[f] += __shfl_xor_sync(0xffffffffu, acc[f], o, G);
+    if (sub != 0 || !valid) continue;
+    if (lng) {   // chunk partials in chunk order
+#pragma unroll
+      for (int f = 0; f < NA; ++f) acc[f] = 0.0;
+      const int64_t c0 = v.c0[i], nch = (e - b + ROWS_CH - 1) / ROWS_CH;
+      for (int64_t c = c0; c < c0 + nch; ++c)
+#pragma unroll
+        for (int f = 0; f < NA; ++f) acc[f] += __ldcg(v.acc + c * ROWS_NA_MAX + f);
+    }
+    op.finish_row(i, e - b, xi, acc, part);
+  }
+  block_sum<NP, RTB>(part, s_red);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int f = 0; f < NP; ++f) v.part[(int64_t)blockIdx.x * ROWS_NP_MAX + f] = part[f];
+  }
+  if (!last_block_ticket(v.ticket, gridDim.x)) return;
+  double t[NP];
+#pragma unroll
+  for (int f = 0; f < NP; ++f) t[f] = 0.0;
+  for (int bb = threadIdx.x; bb < (int)gridDim.x; bb += RTB)
+#pragma unroll
+    for (int f = 0; f < NP; ++f) t[f] += __ldcg(v.part + (int64_t)bb * ROWS_NP_MAX + f);
+  block_sum<NP, RTB>(t, s_red);
+  if (threadIdx.x == 0) {
+    op.finalize(t);
+    *v.ticket = 0u;
+  }
+}
+
+// Launch a row operator on a plan built for (rp, col) with nrows rows.  The grid is fixed per
+// (plan, operator instantiation): #SMs x occupancy, so partials are reduced in a fixed order.
+template <int WT, class Op>
+fj_status rows_op(const RowsPlan& R, int64_t nrows, const int32_t* col, const void* w, const Op& op,
+                  cudaStream_t st) {
+  static int occ = 0;   // per instantiation
+  if (occ == 0) {
+    FJ_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_op_rows<WT, Op>, RTB, 0));
+    if (occ < 1) occ = 1;
+  }
+  RowsView v{nrows, R.rp32, col, w, R.long_row, R.c0, R.tab, R.n_chunks, R.op_acc, R.op_part, R.op_ticket};
+  if (R.n_chunks > 0) {
+    k_op_chunks<WT, Op><<<R.grid_chunks, RTB, 0, st>>>(v, op);
+    FJ_CK_LAUNCH();
+  }
+  int64_t grid = (int64_t)R.num_sms * occ;
+  const int64_t need = (nrows * FJ_ROWS_G + RTB - 1) / RTB;
+  if (grid > need) grid = need > 0 ? need : 1;
+  if (grid > R.grid_op_max) grid = R.grid_op_max;
+  k_op_rows<WT, Op><<<(unsigned)grid, RTB, 0, st>>>(v, op);
   FJ_CK_LAUNCH();
   return FJ_OK;
 }

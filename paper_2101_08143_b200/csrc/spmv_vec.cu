@@ -546,6 +546,7 @@ static fj_status get_vec_ws(fj_graph* g, int k, cudaStream_t st, VecWs** out) {
 // The warp-item engine on the vector schedule (sv: VEC_ITEMS merge items per lane), vector values.
 template <int WT, class Op>
 static fj_status launch_vec_items(const fj_graph* g, const VecWs* w, const Op& op, cudaStream_t st) {
+  if (w->rows.mode != 0) return rows_op<WT>(w->rows, g->n, g->col, g->w, op, st);   // rows.cuh
   static int occ = 0;   // per instantiation
   if (occ == 0) {
     FJ_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, warp_kernel<WT, Op>, WTPB, 0));

@@ -25,6 +25,9 @@ for name in CASES:
     z2, _, rep2 = G.approxim(Sd)                                                   # repeat: bitwise
     z3, _, rep3 = G.approxim(Sd, opts=fj.SolveOpts.make(use_cuda_graph=False))   # host-driven loop
     y = G.apply(Sd)                                                              # (I+L) S
+    zs, reps = G.solve(Sd)                                   # fj_solve: the true-residual pass runs
+    out[name + "/zs"] = zs.cpu().numpy()
+    out[name + "/solve"] = np.array([reps["rel_res_true"], reps["converged"]])
     out[name + "/z"] = z.cpu().numpy()
     out[name + "/y"] = y.cpu().numpy()
     out[name + "/q"] = np.array([[qc[key] for key in ["CI", "D", "P", "C", "Idc", "PDI"]] for qc in q])

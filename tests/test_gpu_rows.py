@@ -66,9 +66,13 @@ def test_rows_product_modes_vs_oracle(runs, oracle_results, mode, name):
     assert conv == 1 and rel <= 1e-10 and bk == (S.shape[1] if S.shape[1] > 1 else 0)
     assert r[name + "/same"].all(), r[name + "/same"]     # repeat bitwise, graph == host loop
     assert np.all(np.abs(r[name + "/y"] - Y) <= 1e-13 * T + 1e-300)   # any summation order
+    rs, cs = r[name + "/solve"]
+    assert cs == 1 and rs <= 1e-10                         # fj_solve's true-residual pass
+    Zs = r[name + "/zs"].reshape(S.shape)
     Z, Q, E, RS = r[name + "/z"], r[name + "/q"], r[name + "/eps"], r[name + "/res"]
     for c, (zo, qo) in enumerate(cols):
         assert np.max(np.abs(Z[:, c] - zo)) < 1e-9
+        assert np.max(np.abs(Zs[:, c] - zo)) < 1e-9
         if np.ptp(S[:, c]) == 0:                           # consensus column: z = s exactly
             assert np.array_equal(Z[:, c], S[:, c])
             continue
