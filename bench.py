@@ -226,8 +226,11 @@ def main():
     ap.add_argument("--no-cuda-graph", action="store_true",
                     help="host-driven PCG loop (same kernels); ncu cannot see kernels inside conditional graphs")
     args = ap.parse_args()
+    os.environ.setdefault("NCCL_DEBUG", "WARN")
+    # NCCL prints its version banner (and any warning) on stdout at WARN: send it to stderr so that
+    # rank 0's stdout is the one JSON line
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     ws, rank, local = dist_init()
-    os.environ.setdefault("NCCL_DEBUG", "WARN")   # keep rank 0's stdout to the one JSON line
     if args.impl == "reference":
         return run_reference(args, ws, rank)
 

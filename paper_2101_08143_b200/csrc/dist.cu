@@ -23,6 +23,7 @@
 #include <cub/cub.cuh>
 
 #include "ops.cuh"
+#include "rows.cuh"
 #include "vec.cuh"
 #include "workspace.cuh"
 
@@ -501,6 +502,7 @@ struct SplitCsr {
   uint8_t* bnd = nullptr;
   Sched sd[2], so[2];             // [0] scalar engine (KP = 1), [1] vector engine (KP > 1)
   TileScratch tsd[2], tso[2];
+  RowsPlan pd[2], po[2];          // the lean row kernel's plans of the two views (rows.cuh)
 };
 
 struct CgState {
@@ -546,6 +548,7 @@ static void free_cg(DistInfo* d) {
   dfree(sp.bnd);
   for (int f = 0; f < 2; ++f) {
     free_sched(sp.sd[f]); free_sched(sp.so[f]);
+    rows_plan_free(sp.pd[f]); rows_plan_free(sp.po[f]);
     free_ts(sp.tsd[f]); free_ts(sp.tso[f]);
   }
   dfree(c->u); dfree(c->w); dfree(c->p); dfree(c->s); dfree(c->x); dfree(c->r);
@@ -684,6 +687,9 @@ static fj_status ensure_split(fj_graph* g, CgWs* c, int f, cudaStream_t st) {
     FJ_TRY(build_schedule(&vo, P, sp.so[f], st));
     FJ_TRY(alloc_ts(sp.tsd[f], c->grid_max, sp.sd[f], KVMAX, st));
     FJ_TRY(alloc_ts(sp.tso[f], c->grid_max, sp.so[f], KVMAX, st));
+    // the same two views on the lean row kernel (one pass each; FJ_ROWS=0 keeps the engine)
+    FJ_TRY(rows_plan_build_csr(n, sp.nnz_d, sp.rp_d, sp.col_d, f == 0 ? 1 : 4, g->num_sms, sp.pd[f], st));
+    FJ_TRY(rows_plan_build_csr(sp.n_bnd, sp.nnz_o, sp.rp_o, sp.col_o, f == 0 ? 1 : 4, g->num_sms, sp.po[f], st));
   }
   return FJ_OK;
 }
@@ -815,9 +821,11 @@ static fj_status cg_product(fj_graph* g, CgWs* c, const double* u_in, cudaStream
   auto run = [&](auto wt) -> fj_status {
     constexpr int WT = decltype(wt)::value;
     CgDiagOp<WT, KP> od{u, c->w, c->dpart, done};
-    FJ_TRY((launch_view<WT>(g, sp.sd[f], sp.rp_d, sp.col_d, sp.w_d, g->n, sp.nnz_d, sp.tsd[f], c->grid_max, od, st)));
+    if (sp.pd[f].mode != 0) FJ_TRY((rows_op<WT>(sp.pd[f], g->n, sp.col_d, sp.w_d, od, st)));
+    else FJ_TRY((launch_view<WT>(g, sp.sd[f], sp.rp_d, sp.col_d, sp.w_d, g->n, sp.nnz_d, sp.tsd[f], c->grid_max, od, st)));
     if (overlap) FJ_CK(cudaStreamWaitEvent(st, c->ev_join, 0));
     CgOffOp<WT, KP> oo{u, c->w, sp.rows_o, c->dpart, c->red, done};
+    if (sp.po[f].mode != 0) return rows_op<WT>(sp.po[f], sp.n_bnd, sp.col_o, sp.w_o, oo, st);
     return launch_view<WT>(g, sp.so[f], sp.rp_o, sp.col_o, sp.w_o, sp.n_bnd, sp.nnz_o, sp.tso[f], c->grid_max, oo, st);
   };
   switch (g->wtype) {
@@ -1175,7 +1183,12 @@ static fj_status dist_cg_t(fj_graph* g, int k, const double* sv, double* z, int6
       } else {
         for (int u = 0; u < CG_UNROLL; ++u) FJ_TRY(cg_iteration<KP>(g, c, k, st));
       }
-      if (graph) count_launch((int64_t)CG_UNROLL * (3 + (d->comm->nranks > 1 && d->n_send > 0 ? 1 : 0)));
+      if (graph) {
+        constexpr int f = KP == 1 ? 0 : 1;
+        const int per_it = 1 + rows_op_launches(c->sp.pd[f]) + rows_op_launches(c->sp.po[f]) +
+                           (d->comm->nranks > 1 && d->n_send > 0 ? 1 : 0);
+        count_launch((int64_t)CG_UNROLL * per_it);
+      }
       FJ_CK(cudaMemcpyAsync(&h, c->cs, sizeof h, cudaMemcpyDeviceToHost, st));
       FJ_CK(cudaStreamSynchronize(st));
       if (h.done) break;

@@ -511,6 +511,8 @@ __global__ void __launch_bounds__(RTB, FJ_ROWS_OP_MINB) k_op_rows(const RowsView
   }
 }
 
+inline int rows_op_launches(const RowsPlan& R) { return R.mode == 0 ? 1 : (R.n_chunks > 0 ? 2 : 1); }
+
 // Launch a row operator on a plan built for (rp, col) with nrows rows.  The grid is fixed per
 // (plan, operator instantiation): #SMs x occupancy, so partials are reduced in a fixed order.
 template <int WT, class Op>
