@@ -51,6 +51,12 @@ static_assert(FJ_ROWS_LONG < 65536 && FJ_ROWS_LONG1 < 65536, "slab offsets are u
 #ifndef FJ_ROWS_U
 #define FJ_ROWS_U 4              // independent gathers in flight per lane
 #endif
+#ifndef FJ_ROWS_G_B
+#define FJ_ROWS_G_B 1            // lanes per row in the slab-B pass (C3: 1 0.465 ms, 2 0.475, 4 0.527)
+#endif
+#ifndef FJ_ROWS_U_B
+#define FJ_ROWS_U_B FJ_ROWS_U
+#endif
 #ifndef FJ_ROWS_MINB
 #define FJ_ROWS_MINB 8           // slab-A pass: 8 x 256 threads per SM (32 registers, no spill)
 #endif
@@ -213,7 +219,7 @@ __global__ void __launch_bounds__(RTB) k_rows_chunks(const RowsArgs a) {
 #endif
 template <int WT, int KP, int KQ, int PASS>
 __global__ void __launch_bounds__(RTB, PASS == 0 ? FJ_ROWS_MINB : FJ_ROWS_MINB_FIN) k_rows(const RowsArgs a) {
-  constexpr int G = FJ_ROWS_G, U = FJ_ROWS_U;
+  constexpr int G = PASS == 1 ? FJ_ROWS_G_B : FJ_ROWS_G, U = PASS == 1 ? FJ_ROWS_U_B : FJ_ROWS_U;
   constexpr bool FIN = PASS != 0;
   __shared__ double s_red[4 * RTB / 32];
   if (rows_skip(a)) return;
