@@ -41,7 +41,38 @@ __global__ void k_rows_plan2(int64_t n, const int64_t* __restrict__ rp, const in
     }
   }
 }
+// Slab-major copies (mode 2, unit weights): cA[i] / cB[i] = slab-A / slab-B entries of short row i
+// (0 for long rows, whose entries the chunk warps sum from col), cA[n] = cB[n] = 0 so their
+// exclusive scans are rpA / rpB with the totals at [n].
+__global__ void k_rows_plan3(int64_t n, const int32_t* __restrict__ rp32, const uint16_t* __restrict__ off,
+                             int64_t long_row, int32_t* __restrict__ cA, int32_t* __restrict__ cB) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n; i += (int64_t)gridDim.x * blockDim.x) {
+    if (i == n) { cA[n] = cB[n] = 0; continue; }
+    const int32_t len = rp32[i + 1] - rp32[i];
+    const bool lng = len > long_row;
+    cA[i] = lng ? 0 : off[i];
+    cB[i] = lng ? 0 : len - off[i];
+  }
+}
+// one warp per row: colA[rpA[i] + t] = col[rp[i] + t], colB[rpB[i] + t] = col[rp[i] + off[i] + t]
+__global__ void k_rows_plan4(int64_t n, const int32_t* __restrict__ rp32, const uint16_t* __restrict__ off,
+                             const int32_t* __restrict__ col, const int32_t* __restrict__ rpA,
+                             const int32_t* __restrict__ rpB, int32_t* __restrict__ colA, int32_t* __restrict__ colB) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x / 32);
+  for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < n; i += nw) {
+    const int32_t b = rp32[i], a0 = rpA[i], na = rpA[i + 1] - a0, b0 = rpB[i], nb = rpB[i + 1] - b0;
+    for (int32_t t = lane; t < na; t += 32) colA[a0 + t] = col[b + t];
+    const int32_t o = off[i];
+    for (int32_t t = lane; t < nb; t += 32) colB[b0 + t] = col[b + o + t];
+  }
+}
 
+// FJ_ROWS_SPLIT (A/B): 1 (default) builds the slab-major copies for mode 2 with unit weights, 0 not
+static int rows_split_knob() {
+  static const int v = [] { const char* e = getenv("FJ_ROWS_SPLIT"); return e ? atoi(e) : 1; }();
+  return v;
+}
 
 // FJ_ROWS (A/B, tests): -1 auto (default), 0 merge-path engine, 1 one row pass, 2 two column
 // slabs.  Auto: two slabs when the gathered block (n x kp doubles) is in (64 MB, 160 MB] -- each half
@@ -56,6 +87,7 @@ constexpr int64_t kRowsSlabMin = 64ll << 20, kRowsSlabMax = 160ll << 20;
 void rows_plan_free(RowsPlan& R) {
   dfree(R.off); dfree(R.rp32); dfree(R.c0); dfree(R.tab); dfree(R.chunk_acc); dfree(R.part); dfree(R.ticket);
   dfree(R.op_acc); dfree(R.op_part); dfree(R.op_ticket);
+  dfree(R.rpA); dfree(R.rpB); dfree(R.colA); dfree(R.colB);
   R = RowsPlan{};
 }
 
@@ -68,7 +100,7 @@ static fj_status ralloc(T** p, int64_t count, cudaStream_t st) {
 
 // mode 2 allowed only for a graph's own CSR (two_ok); the knob and the size rule as described above
 static fj_status plan_core(int64_t n, int64_t nnz, const int64_t* row_ptr, const int32_t* col, int kp, int num_sms,
-                           bool two_ok, RowsPlan& R, cudaStream_t st) {
+                           bool two_ok, bool split_ok, RowsPlan& R, cudaStream_t st) {
   rows_plan_free(R);
   const int knob = rows_knob();
   // mode 0, the engine: forced, or a CSR beyond the plan's int32 row_ptr
@@ -113,6 +145,33 @@ static fj_status plan_core(int64_t n, int64_t nnz, const int64_t* row_ptr, const
     dfree(R.off);
     R.off = nullptr;
   }
+  if (two && split_ok && rows_split_knob() && n > 0) {
+    DevBuf<int32_t> cA, cB;
+    FJ_TRY(cA.alloc(n + 1, st));
+    FJ_TRY(cB.alloc(n + 1, st));
+    const unsigned cb1 = (unsigned)std::min<int64_t>((n + 256) / 256, 8192);
+    k_rows_plan3<<<cb1, 256, 0, st>>>(n, R.rp32, R.off, R.long_row, cA.p, cB.p);
+    FJ_CK_LAUNCH();
+    FJ_TRY(ralloc(&R.rpA, n + 1, st));
+    FJ_TRY(ralloc(&R.rpB, n + 1, st));
+    size_t tb = 0;
+    FJ_CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, cA.p, R.rpA, n + 1, st));
+    DevBuf<uint8_t> tmp;
+    FJ_TRY(tmp.alloc((int64_t)tb, st));
+    FJ_CK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, cA.p, R.rpA, n + 1, st));
+    FJ_CK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, cB.p, R.rpB, n + 1, st));
+    count_cub();
+    count_cub();
+    int32_t tot[2] = {0, 0};
+    FJ_CK(cudaMemcpyAsync(&tot[0], R.rpA + n, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    FJ_CK(cudaMemcpyAsync(&tot[1], R.rpB + n, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    FJ_CK(cudaStreamSynchronize(st));
+    FJ_TRY(ralloc(&R.colA, tot[0], st));
+    FJ_TRY(ralloc(&R.colB, tot[1], st));
+    k_rows_plan4<<<(unsigned)std::min<int64_t>((n * 32 + 255) / 256, (int64_t)num_sms * 64), 256, 0, st>>>(
+        n, R.rp32, R.off, col, R.rpA, R.rpB, R.colA, R.colB);
+    FJ_CK_LAUNCH();
+  }
   FJ_TRY(ralloc(&R.tab, 2 * R.n_chunks, st));
   FJ_TRY(ralloc(&R.chunk_acc, 4 * R.n_chunks, st));
   FJ_TRY(ralloc(&R.op_acc, ROWS_NA_MAX * R.n_chunks, st));
@@ -150,12 +209,12 @@ static fj_status plan_core(int64_t n, int64_t nnz, const int64_t* row_ptr, const
 
 fj_status rows_plan_build(fj_graph* g, int kp, RowsPlan& R, cudaStream_t st) {
   if (g->dist) { rows_plan_free(R); return FJ_OK; }   // the distributed path plans its own views
-  return plan_core(g->n, g->nnz, g->row_ptr, g->col, kp, g->num_sms, true, R, st);
+  return plan_core(g->n, g->nnz, g->row_ptr, g->col, kp, g->num_sms, true, g->wtype == FJ_W_UNIT, R, st);
 }
 
 fj_status rows_plan_build_csr(int64_t n, int64_t nnz, const int64_t* row_ptr, const int32_t* col, int kp,
                               int num_sms, RowsPlan& R, cudaStream_t st) {
-  return plan_core(n, nnz, row_ptr, col, kp, num_sms, false, R, st);
+  return plan_core(n, nnz, row_ptr, col, kp, num_sms, false, false, R, st);
 }
 
 }  // namespace fj

@@ -148,18 +148,25 @@ struct RowsArgs {
   PcgScalars* sc1;                      // k = 1 PCG mode (pcg.cu): alpha on device
   double* part;                         // [grid][4] block partials of p^T q
   unsigned int* ticket;                 // [1], self-resetting
+  // slab-major copies of the short rows' entries (unit weights, FJ_ROWS_SPLIT; null: not built):
+  // colA[rpA[i], rpA[i+1]) = row i's slab-A columns, colB[rpB[i], rpB[i+1]) its slab-B columns
+  const int32_t* __restrict__ rpA;
+  const int32_t* __restrict__ rpB;
+  const int32_t* __restrict__ colA;
+  const int32_t* __restrict__ colB;
 };
 
 template <int WT, int KP, int KQ, int U>
-__device__ __forceinline__ void rows_accumulate(const RowsArgs& a, int64_t k, int64_t ke, int stride,
-                                                double (&acc)[KQ], uint64_t ps = 0, uint64_t pg = 0) {
+__device__ __forceinline__ void rows_accumulate(const RowsArgs& a, const int32_t* __restrict__ col, int64_t k,
+                                                int64_t ke, int stride, double (&acc)[KQ], uint64_t ps = 0,
+                                                uint64_t pg = 0) {
   using WS = typename std::conditional<WT == FJ_W_F64, double, float>::type;   // exact for u8 / f32
   for (; k + (int64_t)(U - 1) * stride < ke; k += (int64_t)U * stride) {   // full batches
     int32_t j[U];
     WS wv[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      j[u] = ld_colh(a.col + k + u * stride, ps);
+      j[u] = ld_colh(col + k + u * stride, ps);
       wv[u] = (WT == FJ_W_UNIT) ? (WS)1 : (WS)WeightT<WT>::get(a.w, k + u * stride);
     }
     DVec<KP> v[U];
@@ -171,7 +178,7 @@ __device__ __forceinline__ void rows_accumulate(const RowsArgs& a, int64_t k, in
       for (int c = 0; c < KQ; ++c) acc[c] = (WT == FJ_W_UNIT) ? acc[c] + v[u].v[c] : fma((double)wv[u], v[u].v[c], acc[c]);
   }
   for (; k < ke; k += stride) {
-    const DVec<KP> v = ld_gather<KP>(a.x + (int64_t)ld_colh(a.col + k, ps) * KP, pg);
+    const DVec<KP> v = ld_gather<KP>(a.x + (int64_t)ld_colh(col + k, ps) * KP, pg);
     const double wk = (WT == FJ_W_UNIT) ? 1.0 : (double)WeightT<WT>::get(a.w, k);
 #pragma unroll
     for (int c = 0; c < KQ; ++c) acc[c] = (WT == FJ_W_UNIT) ? acc[c] + v.v[c] : fma(wk, v.v[c], acc[c]);
@@ -191,7 +198,7 @@ __device__ __forceinline__ void rows_chunk_items(const RowsArgs& a, uint64_t ps,
     double acc[KQ];
 #pragma unroll
     for (int f = 0; f < KQ; ++f) acc[f] = 0.0;
-    rows_accumulate<WT, KP, KQ, 4>(a, k0 + lane, k1, 32, acc, ps, pg);
+    rows_accumulate<WT, KP, KQ, 4>(a, a.col, k0 + lane, k1, 32, acc, ps, pg);
 #pragma unroll
     for (int f = 0; f < KQ; ++f) acc[f] = warp_sum(acc[f]);
     if (lane == 0) {
@@ -235,16 +242,29 @@ __global__ void __launch_bounds__(RTB, PASS == 0 ? FJ_ROWS_MINB : FJ_ROWS_MINB_F
   for (int64_t i0 = (blockIdx.x * (int64_t)RTB + (threadIdx.x & ~31)) / G; i0 < a.n; i0 += ng) {
     const int64_t i = i0 + (threadIdx.x & 31) / G;
     const bool valid = i < a.n;
-    const int64_t b = valid ? ld_colh(a.rp32 + i, ps) : 0, e = valid ? ld_colh(a.rp32 + i + 1, ps) : 0;
-    const bool lng = e - b > a.long_row;
-    int64_t kb = b, ke = e;
-    if (PASS == 0 && valid) ke = b + __ldg(a.off + i);
-    if (PASS == 1 && valid) kb = b + __ldg(a.off + i);
-    FJ_DCHECK(kb >= b && ke <= e && kb <= ke);
+    const bool split = PASS != 2 && a.colA != nullptr;   // uniform over the launch
+    int64_t b = 0, e = 0, kb = 0, ke = 0;
+    bool lng = false;
+    if (PASS == 0 && split) {   // slab-major: the row's slab-A entries only (long rows: empty)
+      if (valid) { kb = ld_colh(a.rpA + i, ps); ke = ld_colh(a.rpA + i + 1, ps); }
+    } else {
+      if (valid) { b = ld_colh(a.rp32 + i, ps); e = ld_colh(a.rp32 + i + 1, ps); }
+      lng = e - b > a.long_row;
+      kb = b; ke = e;
+      if (PASS == 1 && split) {
+        if (valid) { kb = ld_colh(a.rpB + i, ps); ke = ld_colh(a.rpB + i + 1, ps); }
+      } else {
+        if (PASS == 0 && valid) ke = b + __ldg(a.off + i);
+        if (PASS == 1 && valid) kb = b + __ldg(a.off + i);
+        FJ_DCHECK(kb >= b && ke <= e && kb <= ke);
+      }
+    }
+    FJ_DCHECK(kb <= ke);
+    const int32_t* __restrict__ colp = !split ? a.col : PASS == 0 ? a.colA : a.colB;
     double acc[KQ];
 #pragma unroll
     for (int f = 0; f < KQ; ++f) acc[f] = 0.0;
-    if (!lng) rows_accumulate<WT, KP, KQ, U>(a, kb + sub, ke, G, acc, ps, pg);
+    if (!lng) rows_accumulate<WT, KP, KQ, U>(a, colp, kb + sub, ke, G, acc, ps, pg);
 #pragma unroll
     for (int o = G / 2; o > 0; o >>= 1)
 #pragma unroll
@@ -342,6 +362,12 @@ struct RowsPlan {
   int64_t* tab = nullptr;            // [n_chunks][2]
   int64_t n_chunks = 0;
   int64_t long_row = 0;
+  // mode 2, unit weights (FJ_ROWS_SPLIT, default on): the short rows' entries in slab-major copies,
+  // so each pass streams only its own entries (no sector of col read by both passes)
+  int32_t* rpA = nullptr;            // [n+1]
+  int32_t* rpB = nullptr;            // [n+1]
+  int32_t* colA = nullptr;           // [rpA[n]]
+  int32_t* colB = nullptr;           // [rpB[n]]
   double* chunk_acc = nullptr;       // [n_chunks][4]
   double* part = nullptr;            // [grid][4]
   unsigned int* ticket = nullptr;
@@ -370,7 +396,7 @@ template <int WT, int KP, int KQ>
 fj_status rows_product(const fj_graph* g, const RowsPlan& R, const double* x, double* y, int opL, int k,
                        VecScalars* vsc, PcgScalars* psc, cudaStream_t st) {
   RowsArgs a{g->n, g->row_ptr, g->col, g->w, R.rp32, R.off, R.c0, R.tab, R.n_chunks, R.long_row, R.chunk_acc,
-             x, y, g->deg, opL, k, vsc, psc, R.part, R.ticket};
+             x, y, g->deg, opL, k, vsc, psc, R.part, R.ticket, R.rpA, R.rpB, R.colA, R.colB};
   if (R.n_chunks > 0 && (R.mode == 1 || !FJ_ROWS_FUSE_CHUNKS)) {
     k_rows_chunks<WT, KP, KQ><<<R.grid_chunks, RTB, 0, st>>>(a);
     FJ_CK_LAUNCH();

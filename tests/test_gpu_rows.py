@@ -1,5 +1,6 @@
-"""The lean row product of the small-k PCG (csrc/rows.cuh) in its three
-selections -- FJ_ROWS=0 (merge-path engine), 1 (one row pass), 2 (two column slabs) -- each run
+"""The lean row product of the small-k PCG (csrc/rows.cuh) in its selections --
+FJ_ROWS=0 (merge-path engine), 1 (one row pass), 2 (two column slabs; unit weights read the
+slab-major column copies), "2s" (two slabs with FJ_ROWS_SPLIT=0: both passes on the CSR) -- each run
 in its own process (the knob is read once per process): every column against the CPU oracle
 (quantities <= 1e-8 and inside their certificates, z to 1e-9), the product (I+L)S against the
 oracle's, bitwise repeatability and graph / host-loop agreement, and the path each run took."""
@@ -16,6 +17,8 @@ from rows_cases import CASES, case_inputs
 pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 KEYS = ["CI", "D", "P", "C", "Idc", "PDI"]
+MODES = (0, 1, 2, "2s")
+PATHS = {0: "engine", 1: "rows", 2: "rows_slabs", "2s": "rows_slabs"}
 
 
 @pytest.fixture(scope="module")
@@ -26,9 +29,9 @@ def runs(tmp_path_factory):
     from paper_2101_08143_b200 import build as B
     B.build()
     out = {}
-    for mode in (0, 1, 2):
+    for mode in MODES:
         f = str(tmp_path_factory.mktemp("rows") / f"m{mode}.npz")
-        env = dict(os.environ, FJ_ROWS=str(mode))
+        env = dict(os.environ, FJ_ROWS=str(mode)[0], FJ_ROWS_SPLIT="0" if mode == "2s" else "1")
         r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "rows_worker.py"), f], env=env,
                            capture_output=True, text=True, timeout=600)
         assert r.returncode == 0, r.stderr[-3000:]
@@ -55,13 +58,13 @@ def oracle_results():
     return res
 
 
-@pytest.mark.parametrize("mode", [0, 1, 2])
+@pytest.mark.parametrize("mode", MODES)
 @pytest.mark.parametrize("name", CASES)
 def test_rows_product_modes_vs_oracle(runs, oracle_results, mode, name):
     r = runs[mode]
     g, S, cols, Y, T = oracle_results[name]
     path = str(r[name + "/path"])
-    assert path == {0: "engine", 1: "rows", 2: "rows_slabs"}[mode], path
+    assert path == PATHS[mode], path
     it, conv, rel, bk = r[name + "/rep"]
     assert conv == 1 and rel <= 1e-10 and bk == (S.shape[1] if S.shape[1] > 1 else 0)
     assert r[name + "/same"].all(), r[name + "/same"]     # repeat bitwise, graph == host loop
@@ -86,7 +89,7 @@ def test_rows_product_modes_vs_oracle(runs, oracle_results, mode, name):
 @pytest.mark.parametrize("name", CASES)
 def test_rows_modes_agree(runs, name):
     """The three product paths reach the same iterates up to rounding (same iteration count +-1)."""
-    its = [int(runs[m][name + "/rep"][0]) for m in (0, 1, 2)]
+    its = [int(runs[m][name + "/rep"][0]) for m in MODES]
     assert max(its) - min(its) <= 1, its
-    for m in (1, 2):
+    for m in MODES[1:]:
         assert np.max(np.abs(runs[m][name + "/z"] - runs[0][name + "/z"])) < 1e-9

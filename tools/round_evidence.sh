@@ -3,8 +3,8 @@
 # of ONE product (all its launches) with its DRAM traffic recorded under the build's source hash.
 # Usage: bash tools/round_evidence.sh <tag> [kernel regex] [launches per product]
 TAG=${1:-r02}
-KREGEX=${2:-"k_rows"}
-NL=${3:-3}
+KREGEX=${2:-"k_rows<"}
+NL=${3:-2}
 mkdir -p gpurun_out
 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests_$TAG.log 2>&1; echo "tests rc=$?" >> gpurun_out/gpu_tests_$TAG.log
 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err; echo "bench rc=$?" >> gpurun_out/bench_$TAG.err
