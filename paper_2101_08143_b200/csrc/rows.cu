@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <climits>
 #include <cstdlib>
+#include <type_traits>
 
 #include "rows.cuh"
 #include "workspace.cuh"
@@ -55,20 +56,30 @@ __global__ void k_rows_plan3(int64_t n, const int32_t* __restrict__ rp32, const 
   }
 }
 // one warp per row: colA[rpA[i] + t] = col[rp[i] + t], colB[rpB[i] + t] = col[rp[i] + off[i] + t]
+// (and the weights alike, T the weight type; T = void: unit weights, no array)
+template <class T>
 __global__ void k_rows_plan4(int64_t n, const int32_t* __restrict__ rp32, const uint16_t* __restrict__ off,
-                             const int32_t* __restrict__ col, const int32_t* __restrict__ rpA,
-                             const int32_t* __restrict__ rpB, int32_t* __restrict__ colA, int32_t* __restrict__ colB) {
+                             const int32_t* __restrict__ col, const void* __restrict__ w,
+                             const int32_t* __restrict__ rpA, const int32_t* __restrict__ rpB,
+                             int32_t* __restrict__ colA, int32_t* __restrict__ colB, void* __restrict__ wA,
+                             void* __restrict__ wB) {
   const int lane = threadIdx.x & 31;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x / 32);
   for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < n; i += nw) {
     const int32_t b = rp32[i], a0 = rpA[i], na = rpA[i + 1] - a0, b0 = rpB[i], nb = rpB[i + 1] - b0;
-    for (int32_t t = lane; t < na; t += 32) colA[a0 + t] = col[b + t];
     const int32_t o = off[i];
+    for (int32_t t = lane; t < na; t += 32) colA[a0 + t] = col[b + t];
     for (int32_t t = lane; t < nb; t += 32) colB[b0 + t] = col[b + o + t];
+    if constexpr (!std::is_void<T>::value) {
+      const T* ws = reinterpret_cast<const T*>(w);
+      for (int32_t t = lane; t < na; t += 32) reinterpret_cast<T*>(wA)[a0 + t] = ws[b + t];
+      for (int32_t t = lane; t < nb; t += 32) reinterpret_cast<T*>(wB)[b0 + t] = ws[b + o + t];
+    }
   }
 }
+template <class T> struct WTag { using type = T; };
 
-// FJ_ROWS_SPLIT (A/B): 1 (default) builds the slab-major copies for mode 2 with unit weights, 0 not
+// FJ_ROWS_SPLIT (A/B): 1 (default) builds the slab-major copies for mode 2, 0 not
 static int rows_split_knob() {
   static const int v = [] { const char* e = getenv("FJ_ROWS_SPLIT"); return e ? atoi(e) : 1; }();
   return v;
@@ -87,7 +98,7 @@ constexpr int64_t kRowsSlabMin = 64ll << 20, kRowsSlabMax = 160ll << 20;
 void rows_plan_free(RowsPlan& R) {
   dfree(R.off); dfree(R.rp32); dfree(R.c0); dfree(R.tab); dfree(R.chunk_acc); dfree(R.part); dfree(R.ticket);
   dfree(R.op_acc); dfree(R.op_part); dfree(R.op_ticket);
-  dfree(R.rpA); dfree(R.rpB); dfree(R.colA); dfree(R.colB);
+  dfree(R.rpA); dfree(R.rpB); dfree(R.colA); dfree(R.colB); dfree(R.wA); dfree(R.wB);
   R = RowsPlan{};
 }
 
@@ -100,7 +111,7 @@ static fj_status ralloc(T** p, int64_t count, cudaStream_t st) {
 
 // mode 2 allowed only for a graph's own CSR (two_ok); the knob and the size rule as described above
 static fj_status plan_core(int64_t n, int64_t nnz, const int64_t* row_ptr, const int32_t* col, int kp, int num_sms,
-                           bool two_ok, bool split_ok, RowsPlan& R, cudaStream_t st) {
+                           bool two_ok, const void* w, int wtype, RowsPlan& R, cudaStream_t st) {
   rows_plan_free(R);
   const int knob = rows_knob();
   // mode 0, the engine: forced, or a CSR beyond the plan's int32 row_ptr
@@ -145,7 +156,7 @@ static fj_status plan_core(int64_t n, int64_t nnz, const int64_t* row_ptr, const
     dfree(R.off);
     R.off = nullptr;
   }
-  if (two && split_ok && rows_split_knob() && n > 0) {
+  if (two && rows_split_knob() && n > 0) {
     DevBuf<int32_t> cA, cB;
     FJ_TRY(cA.alloc(n + 1, st));
     FJ_TRY(cB.alloc(n + 1, st));
@@ -168,8 +179,22 @@ static fj_status plan_core(int64_t n, int64_t nnz, const int64_t* row_ptr, const
     FJ_CK(cudaStreamSynchronize(st));
     FJ_TRY(ralloc(&R.colA, tot[0], st));
     FJ_TRY(ralloc(&R.colB, tot[1], st));
-    k_rows_plan4<<<(unsigned)std::min<int64_t>((n * 32 + 255) / 256, (int64_t)num_sms * 64), 256, 0, st>>>(
-        n, R.rp32, R.off, col, R.rpA, R.rpB, R.colA, R.colB);
+    const int wsz = wtype == FJ_W_U8 ? 1 : wtype == FJ_W_F32 ? 4 : wtype == FJ_W_F64 ? 8 : 0;
+    if (wsz) {
+      FJ_TRY(ralloc(reinterpret_cast<uint8_t**>(&R.wA), (int64_t)tot[0] * wsz, st));
+      FJ_TRY(ralloc(reinterpret_cast<uint8_t**>(&R.wB), (int64_t)tot[1] * wsz, st));
+    }
+    const unsigned cb4 = (unsigned)std::min<int64_t>((n * 32 + 255) / 256, (int64_t)num_sms * 64);
+    auto copy = [&](auto tag) {
+      using T = typename decltype(tag)::type;
+      k_rows_plan4<T><<<cb4, 256, 0, st>>>(n, R.rp32, R.off, col, w, R.rpA, R.rpB, R.colA, R.colB, R.wA, R.wB);
+    };
+    switch (wsz) {
+      case 1: copy(WTag<uint8_t>()); break;
+      case 4: copy(WTag<float>()); break;
+      case 8: copy(WTag<double>()); break;
+      default: copy(WTag<void>()); break;
+    }
     FJ_CK_LAUNCH();
   }
   FJ_TRY(ralloc(&R.tab, 2 * R.n_chunks, st));
@@ -209,12 +234,12 @@ static fj_status plan_core(int64_t n, int64_t nnz, const int64_t* row_ptr, const
 
 fj_status rows_plan_build(fj_graph* g, int kp, RowsPlan& R, cudaStream_t st) {
   if (g->dist) { rows_plan_free(R); return FJ_OK; }   // the distributed path plans its own views
-  return plan_core(g->n, g->nnz, g->row_ptr, g->col, kp, g->num_sms, true, g->wtype == FJ_W_UNIT, R, st);
+  return plan_core(g->n, g->nnz, g->row_ptr, g->col, kp, g->num_sms, true, g->w, g->wtype, R, st);
 }
 
 fj_status rows_plan_build_csr(int64_t n, int64_t nnz, const int64_t* row_ptr, const int32_t* col, int kp,
                               int num_sms, RowsPlan& R, cudaStream_t st) {
-  return plan_core(n, nnz, row_ptr, col, kp, num_sms, false, false, R, st);
+  return plan_core(n, nnz, row_ptr, col, kp, num_sms, false, nullptr, FJ_W_UNIT, R, st);
 }
 
 }  // namespace fj

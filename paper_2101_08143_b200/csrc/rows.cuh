@@ -148,18 +148,21 @@ struct RowsArgs {
   PcgScalars* sc1;                      // k = 1 PCG mode (pcg.cu): alpha on device
   double* part;                         // [grid][4] block partials of p^T q
   unsigned int* ticket;                 // [1], self-resetting
-  // slab-major copies of the short rows' entries (unit weights, FJ_ROWS_SPLIT; null: not built):
-  // colA[rpA[i], rpA[i+1]) = row i's slab-A columns, colB[rpB[i], rpB[i+1]) its slab-B columns
+  // slab-major copies of the short rows' entries (FJ_ROWS_SPLIT; null: not built): colA[rpA[i],
+  // rpA[i+1]) = row i's slab-A columns, colB[rpB[i], rpB[i+1]) its slab-B columns; wA / wB their
+  // weights (null for unit weights)
   const int32_t* __restrict__ rpA;
   const int32_t* __restrict__ rpB;
   const int32_t* __restrict__ colA;
   const int32_t* __restrict__ colB;
+  const void* __restrict__ wA;
+  const void* __restrict__ wB;
 };
 
 template <int WT, int KP, int KQ, int U>
-__device__ __forceinline__ void rows_accumulate(const RowsArgs& a, const int32_t* __restrict__ col, int64_t k,
-                                                int64_t ke, int stride, double (&acc)[KQ], uint64_t ps = 0,
-                                                uint64_t pg = 0) {
+__device__ __forceinline__ void rows_accumulate(const RowsArgs& a, const int32_t* __restrict__ col,
+                                                const void* __restrict__ w, int64_t k, int64_t ke, int stride,
+                                                double (&acc)[KQ], uint64_t ps = 0, uint64_t pg = 0) {
   using WS = typename std::conditional<WT == FJ_W_F64, double, float>::type;   // exact for u8 / f32
   for (; k + (int64_t)(U - 1) * stride < ke; k += (int64_t)U * stride) {   // full batches
     int32_t j[U];
@@ -167,7 +170,7 @@ __device__ __forceinline__ void rows_accumulate(const RowsArgs& a, const int32_t
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       j[u] = ld_colh(col + k + u * stride, ps);
-      wv[u] = (WT == FJ_W_UNIT) ? (WS)1 : (WS)WeightT<WT>::get(a.w, k + u * stride);
+      wv[u] = (WT == FJ_W_UNIT) ? (WS)1 : (WS)WeightT<WT>::get(w, k + u * stride);
     }
     DVec<KP> v[U];
 #pragma unroll
@@ -179,7 +182,7 @@ __device__ __forceinline__ void rows_accumulate(const RowsArgs& a, const int32_t
   }
   for (; k < ke; k += stride) {
     const DVec<KP> v = ld_gather<KP>(a.x + (int64_t)ld_colh(col + k, ps) * KP, pg);
-    const double wk = (WT == FJ_W_UNIT) ? 1.0 : (double)WeightT<WT>::get(a.w, k);
+    const double wk = (WT == FJ_W_UNIT) ? 1.0 : (double)WeightT<WT>::get(w, k);
 #pragma unroll
     for (int c = 0; c < KQ; ++c) acc[c] = (WT == FJ_W_UNIT) ? acc[c] + v.v[c] : fma(wk, v.v[c], acc[c]);
   }
@@ -198,7 +201,7 @@ __device__ __forceinline__ void rows_chunk_items(const RowsArgs& a, uint64_t ps,
     double acc[KQ];
 #pragma unroll
     for (int f = 0; f < KQ; ++f) acc[f] = 0.0;
-    rows_accumulate<WT, KP, KQ, 4>(a, a.col, k0 + lane, k1, 32, acc, ps, pg);
+    rows_accumulate<WT, KP, KQ, 4>(a, a.col, a.w, k0 + lane, k1, 32, acc, ps, pg);
 #pragma unroll
     for (int f = 0; f < KQ; ++f) acc[f] = warp_sum(acc[f]);
     if (lane == 0) {
@@ -261,10 +264,11 @@ __global__ void __launch_bounds__(RTB, PASS == 0 ? FJ_ROWS_MINB : FJ_ROWS_MINB_F
     }
     FJ_DCHECK(kb <= ke);
     const int32_t* __restrict__ colp = !split ? a.col : PASS == 0 ? a.colA : a.colB;
+    const void* __restrict__ wp = !split ? a.w : PASS == 0 ? a.wA : a.wB;
     double acc[KQ];
 #pragma unroll
     for (int f = 0; f < KQ; ++f) acc[f] = 0.0;
-    if (!lng) rows_accumulate<WT, KP, KQ, U>(a, colp, kb + sub, ke, G, acc, ps, pg);
+    if (!lng) rows_accumulate<WT, KP, KQ, U>(a, colp, wp, kb + sub, ke, G, acc, ps, pg);
 #pragma unroll
     for (int o = G / 2; o > 0; o >>= 1)
 #pragma unroll
@@ -362,12 +366,14 @@ struct RowsPlan {
   int64_t* tab = nullptr;            // [n_chunks][2]
   int64_t n_chunks = 0;
   int64_t long_row = 0;
-  // mode 2, unit weights (FJ_ROWS_SPLIT, default on): the short rows' entries in slab-major copies,
+  // mode 2 (FJ_ROWS_SPLIT, default on): the short rows' entries (and weights) in slab-major copies,
   // so each pass streams only its own entries (no sector of col read by both passes)
   int32_t* rpA = nullptr;            // [n+1]
   int32_t* rpB = nullptr;            // [n+1]
   int32_t* colA = nullptr;           // [rpA[n]]
   int32_t* colB = nullptr;           // [rpB[n]]
+  void* wA = nullptr;                // weights of colA / colB (null: unit weights)
+  void* wB = nullptr;
   double* chunk_acc = nullptr;       // [n_chunks][4]
   double* part = nullptr;            // [grid][4]
   unsigned int* ticket = nullptr;
@@ -396,7 +402,7 @@ template <int WT, int KP, int KQ>
 fj_status rows_product(const fj_graph* g, const RowsPlan& R, const double* x, double* y, int opL, int k,
                        VecScalars* vsc, PcgScalars* psc, cudaStream_t st) {
   RowsArgs a{g->n, g->row_ptr, g->col, g->w, R.rp32, R.off, R.c0, R.tab, R.n_chunks, R.long_row, R.chunk_acc,
-             x, y, g->deg, opL, k, vsc, psc, R.part, R.ticket, R.rpA, R.rpB, R.colA, R.colB};
+             x, y, g->deg, opL, k, vsc, psc, R.part, R.ticket, R.rpA, R.rpB, R.colA, R.colB, R.wA, R.wB};
   if (R.n_chunks > 0 && (R.mode == 1 || !FJ_ROWS_FUSE_CHUNKS)) {
     k_rows_chunks<WT, KP, KQ><<<R.grid_chunks, RTB, 0, st>>>(a);
     FJ_CK_LAUNCH();
