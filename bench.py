@@ -42,6 +42,10 @@ def spmv_bytes(n, nnz, wb, k):
 
 
 def spmv_kernel_name(k, path="engine"):
+    if k == 1 and path == "rows":
+        return "k_rows_chunks + k_rows<PASS 2> ((I+L)p SpMV, lean row kernel, one pass, k = 1; DESIGN.md 6.10)"
+    if k == 1 and path == "rows_slabs":
+        return "k_rows<PASS 0> + k_rows<PASS 1> ((I+L)p SpMV, lean row kernel over two column slabs, k = 1)"
     if k == 1:
         return "warp_kernel<ApplyOp> ((I+L)p SpMV, warp-item engine, k = 1)"
     kp = 2 if k <= 2 else 4

@@ -51,8 +51,9 @@ __global__ void k_rows_plan3(int64_t n, const int32_t* __restrict__ rp32, const 
     if (i == n) { cA[n] = cB[n] = 0; continue; }
     const int32_t len = rp32[i + 1] - rp32[i];
     const bool lng = len > long_row;
-    cA[i] = lng ? 0 : off[i];
-    cB[i] = lng ? 0 : len - off[i];
+    const int32_t na = lng ? 0 : off[i], nb = lng ? 0 : len - off[i];
+    cA[i] = FJ_ROWS_PAD_A ? (na + FJ_ROWS_PAD_A - 1) / FJ_ROWS_PAD_A * FJ_ROWS_PAD_A : na;   // padded row lengths
+    cB[i] = FJ_ROWS_PAD_B ? (nb + FJ_ROWS_PAD_B - 1) / FJ_ROWS_PAD_B * FJ_ROWS_PAD_B : nb;
   }
 }
 // one warp per row: colA[rpA[i] + t] = col[rp[i] + t], colB[rpB[i] + t] = col[rp[i] + off[i] + t]
@@ -66,14 +67,17 @@ __global__ void k_rows_plan4(int64_t n, const int32_t* __restrict__ rp32, const 
   const int lane = threadIdx.x & 31;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x / 32);
   for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < n; i += nw) {
-    const int32_t b = rp32[i], a0 = rpA[i], na = rpA[i + 1] - a0, b0 = rpB[i], nb = rpB[i + 1] - b0;
+    // pa / pb: the copy's (possibly padded) row lengths; na / nb the entries (0 for long rows, whose
+    // ranges are empty); pads are column -1 with weight 0
+    const int32_t b = rp32[i], a0 = rpA[i], pa = rpA[i + 1] - a0, b0 = rpB[i], pb = rpB[i + 1] - b0;
     const int32_t o = off[i];
-    for (int32_t t = lane; t < na; t += 32) colA[a0 + t] = col[b + t];
-    for (int32_t t = lane; t < nb; t += 32) colB[b0 + t] = col[b + o + t];
+    const int32_t na = pa ? o : 0, nb = pb ? rp32[i + 1] - b - o : 0;
+    for (int32_t t = lane; t < pa; t += 32) colA[a0 + t] = t < na ? col[b + t] : -1;
+    for (int32_t t = lane; t < pb; t += 32) colB[b0 + t] = t < nb ? col[b + o + t] : -1;
     if constexpr (!std::is_void<T>::value) {
       const T* ws = reinterpret_cast<const T*>(w);
-      for (int32_t t = lane; t < na; t += 32) reinterpret_cast<T*>(wA)[a0 + t] = ws[b + t];
-      for (int32_t t = lane; t < nb; t += 32) reinterpret_cast<T*>(wB)[b0 + t] = ws[b + o + t];
+      for (int32_t t = lane; t < pa; t += 32) reinterpret_cast<T*>(wA)[a0 + t] = t < na ? ws[b + t] : T(0);
+      for (int32_t t = lane; t < pb; t += 32) reinterpret_cast<T*>(wB)[b0 + t] = t < nb ? ws[b + o + t] : T(0);
     }
   }
 }

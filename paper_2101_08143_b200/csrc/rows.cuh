@@ -188,6 +188,48 @@ __device__ __forceinline__ void rows_accumulate(const RowsArgs& a, const int32_t
   }
 }
 
+// Padded slab-major copies (FJ_ROWS_PAD_A / FJ_ROWS_PAD_B = 4; 0: unpadded): each row's entries of the
+// copy start at a multiple of 4 and are padded to a multiple of 4 with column -1 (weight 0), so a
+// lane reads FOUR column indices with one aligned 16-byte load (one L1 wavefront per lane group
+// instead of four, no tail loop) and issues their gathers together; pads gather nothing and add 0.
+// Measured on C3 k = 3 (profiles/r02_ab_rows_pad.log): slab A padded 0.4476 -> 0.4313 ms (kept: the
+// pass is L1TEX-wavefront bound); slab B padded (its rows hold ~5 entries: +30 % of
+// its column stream) 0.470 ms, both 0.453 ms (not kept).
+#ifndef FJ_ROWS_PAD_A
+#define FJ_ROWS_PAD_A 4
+#endif
+#ifndef FJ_ROWS_PAD_B
+#define FJ_ROWS_PAD_B 0
+#endif
+template <int WT, int KP, int KQ>
+__device__ __forceinline__ void rows_accumulate_pad4(const RowsArgs& a, const int32_t* __restrict__ col,
+                                                     const void* __restrict__ w, int64_t k4, int64_t k4e, int stride,
+                                                     double (&acc)[KQ]) {
+  using WS = typename std::conditional<WT == FJ_W_F64, double, float>::type;
+  for (; k4 < k4e; k4 += stride) {
+    const int4 c = __ldg(reinterpret_cast<const int4*>(col) + k4);
+    const int32_t j[4] = {c.x, c.y, c.z, c.w};
+    WS wv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) wv[u] = (WT == FJ_W_UNIT) ? (WS)1 : (WS)WeightT<WT>::get(w, 4 * k4 + u);
+    DVec<KP> v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (j[u] >= 0) {
+        v[u] = ldg_vec<KP>(a.x + (int64_t)j[u] * KP);
+      } else {
+#pragma unroll
+        for (int c2 = 0; c2 < KP; ++c2) v[u].v[c2] = 0.0;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int c2 = 0; c2 < KQ; ++c2)
+        acc[c2] = (WT == FJ_W_UNIT) ? acc[c2] + v[u].v[c2] : fma((double)wv[u], v[u].v[c2], acc[c2]);
+  }
+}
+
 // Long-row chunks: one warp per chunk (grid-stride over the launch's warps), chunk_acc[c] = sum
 // w p_j over the chunk.
 template <int WT, int KP, int KQ>
@@ -268,7 +310,12 @@ __global__ void __launch_bounds__(RTB, PASS == 0 ? FJ_ROWS_MINB : FJ_ROWS_MINB_F
     double acc[KQ];
 #pragma unroll
     for (int f = 0; f < KQ; ++f) acc[f] = 0.0;
-    if (!lng) rows_accumulate<WT, KP, KQ, U>(a, colp, wp, kb + sub, ke, G, acc, ps, pg);
+    constexpr int PAD = PASS == 0 ? FJ_ROWS_PAD_A : PASS == 1 ? FJ_ROWS_PAD_B : 0;
+    if (PAD == 4 && split) {   // padded copies: kb, ke are multiples of 4 (long rows: empty)
+      rows_accumulate_pad4<WT, KP, KQ>(a, colp, wp, (kb >> 2) + sub, ke >> 2, G, acc);
+    } else if (!lng) {
+      rows_accumulate<WT, KP, KQ, U>(a, colp, wp, kb + sub, ke, G, acc, ps, pg);
+    }
 #pragma unroll
     for (int o = G / 2; o > 0; o >>= 1)
 #pragma unroll
