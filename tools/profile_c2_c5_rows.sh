@@ -8,7 +8,7 @@ for co in "c2 natural" "c5 degree"; do
   set -- $co
   PCMD="python tools/spmv_variants.py --config $1 --k 1 --reps 3 --order $2"
   $PCMD > gpurun_out/prof_rows_plain_$1.log 2>&1 && \
-  timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:k_rows" -s 2 -c 2 \
+  timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:k_rows(<|_chunks)" -s 2 -c 2 \
       -o gpurun_out/full_rows_$1_k1 $PCMD > gpurun_out/ncu_full_rows_$1.log 2>&1
   echo "full $1 rc=$?" >> gpurun_out/ncu_full_rows_$1.log
 done

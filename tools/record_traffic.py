@@ -24,7 +24,8 @@ scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 launches = [dict(zip(hdr, vals)) for vals in rows[2:] if len(vals) == len(hdr)]
 tot = sum(float(d[m].replace(",", "")) * scale[u[m]] for d in launches
           for m in ["dram__bytes_read.sum", "dram__bytes_write.sum"])
-tunit = 1e-3 if u["gpu__time_duration.sum"] == "nsecond" else 1
+tunit = {"ns": 1e-3, "nsecond": 1e-3, "us": 1, "usecond": 1, "ms": 1e3, "msecond": 1e3, "s": 1e6, "second": 1e6}[
+    u["gpu__time_duration.sum"]]   # -> microseconds
 dur = sum(float(d["gpu__time_duration.sum"].replace(",", "")) * tunit for d in launches)
 d = launches[0]
 path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
